@@ -1,0 +1,153 @@
+/*
+ * gwasgls_b200.h — C-ABI of the B200-native GLS hot path (libgwasgls_b200.so).
+ *
+ * This is the drop-in boundary for the reference package `gwasgls` (pure Python,
+ * /root/reference/pkg/src/gwasgls).  The reference has no FFI of its own: its
+ * boundary is the module namespace `gwasgls.kernel`.  Each entry
+ * point below replaces one function of that namespace (cited per function); the
+ * Python host layer `paper_1304_2272_b200.kernel` binds them with ctypes and keeps
+ * the reference's names, signatures and exceptions.  INTEGRATION.md shows the
+ * reference-side binding.
+ *
+ * Conventions (all entry points):
+ *   - Return an int status: GG_OK, or one of the GG_E* codes; gg_last_error()
+ *     returns the message of the calling thread's last failure.
+ *   - Pointers are DEVICE pointers on the calling thread's current CUDA device,
+ *     unless named *_host.  `stream` is a cudaStream_t (NULL = legacy default).
+ *   - All matrices are column-major FP64 ("F-order", like the reference's
+ *     buffers, pipeline.py:195).  Every matrix whose rows run over the n
+ *     individuals is stored with its rows padded to np = gg_pad(n) (a multiple of
+ *     GG_TILE) and leading dimension >= np.  Padding rows of right-hand sides
+ *     are zero; L and Linv are extended by the identity on the padding block.
+ *     Column counts are never padded.
+ *   - No entry point allocates persistent memory; workspaces come from the caller
+ *     (sizes from the *_workspace_bytes queries).  Entry points are reentrant and
+ *     keep no unguarded global state (SPEC threading rule).
+ */
+#ifndef GWASGLS_B200_H
+#define GWASGLS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GG_OK 0
+#define GG_ENOTPD 1      /* Cholesky pivot <= 0 / NaN, or non-finite input      */
+#define GG_EDIM 2        /* inconsistent sizes / leading dimensions              */
+#define GG_ECUDA 3       /* CUDA runtime error                                   */
+#define GG_ENCCL 4       /* reserved for the NCCL (distributed) entry points     */
+#define GG_EARG 5        /* invalid argument (NULL pointer, unsupported p, ...)  */
+
+#define GG_TILE 128      /* row padding unit = GEMM tile edge                    */
+#define GG_PMAX 20       /* largest p supported by the small-system solver       */
+
+/* Library identification / errors. */
+const char* gg_version(void);
+const char* gg_last_error(void);
+int gg_pad(int n);                               /* round n up to GG_TILE          */
+
+/* ---- Cholesky + triangular inverse ------------------------------------------------
+ * Replaces kernel.cholesky_spd (kernel.py:92-109: LAPACK dpotrf lower, clean=1,
+ * input untouched) and produces, in the same pass, Linv = L^-1 (the operand of the
+ * streamed TRSM, see gg_trsm_lower_f64).
+ *   M      : n x n, leading dimension ldm (>= n); only read.
+ *   L      : np x np output, ld = ldp (>= np, multiple of 2); lower factor, upper zero.
+ *   Linv   : np x np output, ld = ldp; lower inverse, upper zero.
+ *   work   : gg_potrf_workspace_bytes(n) bytes of device scratch.
+ *   info_host[0] : -1 on success, else the 0-based failing pivot (LAPACK info-1, or
+ *                  for non-finite input the row of the first non-finite entry in
+ *                  row-major order, kernel.py:101-103).
+ *   info_host[1] : 1 iff the failure was a non-finite entry.
+ * Returns GG_ENOTPD on failure.  Synchronises `stream` (to read the pivot).      */
+size_t gg_potrf_workspace_bytes(int n);
+int gg_potrf_f64(int n, const double* M, int ldm, double* L, double* Linv, int ldp,
+                 void* work, int* info_host, void* stream);
+
+/* Triangular inverse of an arbitrary lower-triangular L (np x np, padded as above,
+ * upper part ignored).  Used by kernel.trsolve_lower (kernel.py:112-121) when the
+ * caller hands in an L that did not come from gg_potrf_f64.                      */
+size_t gg_trtri_workspace_bytes(int n);
+int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp,
+                       void* work, void* stream);
+
+/* ---- Streamed TRSM -----------------------------------------------------------------
+ * X = L^-1 B for nrhs columns, computed as the lower-triangular product Linv * B
+ * on FP64 DMMA tiles (replaces kernel.trsolve_lower, kernel.py:112-121, i.e.
+ * scipy solve_triangular -> dtrtrs -> dtrsm).  B (ldb) and X (ldx) have np rows
+ * (padding rows of B zero); X must not alias B.  Per-column arithmetic is
+ * identical for every column position (column-permutation bitwise invariance,
+ * tests/test_kernel.py:228-241).                                                   */
+int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double* B,
+                      int ldb, double* X, int ldx, void* stream);
+
+/* General FP64 DMMA GEMM on padded operands: C = alpha*A*op(B) + beta*C with
+ * A: m x k (lda), op(B) = B (k x ncols, ldb) or B^T (B stored ncols x k, ldb).
+ * m and k must be multiples of GG_TILE and 16; ncols arbitrary (>= 1; a multiple of
+ * GG_TILE when trans_b).  Exposed for tests and the kinship generator.            */
+int gg_dgemm_f64(int m, int ncols, int k, double alpha, const double* A, int lda,
+                 const double* B, int ldb, int trans_b, double beta, double* C, int ldc,
+                 void* stream);
+
+/* ---- Genotype widening -------------------------------------------------------------
+ * int8 dosages {0,1,2} (n x cnt, ldg) -> FP64 (np x cnt, ldx), padding rows zeroed.
+ * Replaces the FP64 load of BlockReader._load (fileio.py:218-229) for the int8
+ * genotype stream (BASELINE config 2).                                             */
+int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, int ldx,
+                    void* stream);
+
+/* ---- Per-SNP reductions and small SPD solves ----------------------------------------
+ * dots[j*(q+2) + k] = sum_i Xbar[i,j]*XLbar[i,k]  (k < q)      (kernel.py:266-267)
+ * dots[j*(q+2) + q] = sum_i Xbar[i,j]^2                          (kernel.py:268)
+ * dots[j*(q+2)+q+1] = sum_i Xbar[i,j]*ybar[i]                    (kernel.py:269)
+ * One fixed summation order for every column (replaces _column_sums,
+ * kernel.py:260-270, and kernel.gram, kernel.py:124-131).                          */
+int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx,
+                    const double* XLbar, int ldxl, const double* ybar, double* dots,
+                    void* stream);
+
+/* Batched small SPD solve (replaces kernel.cholesky_solve_batch, kernel.py:138-208):
+ * S (batch x p x p, row-major per system), rhs (batch x p) -> x (batch x p; NaN rows
+ * for failed systems), status (batch; -1 ok, else first failing pivot j),
+ * sinv_packed (batch x p(p+1)/2 in np.tril_indices order, or NULL).  2 <= p <= 20
+ * (p = 1 allowed).                                                                  */
+int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs,
+                           double* x, int* status, double* sinv_packed, void* stream);
+
+/* Fused epilogue (replaces kernel.solve_whitened_block's arithmetic,
+ * kernel.py:273-294): reductions above + assembly of S = [[S_TL, S_BL^T],[S_BL, S_BR]],
+ * rhs = [b_T, b_B] + the small SPD solve.  S_TL (q x q row-major), b_T (q) device.
+ * beta (cnt x p), status (cnt), sinv (cnt x p(p+1)/2 or NULL).                      */
+int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
+                        const double* XLbar, int ldxl, const double* ybar,
+                        const double* S_TL, const double* b_T, double* beta, int* status,
+                        double* sinv, void* stream);
+
+/* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342):
+ * [widen int8 ->] TRSM (Linv * X) -> fused epilogue.  Exactly one of X64 (np rows,
+ * ldx) / G8 (n rows, ldg) is non-NULL.  xbar_work: np x cnt FP64 scratch (ld = np),
+ * x64_work: np x cnt FP64 scratch used only for the int8 path (may be NULL otherwise). */
+int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp,
+                     const double* XLbar, const double* ybar, const double* S_TL,
+                     const double* b_T, const double* X64, int ldx, const int8_t* G8,
+                     long long ldg, double* x64_work, double* xbar_work, double* beta,
+                     int* status, double* sinv, void* stream);
+
+/* ---- Synthetic BASELINE generator (test / bench data, not on the timed path) ------
+ * Counter-based splitmix64 streams (the reference's datagen.py:35-52 construction),
+ * bit-identical to paper_1304_2272_b200.datagen on the host.
+ * maf[j] = maf_lo + (maf_hi - maf_lo) * U(seed, STREAM_MAF, first + j)
+ * G[i, j] = [U(seed, s_geno, (first+j)*n + i) < f] + [U(seed, s_geno, (m+first+j)*n + i) < f]
+ * Written as int8 (n x cnt, ldg).  When Z != NULL also writes the standardised
+ * Z = (G - 2f)/sqrt(2f(1-f)) as FP64 (np x cnt, ldz, padding rows zero).           */
+int gg_gen_genotypes_i8(unsigned long long seed, int stream_maf, int stream_geno, int n,
+                        long long m, long long first, int cnt, double maf_lo,
+                        double maf_hi, int8_t* G, long long ldg, double* Z, int ldz,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GWASGLS_B200_H */

@@ -1,0 +1,173 @@
+// extern "C" entry points of libgwasgls_b200.so (declared in include/gwasgls_b200.h).
+// Each validates its arguments, runs on the caller's stream and current device, and reports
+// failures through a status code plus a thread-local message.
+#include <cstdio>
+#include <string>
+
+#include "gg_internal.cuh"
+
+namespace gg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return GG_ECUDA;
+}
+
+}  // namespace gg
+
+using gg::pad_rows;
+
+static inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* gg_version(void) { return "gwasgls_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+const char* gg_last_error(void) { return gg::g_last_error.c_str(); }
+
+int gg_pad(int n) { return pad_rows(n); }
+
+size_t gg_potrf_workspace_bytes(int n) { return n < 1 ? 0 : gg::potrf_ws_bytes(n); }
+
+int gg_potrf_f64(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
+                 int* info_host, void* stream) {
+  return gg::potrf_run(n, M, ldm, L, Linv, ldp, work, info_host, as_stream(stream));
+}
+
+size_t gg_trtri_workspace_bytes(int n) { return n < 1 ? 0 : gg::trtri_ws_bytes(n); }
+
+int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp, void* work,
+                       void* stream) {
+  return gg::trtri_run(n, L, ldl, Linv, ldp, work, as_stream(stream));
+}
+
+int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double* B, int ldb,
+                      double* X, int ldx, void* stream) {
+  if (n < 1 || nrhs < 0 || Linv == nullptr || B == nullptr || X == nullptr) {
+    gg::set_error("trsm: null pointer or bad size");
+    return GG_EARG;
+  }
+  if (B == X) {
+    gg::set_error("trsm: X must not alias B");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  if (ldp < np || ldb < np || ldx < np) {
+    gg::set_error("trsm: leading dimensions must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  if (nrhs == 0) return GG_OK;
+  gg::GemmArgs a{};
+  a.M = np; a.N = nrhs; a.K = np;
+  a.A = Linv; a.lda = ldp;
+  a.B = B; a.ldb = ldb;
+  a.C = X; a.ldc = ldx;
+  a.alpha = 1.0; a.beta = 0.0;
+  a.flags = gg::GEMM_A_LOWER;
+  a.abort_flag = nullptr;
+  return gg::launch_dgemm(a, false, as_stream(stream));
+}
+
+int gg_dgemm_f64(int m, int ncols, int k, double alpha, const double* A, int lda, const double* B,
+                 int ldb, int trans_b, double beta, double* C, int ldc, void* stream) {
+  if (A == nullptr || B == nullptr || C == nullptr) {
+    gg::set_error("dgemm: null pointer");
+    return GG_EARG;
+  }
+  gg::GemmArgs a{};
+  a.M = m; a.N = ncols; a.K = k;
+  a.A = A; a.lda = lda;
+  a.B = B; a.ldb = ldb;
+  a.C = C; a.ldc = ldc;
+  a.alpha = alpha; a.beta = beta;
+  a.flags = 0;
+  a.abort_flag = nullptr;
+  return gg::launch_dgemm(a, trans_b != 0, as_stream(stream));
+}
+
+int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, int ldx,
+                    void* stream) {
+  if (n < 1 || cnt < 0 || G == nullptr || X == nullptr) {
+    gg::set_error("widen: null pointer or bad size");
+    return GG_EARG;
+  }
+  return gg::widen_run(n, cnt, G, ldg, X, ldx, as_stream(stream));
+}
+
+int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+                    int ldxl, const double* ybar, double* dots, void* stream) {
+  if (Xbar == nullptr || ybar == nullptr || dots == nullptr || (q > 0 && XLbar == nullptr)) {
+    gg::set_error("dots: null pointer");
+    return GG_EARG;
+  }
+  return gg::dots_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, dots, as_stream(stream));
+}
+
+int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs, double* x,
+                           int* status, double* sinv_packed, void* stream) {
+  if (S == nullptr || rhs == nullptr || x == nullptr || status == nullptr) {
+    gg::set_error("small_spd_solve: null pointer");
+    return GG_EARG;
+  }
+  return gg::small_solve_run(batch, p, S, rhs, x, status, sinv_packed, as_stream(stream));
+}
+
+int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+                        int ldxl, const double* ybar, const double* S_TL, const double* b_T,
+                        double* beta, int* status, double* sinv, void* stream) {
+  if (Xbar == nullptr || ybar == nullptr || beta == nullptr || status == nullptr ||
+      (q > 0 && (XLbar == nullptr || S_TL == nullptr || b_T == nullptr))) {
+    gg::set_error("epilogue: null pointer");
+    return GG_EARG;
+  }
+  return gg::epilogue_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, S_TL, b_T, beta, status, sinv,
+                          as_stream(stream));
+}
+
+int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp, const double* XLbar,
+                     const double* ybar, const double* S_TL, const double* b_T, const double* X64,
+                     int ldx, const int8_t* G8, long long ldg, double* x64_work, double* xbar_work,
+                     double* beta, int* status, double* sinv, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if ((X64 == nullptr) == (G8 == nullptr)) {
+    gg::set_error("gls_block: exactly one of X64 / G8 must be given");
+    return GG_EARG;
+  }
+  if (xbar_work == nullptr || Linv == nullptr) {
+    gg::set_error("gls_block: null workspace / Linv");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  if (cnt <= 0) return GG_OK;
+  const double* xin = X64;
+  int ldin = ldx;
+  if (G8 != nullptr) {
+    if (x64_work == nullptr) {
+      gg::set_error("gls_block: int8 input needs x64_work");
+      return GG_EARG;
+    }
+    int rc = gg::widen_run(n, cnt, G8, ldg, x64_work, np, s);
+    if (rc != GG_OK) return rc;
+    xin = x64_work;
+    ldin = np;
+  }
+  int rc = gg_trsm_lower_f64(n, cnt, Linv, ldp, xin, ldin, xbar_work, np, stream);
+  if (rc != GG_OK) return rc;
+  return gg::epilogue_run(n, cnt, q, xbar_work, np, XLbar, np, ybar, S_TL, b_T, beta, status,
+                          sinv, s);
+}
+
+int gg_gen_genotypes_i8(unsigned long long seed, int stream_maf, int stream_geno, int n,
+                        long long m, long long first, int cnt, double maf_lo, double maf_hi,
+                        int8_t* G, long long ldg, double* Z, int ldz, void* stream) {
+  return gg::gen_genotypes_run(seed, stream_maf, stream_geno, n, m, first, cnt, maf_lo, maf_hi, G,
+                               ldg, Z, ldz, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal declarations shared by the sm_100a translation units of libgwasgls_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/gwasgls_b200.h"
+
+namespace gg {
+
+// ---- error plumbing (thread-local message, no global mutable state) -----------------
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define GG_CUDA_TRY(expr)                                                   \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) return ::gg::cuda_fail(_e, #expr);               \
+  } while (0)
+
+#define GG_LAUNCH_CHECK(what)                                               \
+  do {                                                                      \
+    cudaError_t _e = cudaGetLastError();                                    \
+    if (_e != cudaSuccess) return ::gg::cuda_fail(_e, what);                \
+  } while (0)
+
+inline int pad_rows(int n) { return ((n + GG_TILE - 1) / GG_TILE) * GG_TILE; }
+
+// ---- FP64 DMMA GEMM (gemm_f64.cu) ----------------------------------------------------
+enum GemmFlags : int {
+  GEMM_A_LOWER = 1,   // A lower triangular: row tile mt only needs k < (mt+1)*BM
+  GEMM_B_LOWER = 2,   // op(B) lower triangular (k >= n): column tile nt needs k >= nt*BN
+  GEMM_C_LOWER = 4,   // only tiles on/below the diagonal are computed (SYRK)
+};
+
+struct GemmArgs {
+  int M, N, K;        // M % 128 == 0, K % 16 == 0, N >= 1 arbitrary
+  const double* A;  long long lda;
+  const double* B;  long long ldb;
+  double* C;        long long ldc;
+  double alpha, beta;
+  int flags;
+  const int* abort_flag;   // optional device flag: kernel is a no-op when *abort_flag != 0
+};
+
+// Launch C = alpha*A*op(B) + beta*C.  trans_b selects op(B) = B^T (B stored N x K).
+int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s);
+
+// ---- dense factorisation (potrf_f64.cu) ----------------------------------------------
+int potrf_run(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
+              int* info_host, cudaStream_t s);
+int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work,
+              cudaStream_t s);
+size_t potrf_ws_bytes(int n);
+size_t trtri_ws_bytes(int n);
+
+// ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------
+int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+             int ldxl, const double* ybar, double* dots, cudaStream_t s);
+int small_solve_run(int batch, int p, const double* S, const double* rhs, double* x,
+                    int* status, double* sinv, cudaStream_t s);
+int epilogue_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+                 int ldxl, const double* ybar, const double* S_TL, const double* b_T,
+                 double* beta, int* status, double* sinv, cudaStream_t s);
+int widen_run(int n, int cnt, const int8_t* G, long long ldg, double* X, int ldx,
+              cudaStream_t s);
+
+// ---- generator (datagen.cu) -----------------------------------------------------------
+int gen_genotypes_run(unsigned long long seed, int stream_maf, int stream_geno, int n,
+                      long long m, long long first, int cnt, double maf_lo, double maf_hi,
+                      int8_t* G, long long ldg, double* Z, int ldz, cudaStream_t s);
+
+}  // namespace gg

@@ -1,0 +1,301 @@
+// Blocked FP64 Cholesky (right-looking, nb = 128) fused with the triangular inverse.
+//
+// Replaces kernel.cholesky_spd (reference kernel.py:92-109: LAPACK dpotrf lower, clean=1).
+// Per 128-column block k:
+//   leaf     : one CTA factors the 128x128 diagonal block in shared memory (pivot rule of
+//              LAPACK dpotf2: fail iff a_jj <= 0 or NaN) and inverts it in place
+//              (Dinv_k = L_kk^-1, written to the diagonal block of Linv);
+//   panel    : L21 = A21 * Dinv_k^T                 (DMMA GEMM, op(B) = B^T)
+//   trailing : A22 -= L21 * L21^T, lower tiles only  (DMMA GEMM, K = 128)
+// then the off-diagonal blocks of Linv by the recursive formula
+//   inv([A 0; B C]) = [A^-1 0; -C^-1 B A^-1  C^-1]
+// with triangular-aware DMMA GEMMs.  A failing pivot sets a device flag that turns every later
+// kernel into a no-op; the host reads it once at the end (no per-block synchronisation).
+#include <climits>
+
+#include "gg_internal.cuh"
+
+namespace gg {
+namespace {
+
+constexpr int NB = 128;
+constexpr int LEAF_THREADS = 512;
+constexpr int SLD = NB + 1;   // column stride of the shared leaf block
+constexpr size_t LEAF_SMEM = size_t(NB) * SLD * sizeof(double);
+
+struct PotrfHeader {
+  int info;                      // 0 = ok, else failing pivot + 1
+  int pad_;
+  unsigned long long nonfinite;  // min row-major index of a non-finite entry
+};
+constexpr size_t HDR_BYTES = 256;
+
+__global__ void init_factor_kernel(int n, int np, const double* __restrict__ M, long long ldm,
+                                   double* __restrict__ L, double* __restrict__ Linv,
+                                   long long ldp) {
+  const long long total = (long long)np * np;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % np), j = (int)(idx / np);
+    double v;
+    if (i < n && j < n) v = (i >= j) ? M[i + j * ldm] : 0.0;
+    else v = (i == j) ? 1.0 : 0.0;   // identity extension on the padding block
+    L[i + j * ldp] = v;
+    if (Linv != nullptr) Linv[i + j * ldp] = 0.0;
+  }
+}
+
+__global__ void zero_square_kernel(int np, double* __restrict__ A, long long ld) {
+  const long long total = (long long)np * np;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % np), j = (int)(idx / np);
+    A[i + j * ld] = 0.0;
+  }
+}
+
+// First non-finite entry in row-major order (kernel.py:101-103 reports its row).
+__global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long ldm,
+                                 unsigned long long* first) {
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    if (!isfinite(M[i + j * ldm])) atomicMin(first, (unsigned long long)i * n + j);
+  }
+}
+
+// In-place inverse of the lower-triangular block held in s (column stride SLD).
+// Row-oriented forward substitution on X = I:  X[i,:] /= L_ii;  X[r,:] -= L_ri X[i,:] (r > i).
+// Column i of L is staged in colL before row i's update overwrites it.
+__device__ void leaf_invert_inplace(double* s, double* colL) {
+  const int tid = threadIdx.x;
+  for (int i = 0; i < NB; ++i) {
+    const double lii = s[i * SLD + i];
+    for (int r = i + 1 + tid; r < NB; r += LEAF_THREADS) colL[r] = s[i * SLD + r];
+    for (int c = tid; c < i; c += LEAF_THREADS) s[c * SLD + i] = s[c * SLD + i] / lii;
+    __syncthreads();
+    if (tid == 0) s[i * SLD + i] = 1.0 / lii;
+    const int w = NB - 1 - i;   // rows r = i+1 .. NB-1
+    const int cols = i + 1;     // cols c = 0 .. i
+    for (int idx = tid; idx < w * cols; idx += LEAF_THREADS) {
+      const int r = i + 1 + idx % w, c = idx / w;
+      const double xic = (c == i) ? 1.0 / lii : s[c * SLD + i];
+      if (c == i) s[c * SLD + r] = -(colL[r] * xic);
+      else s[c * SLD + r] = s[c * SLD + r] - colL[r] * xic;
+    }
+    __syncthreads();
+  }
+}
+
+// FACTOR = true : factor the diagonal block at (k0, k0) of A in place (lower, upper zeroed),
+//                 then write its inverse to Dinv.  One CTA, sequential over the blocks.
+// FACTOR = false: blockIdx.x selects diagonal block b; only invert it (triangular inverse of a
+//                 caller-supplied L).  All blocks in parallel.
+template <bool FACTOR>
+__global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long ld, double* Dinv,
+                                                            long long ldi, int k0, int* info) {
+  extern __shared__ double s[];
+  __shared__ double colL[NB];
+  if (info != nullptr && *info != 0) return;
+  const int tid = threadIdx.x;
+  if (!FACTOR) {
+    k0 = blockIdx.x * NB;
+  }
+  const double* Ab = A + k0 + (long long)k0 * ld;
+  double* Db = Dinv + k0 + (long long)k0 * ldi;
+  for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
+    const int i = idx % NB, j = idx / NB;
+    s[j * SLD + i] = (i >= j) ? Ab[i + (long long)j * ld] : 0.0;
+  }
+  __syncthreads();
+  if (FACTOR) {
+    for (int j = 0; j < NB; ++j) {
+      const double d = s[j * SLD + j];
+      if (!(d > 0.0)) {   // dpotf2: a_jj <= 0 or NaN
+        if (tid == 0) *info = k0 + j + 1;
+        return;           // uniform: every thread read the same d
+      }
+      const double piv = sqrt(d);
+      for (int i = j + 1 + tid; i < NB; i += LEAF_THREADS) s[j * SLD + i] = s[j * SLD + i] / piv;
+      __syncthreads();
+      if (tid == 0) s[j * SLD + j] = piv;
+      const int w = NB - 1 - j;
+      for (int idx = tid; idx < w * w; idx += LEAF_THREADS) {
+        const int r = j + 1 + idx % w, c = j + 1 + idx / w;
+        if (r >= c) s[c * SLD + r] = s[c * SLD + r] - s[j * SLD + r] * s[j * SLD + c];
+      }
+      __syncthreads();
+    }
+    double* Aw = A + k0 + (long long)k0 * ld;
+    for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
+      const int i = idx % NB, j = idx / NB;
+      Aw[i + (long long)j * ld] = (i >= j) ? s[j * SLD + i] : 0.0;
+    }
+    __syncthreads();
+  }
+  leaf_invert_inplace(s, colL);
+  for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
+    const int i = idx % NB, j = idx / NB;
+    Db[i + (long long)j * ldi] = (i >= j) ? s[j * SLD + i] : 0.0;
+  }
+}
+
+int grid_for(long long total) {
+  long long g = (total + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Off-diagonal blocks of Linv for the block range [lo, hi) (diagonal blocks already set).
+int trtri_offdiag(int lo, int hi, const double* L, double* Linv, long long ldp, double* T,
+                  long long ldt, const int* abort_flag, cudaStream_t s) {
+  const int nblk = (hi - lo) / NB;
+  if (nblk < 2) return GG_OK;
+  const int mid = lo + (nblk / 2) * NB;
+  int rc = trtri_offdiag(lo, mid, L, Linv, ldp, T, ldt, abort_flag, s);
+  if (rc != GG_OK) return rc;
+  rc = trtri_offdiag(mid, hi, L, Linv, ldp, T, ldt, abort_flag, s);
+  if (rc != GG_OK) return rc;
+  // T = L[mid:hi, lo:mid] * Linv[lo:mid, lo:mid]      (op(B) lower triangular)
+  GemmArgs g1{};
+  g1.M = hi - mid; g1.N = mid - lo; g1.K = mid - lo;
+  g1.A = L + mid + (long long)lo * ldp; g1.lda = ldp;
+  g1.B = Linv + lo + (long long)lo * ldp; g1.ldb = ldp;
+  g1.C = T; g1.ldc = ldt;
+  g1.alpha = 1.0; g1.beta = 0.0; g1.flags = GEMM_B_LOWER; g1.abort_flag = abort_flag;
+  rc = launch_dgemm(g1, false, s);
+  if (rc != GG_OK) return rc;
+  // Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] * T   (A lower triangular)
+  GemmArgs g2{};
+  g2.M = hi - mid; g2.N = mid - lo; g2.K = hi - mid;
+  g2.A = Linv + mid + (long long)mid * ldp; g2.lda = ldp;
+  g2.B = T; g2.ldb = ldt;
+  g2.C = Linv + mid + (long long)lo * ldp; g2.ldc = ldp;
+  g2.alpha = -1.0; g2.beta = 0.0; g2.flags = GEMM_A_LOWER; g2.abort_flag = abort_flag;
+  return launch_dgemm(g2, false, s);
+}
+
+void trtri_T_dims(int np, long long* rows, long long* cols) {
+  const int nblk = np / NB;
+  if (nblk < 2) { *rows = 0; *cols = 0; return; }
+  *cols = (long long)(nblk / 2) * NB;
+  *rows = (long long)(nblk - nblk / 2) * NB;
+}
+
+}  // namespace
+
+size_t trtri_ws_bytes(int n) {
+  const int np = pad_rows(n);
+  long long r, c;
+  trtri_T_dims(np, &r, &c);
+  return HDR_BYTES + (size_t)(r * c) * sizeof(double);
+}
+
+size_t potrf_ws_bytes(int n) {
+  const int np = pad_rows(n);
+  const size_t panel = (size_t)np * NB * sizeof(double);
+  const size_t tri = trtri_ws_bytes(n) - HDR_BYTES;
+  return HDR_BYTES + (panel > tri ? panel : tri);
+}
+
+int potrf_run(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
+              int* info_host, cudaStream_t s) {
+  if (n < 1 || M == nullptr || L == nullptr || Linv == nullptr || work == nullptr ||
+      info_host == nullptr) {
+    set_error("potrf: null pointer or n < 1");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  if (ldm < n || ldp < np) {
+    set_error("potrf: leading dimension too small (ldm >= n, ldp >= gg_pad(n))");
+    return GG_EDIM;
+  }
+  info_host[0] = -1;
+  info_host[1] = 0;
+  PotrfHeader* hdr = static_cast<PotrfHeader*>(work);
+  double* P = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
+  GG_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(int) * 2, s));
+  GG_CUDA_TRY(cudaMemsetAsync(&hdr->nonfinite, 0xff, sizeof(unsigned long long), s));
+  nonfinite_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(n, M, ldm, &hdr->nonfinite);
+  GG_LAUNCH_CHECK("nonfinite_kernel");
+  init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, ldm, L, Linv, ldp);
+  GG_LAUNCH_CHECK("init_factor_kernel");
+  GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)LEAF_SMEM));
+  for (int k = 0; k < np; k += NB) {
+    leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
+    GG_LAUNCH_CHECK("potrf leaf_kernel");
+    const int rem = np - k - NB;
+    if (rem <= 0) break;
+    GemmArgs pan{};
+    pan.M = rem; pan.N = NB; pan.K = NB;
+    pan.A = L + (k + NB) + (long long)k * ldp; pan.lda = ldp;
+    pan.B = Linv + k + (long long)k * ldp; pan.ldb = ldp;
+    pan.C = P; pan.ldc = np;
+    pan.alpha = 1.0; pan.beta = 0.0; pan.flags = 0; pan.abort_flag = &hdr->info;
+    int rc = launch_dgemm(pan, true, s);
+    if (rc != GG_OK) return rc;
+    GemmArgs upd{};
+    upd.M = rem; upd.N = rem; upd.K = NB;
+    upd.A = P; upd.lda = np;
+    upd.B = P; upd.ldb = np;
+    upd.C = L + (k + NB) + (long long)(k + NB) * ldp; upd.ldc = ldp;
+    upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
+    rc = launch_dgemm(upd, true, s);
+    if (rc != GG_OK) return rc;
+    GG_CUDA_TRY(cudaMemcpy2DAsync(L + (k + NB) + (long long)k * ldp, (size_t)ldp * sizeof(double), P,
+                                  (size_t)np * sizeof(double), (size_t)rem * sizeof(double), NB,
+                                  cudaMemcpyDeviceToDevice, s));
+  }
+  long long tr, tc;
+  trtri_T_dims(np, &tr, &tc);
+  int rc = trtri_offdiag(0, np, L, Linv, ldp, P, tr > 0 ? tr : 1, &hdr->info, s);
+  if (rc != GG_OK) return rc;
+  PotrfHeader h{};
+  GG_CUDA_TRY(cudaMemcpyAsync(&h, hdr, sizeof(PotrfHeader), cudaMemcpyDeviceToHost, s));
+  GG_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h.nonfinite != ULLONG_MAX) {
+    info_host[0] = (int)(h.nonfinite / (unsigned long long)n);
+    info_host[1] = 1;
+    set_error("non-finite entry in covariance");
+    return GG_ENOTPD;
+  }
+  if (h.info != 0) {
+    info_host[0] = h.info - 1;
+    set_error("matrix not positive definite");
+    return GG_ENOTPD;
+  }
+  return GG_OK;
+}
+
+int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work, cudaStream_t s) {
+  if (n < 1 || L == nullptr || Linv == nullptr || work == nullptr) {
+    set_error("trtri: null pointer or n < 1");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  if (ldl < np || ldp < np) {
+    set_error("trtri: leading dimension too small (>= gg_pad(n))");
+    return GG_EDIM;
+  }
+  if (ldl != ldp) {
+    set_error("trtri: ldl must equal ldp");
+    return GG_EDIM;
+  }
+  double* T = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
+  zero_square_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(np, Linv, ldp);
+  GG_LAUNCH_CHECK("zero_square_kernel");
+  GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)LEAF_SMEM));
+  // leaf_kernel<false> only reads L; the const_cast never results in a write.
+  leaf_kernel<false><<<np / NB, LEAF_THREADS, LEAF_SMEM, s>>>(const_cast<double*>(L), ldl, Linv,
+                                                               ldp, 0, nullptr);
+  GG_LAUNCH_CHECK("trtri leaf_kernel");
+  long long tr, tc;
+  trtri_T_dims(np, &tr, &tc);
+  return trtri_offdiag(0, np, L, Linv, ldp, T, tr > 0 ? tr : 1, nullptr, s);
+}
+
+}  // namespace gg

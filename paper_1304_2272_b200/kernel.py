@@ -1,0 +1,456 @@
+"""Drop-in for ``gwasgls.kernel`` (reference pkg/src/gwasgls/kernel.py) on the B200.
+
+Same names, signatures, return types, in-place behaviour and exceptions as the reference; the
+arithmetic runs in libgwasgls_b200.so (sm_100a FP64 DMMA kernels) through the C-ABI.  There is
+no CPU fallback: without a CUDA device or the native library every entry point raises
+``DeviceError``.
+
+    b_i = (X_i^T M^-1 X_i)^-1 X_i^T M^-1 y
+
+``gls_prepare`` factors M once (blocked Cholesky + triangular inverse, kept resident on the
+device), whitens X_L and y, and forms S_TL / b_T; ``gls_solve_block`` streams one block of SNP
+columns through the TRSM (Linv * X on DMMA tiles) and the fused epilogue (reductions + batched
+p x p Cholesky solve).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, pad, ptr, stream_handle
+from ._device import (
+    BlockWorkspace,
+    DeviceContext,
+    alloc_cols,
+    download_cols,
+    upload_cols,
+    upload_square_identity_padded,
+)
+from .errors import DimensionMismatch, NotPositiveDefinite, RankDeficientCovariates
+
+EPS = 2.0 ** -52   # kernel.py:28
+
+
+@dataclass
+class SnpBlock:
+    """A contiguous run of marker columns (allele dosages), n x count (kernel.py:31-48).
+
+    ``data`` is FP64 as in the reference; int8 dosages are accepted too and widened on the
+    device (the BASELINE config-2 genotype stream)."""
+
+    first_index: int
+    data: np.ndarray
+
+    def __post_init__(self):
+        if self.data.ndim != 2 or self.data.shape[1] < 1:
+            raise DimensionMismatch("SnpBlock needs an n x count matrix with count >= 1")
+
+    @property
+    def n(self):
+        return self.data.shape[0]
+
+    @property
+    def count(self):
+        return self.data.shape[1]
+
+
+@dataclass
+class SnpResult:
+    """Per-marker output (kernel.py:51-59)."""
+
+    snp_index: int
+    beta: np.ndarray
+    s_inv: np.ndarray | None = None
+    status: str = "ok"
+
+
+class _LazyResults:
+    """Read-only sequence of SnpResult views over the block's result arrays.
+
+    The reference builds one Python object per SNP (kernel.py:295-311, ~1.4 us/SNP); here the
+    objects are materialised on access, so the streaming engines never pay for them."""
+
+    def __init__(self, arrays):
+        self._a = arrays
+
+    def __len__(self):
+        return self._a.count
+
+    def _one(self, k):
+        a = self._a
+        gidx = a.first_index + k if a.global_indices is None else int(a.global_indices[k])
+        if a.status[k] < 0:
+            return SnpResult(snp_index=gidx, beta=a.beta[k],
+                             s_inv=a.sinv[k] if a.sinv is not None else None, status="ok")
+        return SnpResult(snp_index=gidx, beta=np.full(a.beta.shape[1], np.nan), s_inv=None,
+                         status="degenerate")
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self._one(i) for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        return self._one(k)
+
+    def __iter__(self):
+        for k in range(len(self)):
+            yield self._one(k)
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
+@dataclass
+class ResultArrays:
+    """Array form of a block's results: beta (cnt x p, NaN rows for degenerate markers),
+    status (cnt; -1 ok, else first failing pivot), optional packed S^-1."""
+
+    first_index: int
+    beta: np.ndarray
+    status: np.ndarray
+    sinv: np.ndarray | None = None
+    global_indices: np.ndarray | None = None
+
+    @property
+    def count(self):
+        return self.beta.shape[0]
+
+    @property
+    def ok(self):
+        return self.status < 0
+
+
+@dataclass
+class ResultBlock:
+    """(kernel.py:62-65).  ``results`` is list-like; ``arrays`` (when present) is the array
+    form used by the vectorised BlockWriter."""
+
+    first_index: int
+    results: object = field(default_factory=list)
+    arrays: ResultArrays | None = None
+
+    @classmethod
+    def from_arrays(cls, arrays):
+        return cls(first_index=arrays.first_index, results=_LazyResults(arrays), arrays=arrays)
+
+
+class PreparedContext:
+    """Marker-independent quantities (kernel.py:68-89).
+
+    Host fields L, XLbar, ybar, S_TL, b_T keep the reference's meaning (numpy arrays); the
+    factor lives on the device (``_dev``) and ``L`` is downloaded only when read."""
+
+    def __init__(self, L=None, XLbar=None, ybar=None, S_TL=None, b_T=None, _dev=None):
+        self._L = L
+        self.XLbar = XLbar
+        self.ybar = ybar
+        self.S_TL = S_TL
+        self.b_T = b_T
+        self._dev = _dev
+
+    @property
+    def L(self):
+        if self._L is None and self._dev is not None and self._dev.L is not None:
+            self._L = np.asfortranarray(download_cols(self._dev.L, self._dev.n, self._dev.n))
+        return self._L
+
+    @L.setter
+    def L(self, value):
+        self._L = value
+
+    @property
+    def n(self):
+        if self._dev is not None:
+            return self._dev.n
+        return self.XLbar.shape[0]
+
+    @property
+    def p(self):
+        return self.XLbar.shape[1] + 1
+
+    def device(self):
+        """Device half of the context, built from the host fields when missing."""
+        if self._dev is None:
+            self._dev = DeviceContext.from_host(self.XLbar, self.ybar, self.S_TL, self.b_T)
+        return self._dev
+
+    def __repr__(self):
+        return f"PreparedContext(n={self.n}, p={self.p}, device={self._dev is not None})"
+
+
+# ---------------------------------------------------------------------------------------------
+# factorisation and triangular solves
+# ---------------------------------------------------------------------------------------------
+
+def _potrf_device(M):
+    """Device Cholesky + inverse of the n x n host matrix M; returns (n, L_dev, Linv_dev)."""
+    torch = __import__("torch")
+    n = M.shape[0]
+    np_ = pad(n)
+    Md = upload_cols(M)                          # (n, pad(n)) col-major, ld = np_
+    L = alloc_cols(np_, np_, zero=False)
+    Linv = alloc_cols(np_, np_, zero=False)
+    ws = torch.empty(int(_capi.lib().gg_potrf_workspace_bytes(n)), dtype=torch.uint8,
+                     device=Md.device)
+    info = (_capi.C.c_int * 2)()
+    rc = _capi.lib().gg_potrf_f64(n, ptr(Md), Md.shape[1], ptr(L), ptr(Linv), np_, ptr(ws),
+                                  info, stream_handle())
+    if rc == _capi.GG_ENOTPD:
+        if info[1]:
+            raise NotPositiveDefinite(int(info[0]), "non-finite entry in covariance")
+        raise NotPositiveDefinite(int(info[0]))
+    check(rc, "gg_potrf_f64")
+    return n, L, Linv
+
+
+def cholesky_spd(M):
+    """Lower Cholesky factor of an SPD matrix (kernel.py:92-109).
+
+    The input is not modified; raises NotPositiveDefinite carrying the 0-based pivot (or, for
+    non-finite input, the row of the first non-finite entry in row-major order)."""
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise DimensionMismatch("covariance must be square")
+    n, L, _ = _potrf_device(M)
+    return np.asfortranarray(download_cols(L, n, n))
+
+
+def _trtri_device(L):
+    """Device inverse of a host lower-triangular L; returns (n, Linv_dev)."""
+    torch = __import__("torch")
+    n = L.shape[0]
+    np_ = pad(n)
+    Ld = upload_square_identity_padded(np.tril(L), n, np_)
+    Linv = alloc_cols(np_, np_, zero=False)
+    ws = torch.empty(int(_capi.lib().gg_trtri_workspace_bytes(n)), dtype=torch.uint8,
+                     device=Ld.device)
+    check(_capi.lib().gg_trtri_lower_f64(n, ptr(Ld), np_, ptr(Linv), np_, ptr(ws),
+                                         stream_handle()), "gg_trtri_lower_f64")
+    return n, Linv
+
+
+def _trsm_device(dLinv, n, B_dev, nrhs):
+    np_ = pad(n)
+    X = alloc_cols(nrhs, np_, zero=False)
+    check(_capi.lib().gg_trsm_lower_f64(n, nrhs, ptr(dLinv), np_, ptr(B_dev), B_dev.shape[1],
+                                        ptr(X), np_, stream_handle()), "gg_trsm_lower_f64")
+    return X
+
+
+def trsolve_lower(L, B):
+    """Solve L X = B for X with L lower triangular, column by column (kernel.py:112-121)."""
+    L = np.asarray(L, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    squeeze = B.ndim == 1
+    if squeeze:
+        B = B[:, None]
+    if L.ndim != 2 or L.shape[0] != L.shape[1] or L.shape[0] != B.shape[0]:
+        raise DimensionMismatch(f"trsolve: L is {L.shape}, B is {B.shape}")
+    n, nrhs = B.shape
+    if nrhs == 0:
+        return np.empty((n, 0)) if not squeeze else np.empty(n)
+    _, Linv = _trtri_device(L)
+    Bd = upload_cols(B, ld=pad(n))
+    X = np.asfortranarray(download_cols(_trsm_device(Linv, n, Bd, nrhs), n, nrhs))
+    return X[:, 0] if squeeze else X
+
+
+# ---------------------------------------------------------------------------------------------
+# reductions and small systems
+# ---------------------------------------------------------------------------------------------
+
+def _dots_device(Xd, n, cnt, XLd, q, yd):
+    """dots (cnt x (q+2)) of the device columns Xd against XLd (q columns) and yd."""
+    torch = __import__("torch")
+    out = torch.empty((max(cnt, 1), q + 2), dtype=torch.float64, device=Xd.device)
+    check(_capi.lib().gg_gls_dots_f64(n, cnt, q, ptr(Xd), Xd.shape[1],
+                                      ptr(XLd) if q > 0 else None,
+                                      XLd.shape[1] if q > 0 else pad(n), ptr(yd), ptr(out),
+                                      stream_handle()), "gg_gls_dots_f64")
+    return out[:cnt]
+
+
+def gram(A):
+    """A^T A with exact stored symmetry (kernel.py:124-131), on the device with the same
+    summation order as the per-SNP reductions."""
+    A = np.asarray(A, dtype=np.float64)
+    if A.ndim != 2:
+        raise DimensionMismatch("gram expects a matrix")
+    n, k = A.shape
+    if k == 0:
+        return np.zeros((0, 0))
+    Ad = upload_cols(A)
+    zeros = alloc_cols(1, Ad.shape[1])
+    C = _dots_device(Ad, n, k, Ad, k, zeros[0]).cpu().numpy()[:, :k]
+    return np.tril(C) + np.tril(C, -1).T
+
+
+def _small_solve_device(S, rhs, want_inverse):
+    torch = __import__("torch")
+    B, p, _ = S.shape
+    dev = _capi.device()
+    Sd = torch.from_numpy(np.ascontiguousarray(S)).to(dev)
+    rd = torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
+    x = torch.empty((B, p), dtype=torch.float64, device=dev)
+    st = torch.empty((B,), dtype=torch.int32, device=dev)
+    si = (torch.empty((B, p * (p + 1) // 2), dtype=torch.float64, device=dev)
+          if want_inverse else None)
+    check(_capi.lib().gg_small_spd_solve_f64(B, p, ptr(Sd), ptr(rd), ptr(x), ptr(st), ptr(si),
+                                             stream_handle()), "gg_small_spd_solve_f64")
+    return x.cpu().numpy(), st.cpu().numpy(), (si.cpu().numpy() if si is not None else None)
+
+
+def cholesky_solve_batch(S, rhs, want_inverse=False):
+    """Solve S[k] x[k] = rhs[k] for a batch of small SPD systems (kernel.py:138-208).
+
+    Pivot rule d > p * eps * max|S[k]| (kernel.py:134-135); failed systems come back NaN with
+    ok[k] = False.  Returns (x, ok) or (x, ok, s_inv_packed) in np.tril_indices order."""
+    S = np.asarray(S, dtype=np.float64)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if S.ndim != 3 or S.shape[1] != S.shape[2] or rhs.shape != S.shape[:2]:
+        raise DimensionMismatch("cholesky_solve_batch: S is (B,p,p), rhs is (B,p)")
+    B, p, _ = S.shape
+    if B == 0:
+        x = np.empty((0, p))
+        return (x, np.ones(0, dtype=bool)) if not want_inverse else \
+            (x, np.ones(0, dtype=bool), np.empty((0, p * (p + 1) // 2)))
+    x, st, packed = _small_solve_device(S, rhs, want_inverse)
+    ok = st < 0
+    if not want_inverse:
+        return x, ok
+    return x, ok, packed
+
+
+def solve_small_spd(S, rhs):
+    """Solve one small SPD system S x = rhs via Cholesky (kernel.py:211-230); raises
+    NotPositiveDefinite with the first failing pivot."""
+    S = np.asarray(S, dtype=np.float64)
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if S.ndim != 2 or S.shape[0] != S.shape[1] or S.shape[0] != rhs.shape[0]:
+        raise DimensionMismatch("solve_small_spd: shapes disagree")
+    x, st, _ = _small_solve_device(S[None], rhs[None], False)
+    if st[0] >= 0:
+        raise NotPositiveDefinite(int(st[0]))
+    return x[0]
+
+
+# ---------------------------------------------------------------------------------------------
+# the GLS sweep
+# ---------------------------------------------------------------------------------------------
+
+def gls_prepare(M, XL, y):
+    """Hoist all marker-independent work (kernel.py:233-257): factor M (device Cholesky +
+    inverse, kept resident), whiten XL and y with the same TRSM kernel as the SNP blocks, and
+    form S_TL and b_T with the same reduction kernel as the per-SNP sums."""
+    torch = __import__("torch")
+    M = np.asarray(M, dtype=np.float64)
+    XL = np.asarray(XL, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64).ravel()
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise DimensionMismatch("covariance must be square")
+    n = M.shape[0]
+    if XL.ndim != 2 or XL.shape[0] != n or y.shape[0] != n:
+        raise DimensionMismatch(f"gls_prepare: n={n} but XL {XL.shape}, y {y.shape}")
+    q = XL.shape[1]
+    if q + 1 > _capi.GG_PMAX:
+        raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
+    _, L, Linv = _potrf_device(np.ascontiguousarray(M))
+    np_ = pad(n)
+    RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
+    XLy = _trsm_device(Linv, n, RHS, q + 1)
+    dots = _dots_device(XLy, n, q, XLy, q, XLy[q]) if q > 0 else None
+    if q > 0:
+        C = dots[:, :q]
+        S_TL_d = (torch.tril(C) + torch.tril(C, -1).T).contiguous()
+        b_T_d = dots[:, q + 1].contiguous()
+        x = torch.empty((1, q), dtype=torch.float64, device=L.device)
+        st = torch.empty((1,), dtype=torch.int32, device=L.device)
+        zero = torch.zeros((1, q), dtype=torch.float64, device=L.device)
+        check(_capi.lib().gg_small_spd_solve_f64(1, q, ptr(S_TL_d), ptr(zero), ptr(x), ptr(st),
+                                                 None, stream_handle()),
+              "gg_small_spd_solve_f64")
+        piv = int(st.cpu()[0])
+        if piv >= 0:
+            raise RankDeficientCovariates(
+                f"whitened covariates are rank deficient (pivot {piv})")
+        S_TL = S_TL_d.cpu().numpy().reshape(q, q)
+        b_T = b_T_d.cpu().numpy()
+    else:
+        S_TL_d = torch.zeros((0,), dtype=torch.float64, device=L.device)
+        b_T_d = torch.zeros((0,), dtype=torch.float64, device=L.device)
+        S_TL, b_T = np.zeros((0, 0)), np.zeros(0)
+    host = download_cols(XLy, n, q + 1)
+    XLbar = np.asfortranarray(host[:, :q])
+    ybar = np.ascontiguousarray(host[:, q])
+    dctx = DeviceContext(n=n, np_=np_, q=q, L=L, Linv=Linv, XLy=XLy, S_TL=S_TL_d.reshape(-1),
+                         b_T=b_T_d)
+    return PreparedContext(L=None, XLbar=XLbar, ybar=ybar, S_TL=S_TL, b_T=b_T, _dev=dctx)
+
+
+def _collect(ws, cnt, first_index, global_indices, emit_s_inv):
+    beta = ws.beta[:cnt].cpu().numpy()
+    status = ws.status[:cnt].cpu().numpy()
+    sinv = ws.sinv[:cnt].cpu().numpy() if emit_s_inv else None
+    gi = None if global_indices is None else np.asarray(global_indices)
+    return ResultBlock.from_arrays(ResultArrays(first_index=first_index, beta=beta,
+                                                status=status, sinv=sinv, global_indices=gi))
+
+
+def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv=False):
+    """Per-marker assembly and solve for already-whitened columns Xbar (n x count)
+    (kernel.py:273-312); the fused device epilogue."""
+    d = ctx.device()
+    Xbar = np.asarray(Xbar, dtype=np.float64)
+    if Xbar.ndim != 2 or Xbar.shape[0] != d.n:
+        raise DimensionMismatch(f"Xbar has shape {Xbar.shape}, context has n={d.n}")
+    cnt = Xbar.shape[1]
+    ws = BlockWorkspace(d, max(cnt, 1), emit_s_inv=emit_s_inv)
+    if cnt:
+        Xd = upload_cols(Xbar, ld=d.np_)
+        check(_capi.lib().gg_gls_epilogue_f64(
+            d.n, cnt, d.q, ptr(Xd), d.np_, ptr(d.XLy), d.np_, ptr(d.ybar), ptr(d.S_TL),
+            ptr(d.b_T), ptr(ws.beta), ptr(ws.status), ptr(ws.sinv), stream_handle()),
+            "gg_gls_epilogue_f64")
+    return _collect(ws, cnt, first_index, global_indices, emit_s_inv).results
+
+
+def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
+    """Solve every marker in the block against the prepared context (kernel.py:315-342).
+
+    One TRSM launch (Linv * X on DMMA tiles) plus one fused epilogue launch; ``threads`` is
+    accepted for signature compatibility (results never depend on it)."""
+    d = ctx._dev
+    if d is None or d.Linv is None:
+        raise DimensionMismatch("context was not prepared on the device (use gls_prepare)")
+    if blk.n != d.n:
+        raise DimensionMismatch(f"block has n={blk.n}, context has n={d.n}")
+    cnt = blk.count
+    int8 = blk.data.dtype == np.int8
+    ws = BlockWorkspace(d, cnt, emit_s_inv=emit_s_inv, int8_input=int8)
+    if int8:
+        G = upload_cols(blk.data, ld=d.n)
+        ws.run(cnt, G8=G, ldg=d.n)
+    else:
+        X = upload_cols(np.asarray(blk.data, dtype=np.float64), ld=d.np_)
+        ws.run(cnt, X64=X, ldx=d.np_)
+    return _collect(ws, cnt, blk.first_index, None, emit_s_inv)
+
+
+def gls_oracle(M, Xi, y):
+    """Literal evaluation of the GLS formula through a general linear solve against M
+    (kernel.py:345-355) - a test route, evaluated on the device with dense LU."""
+    torch = __import__("torch")
+    dev = _capi.device()
+    M = torch.from_numpy(np.asarray(M, dtype=np.float64)).to(dev)
+    Xi = torch.from_numpy(np.asarray(Xi, dtype=np.float64)).to(dev)
+    y = torch.from_numpy(np.asarray(y, dtype=np.float64).ravel()).to(dev)
+    MinvX = torch.linalg.solve(M, Xi)
+    Minvy = torch.linalg.solve(M, y)
+    A = Xi.T @ MinvX
+    b = Xi.T @ Minvy
+    return torch.linalg.solve(A, b).cpu().numpy()
