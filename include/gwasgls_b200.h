@@ -135,6 +135,13 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp,
                      long long ldg, double* x64_work, double* xbar_work, double* beta,
                      int* status, double* sinv, void* stream);
 
+/* ---- Stream plumbing ----------------------------------------------------------------
+ * Pitched asynchronous copy (host<->device or device<->device) on `stream`; used by the
+ * double-buffered genotype stream (pinned n x cnt host block -> np-padded device block).
+ * kind: 1 = host to device, 2 = device to host, 3 = device to device.                */
+int gg_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                      size_t height, int kind, void* stream);
+
 /* ---- Synthetic BASELINE generator (test / bench data, not on the timed path) ------
  * Counter-based splitmix64 streams (the reference's datagen.py:35-52 construction),
  * bit-identical to paper_1304_2272_b200.datagen on the host.

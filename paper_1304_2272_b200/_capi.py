@@ -41,6 +41,7 @@ SIGNATURES = {
                                  _vp]),
     "gg_gls_block_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _ll, _vp,
                               _vp, _vp, _vp, _vp, _vp]),
+    "gg_memcpy2d_async": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _i, _vp]),
     "gg_gen_genotypes_i8": (_i, [_ull, _i, _i, _i, _ll, _ll, _i, _d, _d, _vp, _ll, _vp, _i,
                                  _vp]),
 }

@@ -163,6 +163,22 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp, const d
                           sinv, s);
 }
 
+int gg_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                      size_t height, int kind, void* stream) {
+  cudaMemcpyKind k;
+  switch (kind) {
+    case 1: k = cudaMemcpyHostToDevice; break;
+    case 2: k = cudaMemcpyDeviceToHost; break;
+    case 3: k = cudaMemcpyDeviceToDevice; break;
+    default:
+      gg::set_error("memcpy2d: kind must be 1, 2 or 3");
+      return GG_EARG;
+  }
+  if (height == 0 || width == 0) return GG_OK;
+  GG_CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, k, as_stream(stream)));
+  return GG_OK;
+}
+
 int gg_gen_genotypes_i8(unsigned long long seed, int stream_maf, int stream_geno, int n,
                         long long m, long long first, int cnt, double maf_lo, double maf_hi,
                         int8_t* G, long long ldg, double* Z, int ldz, void* stream) {

@@ -1,0 +1,407 @@
+"""Streaming drivers on the B200: the paper's double-buffered out-of-core loop (PAPER.md:259-295,
+reference pipeline.py:1-238) recast for a GPU.
+
+    load_start(first)                          host thread: file -> pinned region
+    for each block:
+        load_wait(current); load_start(next)   (region reuse gated by its H2D event)
+        H2D current on the copy stream         (pitched copy into the np-padded device block)
+        whiten + solve on the compute stream   (DMMA TRSM + fused epilogue, one launch each)
+        D2H results into the region's pinned result buffer
+        collect previous block; store_start(previous records)
+    store_wait(last)
+
+Two regions alternate; a region under in-flight transfer is never touched (rendezvous through
+CUDA events on the device side and tickets on the host side).  Per-column arithmetic does not
+depend on the block size, so incore, ooc at any m_blk, and the sharded engine agree bitwise.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _capi, fileio, kernel
+from ._capi import check, ptr
+from ._device import BlockWorkspace, alloc_cols
+from .errors import ConfigError
+
+DEFAULT_M_BLK = 5000          # pipeline.py:30
+GPU_M_BLK = 8192              # BASELINE configs 1-3
+MEM_BUDGET_ENV = "GWAS_GLS_MEM_BUDGET_BYTES"
+
+
+@dataclass
+class BlockPlan:
+    m: int
+    m_blk: int
+    blocks: list
+
+
+def block_plan(m, m_blk):
+    """Contiguous disjoint blocks of at most m_blk columns covering [0, m) (pipeline.py:41-46)."""
+    if m < 1 or m_blk < 1:
+        raise ConfigError("m and m_blk must be >= 1")
+    return BlockPlan(m=m, m_blk=m_blk,
+                     blocks=[(f, min(m_blk, m - f)) for f in range(0, m, m_blk)])
+
+
+@dataclass
+class RunSummary:
+    """Single-record run report; serialises to one key=value line (pipeline.py:49-99).
+    GPU runs add ``gpus``, ``t_device`` (device seconds of the stream) and ``snps_per_s``."""
+
+    mode: str = ""
+    n: int = 0
+    m: int = 0
+    p: int = 0
+    m_blk: int = 0
+    np_: int = 1
+    threads: int = 1
+    t_prepare: float = 0.0
+    t_compute: float = 0.0
+    t_io_wait: float = 0.0
+    t_redistribute: float = 0.0
+    t_total: float = 0.0
+    bytes_read: int = 0
+    bytes_written: int = 0
+    peak_resident_est: int = 0
+    buffer_regions: int = 0
+    combine_bytes: int = 0
+    localpart_bytes: int = 0
+    seed: int = -1
+    gpus: int = 1
+    t_device: float = 0.0
+    snps_per_s: float = 0.0
+    block_cpu_times: list = field(default_factory=list)
+
+    def to_record(self):
+        parts = []
+        for f in fields(self):
+            v = getattr(self, f.name)
+            if isinstance(v, list):
+                continue
+            parts.append(f"{f.name}={v:.6f}" if isinstance(v, float) else f"{f.name}={v}")
+        return " ".join(parts)
+
+    @classmethod
+    def from_record(cls, line):
+        typed = {f.name: f.type for f in fields(cls)}
+        kw = {}
+        for tok in line.split():
+            k, v = tok.split("=", 1)
+            t = typed.get(k)
+            if t is None:
+                continue
+            kw[k] = v if t in (str, "str") else float(v) if t in (float, "float") else int(v)
+        return cls(**kw)
+
+
+@dataclass
+class SolvePaths:
+    cov: str
+    covariates: str
+    pheno: str
+    geno: str
+    out: str
+
+
+@dataclass
+class SolveConfig:
+    m_blk: int = DEFAULT_M_BLK
+    threads: int = 1
+    emit_s_inv: bool = False
+    mem_budget_bytes: int | None = None
+
+    def budget(self):
+        if self.mem_budget_bytes is not None:
+            return self.mem_budget_bytes
+        env = os.environ.get(MEM_BUDGET_ENV)
+        return int(env) if env else None
+
+
+def _load_prepare(paths):
+    t0 = time.perf_counter()
+    M = fileio.read_matrix(paths.cov, "GWAM")
+    XL = fileio.read_matrix(paths.covariates, "GWAC")
+    y = fileio.read_matrix(paths.pheno, "GWAY")
+    ctx = kernel.gls_prepare(M, XL, y)
+    return ctx, time.perf_counter() - t0, M.nbytes
+
+
+# ---------------------------------------------------------------------------------------------
+# the device stream
+# ---------------------------------------------------------------------------------------------
+
+class StreamEngine:
+    """Two-region host->device genotype stream with asynchronous result return.
+
+    ``submit(slot, host_block, first, cnt)`` enqueues H2D (copy stream) -> TRSM + epilogue
+    (compute stream) -> D2H of the results into the slot's pinned buffers; ``collect(slot)``
+    waits for that slot and returns its ResultArrays.  host_block is an n x >= cnt Fortran-
+    ordered (ideally pinned) array of float64 or int8."""
+
+    REGIONS = 2
+
+    def __init__(self, ctx, m_blk, int8=False, emit_s_inv=False):
+        import torch
+
+        self.torch = torch
+        self.d = ctx._dev
+        if self.d is None or self.d.Linv is None:
+            raise ConfigError("StreamEngine needs a device-prepared context")
+        self.m_blk = int(m_blk)
+        self.int8 = bool(int8)
+        self.emit_s_inv = bool(emit_s_inv)
+        d = self.d
+        self.ld_in = d.n if self.int8 else d.np_
+        dt = torch.int8 if self.int8 else torch.float64
+        self.ws = [BlockWorkspace(d, self.m_blk, emit_s_inv, self.int8) for _ in range(self.REGIONS)]
+        self.dev_in = [alloc_cols(self.m_blk, self.ld_in, dtype=dt) for _ in range(self.REGIONS)]
+        p = d.p
+        self.h_beta = [torch.empty((self.m_blk, p), dtype=torch.float64).pin_memory()
+                       for _ in range(self.REGIONS)]
+        self.h_status = [torch.empty((self.m_blk,), dtype=torch.int32).pin_memory()
+                         for _ in range(self.REGIONS)]
+        self.h_sinv = [torch.empty((self.m_blk, p * (p + 1) // 2), dtype=torch.float64)
+                       .pin_memory() if emit_s_inv else None for _ in range(self.REGIONS)]
+        self.copy_stream = torch.cuda.Stream()
+        self.compute_stream = torch.cuda.Stream()
+        self.h2d_done = [torch.cuda.Event() for _ in range(self.REGIONS)]
+        self.done = [torch.cuda.Event(enable_timing=True) for _ in range(self.REGIONS)]
+        self.start_ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.REGIONS)]
+        self.meta = [None] * self.REGIONS
+        self.busy = [False] * self.REGIONS
+        self.device_ms = 0.0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def wait_h2d(self, slot):
+        """Host rendezvous: the slot's host input region may be refilled after this."""
+        self.h2d_done[slot].synchronize()
+
+    def submit(self, slot, host_block, first, cnt, global_indices=None):
+        torch = self.torch
+        if self.busy[slot]:
+            raise ConfigError(f"stream slot {slot} still in flight")
+        d = self.d
+        item = 1 if self.int8 else 8
+        hb = host_block
+        if hb.shape[0] != d.n or hb.shape[1] < cnt or not hb.flags.f_contiguous:
+            raise ConfigError("host block must be n x >= cnt and Fortran-ordered")
+        if hb.dtype != (np.int8 if self.int8 else np.float64):
+            raise ConfigError(f"host block dtype {hb.dtype} does not match the stream")
+        dst = self.dev_in[slot]
+        with torch.cuda.stream(self.copy_stream):
+            # the device input region is free once the previous compute on this slot is done
+            self.copy_stream.wait_event(self.done[slot])
+            rc = _capi.lib().gg_memcpy2d_async(
+                ptr(dst), self.ld_in * item, _capi.C.c_void_p(hb.ctypes.data), d.n * item,
+                d.n * item, int(cnt), 1, _capi.C.c_void_p(self.copy_stream.cuda_stream))
+            check(rc, "gg_memcpy2d_async")
+            self.h2d_done[slot].record(self.copy_stream)
+        self.h2d_bytes += d.n * item * cnt
+        ws = self.ws[slot]
+        with torch.cuda.stream(self.compute_stream):
+            self.compute_stream.wait_event(self.h2d_done[slot])
+            self.start_ev[slot].record(self.compute_stream)
+            s = _capi.C.c_void_p(self.compute_stream.cuda_stream)
+            if self.int8:
+                ws.run(cnt, G8=dst, ldg=self.ld_in, stream=s)
+            else:
+                ws.run(cnt, X64=dst, ldx=self.ld_in, stream=s)
+            self.h_beta[slot][:cnt].copy_(ws.beta[:cnt], non_blocking=True)
+            self.h_status[slot][:cnt].copy_(ws.status[:cnt], non_blocking=True)
+            if self.emit_s_inv:
+                self.h_sinv[slot][:cnt].copy_(ws.sinv[:cnt], non_blocking=True)
+            self.done[slot].record(self.compute_stream)
+        self.d2h_bytes += cnt * (8 * d.p + 4 + (8 * d.p * (d.p + 1) // 2 if self.emit_s_inv else 0))
+        self.meta[slot] = (first, cnt, global_indices)
+        self.busy[slot] = True
+
+    def collect(self, slot):
+        self.done[slot].synchronize()
+        self.device_ms += self.start_ev[slot].elapsed_time(self.done[slot])
+        first, cnt, gi = self.meta[slot]
+        self.busy[slot] = False
+        return kernel.ResultArrays(
+            first_index=first,
+            beta=self.h_beta[slot][:cnt].numpy().copy(),
+            status=self.h_status[slot][:cnt].numpy().copy(),
+            sinv=self.h_sinv[slot][:cnt].numpy().copy() if self.emit_s_inv else None,
+            global_indices=gi)
+
+
+def pinned_empty(n, cols, dtype):
+    """Pinned, Fortran-ordered n x cols host buffer (numpy view of pinned torch storage)."""
+    import torch
+
+    tdt = torch.int8 if np.dtype(dtype) == np.int8 else torch.float64
+    t = torch.empty((cols, n), dtype=tdt).pin_memory()
+    return t.numpy().T, t       # keep the torch tensor alive alongside the view
+
+
+def stream_blocks(engine, blocks, fill, on_result):
+    """Generic double-buffered loop.
+
+    blocks   : [(first, count)] in order
+    fill     : fill(slot, first, count) -> host block (n x >= count, F-order) ready to copy;
+               may return a ticket-like callable for asynchronous loads (see run_ooc)
+    on_result: on_result(ResultArrays) for each block, in order
+    Returns (t_io_wait, block_cpu_times)."""
+    t_wait = 0.0
+    cpu_times = []
+    nb = len(blocks)
+    pending = None           # slot whose results are not yet collected
+    for bi, (first, cnt) in enumerate(blocks):
+        slot = bi % StreamEngine.REGIONS
+        cpu0 = time.process_time()
+        t0 = time.perf_counter()
+        host_block = fill(slot, first, cnt, bi, nb)
+        t_wait += time.perf_counter() - t0
+        engine.submit(slot, host_block, first, cnt)
+        if pending is not None:
+            on_result(engine.collect(pending))
+        pending = slot
+        cpu_times.append(time.process_time() - cpu0)
+    if pending is not None:
+        on_result(engine.collect(pending))
+    return t_wait, cpu_times
+
+
+def _run_stream(paths, cfg, mode, m_blk_override=None):
+    cfg = cfg or SolveConfig()
+    t_start = time.perf_counter()
+    geno_bytes, n, m = fileio.total_genotype_bytes(paths.geno)
+    kind = fileio.genotype_kind(paths.geno)
+    int8 = kind == "GWAI"
+    item = 1 if int8 else 8
+    ctx, t_prep, m_bytes = _load_prepare(paths)
+    p = ctx.p
+    flags = 1 if cfg.emit_s_inv else 0
+    rsz = fileio.record_size(p, flags)
+    m_blk = min(m_blk_override or cfg.m_blk, m)
+    plan = block_plan(m, m_blk)
+    reader = fileio.BlockReader(paths.geno)
+    writer = fileio.BlockWriter(paths.out, m, p, flags)
+    engine = StreamEngine(ctx, m_blk, int8=int8, emit_s_inv=cfg.emit_s_inv)
+    dtype = np.int8 if int8 else np.float64
+    regions = [pinned_empty(n, m_blk, dtype) for _ in range(StreamEngine.REGIONS)]
+    in_bufs = [r[0] for r in regions]
+    rec_bufs = [np.empty((m_blk, rsz // 8)) for _ in range(StreamEngine.REGIONS)]
+    state = {"ticket": None, "store": None, "rec": 0, "io": 0.0}
+
+    def fill(slot, first, cnt, bi, nb):
+        if state["ticket"] is None:          # first block: synchronous start
+            state["ticket"] = reader.start(first, cnt, in_bufs[slot])
+        blk = reader.wait(state["ticket"])
+        state["ticket"] = None
+        if bi + 1 < nb:
+            nslot = (slot + 1) % StreamEngine.REGIONS
+            engine.wait_h2d(nslot)           # its previous H2D must be finished
+            nfirst, ncnt = plan.blocks[bi + 1]
+            state["ticket"] = reader.start(nfirst, ncnt, in_bufs[nslot])
+        return blk.data if blk.data.flags.f_contiguous else in_bufs[slot]
+
+    def on_result(arr):
+        t0 = time.perf_counter()
+        if state["store"] is not None:
+            writer.wait(state["store"])
+        state["io"] += time.perf_counter() - t0
+        k = state["rec"] % StreamEngine.REGIONS
+        state["rec"] += 1
+        rec = writer.encode(kernel.ResultBlock.from_arrays(arr))
+        buf = rec_bufs[k][:rec.shape[0]]
+        buf[...] = rec
+        state["store"] = writer.start_records(arr.first_index, buf, key=id(rec_bufs[k]))
+
+    t0 = time.perf_counter()
+    t_wait, cpu_times = stream_blocks(engine, plan.blocks, fill, on_result)
+    t_loop = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    if state["store"] is not None:
+        writer.wait(state["store"])
+    state["io"] += time.perf_counter() - t1
+    reader.close()
+    writer.close()
+    t_total = time.perf_counter() - t_start
+    t_io = t_wait + state["io"]
+    return RunSummary(
+        mode=mode, n=n, m=m, p=p, m_blk=m_blk, np_=1, threads=cfg.threads,
+        t_prepare=t_prep, t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io, t_total=t_total,
+        bytes_read=reader.bytes_read + m_bytes, bytes_written=writer.bytes_written,
+        peak_resident_est=8 * n * n + 2 * (item * n * m_blk + m_blk * rsz) + 8 * n * p,
+        buffer_regions=StreamEngine.REGIONS, gpus=1, t_device=engine.device_ms / 1e3,
+        snps_per_s=m / t_loop if t_loop > 0 else 0.0, block_cpu_times=cpu_times)
+
+
+def run_incore(paths, cfg=None):
+    """Whole-genotype engine (pipeline.py:134-171).  The genotypes must fit the memory budget
+    (ConfigError otherwise); on the GPU they are solved in device-sized slices of the same
+    per-column arithmetic, so the result equals a single block bitwise."""
+    cfg = cfg or SolveConfig()
+    geno_bytes, n, m = fileio.total_genotype_bytes(paths.geno)
+    budget = cfg.budget()
+    need = geno_bytes + 8 * n * n
+    if budget is not None and need > budget:
+        raise ConfigError(f"in-core run needs {need} bytes (genotypes + covariance), "
+                          f"budget is {budget}")
+    s = _run_stream(paths, cfg, "incore", m_blk_override=min(m, GPU_M_BLK))
+    s.buffer_regions = 1
+    s.m_blk = m
+    return s
+
+
+def run_ooc(paths, cfg=None):
+    """Out-of-core engine (pipeline.py:174-238): two buffer regions, asynchronous file loads,
+    H2D on a copy stream, compute on a compute stream, asynchronous result stores."""
+    cfg = cfg or SolveConfig()
+    geno_bytes, n, m = fileio.total_genotype_bytes(paths.geno)
+    item = 1 if fileio.genotype_kind(paths.geno) == "GWAI" else 8
+    m_blk = min(cfg.m_blk, m)
+    p = fileio.read_dims(paths.covariates, "GWAC")[1] + 1
+    rsz = fileio.record_size(p, 1 if cfg.emit_s_inv else 0)
+    budget = cfg.budget()
+    region = item * n * m_blk + m_blk * rsz
+    if budget is not None and 2 * region > budget:
+        raise ConfigError(f"two buffer regions need {2 * region} bytes, budget is {budget}")
+    return _run_stream(paths, cfg, "ooc")
+
+
+def solve_array(ctx, X, m_blk=GPU_M_BLK, emit_s_inv=False, first_index=0, engine=None):
+    """Public array entry point of the stream: solve every column of the host genotype matrix
+    X (n x m, FP64 or int8, Fortran-ordered; pinned memory gives overlapped H2D) against a
+    device-prepared context.  Returns ResultArrays for all m markers."""
+    X = np.asarray(X)
+    if not X.flags.f_contiguous:
+        X = np.asfortranarray(X)
+    n, m = X.shape
+    int8 = X.dtype == np.int8
+    if engine is None:
+        engine = StreamEngine(ctx, min(m_blk, m), int8=int8, emit_s_inv=emit_s_inv)
+    m_blk = engine.m_blk
+    plan = block_plan(m, m_blk)
+    p = ctx.p
+    beta = np.empty((m, p))
+    status = np.empty(m, dtype=np.int32)
+    sinv = np.empty((m, p * (p + 1) // 2)) if emit_s_inv else None
+
+    def fill(slot, first, cnt, bi, nb):
+        return X[:, first:first + cnt]
+
+    def on_result(arr):
+        f = arr.first_index - first_index
+        beta[f:f + arr.count] = arr.beta
+        status[f:f + arr.count] = arr.status
+        if sinv is not None:
+            sinv[f:f + arr.count] = arr.sinv
+
+    blocks = [(first_index + f, c) for f, c in plan.blocks]
+
+    def fill_off(slot, first, cnt, bi, nb):
+        return fill(slot, first - first_index, cnt, bi, nb)
+
+    stream_blocks(engine, blocks, fill_off, on_result)
+    return kernel.ResultArrays(first_index=first_index, beta=beta, status=status, sinv=sinv)
