@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark of the GLS hot path on B200 (BASELINE.json configs[1], the metric's config).
+
+Workload: n = 10,000 individuals, p = 4, m = 200,000 SNPs per GPU, FP64, blocks of 8,192 SNPs
+(24 full + one 3,392 tail), seeded synthetic BASELINE data.  One STEP is one
+full sweep of the rank's 200,000 SNPs: per block one DMMA TRSM launch (Xbar = Linv * X) and one
+fused epilogue launch (reductions + batched 4x4 Cholesky solve).  The genotypes (FP64, 16.2 GB
+per GPU) are resident in HBM when the timed region starts; they are larger than L2, so no L2
+flush is needed.  gls_prepare (Cholesky + inverse) runs once, outside the step, timed apart.
+
+Multi-GPU (torchrun): SNP-sharded weak scaling — rank r owns markers [r*m, (r+1)*m) of an
+N*m-marker panel; L is factored redundantly on every rank; no collective in the timed region
+except the barriers that bracket it; time = max over ranks of the CUDA-event time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "GLS solves (SNPs/sec) at 1/2/4/8 B200; TRSM FP64 TFLOP/s vs FP64 peak"
+UNIT = "SNPs/s"
+# FP64 roofline denominator.  MEASURED_PEAKS.json carries no FP64 figure, so the peak is our own
+# measurement on this pool's B200s: DMMA m8n8k4 sustained over 200 launches at 1965 MHz
+# (tools/fp64_peak.cu, profiles/r01_fp64_peak.log).  cuBLAS DGEMM 8192^3 reached 35.48 there.
+FP64_PEAK_TFLOPS = 37.09
+FP64_PEAK_SOURCE = ("measured: DMMA m8n8k4 sustained 37.09 TF/s @1965 MHz, tools/fp64_peak.cu "
+                    "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry")
+CPU_SAMPLE_SNPS = 4096
+REF_SAMPLE_SNPS = 2048
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--m", type=int, default=None, help="SNPs per GPU (default: the config's m)")
+    ap.add_argument("--m-blk", type=int, default=8192)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-dtype", choices=["f64", "i8"], default="f64")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "power_w_max": max(power) if power else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the TRSM kernel from the committed ncu --set full summary."""
+    path = os.path.join(REPO, "profiles", "ncu_trsm_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1304_2272_b200 import _capi, datagen, kernel, pipeline
+    from paper_1304_2272_b200._capi import check, ptr
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lib = _capi.lib()
+    spec = datagen.CONFIGS[args.config]
+    m = args.m or spec.m
+    spec = dataclasses.replace(spec, m=m * world)     # the N*m-marker panel
+    n, p = spec.n, spec.p
+    q = p - 1
+    np_ = _capi.pad(n)
+    m_blk = args.m_blk
+
+    # ---- data (identical M on every rank; rank-local marker range) --------------------------
+    t0 = time.perf_counter()
+    M = datagen.kinship_covariance_device(spec).cpu().numpy()
+    XL, y = datagen.covariates_host(spec)
+    torch.cuda.synchronize()
+    t_gen_m = time.perf_counter() - t0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    ctx = kernel.gls_prepare(M, XL, y)
+    e1.record()
+    torch.cuda.synchronize()
+    t_prepare = time.perf_counter() - t0
+    prepare_ms_device = e0.elapsed_time(e1)
+    d = ctx._dev
+    X = torch.empty((m, np_), dtype=torch.float64, device=dev)
+    X[:, n:].zero_()
+    G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
+    first_marker = rank * m
+    for j0 in range(0, m, m_blk):
+        cnt = min(m_blk, m - j0)
+        datagen.genotypes_device(spec, first_marker + j0, cnt, out=G)
+        check(lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(X[j0:]), np_,
+                                  _capi.stream_handle()), "widen")
+    del G
+    xbar = torch.empty((m_blk, np_), dtype=torch.float64, device=dev)
+    beta = torch.empty((m, p), dtype=torch.float64, device=dev)
+    status = torch.empty((m,), dtype=torch.int32, device=dev)
+    plan = pipeline.block_plan(m, m_blk).blocks
+    stream = torch.cuda.current_stream()
+    sh = _capi.C.c_void_p(stream.cuda_stream)
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in plan]
+
+    def step(record):
+        for i, (f, c) in enumerate(plan):
+            if record:
+                ev_pairs[i][0].record(stream)
+            rc = lib.gg_trsm_lower_f64(n, c, ptr(d.Linv), np_, ptr(X[f]), np_, ptr(xbar), np_, sh)
+            if record:
+                ev_pairs[i][1].record(stream)
+            rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(xbar), np_, ptr(d.XLy), np_, ptr(d.ybar),
+                                          ptr(d.S_TL), ptr(d.b_T), ptr(beta[f]), ptr(status[f]),
+                                          None, sh)
+            if rc:
+                raise RuntimeError(_capi.last_error())
+        return None
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trsm_ms = 0.0
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(True)
+        if k == 0:
+            pass
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    for a, b in ev_pairs:
+        trsm_ms += a.elapsed_time(b)     # last step's per-launch times
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    barrier()
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ok_all = bool((status >= 0).sum().item() == 0)
+    snps_per_step_total = m * world
+    value = snps_per_step_total * args.steps / (elapsed_ms / 1e3)
+    flops_per_step = float(n) * n * m
+    trsm_tflops = flops_per_step / (trsm_ms / 1e3) / 1e12
+    step_tflops = flops_per_step * args.steps / (elapsed_ms / 1e3) / 1e12
+    traffic_full, ncu = load_traffic()
+
+    # ---- e2e through the public stream API with host buffers --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline)
+
+    # ---- CPU baseline + sampled parity on rank 0 at N = 1 -----------------------------------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, parity = run_cpu_baseline(M, XL, y, X, n, beta, status, np)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}, m={m} SNPs "
+                            f"per GPU, FP64, blocks of {m_blk}; step = TRSM + fused epilogue "
+                            f"over all m SNPs",
+                "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": m_blk,
+                "blocks_per_step": len(plan), "parallelism": f"snp-shard x{world}",
+                "l2": "inputs larger than L2 (FP64 genotypes resident in HBM: "
+                      f"{m * np_ * 8 / 1e9:.1f} GB per GPU)",
+                "t_prepare_s": round(t_prepare, 4),
+                "prepare_device_ms": round(prepare_ms_device, 2),
+                "t_generate_M_s": round(t_gen_m, 2),
+                "step_fp64_tflops": round(step_tflops, 3),
+                "all_snps_ok": ok_all,
+            },
+            "roofline": {
+                "bound": "tensor", "kernel": "dgemm_dmma_kernel<false> (TRSM Xbar = Linv*X)",
+                "achieved": round(trsm_tflops, 3), "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": round(trsm_tflops / FP64_PEAK_TFLOPS, 4),
+                "traffic": traffic_full,
+                "algorithmic_unit": "n^2 FLOP per SNP (LAPACK dtrsm count) x SNPs per launch",
+                "peak_source": FP64_PEAK_SOURCE,
+                "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
+            },
+            "gpu_launches": 2 * len(plan) * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "parity": parity,
+        }
+        if ncu is not None:
+            line["roofline"]["traffic_source"] = ncu.get("source")
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
+    """Same metric through pipeline.solve_array with host genotypes: every step H2D-copies all
+    m markers from pinned host memory (double-buffered, copy stream) and reads the results back."""
+    np_ = X.shape[1]
+    try:
+        if args.e2e_dtype == "f64":
+            host_t = torch.empty((m, n), dtype=torch.float64).pin_memory()
+            host_t.copy_(X[:, :n])
+        else:
+            raise RuntimeError("int8 requested")
+    except RuntimeError:
+        host_t = torch.empty((m, n), dtype=torch.int8).pin_memory()
+        host_t.copy_(X[:, :n].to(torch.int8))
+    Xh = host_t.numpy().T                     # n x m, Fortran-ordered view of pinned memory
+    int8 = Xh.dtype == np.int8
+    engine = pipeline.StreamEngine(ctx, args.m_blk, int8=int8)
+    res = pipeline.solve_array(ctx, Xh, engine=engine)      # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    h0, d0 = engine.h2d_bytes, engine.d2h_bytes
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = pipeline.solve_array(ctx, Xh, engine=engine)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    ok = bool(np.all(res.ok))
+    del host_t
+    return {"value": round(m * world * args.steps / dt, 1), "unit": UNIT,
+            "h2d_bytes_per_step": int((engine.h2d_bytes - h0) // args.steps),
+            "d2h_bytes_per_step": int((engine.d2h_bytes - d0) // args.steps),
+            "api": "paper_1304_2272_b200.pipeline.solve_array (pinned host "
+                   f"{'int8' if int8 else 'FP64'} genotypes, double-buffered H2D)",
+            "all_snps_ok": ok}
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads", 1) for i in threadpool_info()
+                    if i.get("user_api") == "blas"), default=os.cpu_count())
+    except Exception:   # pragma: no cover
+        return os.cpu_count()
+
+
+def run_cpu_baseline(M, XL, y, X, n, beta, status, np):
+    """The CPU oracle (numpy/scipy restatement of the reference, oracle/gls_ref.py) on this
+    host's cores: gls_prepare once, then one block of CPU_SAMPLE_SNPS markers; doubles as the
+    sampled parity check of the GPU results."""
+    from oracle import gls_ref as O
+
+    S = CPU_SAMPLE_SNPS
+    Xs = X[:S, :n].cpu().numpy().T.copy(order="F")
+    t0 = time.perf_counter()
+    octx = O.gls_prepare(M, XL, y)
+    t_prep = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ob, ok = O.gls_solve_block(octx, Xs)
+    t = time.perf_counter() - t0
+    gb = beta[:S].cpu().numpy()
+    gs = status[:S].cpu().numpy()
+    gb = np.where((gs < 0)[:, None], gb, np.nan)
+    rel, mism = O.compare(gb, ob)
+    cpu = {"value": round(S / t, 2), "unit": UNIT, "cores": _blas_threads(), "kind": "port",
+           "sample": f"oracle gls_solve_block on the first {S} SNPs of the workload at n={n} "
+                     f"(prepare {t_prep:.2f} s excluded, like the GPU value)",
+           "t_prepare_s": round(t_prep, 3)}
+    parity = {"snps": S, "max_rel": rel, "status_mismatches": mism, "tol": 1e-9,
+              "within": bool(mism == 0 and rel <= 1e-9)}
+    return cpu, parity
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm: the reference's CPU implementation of the path (the oracle port) on host cores
+# ---------------------------------------------------------------------------------------------
+
+def run_reference(args):
+    import numpy as np
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import datagen
+
+    spec = datagen.CONFIGS[args.config]
+    n, p = spec.n, spec.p
+    S = REF_SAMPLE_SNPS
+    t0 = time.perf_counter()
+    M = datagen.kinship_covariance_host(spec)
+    XL, y = datagen.covariates_host(spec)
+    G = datagen.genotypes_host(spec.seed, n, spec.m, 0, S).astype(np.float64, order="F")
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    octx = O.gls_prepare(M, XL, y)
+    t_prep = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        O.gls_solve_block(octx, G)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.gls_solve_block(octx, G)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = S * args.steps / tot
+    cores = _blas_threads()
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}; each step "
+                               f"= one {S}-SNP block through the reference CPU path",
+                   "n": n, "p": p, "sample_snps_per_step": S, "t_prepare_s": round(t_prep, 3),
+                   "t_generate_s": round(t_gen, 2)},
+        "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{S}-SNP block of the config-{args.config} workload per step "
+                                   "(oracle/gls_ref.py: scipy dtrsm + numpy reductions + batched "
+                                   "p x p Cholesky, as kernel.py:315-342)"},
+        "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

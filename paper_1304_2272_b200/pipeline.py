@@ -271,26 +271,17 @@ def stream_blocks(engine, blocks, fill, on_result):
     return t_wait, cpu_times
 
 
-def _run_stream(paths, cfg, mode, m_blk_override=None):
-    cfg = cfg or SolveConfig()
-    t_start = time.perf_counter()
-    geno_bytes, n, m = fileio.total_genotype_bytes(paths.geno)
-    kind = fileio.genotype_kind(paths.geno)
-    int8 = kind == "GWAI"
-    item = 1 if int8 else 8
-    ctx, t_prep, m_bytes = _load_prepare(paths)
-    p = ctx.p
-    flags = 1 if cfg.emit_s_inv else 0
-    rsz = fileio.record_size(p, flags)
-    m_blk = min(m_blk_override or cfg.m_blk, m)
-    plan = block_plan(m, m_blk)
-    reader = fileio.BlockReader(paths.geno)
-    writer = fileio.BlockWriter(paths.out, m, p, flags)
-    engine = StreamEngine(ctx, m_blk, int8=int8, emit_s_inv=cfg.emit_s_inv)
+def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False):
+    """Double-buffered file -> GPU -> file loop over ``blocks`` (any subset of the plan, e.g.
+    one rank's shard).  Returns (engine, t_io_wait, block_cpu_times, t_loop)."""
+    n = reader.n
+    int8 = reader.kind == "GWAI"
+    engine = StreamEngine(ctx, m_blk, int8=int8, emit_s_inv=emit_s_inv)
     dtype = np.int8 if int8 else np.float64
     regions = [pinned_empty(n, m_blk, dtype) for _ in range(StreamEngine.REGIONS)]
     in_bufs = [r[0] for r in regions]
-    rec_bufs = [np.empty((m_blk, rsz // 8)) for _ in range(StreamEngine.REGIONS)]
+    width = writer._rsz // 8
+    rec_bufs = [np.empty((m_blk, width)) for _ in range(StreamEngine.REGIONS)]
     state = {"ticket": None, "store": None, "rec": 0, "io": 0.0}
 
     def fill(slot, first, cnt, bi, nb):
@@ -301,9 +292,9 @@ def _run_stream(paths, cfg, mode, m_blk_override=None):
         if bi + 1 < nb:
             nslot = (slot + 1) % StreamEngine.REGIONS
             engine.wait_h2d(nslot)           # its previous H2D must be finished
-            nfirst, ncnt = plan.blocks[bi + 1]
+            nfirst, ncnt = blocks[bi + 1]
             state["ticket"] = reader.start(nfirst, ncnt, in_bufs[nslot])
-        return blk.data if blk.data.flags.f_contiguous else in_bufs[slot]
+        return blk.data
 
     def on_result(arr):
         t0 = time.perf_counter()
@@ -318,19 +309,38 @@ def _run_stream(paths, cfg, mode, m_blk_override=None):
         state["store"] = writer.start_records(arr.first_index, buf, key=id(rec_bufs[k]))
 
     t0 = time.perf_counter()
-    t_wait, cpu_times = stream_blocks(engine, plan.blocks, fill, on_result)
-    t_loop = time.perf_counter() - t0
+    t_wait, cpu_times = stream_blocks(engine, blocks, fill, on_result)
     t1 = time.perf_counter()
     if state["store"] is not None:
         writer.wait(state["store"])
-    state["io"] += time.perf_counter() - t1
-    reader.close()
-    writer.close()
-    t_total = time.perf_counter() - t_start
-    t_io = t_wait + state["io"]
+    t_end = time.perf_counter()
+    state["io"] += t_end - t1
+    return engine, t_wait + state["io"], cpu_times, t_end - t0
+
+
+def _run_stream(paths, cfg, mode, m_blk_override=None):
+    cfg = cfg or SolveConfig()
+    t_start = time.perf_counter()
+    geno_bytes, n, m = fileio.total_genotype_bytes(paths.geno)
+    item = 1 if fileio.genotype_kind(paths.geno) == "GWAI" else 8
+    ctx, t_prep, m_bytes = _load_prepare(paths)
+    p = ctx.p
+    flags = 1 if cfg.emit_s_inv else 0
+    rsz = fileio.record_size(p, flags)
+    m_blk = min(m_blk_override or cfg.m_blk, m)
+    plan = block_plan(m, m_blk)
+    reader = fileio.BlockReader(paths.geno)
+    writer = fileio.BlockWriter(paths.out, m, p, flags)
+    try:
+        engine, t_io, cpu_times, t_loop = stream_file_blocks(ctx, reader, writer, plan.blocks,
+                                                             m_blk, cfg.emit_s_inv)
+    finally:
+        reader.close()
+        writer.close()
     return RunSummary(
         mode=mode, n=n, m=m, p=p, m_blk=m_blk, np_=1, threads=cfg.threads,
-        t_prepare=t_prep, t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io, t_total=t_total,
+        t_prepare=t_prep, t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io,
+        t_total=time.perf_counter() - t_start,
         bytes_read=reader.bytes_read + m_bytes, bytes_written=writer.bytes_written,
         peak_resident_est=8 * n * n + 2 * (item * n * m_blk + m_blk * rsz) + 8 * n * p,
         buffer_regions=StreamEngine.REGIONS, gpus=1, t_device=engine.device_ms / 1e3,
