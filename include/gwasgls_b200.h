@@ -53,7 +53,8 @@ int gg_pad(int n);                               /* round n up to GG_TILE       
  * Replaces kernel.cholesky_spd (kernel.py:92-109: LAPACK dpotrf lower, clean=1,
  * input untouched) and produces, in the same pass, Linv = L^-1 (the operand of the
  * streamed TRSM, see gg_trsm_lower_f64).
- *   M      : n x n, leading dimension ldm (>= n); only read.
+ *   M      : n x n, leading dimension ldm (>= n); only read.  m_row_major = 1 reads M in
+ *            row-major order (a C-contiguous numpy array uploaded as is), 0 column-major.
  *   L      : np x np output, ld = ldp (>= np, multiple of 2); lower factor, upper zero.
  *   Linv   : np x np output, ld = ldp; lower inverse, upper zero.
  *   work   : gg_potrf_workspace_bytes(n) bytes of device scratch.
@@ -63,8 +64,8 @@ int gg_pad(int n);                               /* round n up to GG_TILE       
  *   info_host[1] : 1 iff the failure was a non-finite entry.
  * Returns GG_ENOTPD on failure.  Synchronises `stream` (to read the pivot).      */
 size_t gg_potrf_workspace_bytes(int n);
-int gg_potrf_f64(int n, const double* M, int ldm, double* L, double* Linv, int ldp,
-                 void* work, int* info_host, void* stream);
+int gg_potrf_f64(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv,
+                 int ldp, void* work, int* info_host, void* stream);
 
 /* Triangular inverse of an arbitrary lower-triangular L (np x np, padded as above,
  * upper part ignored).  Used by kernel.trsolve_lower (kernel.py:112-121) when the
@@ -82,6 +83,18 @@ int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp,
  * tests/test_kernel.py:228-241).                                                   */
 int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double* B,
                       int ldb, double* X, int ldx, void* stream);
+
+/* The production TRSM: same product with the inverse stored ROW-major (LinvT: element
+ * (i, k) of Linv at LinvT[k + i*ldp], upper part zero) so both operands are K-major.
+ * Persistent warp-specialised kernel: TMA (cp.async.bulk.tensor, 128B swizzle) into a
+ * 6-stage mbarrier ring, DMMA consumers.  Bitwise identical to gg_trsm_lower_f64.
+ * Operands 16-byte aligned; padding rows of B zero.                                     */
+int gg_trsm_lower_rm_f64(int n, int nrhs, const double* LinvT, int ldp, const double* B,
+                         int ldb, double* X, int ldx, void* stream);
+
+/* Square transpose (np x np, np a multiple of 32): T = A^T (column-major both).
+ * Turns the Linv produced by gg_potrf_f64 into the LinvT operand above.              */
+int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream);
 
 /* General FP64 DMMA GEMM on padded operands: C = alpha*A*op(B) + beta*C with
  * A: m x k (lda), op(B) = B (k x ncols, ldb) or B^T (B stored ncols x k, ldb).
@@ -126,10 +139,11 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                         double* sinv, void* stream);
 
 /* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342):
- * [widen int8 ->] TRSM (Linv * X) -> fused epilogue.  Exactly one of X64 (np rows,
+ * [widen int8 ->] TRSM (row-major inverse LinvT, see gg_trsm_lower_rm_f64) -> fused
+ * epilogue.  Exactly one of X64 (np rows,
  * ldx) / G8 (n rows, ldg) is non-NULL.  xbar_work: np x cnt FP64 scratch (ld = np),
  * x64_work: np x cnt FP64 scratch used only for the int8 path (may be NULL otherwise). */
-int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp,
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp,
                      const double* XLbar, const double* ybar, const double* S_TL,
                      const double* b_T, const double* X64, int ldx, const int8_t* G8,
                      long long ldg, double* x64_work, double* xbar_work, double* beta,

@@ -29,10 +29,12 @@ SIGNATURES = {
     "gg_last_error": (C.c_char_p, []),
     "gg_pad": (_i, [_i]),
     "gg_potrf_workspace_bytes": (_sz, [_i]),
-    "gg_potrf_f64": (_i, [_i, _vp, _i, _vp, _vp, _i, _vp, _ip, _vp]),
+    "gg_potrf_f64": (_i, [_i, _vp, _i, _i, _vp, _vp, _i, _vp, _ip, _vp]),
     "gg_trtri_workspace_bytes": (_sz, [_i]),
     "gg_trtri_lower_f64": (_i, [_i, _vp, _i, _vp, _i, _vp, _vp]),
     "gg_trsm_lower_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
+    "gg_trsm_lower_rm_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
+    "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
     "gg_widen_i8_f64": (_i, [_i, _i, _vp, _ll, _vp, _i, _vp]),
     "gg_gls_dots_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp]),

@@ -35,9 +35,9 @@ int gg_pad(int n) { return pad_rows(n); }
 
 size_t gg_potrf_workspace_bytes(int n) { return n < 1 ? 0 : gg::potrf_ws_bytes(n); }
 
-int gg_potrf_f64(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
-                 int* info_host, void* stream) {
-  return gg::potrf_run(n, M, ldm, L, Linv, ldp, work, info_host, as_stream(stream));
+int gg_potrf_f64(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv,
+                 int ldp, void* work, int* info_host, void* stream) {
+  return gg::potrf_run(n, M, ldm, m_row_major, L, Linv, ldp, work, info_host, as_stream(stream));
 }
 
 size_t gg_trtri_workspace_bytes(int n) { return n < 1 ? 0 : gg::trtri_ws_bytes(n); }
@@ -72,6 +72,27 @@ int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double
   a.flags = gg::GEMM_A_LOWER;
   a.abort_flag = nullptr;
   return gg::launch_dgemm(a, false, as_stream(stream));
+}
+
+int gg_trsm_lower_rm_f64(int n, int nrhs, const double* LinvT, int ldp, const double* B,
+                         int ldb, double* X, int ldx, void* stream) {
+  if (n < 1 || nrhs < 0 || LinvT == nullptr || B == nullptr || X == nullptr) {
+    gg::set_error("trsm: null pointer or bad size");
+    return GG_EARG;
+  }
+  if (B == X) {
+    gg::set_error("trsm: X must not alias B");
+    return GG_EARG;
+  }
+  return gg::trsm_rowmajor_run(n, nrhs, LinvT, ldp, B, ldb, X, ldx, as_stream(stream));
+}
+
+int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream) {
+  if (A == nullptr || T == nullptr || A == T) {
+    gg::set_error("transpose: null or aliased pointers");
+    return GG_EARG;
+  }
+  return gg::transpose_square_run(np, A, lda, T, ldt, as_stream(stream));
 }
 
 int gg_dgemm_f64(int m, int ncols, int k, double alpha, const double* A, int lda, const double* B,
@@ -130,7 +151,7 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, cons
                           as_stream(stream));
 }
 
-int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp, const double* XLbar,
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp, const double* XLbar,
                      const double* ybar, const double* S_TL, const double* b_T, const double* X64,
                      int ldx, const int8_t* G8, long long ldg, double* x64_work, double* xbar_work,
                      double* beta, int* status, double* sinv, void* stream) {
@@ -139,8 +160,8 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp, const d
     gg::set_error("gls_block: exactly one of X64 / G8 must be given");
     return GG_EARG;
   }
-  if (xbar_work == nullptr || Linv == nullptr) {
-    gg::set_error("gls_block: null workspace / Linv");
+  if (xbar_work == nullptr || LinvT == nullptr) {
+    gg::set_error("gls_block: null workspace / LinvT");
     return GG_EARG;
   }
   const int np = pad_rows(n);
@@ -157,7 +178,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* Linv, int ldp, const d
     xin = x64_work;
     ldin = np;
   }
-  int rc = gg_trsm_lower_f64(n, cnt, Linv, ldp, xin, ldin, xbar_work, np, stream);
+  int rc = gg::trsm_rowmajor_run(n, cnt, LinvT, ldp, xin, ldin, xbar_work, np, s);
   if (rc != GG_OK) return rc;
   return gg::epilogue_run(n, cnt, q, xbar_work, np, XLbar, np, ybar, S_TL, b_T, beta, status,
                           sinv, s);

@@ -48,12 +48,18 @@ struct GemmArgs {
 int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s);
 
 // ---- dense factorisation (potrf_f64.cu) ----------------------------------------------
-int potrf_run(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
+int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv, int ldp,
+              void* work,
               int* info_host, cudaStream_t s);
 int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work,
               cudaStream_t s);
 size_t potrf_ws_bytes(int n);
 size_t trtri_ws_bytes(int n);
+
+// ---- TMA/DMMA streamed TRSM (trsm_tma.cu) -------------------------------------------------
+int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,
+                      double* X, int ldx, cudaStream_t s);
+int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, cudaStream_t s);
 
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------
 int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,

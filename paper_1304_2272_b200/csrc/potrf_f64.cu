@@ -30,7 +30,7 @@ struct PotrfHeader {
 };
 constexpr size_t HDR_BYTES = 256;
 
-__global__ void init_factor_kernel(int n, int np, const double* __restrict__ M, long long ldm,
+__global__ void init_factor_kernel(int n, int np, const double* __restrict__ M, long long rs, long long cs,
                                    double* __restrict__ L, double* __restrict__ Linv,
                                    long long ldp) {
   const long long total = (long long)np * np;
@@ -38,7 +38,7 @@ __global__ void init_factor_kernel(int n, int np, const double* __restrict__ M, 
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % np), j = (int)(idx / np);
     double v;
-    if (i < n && j < n) v = (i >= j) ? M[i + j * ldm] : 0.0;
+    if (i < n && j < n) v = (i >= j) ? M[i * rs + j * cs] : 0.0;
     else v = (i == j) ? 1.0 : 0.0;   // identity extension on the padding block
     L[i + j * ldp] = v;
     if (Linv != nullptr) Linv[i + j * ldp] = 0.0;
@@ -55,13 +55,13 @@ __global__ void zero_square_kernel(int np, double* __restrict__ A, long long ld)
 }
 
 // First non-finite entry in row-major order (kernel.py:101-103 reports its row).
-__global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long ldm,
+__global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long rs, long long cs,
                                  unsigned long long* first) {
   const long long total = (long long)n * n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % n), j = (int)(idx / n);
-    if (!isfinite(M[i + j * ldm])) atomicMin(first, (unsigned long long)i * n + j);
+    if (!isfinite(M[i * rs + j * cs])) atomicMin(first, (unsigned long long)i * n + j);
   }
 }
 
@@ -200,7 +200,7 @@ size_t potrf_ws_bytes(int n) {
   return HDR_BYTES + (panel > tri ? panel : tri);
 }
 
-int potrf_run(int n, const double* M, int ldm, double* L, double* Linv, int ldp, void* work,
+int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv, int ldp, void* work,
               int* info_host, cudaStream_t s) {
   if (n < 1 || M == nullptr || L == nullptr || Linv == nullptr || work == nullptr ||
       info_host == nullptr) {
@@ -218,9 +218,10 @@ int potrf_run(int n, const double* M, int ldm, double* L, double* Linv, int ldp,
   double* P = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
   GG_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(int) * 2, s));
   GG_CUDA_TRY(cudaMemsetAsync(&hdr->nonfinite, 0xff, sizeof(unsigned long long), s));
-  nonfinite_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(n, M, ldm, &hdr->nonfinite);
+  const long long rs = m_row_major ? ldm : 1, cs = m_row_major ? 1 : ldm;
+  nonfinite_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(n, M, rs, cs, &hdr->nonfinite);
   GG_LAUNCH_CHECK("nonfinite_kernel");
-  init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, ldm, L, Linv, ldp);
+  init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, rs, cs, L, Linv, ldp);
   GG_LAUNCH_CHECK("init_factor_kernel");
   GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)LEAF_SMEM));

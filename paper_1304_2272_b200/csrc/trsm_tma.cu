@@ -1,0 +1,333 @@
+// Streamed TRSM  Xbar = Linv * X  as a persistent, warp-specialised TMA + DMMA kernel (sm_100a).
+//
+// The dominant cost of the GLS sweep (n^2 FLOP per SNP).  Design:
+//   * operands are K-major: A = Linv stored row-major ("LinvT", k contiguous per row m, upper part
+//     zero) and B = X column-major (k contiguous per SNP column); both are moved by TMA
+//     (cp.async.bulk.tensor.2d) as 128 x 16 FP64 boxes with the 128-byte swizzle;
+//   * warp 8 is the producer: one elected lane walks the CTA's tile sequence and keeps a
+//     6-stage ring of (A, B) boxes full (mbarrier full/empty pairs, expect_tx byte counts);
+//   * warps 0-7 are consumers: 2 x 4 warp grid, 64 x 32 warp tile = 8 x 4 DMMA.8x8x4 fragments;
+//     no CTA-wide barrier in the main loop — a warp waits only on the stage it needs;
+//   * fragment rows/columns are permuted (row = 16*(i/2) + 2*g + (i&1)) so the swizzled
+//     fragment loads are bank-conflict free and the two row-fragments of a pair store as one
+//     16-byte vector per lane (4 full 128-byte lines per warp store);
+//   * persistent grid (one CTA per SM), tiles in heavy-first order dealt in a snake so the
+//     triangular work (row tile mt needs k < (mt+1)*128) balances across SMs; the producer runs
+//     ahead across tile boundaries, hiding each tile's prologue behind the previous epilogue.
+// Per-element accumulation order (k ascending in DMMA k=4 chunks) is the same as the cp.async
+// GEMM (gemm_f64.cu), so both kernels give bitwise-identical Xbar columns.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "gg_internal.cuh"
+
+namespace gg {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int STAGES = 6;
+constexpr int CONSUMER_WARPS = 8;
+constexpr int THREADS = (CONSUMER_WARPS + 1) * 32;
+constexpr int TILE_BYTES = BM * BK * 8;                 // 16 KB per operand box
+constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TrsmArgs {
+  int N;          // columns (SNPs)
+  int num_mt;     // np / 128
+  int num_nt;     // ceil(N / 128)
+  double* C;
+  long long ldc;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// tile t of the heavy-first order -> (mt, nt)
+__device__ __forceinline__ void tile_coords(int t, int num_mt, int num_nt, int& mt, int& nt) {
+  mt = num_mt - 1 - t / num_nt;
+  nt = t % num_nt;
+}
+
+// r-th tile handled by CTA b of G (snake deal)
+__device__ __forceinline__ int tile_of(int r, int b, int G) {
+  return r * G + ((r & 1) ? (G - 1 - b) : b);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    trsm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    TrsmArgs a) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  const unsigned sbase = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars);
+  const unsigned empty0 = smem_u32(bars + STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int total = a.num_mt * a.num_nt;
+  const int G = gridDim.x, b = blockIdx.x;
+
+  if (warp == CONSUMER_WARPS) {
+    // ------------------------------ producer -------------------------------------------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<unsigned long long>(&tmA))
+                   : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<unsigned long long>(&tmB))
+                   : "memory");
+      int stage = 0;
+      unsigned phase = 0;
+      for (int r = 0;; ++r) {
+        const int t = tile_of(r, b, G);
+        if (t >= total) break;
+        int mt, nt;
+        tile_coords(t, a.num_mt, a.num_nt, mt, nt);
+        const int nk = (mt + 1) * (BM / BK);   // triangular: k < (mt+1)*128
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const unsigned fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          const unsigned dA = sbase + stage * STAGE_BYTES;
+          tma_load_2d(dA, &tmA, fb, kt * BK, mt * BM);
+          tma_load_2d(dA + TILE_BYTES, &tmB, fb, kt * BK, nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers ------------------------------------------------
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  // byte offsets of this lane's fragment rows inside a 128-row swizzled box, and their swizzle
+  unsigned a_row[8], b_row[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a_row[i] = (wm * 64 + 16 * (i >> 1) + 2 * g + (i & 1));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) b_row[j] = (wn * 32 + 16 * (j >> 1) + 2 * g + (j & 1));
+
+  int stage = 0;
+  unsigned phase = 0;
+  for (int r = 0;; ++r) {
+    const int t = tile_of(r, b, G);
+    if (t >= total) break;
+    int mt, nt;
+    tile_coords(t, a.num_mt, a.num_nt, mt, nt);
+    const int nk = (mt + 1) * (BM / BK);
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < nk; ++kt) {
+      mbar_wait(full0 + 8 * stage, phase);
+      const unsigned char* As = smem + stage * STAGE_BYTES;
+      const unsigned char* Bs = As + TILE_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        const unsigned kc = (unsigned)((kk >> 1) | (tq >> 1));   // 16-byte chunk of k = kk + tq
+        const unsigned ks = (unsigned)(tq & 1) << 3;
+        double af[8], bf[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          af[i] = *reinterpret_cast<const double*>(As + a_row[i] * 128 +
+                                                   ((kc ^ (a_row[i] & 7)) << 4) + ks);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          bf[j] = *reinterpret_cast<const double*>(Bs + b_row[j] * 128 +
+                                                   ((kc ^ (b_row[j] & 7)) << 4) + ks);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // epilogue: rows (2g, 2g+1) of a fragment pair are adjacent -> one 16-byte store
+    const long long m_base = (long long)mt * BM + wm * 64 + 2 * g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = nt * BN + wn * 32 + 16 * (j >> 1) + 4 * tq + 2 * e + (j & 1);
+        if (col < a.N) {
+          double* cp = a.C + (long long)col * a.ldc + m_base;
+#pragma unroll
+          for (int ip = 0; ip < 4; ++ip) {
+            double2 v = make_double2(acc[2 * ip][j][e], acc[2 * ip + 1][j][e]);
+            *reinterpret_cast<double2*>(cp + 16 * ip) = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---- tensor maps ----------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// K-major FP64 operand: `rows` rows of `kdim` contiguous doubles, row stride ld (doubles).
+int make_kmajor_map(CUtensorMap* map, const double* base, long long kdim, long long rows,
+                    long long ld) {
+  auto fn = encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return GG_ECUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {BK, BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+    return GG_ECUDA;
+  }
+  return GG_OK;
+}
+
+__global__ void transpose_kernel(int np, const double* __restrict__ A, long long lda,
+                                 double* __restrict__ T, long long ldt) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y)
+    tile[j][threadIdx.x] = A[(long long)(bx + j) * lda + by + threadIdx.x];   // column bx+j
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y)
+    T[(long long)(by + j) * ldt + bx + threadIdx.x] = tile[threadIdx.x][j];
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace
+
+int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, cudaStream_t s) {
+  if (np % 32 != 0 || lda < np || ldt < np) {
+    set_error("transpose: np must be a multiple of 32 and ld >= np");
+    return GG_EDIM;
+  }
+  dim3 grid(np / 32, np / 32), block(32, 8);
+  transpose_kernel<<<grid, block, 0, s>>>(np, A, lda, T, ldt);
+  GG_LAUNCH_CHECK("transpose_kernel");
+  return GG_OK;
+}
+
+int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,
+                      double* X, int ldx, cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (ldp < np || ldb < np || ldx < np) {
+    set_error("trsm: leading dimensions must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  if (nrhs <= 0) return GG_OK;
+  if ((reinterpret_cast<uintptr_t>(LinvT) | reinterpret_cast<uintptr_t>(B) |
+       reinterpret_cast<uintptr_t>(X)) & 15) {
+    set_error("trsm: operands must be 16-byte aligned");
+    return GG_EARG;
+  }
+  CUtensorMap mA, mB;
+  int rc = make_kmajor_map(&mA, LinvT, np, np, ldp);
+  if (rc != GG_OK) return rc;
+  rc = make_kmajor_map(&mB, B, np, nrhs, ldb);
+  if (rc != GG_OK) return rc;
+  TrsmArgs a;
+  a.N = nrhs;
+  a.num_mt = np / BM;
+  a.num_nt = (nrhs + BN - 1) / BN;
+  a.C = X;
+  a.ldc = ldx;
+  const int tiles = a.num_mt * a.num_nt;
+  int grid = sm_count();
+  if (grid > tiles) grid = tiles;
+  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)SMEM_BYTES));
+  trsm_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
+  GG_LAUNCH_CHECK("trsm_tma_kernel");
+  return GG_OK;
+}
+
+}  // namespace gg

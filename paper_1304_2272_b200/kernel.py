@@ -27,6 +27,7 @@ from ._device import (
     alloc_cols,
     download_cols,
     upload_cols,
+    transpose_square,
     upload_square_identity_padded,
 )
 from .errors import DimensionMismatch, NotPositiveDefinite, RankDeficientCovariates
@@ -188,24 +189,32 @@ class PreparedContext:
 # ---------------------------------------------------------------------------------------------
 
 def _potrf_device(M):
-    """Device Cholesky + inverse of the n x n host matrix M; returns (n, L_dev, Linv_dev)."""
+    """Device Cholesky + inverse of the n x n host matrix M; returns (n, L_dev, LinvT_dev) with
+    the inverse stored row-major (the K-major operand of the TMA TRSM)."""
     torch = __import__("torch")
     n = M.shape[0]
     np_ = pad(n)
-    Md = upload_cols(M)                          # (n, pad(n)) col-major, ld = np_
+    if isinstance(M, np.ndarray):
+        # the C-contiguous buffer goes up as is; the kernels read it row-major (no host transpose)
+        Md = torch.from_numpy(np.ascontiguousarray(M, dtype=np.float64)).to(_capi.device())
+    else:
+        Md = M.contiguous()                      # device tensor, row-major (n, n)
     L = alloc_cols(np_, np_, zero=False)
     Linv = alloc_cols(np_, np_, zero=False)
     ws = torch.empty(int(_capi.lib().gg_potrf_workspace_bytes(n)), dtype=torch.uint8,
                      device=Md.device)
     info = (_capi.C.c_int * 2)()
-    rc = _capi.lib().gg_potrf_f64(n, ptr(Md), Md.shape[1], ptr(L), ptr(Linv), np_, ptr(ws),
-                                  info, stream_handle())
+    rc = _capi.lib().gg_potrf_f64(n, ptr(Md), n, 1, ptr(L), ptr(Linv), np_, ptr(ws), info,
+                                  stream_handle())
+    del Md
     if rc == _capi.GG_ENOTPD:
         if info[1]:
             raise NotPositiveDefinite(int(info[0]), "non-finite entry in covariance")
         raise NotPositiveDefinite(int(info[0]))
     check(rc, "gg_potrf_f64")
-    return n, L, Linv
+    LinvT = transpose_square(Linv)
+    del Linv
+    return n, L, LinvT
 
 
 def cholesky_spd(M):
@@ -221,7 +230,7 @@ def cholesky_spd(M):
 
 
 def _trtri_device(L):
-    """Device inverse of a host lower-triangular L; returns (n, Linv_dev)."""
+    """Device inverse of a host lower-triangular L; returns (n, LinvT_dev) (row-major)."""
     torch = __import__("torch")
     n = L.shape[0]
     np_ = pad(n)
@@ -231,14 +240,15 @@ def _trtri_device(L):
                      device=Ld.device)
     check(_capi.lib().gg_trtri_lower_f64(n, ptr(Ld), np_, ptr(Linv), np_, ptr(ws),
                                          stream_handle()), "gg_trtri_lower_f64")
-    return n, Linv
+    return n, transpose_square(Linv)
 
 
-def _trsm_device(dLinv, n, B_dev, nrhs):
+def _trsm_device(dLinvT, n, B_dev, nrhs):
+    """X = L^-1 B on the device (TMA/DMMA kernel; LinvT is the row-major inverse)."""
     np_ = pad(n)
     X = alloc_cols(nrhs, np_, zero=False)
-    check(_capi.lib().gg_trsm_lower_f64(n, nrhs, ptr(dLinv), np_, ptr(B_dev), B_dev.shape[1],
-                                        ptr(X), np_, stream_handle()), "gg_trsm_lower_f64")
+    check(_capi.lib().gg_trsm_lower_rm_f64(n, nrhs, ptr(dLinvT), np_, ptr(B_dev), B_dev.shape[1],
+                                           ptr(X), np_, stream_handle()), "gg_trsm_lower_rm_f64")
     return X
 
 
@@ -254,9 +264,9 @@ def trsolve_lower(L, B):
     n, nrhs = B.shape
     if nrhs == 0:
         return np.empty((n, 0)) if not squeeze else np.empty(n)
-    _, Linv = _trtri_device(L)
+    _, LinvT = _trtri_device(L)
     Bd = upload_cols(B, ld=pad(n))
-    X = np.asfortranarray(download_cols(_trsm_device(Linv, n, Bd, nrhs), n, nrhs))
+    X = np.asfortranarray(download_cols(_trsm_device(LinvT, n, Bd, nrhs), n, nrhs))
     return X[:, 0] if squeeze else X
 
 
@@ -359,10 +369,10 @@ def gls_prepare(M, XL, y):
     q = XL.shape[1]
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
-    _, L, Linv = _potrf_device(np.ascontiguousarray(M))
+    _, L, LinvT = _potrf_device(np.ascontiguousarray(M))
     np_ = pad(n)
     RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
-    XLy = _trsm_device(Linv, n, RHS, q + 1)
+    XLy = _trsm_device(LinvT, n, RHS, q + 1)
     dots = _dots_device(XLy, n, q, XLy, q, XLy[q]) if q > 0 else None
     if q > 0:
         C = dots[:, :q]
@@ -387,7 +397,7 @@ def gls_prepare(M, XL, y):
     host = download_cols(XLy, n, q + 1)
     XLbar = np.asfortranarray(host[:, :q])
     ybar = np.ascontiguousarray(host[:, q])
-    dctx = DeviceContext(n=n, np_=np_, q=q, L=L, Linv=Linv, XLy=XLy, S_TL=S_TL_d.reshape(-1),
+    dctx = DeviceContext(n=n, np_=np_, q=q, L=L, LinvT=LinvT, XLy=XLy, S_TL=S_TL_d.reshape(-1),
                          b_T=b_T_d)
     return PreparedContext(L=None, XLbar=XLbar, ybar=ybar, S_TL=S_TL, b_T=b_T, _dev=dctx)
 
@@ -425,7 +435,7 @@ def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
     One TRSM launch (Linv * X on DMMA tiles) plus one fused epilogue launch; ``threads`` is
     accepted for signature compatibility (results never depend on it)."""
     d = ctx._dev
-    if d is None or d.Linv is None:
+    if d is None or d.LinvT is None:
         raise DimensionMismatch("context was not prepared on the device (use gls_prepare)")
     if blk.n != d.n:
         raise DimensionMismatch(f"block has n={blk.n}, context has n={d.n}")

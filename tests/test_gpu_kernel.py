@@ -322,3 +322,40 @@ def test_structured_vs_naive_random(K):
         for i in range(5):
             e = O.gls_eq1(M, np.hstack([XL, X[:, i:i + 1]]), y)
             assert maxnorm(rb.results[i].beta - e) <= 1e-8 * max(maxnorm(e), 1.0)
+
+
+def test_tma_trsm_bitwise_equals_cpasync_trsm(K):
+    """The persistent TMA/DMMA TRSM (production) and the cp.async DMMA GEMM give identical bits."""
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._capi import ptr, stream_handle
+    from paper_1304_2272_b200._device import alloc_cols, transpose_square, upload_cols
+
+    for n, nrhs in ((300, 257), (1000, 1), (129, 700)):
+        M = make_spd(n, n)
+        _, L, LinvT = K._potrf_device(M)
+        np_ = _capi.pad(n)
+        Linv = transpose_square(LinvT)
+        B = upload_cols(np.random.default_rng(n).standard_normal((n, nrhs)), ld=np_)
+        X1 = alloc_cols(nrhs, np_)
+        X2 = alloc_cols(nrhs, np_)
+        assert _capi.lib().gg_trsm_lower_f64(n, nrhs, ptr(Linv), np_, ptr(B), np_, ptr(X1), np_,
+                                             stream_handle()) == 0
+        assert _capi.lib().gg_trsm_lower_rm_f64(n, nrhs, ptr(LinvT), np_, ptr(B), np_, ptr(X2),
+                                                np_, stream_handle()) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(X1, X2)
+
+
+def test_cholesky_reads_lower_triangle_and_checks_all_entries(K):
+    from paper_1304_2272_b200.errors import NotPositiveDefinite
+
+    M = make_spd(40, 3)
+    A = M.copy()
+    A[np.triu_indices(40, 1)] = 7.0          # garbage above the diagonal: dpotrf(lower) ignores it
+    assert np.array_equal(K.cholesky_spd(A), K.cholesky_spd(M))
+    A[3, 30] = np.inf                        # but a non-finite entry anywhere is refused
+    with pytest.raises(NotPositiveDefinite) as e:
+        K.cholesky_spd(A)
+    assert e.value.pivot_index == 3
