@@ -105,6 +105,12 @@ class _LazyResults:
     def __eq__(self, other):
         return list(self) == list(other)
 
+    def __add__(self, other):
+        return list(self) + list(other)
+
+    def __radd__(self, other):
+        return list(other) + list(self)
+
 
 @dataclass
 class ResultArrays:
@@ -411,10 +417,26 @@ def _collect(ws, cnt, first_index, global_indices, emit_s_inv):
                                                 status=status, sinv=sinv, global_indices=gi))
 
 
+def device_context(ctx, need_factor=False):
+    """Device half of any PreparedContext-like object (ours, or the reference's dataclass built
+    by a caller such as run_dist, distgrid.py:385).  Built from the host fields on first use and
+    cached on the object; with ``need_factor`` the row-major inverse is derived from ``ctx.L``."""
+    d = getattr(ctx, "_dev", None)
+    if d is None:
+        d = DeviceContext.from_host(ctx.XLbar, ctx.ybar, ctx.S_TL, ctx.b_T)
+        ctx._dev = d
+    if need_factor and d.LinvT is None:
+        L = np.asarray(ctx.L, dtype=np.float64)
+        if L.ndim != 2 or L.shape != (d.n, d.n):
+            raise DimensionMismatch("context has no usable Cholesky factor for the TRSM")
+        _, d.LinvT = _trtri_device(L)
+    return d
+
+
 def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv=False):
     """Per-marker assembly and solve for already-whitened columns Xbar (n x count)
-    (kernel.py:273-312); the fused device epilogue."""
-    d = ctx.device()
+    (kernel.py:273-312); the fused device epilogue.  Returns a list of SnpResult."""
+    d = device_context(ctx)
     Xbar = np.asarray(Xbar, dtype=np.float64)
     if Xbar.ndim != 2 or Xbar.shape[0] != d.n:
         raise DimensionMismatch(f"Xbar has shape {Xbar.shape}, context has n={d.n}")
@@ -426,7 +448,7 @@ def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv
             d.n, cnt, d.q, ptr(Xd), d.np_, ptr(d.XLy), d.np_, ptr(d.ybar), ptr(d.S_TL),
             ptr(d.b_T), ptr(ws.beta), ptr(ws.status), ptr(ws.sinv), stream_handle()),
             "gg_gls_epilogue_f64")
-    return _collect(ws, cnt, first_index, global_indices, emit_s_inv).results
+    return list(_collect(ws, cnt, first_index, global_indices, emit_s_inv).results)
 
 
 def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
@@ -434,9 +456,7 @@ def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
 
     One TRSM launch (Linv * X on DMMA tiles) plus one fused epilogue launch; ``threads`` is
     accepted for signature compatibility (results never depend on it)."""
-    d = ctx._dev
-    if d is None or d.LinvT is None:
-        raise DimensionMismatch("context was not prepared on the device (use gls_prepare)")
+    d = device_context(ctx, need_factor=True)
     if blk.n != d.n:
         raise DimensionMismatch(f"block has n={blk.n}, context has n={d.n}")
     cnt = blk.count
