@@ -48,8 +48,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--m", type=int, default=None, help="SNPs per GPU (default: the config's m)")
-    ap.add_argument("--m-blk", type=int, default=8192)
+    ap.add_argument("--snps", type=int, default=None, help="SNPs per GPU (default: config's m)")
+    ap.add_argument("--block-snps", type=int, default=8192)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-dtype", choices=["f64", "i8"], default="f64")
@@ -137,34 +137,37 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     lib = _capi.lib()
     spec = datagen.CONFIGS[args.config]
-    m = args.m or spec.m
+    m = args.snps or spec.m
     spec = dataclasses.replace(spec, m=m * world)     # the N*m-marker panel
     n, p = spec.n, spec.p
     q = p - 1
     np_ = _capi.pad(n)
-    m_blk = args.m_blk
+    m_blk = args.block_snps
 
     # ---- data (identical M on every rank; rank-local marker range) --------------------------
     t0 = time.perf_counter()
-    M = datagen.kinship_covariance_device(spec).cpu().numpy()
+    Md = datagen.kinship_covariance_device(spec)          # (n, n) on the device
     XL, y = datagen.covariates_host(spec)
     torch.cuda.synchronize()
     t_gen_m = time.perf_counter() - t0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
-    ctx = kernel.gls_prepare(M, XL, y)
+    ctx = kernel.gls_prepare(Md, XL, y)                  # device-resident M, no host round trip
     e1.record()
     torch.cuda.synchronize()
     t_prepare = time.perf_counter() - t0
     prepare_ms_device = e0.elapsed_time(e1)
     d = ctx._dev
+    M = Md.cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    del Md
     X = torch.empty((m, np_), dtype=torch.float64, device=dev)
     X[:, n:].zero_()
     G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
@@ -200,7 +203,7 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -224,7 +227,7 @@ def run_ours(args):
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     barrier()
-    if world > 1:
+    if use_dist:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
@@ -239,7 +242,8 @@ def run_ours(args):
     # ---- e2e through the public stream API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline)
+        e2e = run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist if use_dist else None,
+                      pipeline)
 
     # ---- CPU baseline + sampled parity on rank 0 at N = 1 -----------------------------------
     cpu = None
@@ -285,7 +289,7 @@ def run_ours(args):
         if ncu is not None:
             line["roofline"]["traffic_source"] = ncu.get("source")
         print(json.dumps(line))
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -293,9 +297,16 @@ def run_ours(args):
 def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
     """Same metric through pipeline.solve_array with host genotypes: every step H2D-copies all
     m markers from pinned host memory (double-buffered, copy stream) and reads the results back."""
-    np_ = X.shape[1]
+    dtype = args.e2e_dtype
+    try:   # FP64 host genotypes need m*n*8 pinned bytes per rank; keep well inside host RAM
+        import psutil
+
+        if world * m * n * 8 > 0.5 * psutil.virtual_memory().available:
+            dtype = "i8"
+    except ImportError:
+        pass
     try:
-        if args.e2e_dtype == "f64":
+        if dtype == "f64":
             host_t = torch.empty((m, n), dtype=torch.float64).pin_memory()
             host_t.copy_(X[:, :n])
         else:
@@ -305,10 +316,10 @@ def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
         host_t.copy_(X[:, :n].to(torch.int8))
     Xh = host_t.numpy().T                     # n x m, Fortran-ordered view of pinned memory
     int8 = Xh.dtype == np.int8
-    engine = pipeline.StreamEngine(ctx, args.m_blk, int8=int8)
+    engine = pipeline.StreamEngine(ctx, args.block_snps, int8=int8)
     res = pipeline.solve_array(ctx, Xh, engine=engine)      # warm-up
     torch.cuda.synchronize()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     h0, d0 = engine.h2d_bytes, engine.d2h_bytes
     t0 = time.perf_counter()
@@ -316,7 +327,7 @@ def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
         res = pipeline.solve_array(ctx, Xh, engine=engine)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if world > 1:
+    if dist is not None:
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())

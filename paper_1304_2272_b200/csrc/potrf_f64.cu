@@ -12,6 +12,8 @@
 // with triangular-aware DMMA GEMMs.  A failing pivot sets a device flag that turns every later
 // kernel into a no-op; the host reads it once at the end (no per-block synchronisation).
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "gg_internal.cuh"
 
@@ -20,8 +22,7 @@ namespace {
 
 constexpr int NB = 128;
 constexpr int LEAF_THREADS = 512;
-constexpr int SLD = NB + 1;   // column stride of the shared leaf block
-constexpr size_t LEAF_SMEM = size_t(NB) * SLD * sizeof(double);
+constexpr size_t LEAF_SMEM = 0;   // register-resident leaf (static shared only)
 
 struct PotrfHeader {
   int info;                      // 0 = ok, else failing pivot + 1
@@ -65,80 +66,153 @@ __global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long 
   }
 }
 
-// In-place inverse of the lower-triangular block held in s (column stride SLD).
-// Row-oriented forward substitution on X = I:  X[i,:] /= L_ii;  X[r,:] -= L_ri X[i,:] (r > i).
-// Column i of L is staged in colL before row i's update overwrites it.
-__device__ void leaf_invert_inplace(double* s, double* colL) {
-  const int tid = threadIdx.x;
-  for (int i = 0; i < NB; ++i) {
-    const double lii = s[i * SLD + i];
-    for (int r = i + 1 + tid; r < NB; r += LEAF_THREADS) colL[r] = s[i * SLD + r];
-    for (int c = tid; c < i; c += LEAF_THREADS) s[c * SLD + i] = s[c * SLD + i] / lii;
-    __syncthreads();
-    if (tid == 0) s[i * SLD + i] = 1.0 / lii;
-    const int w = NB - 1 - i;   // rows r = i+1 .. NB-1
-    const int cols = i + 1;     // cols c = 0 .. i
-    for (int idx = tid; idx < w * cols; idx += LEAF_THREADS) {
-      const int r = i + 1 + idx % w, c = idx / w;
-      const double xic = (c == i) ? 1.0 / lii : s[c * SLD + i];
-      if (c == i) s[c * SLD + r] = -(colL[r] * xic);
-      else s[c * SLD + r] = s[c * SLD + r] - colL[r] * xic;
-    }
-    __syncthreads();
-  }
-}
+// Register-resident 128 x 128 leaf.  512 threads; thread (tx = tid % 32, ty = tid / 32) owns
+// the 32 elements (r, c) = (tx + 32a, ty + 16b), a < 4, b < 8, in v[a][b] (lower part only; the
+// upper part is kept zero).  Shared memory holds only the broadcast vectors of each step.
+struct LeafShared {
+  double col[2][NB];   // scaled column j of L (phase 1), double-buffered by step parity
+  double rowx[NB];     // final row i of the inverse (phase 2)
+  double colL[NB];     // column i of L, staged before the in-place overwrite (phase 2)
+  double diag[NB];     // pivots L_jj
+  double d;            // current pivot candidate
+};
 
-// FACTOR = true : factor the diagonal block at (k0, k0) of A in place (lower, upper zeroed),
-//                 then write its inverse to Dinv.  One CTA, sequential over the blocks.
+// FACTOR = true : factor the diagonal block at (k0, k0) of A in place (lower, upper zeroed,
+//                 dpotf2 pivot rule: fail iff a_jj <= 0 or NaN), then write its inverse to Dinv.
+//                 One CTA; the blocks are processed in order by the host loop.
 // FACTOR = false: blockIdx.x selects diagonal block b; only invert it (triangular inverse of a
 //                 caller-supplied L).  All blocks in parallel.
 template <bool FACTOR>
 __global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long ld, double* Dinv,
                                                             long long ldi, int k0, int* info) {
-  extern __shared__ double s[];
-  __shared__ double colL[NB];
+  __shared__ LeafShared sh;
   if (info != nullptr && *info != 0) return;
-  const int tid = threadIdx.x;
-  if (!FACTOR) {
-    k0 = blockIdx.x * NB;
-  }
+  if (!FACTOR) k0 = blockIdx.x * NB;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const double* Ab = A + k0 + (long long)k0 * ld;
-  double* Db = Dinv + k0 + (long long)k0 * ldi;
-  for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
-    const int i = idx % NB, j = idx / NB;
-    s[j * SLD + i] = (i >= j) ? Ab[i + (long long)j * ld] : 0.0;
-  }
-  __syncthreads();
+  double v[4][8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = tx + 32 * a, c = ty + 16 * b;
+      v[a][b] = (r >= c) ? Ab[r + (long long)c * ld] : 0.0;
+    }
+
   if (FACTOR) {
+    // ---- phase 1: right-looking Cholesky --------------------------------------------------
+    if (tx == 0 && ty == 0) sh.d = v[0][0];
+    __syncthreads();
     for (int j = 0; j < NB; ++j) {
-      const double d = s[j * SLD + j];
-      if (!(d > 0.0)) {   // dpotf2: a_jj <= 0 or NaN
+      const double d = sh.d;
+      if (!(d > 0.0)) {                       // uniform decision
         if (tid == 0) *info = k0 + j + 1;
-        return;           // uniform: every thread read the same d
+        return;
       }
       const double piv = sqrt(d);
-      for (int i = j + 1 + tid; i < NB; i += LEAF_THREADS) s[j * SLD + i] = s[j * SLD + i] / piv;
+      double* col = sh.col[j & 1];
+      const int bj = j >> 4;
+      if (ty == (j & 15)) {                   // owners of column j
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (b != bj) continue;
+            const int r = tx + 32 * a;
+            if (r > j) {
+              v[a][b] = v[a][b] / piv;
+              col[r] = v[a][b];
+            } else if (r == j) {
+              v[a][b] = piv;
+              sh.diag[j] = piv;
+            }
+          }
+      }
       __syncthreads();
-      if (tid == 0) s[j * SLD + j] = piv;
-      const int w = NB - 1 - j;
-      for (int idx = tid; idx < w * w; idx += LEAF_THREADS) {
-        const int r = j + 1 + idx % w, c = j + 1 + idx / w;
-        if (r >= c) s[c * SLD + r] = s[c * SLD + r] - s[j * SLD + r] * s[j * SLD + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = tx + 32 * a;
+        if (r <= j) continue;
+        const double lr = col[r];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const int c = ty + 16 * b;
+          if (c > j && c <= r) {
+            v[a][b] = v[a][b] - lr * col[c];
+            if (r == j + 1 && c == j + 1) sh.d = v[a][b];   // next pivot candidate
+          }
+        }
       }
       __syncthreads();
     }
     double* Aw = A + k0 + (long long)k0 * ld;
-    for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
-      const int i = idx % NB, j = idx / NB;
-      Aw[i + (long long)j * ld] = (i >= j) ? s[j * SLD + i] : 0.0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = tx + 32 * a, c = ty + 16 * b;
+        Aw[r + (long long)c * ld] = (r >= c) ? v[a][b] : 0.0;
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (tx + 32 * a == ty + 16 * b) sh.diag[tx + 32 * a] = v[a][b];
+    __syncthreads();
+  }
+
+  // ---- phase 2: in-place inverse (row-oriented forward substitution on X = I) -------------
+  for (int i = 0; i < NB; ++i) {
+    const double lii = sh.diag[i];
+    const double inv_ii = 1.0 / lii;
+    const int ai = i >> 5, bi = i >> 4;
+    if (ty == (i & 15)) {                     // stage column i of L (rows > i)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (b == bi && tx + 32 * a > i) sh.colL[tx + 32 * a] = v[a][b];
+    }
+    if (tx == (i & 31)) {                     // finalize row i of X
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (a != ai) continue;
+          const int c = ty + 16 * b;
+          if (c < i) {
+            v[a][b] = v[a][b] / lii;
+            sh.rowx[c] = v[a][b];
+          } else if (c == i) {
+            v[a][b] = inv_ii;
+            sh.rowx[c] = inv_ii;
+          }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = tx + 32 * a;
+      if (r <= i) continue;
+      const double lri = sh.colL[r];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int c = ty + 16 * b;
+        if (c < i) v[a][b] = v[a][b] - lri * sh.rowx[c];
+        else if (c == i) v[a][b] = -(lri * inv_ii);
+      }
     }
     __syncthreads();
   }
-  leaf_invert_inplace(s, colL);
-  for (int idx = tid; idx < NB * NB; idx += LEAF_THREADS) {
-    const int i = idx % NB, j = idx / NB;
-    Db[i + (long long)j * ldi] = (i >= j) ? s[j * SLD + i] : 0.0;
-  }
+  double* Db = Dinv + k0 + (long long)k0 * ldi;
+#pragma unroll
+  for (int b = 0; b < 8; ++b)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = tx + 32 * a, c = ty + 16 * b;
+      Db[r + (long long)c * ldi] = (r >= c) ? v[a][b] : 0.0;
+    }
 }
 
 int grid_for(long long total) {
@@ -223,11 +297,25 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   GG_LAUNCH_CHECK("nonfinite_kernel");
   init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, rs, cs, L, Linv, ldp);
   GG_LAUNCH_CHECK("init_factor_kernel");
-  GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)LEAF_SMEM));
+  // optional phase timing (GG_POTRF_TIMING=1): leaf / panel / trailing / inverse, to stderr
+  const bool timing = getenv("GG_POTRF_TIMING") != nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  float t_leaf = 0.f, t_pan = 0.f, t_upd = 0.f, t_inv = 0.f;
+  if (timing)
+    for (auto& e : ev) cudaEventCreate(&e);
+  auto lap = [&](float& acc, cudaEvent_t a, cudaEvent_t b) {
+    if (!timing) return;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    acc += ms;
+  };
   for (int k = 0; k < np; k += NB) {
+    if (timing) cudaEventRecord(ev[0], s);
     leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
     GG_LAUNCH_CHECK("potrf leaf_kernel");
+    lap(t_leaf, ev[0], ev[1]);
     const int rem = np - k - NB;
     if (rem <= 0) break;
     GemmArgs pan{};
@@ -238,6 +326,7 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
     pan.alpha = 1.0; pan.beta = 0.0; pan.flags = 0; pan.abort_flag = &hdr->info;
     int rc = launch_dgemm(pan, true, s);
     if (rc != GG_OK) return rc;
+    lap(t_pan, ev[1], ev[2]);
     GemmArgs upd{};
     upd.M = rem; upd.N = rem; upd.K = NB;
     upd.A = P; upd.lda = np;
@@ -249,11 +338,19 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
     GG_CUDA_TRY(cudaMemcpy2DAsync(L + (k + NB) + (long long)k * ldp, (size_t)ldp * sizeof(double), P,
                                   (size_t)np * sizeof(double), (size_t)rem * sizeof(double), NB,
                                   cudaMemcpyDeviceToDevice, s));
+    lap(t_upd, ev[2], ev[3]);
   }
+  if (timing) cudaEventRecord(ev[0], s);
   long long tr, tc;
   trtri_T_dims(np, &tr, &tc);
   int rc = trtri_offdiag(0, np, L, Linv, ldp, P, tr > 0 ? tr : 1, &hdr->info, s);
   if (rc != GG_OK) return rc;
+  lap(t_inv, ev[0], ev[1]);
+  if (timing) {
+    fprintf(stderr, "[gg potrf n=%d] leaf %.2f ms, panel %.2f ms, trailing %.2f ms, inverse %.2f ms\n",
+            n, t_leaf, t_pan, t_upd, t_inv);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   PotrfHeader h{};
   GG_CUDA_TRY(cudaMemcpyAsync(&h, hdr, sizeof(PotrfHeader), cudaMemcpyDeviceToHost, s));
   GG_CUDA_TRY(cudaStreamSynchronize(s));
@@ -288,8 +385,6 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
   double* T = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
   zero_square_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(np, Linv, ldp);
   GG_LAUNCH_CHECK("zero_square_kernel");
-  GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)LEAF_SMEM));
   // leaf_kernel<false> only reads L; the const_cast never results in a write.
   leaf_kernel<false><<<np / NB, LEAF_THREADS, LEAF_SMEM, s>>>(const_cast<double*>(L), ldl, Linv,
                                                                ldp, 0, nullptr);

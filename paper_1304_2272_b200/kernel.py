@@ -362,9 +362,13 @@ def solve_small_spd(S, rhs):
 def gls_prepare(M, XL, y):
     """Hoist all marker-independent work (kernel.py:233-257): factor M (device Cholesky +
     inverse, kept resident), whiten XL and y with the same TRSM kernel as the SNP blocks, and
-    form S_TL and b_T with the same reduction kernel as the per-SNP sums."""
+    form S_TL and b_T with the same reduction kernel as the per-SNP sums.
+
+    M may also be a CUDA float64 tensor (n, n) already resident on the device (row-major, as a
+    C-contiguous array would be): the factorisation then reads it in place, no host round trip."""
     torch = __import__("torch")
-    M = np.asarray(M, dtype=np.float64)
+    if not (isinstance(M, torch.Tensor) and M.is_cuda and M.dtype == torch.float64):
+        M = np.ascontiguousarray(M, dtype=np.float64)
     XL = np.asarray(XL, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64).ravel()
     if M.ndim != 2 or M.shape[0] != M.shape[1]:
@@ -375,7 +379,7 @@ def gls_prepare(M, XL, y):
     q = XL.shape[1]
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
-    _, L, LinvT = _potrf_device(np.ascontiguousarray(M))
+    _, L, LinvT = _potrf_device(M)
     np_ = pad(n)
     RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
     XLy = _trsm_device(LinvT, n, RHS, q + 1)
