@@ -191,7 +191,8 @@ def run_ours(args):
         for i, (f, c) in enumerate(plan):
             if record:
                 ev_pairs[i][0].record(stream)
-            rc = lib.gg_trsm_lower_rm_f64(n, c, ptr(d.LinvT), np_, ptr(X[f]), np_, ptr(xbar), np_, sh)
+            rc = lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(X[f]), np_, ptr(xbar), np_,
+                                              sh)
             if record:
                 ev_pairs[i][1].record(stream)
             rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(xbar), np_, ptr(d.XLy), np_, ptr(d.ybar),

@@ -92,6 +92,17 @@ int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double
 int gg_trsm_lower_rm_f64(int n, int nrhs, const double* LinvT, int ldp, const double* B,
                          int ldb, double* X, int ldx, void* stream);
 
+/* The packed layout of the inverse used by the streamed sweep: only the 128 x 16 tiles on or
+ * below the diagonal, tile-major (tile (mt, kt), kt < 8*(mt+1), at index 4*mt*(mt+1) + kt;
+ * each tile 128 rows x 16 k, k contiguous).  Half the memory of the square inverse (the
+ * 150,000^2 inverse of BASELINE config 4 fits one GPU: 90 GB), and one 3-D TMA box per tile.
+ * gg_pack_lower_f64 converts a column-major (row_major = 0) or row-major (1) square inverse. */
+size_t gg_packed_lower_bytes(int n);
+int gg_pack_lower_f64(int n, const double* A, int lda, int row_major, double* LinvP,
+                      void* stream);
+int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double* B, int ldb,
+                             double* X, int ldx, void* stream);
+
 /* Square transpose (np x np, np a multiple of 32): T = A^T (column-major both).
  * Turns the Linv produced by gg_potrf_f64 into the LinvT operand above.              */
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream);
@@ -139,11 +150,11 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                         double* sinv, void* stream);
 
 /* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342):
- * [widen int8 ->] TRSM (row-major inverse LinvT, see gg_trsm_lower_rm_f64) -> fused
- * epilogue.  Exactly one of X64 (np rows,
+ * [widen int8 ->] TRSM (packed inverse LinvP, see gg_trsm_lower_packed_f64) -> fused
+ * epilogue.  XLbar has leading dimension gg_pad(n).  Exactly one of X64 (np rows,
  * ldx) / G8 (n rows, ldg) is non-NULL.  xbar_work: np x cnt FP64 scratch (ld = np),
  * x64_work: np x cnt FP64 scratch used only for the int8 path (may be NULL otherwise). */
-int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp,
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP,
                      const double* XLbar, const double* ybar, const double* S_TL,
                      const double* b_T, const double* X64, int ldx, const int8_t* G8,
                      long long ldg, double* x64_work, double* xbar_work, double* beta,

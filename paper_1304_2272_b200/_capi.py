@@ -34,6 +34,9 @@ SIGNATURES = {
     "gg_trtri_lower_f64": (_i, [_i, _vp, _i, _vp, _i, _vp, _vp]),
     "gg_trsm_lower_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
     "gg_trsm_lower_rm_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
+    "gg_packed_lower_bytes": (_sz, [_i]),
+    "gg_pack_lower_f64": (_i, [_i, _vp, _i, _i, _vp, _vp]),
+    "gg_trsm_lower_packed_f64": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
     "gg_widen_i8_f64": (_i, [_i, _i, _vp, _ll, _vp, _i, _vp]),
@@ -41,7 +44,7 @@ SIGNATURES = {
     "gg_small_spd_solve_f64": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gg_gls_epilogue_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _vp]),
-    "gg_gls_block_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _ll, _vp,
+    "gg_gls_block_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _ll, _vp,
                               _vp, _vp, _vp, _vp, _vp]),
     "gg_memcpy2d_async": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _i, _vp]),
     "gg_gen_genotypes_i8": (_i, [_ull, _i, _i, _i, _ll, _ll, _i, _d, _d, _vp, _ll, _vp, _i,

@@ -91,7 +91,7 @@ class DeviceContext:
     np_: int
     q: int
     L: object          # (np, np) col-major factor, or None (contexts built from host fields)
-    LinvT: object      # (np, np) inverse stored ROW-major (K-major TMA operand), or None
+    LinvP: object      # packed tile-major lower inverse (TMA TRSM operand), or None
     XLy: object        # (q + 1, np): whitened covariates, then whitened phenotype
     S_TL: object       # (q * q,) row-major
     b_T: object        # (q,)
@@ -121,7 +121,7 @@ class DeviceContext:
         dev = XLy.device
         S = torch.from_numpy(np.ascontiguousarray(S_TL, dtype=np.float64).ravel()).to(dev)
         b = torch.from_numpy(np.ascontiguousarray(b_T, dtype=np.float64).ravel()).to(dev)
-        return cls(n=n, np_=np_, q=q, L=None, LinvT=None, XLy=XLy, S_TL=S, b_T=b)
+        return cls(n=n, np_=np_, q=q, L=None, LinvP=None, XLy=XLy, S_TL=S, b_T=b)
 
 
 class BlockWorkspace:
@@ -146,11 +146,11 @@ class BlockWorkspace:
         d = self.dctx
         if cnt > self.m_blk:
             raise ValueError("block larger than the workspace")
-        if d.LinvT is None:
+        if d.LinvP is None:
             raise ValueError("context has no device factor (prepared from host fields only)")
         s = stream_handle() if stream is None else stream
         rc = _capi.lib().gg_gls_block_f64(
-            d.n, d.q, int(cnt), ptr(d.LinvT), d.np_, ptr(d.XLy), ptr(d.ybar), ptr(d.S_TL),
+            d.n, d.q, int(cnt), ptr(d.LinvP), ptr(d.XLy), ptr(d.ybar), ptr(d.S_TL),
             ptr(d.b_T), ptr(X64), int(ldx), ptr(G8), int(ldg), ptr(self.x64), ptr(self.xbar),
             ptr(self.beta), ptr(self.status), ptr(self.sinv), s)
         check(rc, "gg_gls_block_f64")

@@ -87,6 +87,32 @@ int gg_trsm_lower_rm_f64(int n, int nrhs, const double* LinvT, int ldp, const do
   return gg::trsm_rowmajor_run(n, nrhs, LinvT, ldp, B, ldb, X, ldx, as_stream(stream));
 }
 
+size_t gg_packed_lower_bytes(int n) {
+  return n < 1 ? 0 : gg::packed_lower_elems(n) * sizeof(double);
+}
+
+int gg_pack_lower_f64(int n, const double* A, int lda, int row_major, double* LinvP,
+                      void* stream) {
+  if (n < 1 || A == nullptr || LinvP == nullptr) {
+    gg::set_error("pack_lower: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::pack_lower_run(n, A, lda, row_major, LinvP, as_stream(stream));
+}
+
+int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double* B, int ldb,
+                             double* X, int ldx, void* stream) {
+  if (n < 1 || nrhs < 0 || LinvP == nullptr || B == nullptr || X == nullptr) {
+    gg::set_error("trsm: null pointer or bad size");
+    return GG_EARG;
+  }
+  if (B == X) {
+    gg::set_error("trsm: X must not alias B");
+    return GG_EARG;
+  }
+  return gg::trsm_packed_run(n, nrhs, LinvP, B, ldb, X, ldx, as_stream(stream));
+}
+
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream) {
   if (A == nullptr || T == nullptr || A == T) {
     gg::set_error("transpose: null or aliased pointers");
@@ -151,7 +177,7 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, cons
                           as_stream(stream));
 }
 
-int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp, const double* XLbar,
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const double* XLbar,
                      const double* ybar, const double* S_TL, const double* b_T, const double* X64,
                      int ldx, const int8_t* G8, long long ldg, double* x64_work, double* xbar_work,
                      double* beta, int* status, double* sinv, void* stream) {
@@ -160,8 +186,8 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp, const 
     gg::set_error("gls_block: exactly one of X64 / G8 must be given");
     return GG_EARG;
   }
-  if (xbar_work == nullptr || LinvT == nullptr) {
-    gg::set_error("gls_block: null workspace / LinvT");
+  if (xbar_work == nullptr || LinvP == nullptr) {
+    gg::set_error("gls_block: null workspace / LinvP");
     return GG_EARG;
   }
   const int np = pad_rows(n);
@@ -178,7 +204,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvT, int ldp, const 
     xin = x64_work;
     ldin = np;
   }
-  int rc = gg::trsm_rowmajor_run(n, cnt, LinvT, ldp, xin, ldin, xbar_work, np, s);
+  int rc = gg::trsm_packed_run(n, cnt, LinvP, xin, ldin, xbar_work, np, s);
   if (rc != GG_OK) return rc;
   return gg::epilogue_run(n, cnt, q, xbar_work, np, XLbar, np, ybar, S_TL, b_T, beta, status,
                           sinv, s);

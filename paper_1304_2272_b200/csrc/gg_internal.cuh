@@ -59,6 +59,10 @@ size_t trtri_ws_bytes(int n);
 // ---- TMA/DMMA streamed TRSM (trsm_tma.cu) -------------------------------------------------
 int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,
                       double* X, int ldx, cudaStream_t s);
+int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int ldb, double* X,
+                    int ldx, cudaStream_t s);
+size_t packed_lower_elems(int n);
+int pack_lower_run(int n, const double* A, int lda, int row_major, double* P, cudaStream_t s);
 int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, cudaStream_t s);
 
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------

@@ -81,6 +81,15 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c[0]), "+d"(c[1])
@@ -98,6 +107,10 @@ __device__ __forceinline__ int tile_of(int r, int b, int G) {
   return r * G + ((r & 1) ? (G - 1 - b) : b);
 }
 
+// PACKED = false: A is the full row-major inverse (2D map, box at (k, m)).
+// PACKED = true : A is the packed tile-major lower inverse (3D map over 128 x 16 tiles, tile index
+//                 4*mt*(mt+1) + kt; only the tiles on or below the diagonal exist).
+template <bool PACKED>
 __global__ void __launch_bounds__(THREADS, 1)
     trsm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     TrsmArgs a) {
@@ -142,7 +155,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const unsigned fb = full0 + 8 * stage;
           mbar_expect_tx(fb, STAGE_BYTES);
           const unsigned dA = sbase + stage * STAGE_BYTES;
-          tma_load_2d(dA, &tmA, fb, kt * BK, mt * BM);
+          if (PACKED) tma_load_3d(dA, &tmA, fb, 0, 0, 4 * mt * (mt + 1) + kt);
+          else tma_load_2d(dA, &tmA, fb, kt * BK, mt * BM);
           tma_load_2d(dA + TILE_BYTES, &tmB, fb, kt * BK, nt * BN);
           if (++stage == STAGES) {
             stage = 0;
@@ -276,6 +290,26 @@ __global__ void transpose_kernel(int np, const double* __restrict__ A, long long
     T[(long long)(by + j) * ldt + bx + threadIdx.x] = tile[threadIdx.x][j];
 }
 
+// col-major (or row-major) lower inverse -> packed tile-major 128 x 16 tiles (k contiguous)
+__global__ void pack_lower_kernel(int np, const double* __restrict__ A, long long ld, int row_major,
+                                  double* __restrict__ P) {
+  const int nmt = np / BM;
+  const long long ntile = 4LL * nmt * (nmt + 1);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ntile * 2048;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long t = e >> 11;
+    const int within = (int)(e & 2047), r = within >> 4, kk = within & 15;
+    // invert t = 4*mt*(mt+1) + kt with 0 <= kt < 8*(mt+1)
+    int mt = (int)((sqrt(1.0 + (double)t) - 1.0) / 2.0);
+    while (4LL * (mt + 1) * (mt + 2) <= t) ++mt;
+    while (4LL * mt * (mt + 1) > t) --mt;
+    const int kt = (int)(t - 4LL * mt * (mt + 1));
+    const long long i = (long long)mt * BM + r, k = (long long)kt * BK + kk;
+    const double v = (k <= i) ? (row_major ? A[k + i * ld] : A[i + k * ld]) : 0.0;
+    P[e] = v;
+  }
+}
+
 int sm_count() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -296,6 +330,85 @@ int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, c
   return GG_OK;
 }
 
+size_t packed_lower_elems(int n) {
+  const long long nmt = pad_rows(n) / BM;
+  return (size_t)(4LL * nmt * (nmt + 1)) * 2048;
+}
+
+int pack_lower_run(int n, const double* A, int lda, int row_major, double* P, cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (lda < np) {
+    set_error("pack_lower: lda must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  long long grid = ((long long)packed_lower_elems(n) + 255) / 256;
+  if (grid > 148LL * 64) grid = 148LL * 64;
+  pack_lower_kernel<<<(int)grid, 256, 0, s>>>(np, A, lda, row_major, P);
+  GG_LAUNCH_CHECK("pack_lower_kernel");
+  return GG_OK;
+}
+
+static int make_packed_map(CUtensorMap* map, const double* base, long long ntiles) {
+  auto fn = encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return GG_ECUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)BK, (cuuint64_t)BM, (cuuint64_t)ntiles};
+  cuuint64_t strides[2] = {(cuuint64_t)BK * sizeof(double), (cuuint64_t)BK * BM * sizeof(double)};
+  cuuint32_t box[3] = {BK, BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (packed) failed (code " + std::to_string((int)r) + ")");
+    return GG_ECUDA;
+  }
+  return GG_OK;
+}
+
+template <bool PACKED>
+static int launch_trsm(const CUtensorMap& mA, const CUtensorMap& mB, int np, int nrhs, double* X,
+                       int ldx, cudaStream_t s) {
+  TrsmArgs a;
+  a.N = nrhs;
+  a.num_mt = np / BM;
+  a.num_nt = (nrhs + BN - 1) / BN;
+  a.C = X;
+  a.ldc = ldx;
+  const int tiles = a.num_mt * a.num_nt;
+  int grid = sm_count();
+  if (grid > tiles) grid = tiles;
+  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_tma_kernel<PACKED>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+  trsm_tma_kernel<PACKED><<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
+  GG_LAUNCH_CHECK("trsm_tma_kernel");
+  return GG_OK;
+}
+
+int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int ldb, double* X,
+                    int ldx, cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (ldb < np || ldx < np) {
+    set_error("trsm: leading dimensions must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  if (nrhs <= 0) return GG_OK;
+  if ((reinterpret_cast<uintptr_t>(LinvP) | reinterpret_cast<uintptr_t>(B) |
+       reinterpret_cast<uintptr_t>(X)) & 15) {
+    set_error("trsm: operands must be 16-byte aligned");
+    return GG_EARG;
+  }
+  CUtensorMap mA, mB;
+  const long long nmt = np / BM;
+  int rc = make_packed_map(&mA, LinvP, 4LL * nmt * (nmt + 1));
+  if (rc != GG_OK) return rc;
+  rc = make_kmajor_map(&mB, B, np, nrhs, ldb);
+  if (rc != GG_OK) return rc;
+  return launch_trsm<true>(mA, mB, np, nrhs, X, ldx, s);
+}
+
 int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,
                       double* X, int ldx, cudaStream_t s) {
   const int np = pad_rows(n);
@@ -314,20 +427,7 @@ int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const doubl
   if (rc != GG_OK) return rc;
   rc = make_kmajor_map(&mB, B, np, nrhs, ldb);
   if (rc != GG_OK) return rc;
-  TrsmArgs a;
-  a.N = nrhs;
-  a.num_mt = np / BM;
-  a.num_nt = (nrhs + BN - 1) / BN;
-  a.C = X;
-  a.ldc = ldx;
-  const int tiles = a.num_mt * a.num_nt;
-  int grid = sm_count();
-  if (grid > tiles) grid = tiles;
-  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)SMEM_BYTES));
-  trsm_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
-  GG_LAUNCH_CHECK("trsm_tma_kernel");
-  return GG_OK;
+  return launch_trsm<false>(mA, mB, np, nrhs, X, ldx, s);
 }
 
 }  // namespace gg

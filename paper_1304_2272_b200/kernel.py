@@ -27,7 +27,6 @@ from ._device import (
     alloc_cols,
     download_cols,
     upload_cols,
-    transpose_square,
     upload_square_identity_padded,
 )
 from .errors import DimensionMismatch, NotPositiveDefinite, RankDeficientCovariates
@@ -194,9 +193,20 @@ class PreparedContext:
 # factorisation and triangular solves
 # ---------------------------------------------------------------------------------------------
 
-def _potrf_device(M):
-    """Device Cholesky + inverse of the n x n host matrix M; returns (n, L_dev, LinvT_dev) with
-    the inverse stored row-major (the K-major operand of the TMA TRSM)."""
+def _pack_lower(Linv_colmajor, n):
+    """Square column-major inverse -> packed tile-major lower tiles (the TRSM's A operand)."""
+    torch = __import__("torch")
+    P = torch.empty(int(_capi.lib().gg_packed_lower_bytes(n)) // 8, dtype=torch.float64,
+                    device=Linv_colmajor.device)
+    check(_capi.lib().gg_pack_lower_f64(n, ptr(Linv_colmajor), Linv_colmajor.shape[1], 0, ptr(P),
+                                        stream_handle()), "gg_pack_lower_f64")
+    return P
+
+
+def _potrf_device(M, keep_square_inverse=False):
+    """Device Cholesky + inverse of the n x n matrix M (host array, or CUDA tensor read
+    row-major); returns (n, L_dev, LinvP_dev) with the inverse in the packed tile-major layout
+    (the A operand of the TMA TRSM), plus the square column-major inverse if asked."""
     torch = __import__("torch")
     n = M.shape[0]
     np_ = pad(n)
@@ -218,9 +228,11 @@ def _potrf_device(M):
             raise NotPositiveDefinite(int(info[0]), "non-finite entry in covariance")
         raise NotPositiveDefinite(int(info[0]))
     check(rc, "gg_potrf_f64")
-    LinvT = transpose_square(Linv)
+    LinvP = _pack_lower(Linv, n)
+    if keep_square_inverse:
+        return n, L, LinvP, Linv
     del Linv
-    return n, L, LinvT
+    return n, L, LinvP
 
 
 def cholesky_spd(M):
@@ -236,7 +248,7 @@ def cholesky_spd(M):
 
 
 def _trtri_device(L):
-    """Device inverse of a host lower-triangular L; returns (n, LinvT_dev) (row-major)."""
+    """Device inverse of a host lower-triangular L; returns (n, LinvP_dev) (packed tiles)."""
     torch = __import__("torch")
     n = L.shape[0]
     np_ = pad(n)
@@ -246,15 +258,16 @@ def _trtri_device(L):
                      device=Ld.device)
     check(_capi.lib().gg_trtri_lower_f64(n, ptr(Ld), np_, ptr(Linv), np_, ptr(ws),
                                          stream_handle()), "gg_trtri_lower_f64")
-    return n, transpose_square(Linv)
+    return n, _pack_lower(Linv, n)
 
 
-def _trsm_device(dLinvT, n, B_dev, nrhs):
-    """X = L^-1 B on the device (TMA/DMMA kernel; LinvT is the row-major inverse)."""
+def _trsm_device(dLinvP, n, B_dev, nrhs):
+    """X = L^-1 B on the device (TMA/DMMA kernel; LinvP is the packed inverse)."""
     np_ = pad(n)
     X = alloc_cols(nrhs, np_, zero=False)
-    check(_capi.lib().gg_trsm_lower_rm_f64(n, nrhs, ptr(dLinvT), np_, ptr(B_dev), B_dev.shape[1],
-                                           ptr(X), np_, stream_handle()), "gg_trsm_lower_rm_f64")
+    check(_capi.lib().gg_trsm_lower_packed_f64(n, nrhs, ptr(dLinvP), ptr(B_dev), B_dev.shape[1],
+                                               ptr(X), np_, stream_handle()),
+          "gg_trsm_lower_packed_f64")
     return X
 
 
@@ -270,9 +283,9 @@ def trsolve_lower(L, B):
     n, nrhs = B.shape
     if nrhs == 0:
         return np.empty((n, 0)) if not squeeze else np.empty(n)
-    _, LinvT = _trtri_device(L)
+    _, LinvP = _trtri_device(L)
     Bd = upload_cols(B, ld=pad(n))
-    X = np.asfortranarray(download_cols(_trsm_device(LinvT, n, Bd, nrhs), n, nrhs))
+    X = np.asfortranarray(download_cols(_trsm_device(LinvP, n, Bd, nrhs), n, nrhs))
     return X[:, 0] if squeeze else X
 
 
@@ -379,10 +392,10 @@ def gls_prepare(M, XL, y):
     q = XL.shape[1]
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
-    _, L, LinvT = _potrf_device(M)
+    _, L, LinvP = _potrf_device(M)
     np_ = pad(n)
     RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
-    XLy = _trsm_device(LinvT, n, RHS, q + 1)
+    XLy = _trsm_device(LinvP, n, RHS, q + 1)
     dots = _dots_device(XLy, n, q, XLy, q, XLy[q]) if q > 0 else None
     if q > 0:
         C = dots[:, :q]
@@ -407,7 +420,7 @@ def gls_prepare(M, XL, y):
     host = download_cols(XLy, n, q + 1)
     XLbar = np.asfortranarray(host[:, :q])
     ybar = np.ascontiguousarray(host[:, q])
-    dctx = DeviceContext(n=n, np_=np_, q=q, L=L, LinvT=LinvT, XLy=XLy, S_TL=S_TL_d.reshape(-1),
+    dctx = DeviceContext(n=n, np_=np_, q=q, L=L, LinvP=LinvP, XLy=XLy, S_TL=S_TL_d.reshape(-1),
                          b_T=b_T_d)
     return PreparedContext(L=None, XLbar=XLbar, ybar=ybar, S_TL=S_TL, b_T=b_T, _dev=dctx)
 
@@ -429,11 +442,11 @@ def device_context(ctx, need_factor=False):
     if d is None:
         d = DeviceContext.from_host(ctx.XLbar, ctx.ybar, ctx.S_TL, ctx.b_T)
         ctx._dev = d
-    if need_factor and d.LinvT is None:
+    if need_factor and d.LinvP is None:
         L = np.asarray(ctx.L, dtype=np.float64)
         if L.ndim != 2 or L.shape != (d.n, d.n):
             raise DimensionMismatch("context has no usable Cholesky factor for the TRSM")
-        _, d.LinvT = _trtri_device(L)
+        _, d.LinvP = _trtri_device(L)
     return d
 
 

@@ -334,9 +334,9 @@ def test_tma_trsm_bitwise_equals_cpasync_trsm(K):
 
     for n, nrhs in ((300, 257), (1000, 1), (129, 700)):
         M = make_spd(n, n)
-        _, L, LinvT = K._potrf_device(M)
+        _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
         np_ = _capi.pad(n)
-        Linv = transpose_square(LinvT)
+        LinvT = transpose_square(Linv)
         B = upload_cols(np.random.default_rng(n).standard_normal((n, nrhs)), ld=np_)
         X1 = alloc_cols(nrhs, np_)
         X2 = alloc_cols(nrhs, np_)
@@ -344,8 +344,13 @@ def test_tma_trsm_bitwise_equals_cpasync_trsm(K):
                                              stream_handle()) == 0
         assert _capi.lib().gg_trsm_lower_rm_f64(n, nrhs, ptr(LinvT), np_, ptr(B), np_, ptr(X2),
                                                 np_, stream_handle()) == 0
+        X3 = alloc_cols(nrhs, np_)
+        assert _capi.lib().gg_trsm_lower_packed_f64(n, nrhs, ptr(LinvP), ptr(B), np_, ptr(X3),
+                                                    np_, stream_handle()) == 0
         torch.cuda.synchronize()
         assert torch.equal(X1, X2)
+        assert torch.equal(X1, X3)
+        assert LinvP.numel() * 8 == _capi.lib().gg_packed_lower_bytes(n)
 
 
 def test_cholesky_reads_lower_triangle_and_checks_all_entries(K):

@@ -65,13 +65,13 @@ def main():
     beta = torch.empty((args.cnt, d.p), dtype=torch.float64, device="cuda")
     st = torch.empty((args.cnt,), dtype=torch.int32, device="cuda")
     for _ in range(2):
-        check(lib.gg_trsm_lower_rm_f64(n, args.cnt, ptr(d.LinvT), np_, ptr(X), np_, ptr(xbar), np_, s), "trsm")
+        check(lib.gg_trsm_lower_packed_f64(n, args.cnt, ptr(d.LinvP), ptr(X), np_, ptr(xbar), np_, s), "trsm")
     torch.cuda.synchronize()
     for rep in range(args.reps):
         a, b, c = ev(), ev(), ev()
         torch.cuda.nvtx.range_push("hot")
         a.record()
-        check(lib.gg_trsm_lower_rm_f64(n, args.cnt, ptr(d.LinvT), np_, ptr(X), np_, ptr(xbar), np_, s), "trsm")
+        check(lib.gg_trsm_lower_packed_f64(n, args.cnt, ptr(d.LinvP), ptr(X), np_, ptr(xbar), np_, s), "trsm")
         b.record()
         check(lib.gg_gls_epilogue_f64(n, args.cnt, d.q, ptr(xbar), np_, ptr(d.XLy), np_, ptr(d.ybar),
                                       ptr(d.S_TL), ptr(d.b_T), ptr(beta), ptr(st), None, s), "epi")
