@@ -103,6 +103,14 @@ int gg_pack_lower_f64(int n, const double* A, int lda, int row_major, double* Li
 int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double* B, int ldb,
                              double* X, int ldx, void* stream);
 
+/* Distributed (BASELINE config 4) assembly: write this rank's share of a 2D block-cyclic
+ * lower inverse (block nb, a multiple of 128; grid gr x gc; rank at (prow, pcol); local
+ * column-major, leading dimension ldloc) into a full packed buffer, zeros elsewhere.  The
+ * all-reduce sum of every rank's buffer is the packed inverse (disjoint supports: exact).
+ * Replaces the replicated-panel gathers of distgrid.py:215-233 / 317-320.                  */
+int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                                  const double* Bloc, int ldloc, double* LinvP, void* stream);
+
 /* Square transpose (np x np, np a multiple of 32): T = A^T (column-major both).
  * Turns the Linv produced by gg_potrf_f64 into the LinvT operand above.              */
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream);

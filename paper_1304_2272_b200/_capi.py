@@ -36,6 +36,7 @@ SIGNATURES = {
     "gg_trsm_lower_rm_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
     "gg_packed_lower_bytes": (_sz, [_i]),
     "gg_pack_lower_f64": (_i, [_i, _vp, _i, _i, _vp, _vp]),
+    "gg_pack_lower_blockcyclic_f64": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "gg_trsm_lower_packed_f64": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),

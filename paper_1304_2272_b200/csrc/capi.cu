@@ -100,6 +100,16 @@ int gg_pack_lower_f64(int n, const double* A, int lda, int row_major, double* Li
   return gg::pack_lower_run(n, A, lda, row_major, LinvP, as_stream(stream));
 }
 
+int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                                  const double* Bloc, int ldloc, double* LinvP, void* stream) {
+  if (n < 1 || Bloc == nullptr || LinvP == nullptr) {
+    gg::set_error("pack_lower_blockcyclic: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::pack_lower_bc_run(n, nb, grid_r, grid_c, prow, pcol, Bloc, ldloc, LinvP,
+                               as_stream(stream));
+}
+
 int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double* B, int ldb,
                              double* X, int ldx, void* stream) {
   if (n < 1 || nrhs < 0 || LinvP == nullptr || B == nullptr || X == nullptr) {

@@ -63,6 +63,8 @@ int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int l
                     int ldx, cudaStream_t s);
 size_t packed_lower_elems(int n);
 int pack_lower_run(int n, const double* A, int lda, int row_major, double* P, cudaStream_t s);
+int pack_lower_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
+                      double* P, cudaStream_t s);
 int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, cudaStream_t s);
 
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------

@@ -310,6 +310,36 @@ __global__ void pack_lower_kernel(int np, const double* __restrict__ A, long lon
   }
 }
 
+// The same packed layout assembled from one rank's share of a 2D block-cyclic inverse (block nb,
+// grid gr x gc, this rank at (pr, pc), local column-major with leading dimension ldl).  Tiles the
+// rank does not own are written as zeros, so summing every rank's buffer (an all-reduce over
+// disjoint supports) reproduces the full packed inverse exactly.
+__global__ void pack_lower_bc_kernel(int np, int nb, int gr, int gc, int pr, int pc,
+                                     const double* __restrict__ B, long long ldl,
+                                     double* __restrict__ P) {
+  const int nmt = np / BM;
+  const long long ntile = 4LL * nmt * (nmt + 1);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ntile * 2048;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long t = e >> 11;
+    const int within = (int)(e & 2047), r = within >> 4, kk = within & 15;
+    int mt = (int)((sqrt(1.0 + (double)t) - 1.0) / 2.0);
+    while (4LL * (mt + 1) * (mt + 2) <= t) ++mt;
+    while (4LL * mt * (mt + 1) > t) --mt;
+    const int kt = (int)(t - 4LL * mt * (mt + 1));
+    const long long i = (long long)mt * BM + r, k = (long long)kt * BK + kk;
+    double v = 0.0;
+    if (k <= i) {
+      const long long I = i / nb, J = k / nb;
+      if (I % gr == pr && J % gc == pc) {
+        const long long li = (I / gr) * nb + i % nb, lk = (J / gc) * nb + k % nb;
+        v = B[li + lk * ldl];
+      }
+    }
+    P[e] = v;
+  }
+}
+
 int sm_count() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
@@ -345,6 +375,19 @@ int pack_lower_run(int n, const double* A, int lda, int row_major, double* P, cu
   if (grid > 148LL * 64) grid = 148LL * 64;
   pack_lower_kernel<<<(int)grid, 256, 0, s>>>(np, A, lda, row_major, P);
   GG_LAUNCH_CHECK("pack_lower_kernel");
+  return GG_OK;
+}
+
+int pack_lower_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
+                      double* P, cudaStream_t s) {
+  if (nb < BM || nb % BM != 0 || gr < 1 || gc < 1 || pr < 0 || pr >= gr || pc < 0 || pc >= gc) {
+    set_error("pack_lower_blockcyclic: nb must be a multiple of 128 and (pr, pc) inside the grid");
+    return GG_EARG;
+  }
+  long long grid = ((long long)packed_lower_elems(n) + 255) / 256;
+  if (grid > 148LL * 64) grid = 148LL * 64;
+  pack_lower_bc_kernel<<<(int)grid, 256, 0, s>>>(pad_rows(n), nb, gr, gc, pr, pc, B, ldl, P);
+  GG_LAUNCH_CHECK("pack_lower_bc_kernel");
   return GG_OK;
 }
 

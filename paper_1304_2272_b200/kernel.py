@@ -393,17 +393,30 @@ def gls_prepare(M, XL, y):
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
     _, L, LinvP = _potrf_device(M)
+    return prepare_from_inverse(LinvP, n, XL, y, L=L)
+
+
+def prepare_from_inverse(LinvP, n, XL, y, L=None):
+    """The marker-independent tail of gls_prepare (kernel.py:246-257) given the packed inverse:
+    whiten [X_L | y] with the streamed TRSM kernel, S_TL = gram(X_L bar) and b_T with the
+    per-SNP reduction kernel, SPD check of S_TL.  Shared by gls_prepare and the distributed
+    engine (whose factor exists only block-cyclically, so L may be None)."""
+    torch = __import__("torch")
+    XL = np.asarray(XL, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64).ravel()
+    q = XL.shape[1]
     np_ = pad(n)
     RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
     XLy = _trsm_device(LinvP, n, RHS, q + 1)
+    dev = XLy.device
     dots = _dots_device(XLy, n, q, XLy, q, XLy[q]) if q > 0 else None
     if q > 0:
         C = dots[:, :q]
         S_TL_d = (torch.tril(C) + torch.tril(C, -1).T).contiguous()
         b_T_d = dots[:, q + 1].contiguous()
-        x = torch.empty((1, q), dtype=torch.float64, device=L.device)
-        st = torch.empty((1,), dtype=torch.int32, device=L.device)
-        zero = torch.zeros((1, q), dtype=torch.float64, device=L.device)
+        x = torch.empty((1, q), dtype=torch.float64, device=dev)
+        st = torch.empty((1,), dtype=torch.int32, device=dev)
+        zero = torch.zeros((1, q), dtype=torch.float64, device=dev)
         check(_capi.lib().gg_small_spd_solve_f64(1, q, ptr(S_TL_d), ptr(zero), ptr(x), ptr(st),
                                                  None, stream_handle()),
               "gg_small_spd_solve_f64")
@@ -414,8 +427,8 @@ def gls_prepare(M, XL, y):
         S_TL = S_TL_d.cpu().numpy().reshape(q, q)
         b_T = b_T_d.cpu().numpy()
     else:
-        S_TL_d = torch.zeros((0,), dtype=torch.float64, device=L.device)
-        b_T_d = torch.zeros((0,), dtype=torch.float64, device=L.device)
+        S_TL_d = torch.zeros((0,), dtype=torch.float64, device=dev)
+        b_T_d = torch.zeros((0,), dtype=torch.float64, device=dev)
         S_TL, b_T = np.zeros((0, 0)), np.zeros(0)
     host = download_cols(XLy, n, q + 1)
     XLbar = np.asfortranarray(host[:, :q])

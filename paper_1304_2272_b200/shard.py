@@ -10,6 +10,8 @@ collective:
   * each rank streams its blocks through its own double-buffered engine and writes its GWAB
     records at their global offsets (the reference's ranks do the same, distgrid.py:390-446);
   * the only synchronisation is a host barrier around file creation and completion.
+The same ``stream_shard`` runs the sweep of the distributed engine (distgrid.run_dist), whose
+ranks share a replicated packed inverse.
 """
 
 from __future__ import annotations
@@ -20,13 +22,26 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import fileio, kernel
-from .pipeline import RunSummary, block_plan, stream_file_blocks, _load_prepare
+from .pipeline import RunSummary, _load_prepare, block_plan, stream_file_blocks
 
 
 @dataclass
 class ShardConfig:
     m_blk: int = 8192
     emit_s_inv: bool = False
+
+
+@dataclass
+class ShardStats:
+    m: int
+    m_blk: int
+    t_compute: float
+    t_io_wait: float
+    t_loop: float
+    t_device: float
+    bytes_read: int
+    bytes_written: int
+    snps_per_s: float
 
 
 def shard_blocks(m, m_blk, rank, world):
@@ -49,25 +64,19 @@ def _barrier(dist):
         dist.barrier()
 
 
-def run_sharded(paths, cfg=None, prepare_fn=None, solve_fn=None):
-    """SPMD body: call on every rank.  Returns a RunSummary carrying the job totals.
+def stream_shard(paths, ctx, cfg=None, solve_fn=None):
+    """Stream this rank's share of the marker blocks of ``paths.geno`` against ``ctx`` and write
+    their records at global offsets of ``paths.out`` (rank 0 creates the file).  Collective over
+    the initialised process group; returns job-level ShardStats on every rank.
 
-    prepare_fn(paths) -> ctx and solve_fn(ctx, data, first) -> kernel.ResultArrays are
-    injection points for the CPU tests of the sharding logic; by default the rank's GPU runs
-    gls_prepare and the double-buffered device stream."""
+    solve_fn(ctx, data, first) -> kernel.ResultArrays replaces the device stream in the CPU
+    tests of the sharding logic."""
     cfg = cfg or ShardConfig()
     dist = _dist()
     rank = dist.get_rank() if dist else 0
     world = dist.get_world_size() if dist else 1
-    t_start = time.perf_counter()
     _, n, m = fileio.total_genotype_bytes(paths.geno)
     m_blk = min(cfg.m_blk, m)
-    if prepare_fn is None:
-        ctx, t_prep, _ = _load_prepare(paths)
-    else:
-        t0 = time.perf_counter()
-        ctx = prepare_fn(paths)
-        t_prep = time.perf_counter() - t0
     p = ctx.p
     flags = 1 if cfg.emit_s_inv else 0
     if rank == 0:
@@ -102,18 +111,40 @@ def run_sharded(paths, cfg=None, prepare_fn=None, solve_fn=None):
         writer.close()
     _barrier(dist)
     stats = dict(bytes_read=reader.bytes_read, bytes_written=writer.bytes_written,
-                 t_loop=t_loop, t_dev=t_dev, snps=sum(c for _, c in mine))
+                 t_loop=t_loop, t_dev=t_dev)
     if dist is not None:
         allst = [None] * world
         dist.all_gather_object(allst, stats)
     else:
         allst = [stats]
     t_max = max(s["t_loop"] for s in allst)
+    return ShardStats(m=m, m_blk=m_blk, t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io,
+                      t_loop=t_loop, t_device=max(s["t_dev"] for s in allst),
+                      bytes_read=sum(s["bytes_read"] for s in allst),
+                      bytes_written=sum(s["bytes_written"] for s in allst),
+                      snps_per_s=m / t_max if t_max > 0 else 0.0)
+
+
+def run_sharded(paths, cfg=None, prepare_fn=None, solve_fn=None):
+    """SPMD body: call on every rank.  Redundant gls_prepare on the rank's GPU, then
+    ``stream_shard``.  Returns a RunSummary carrying the job totals.
+
+    prepare_fn(paths) -> ctx and solve_fn are injection points for the CPU tests."""
+    cfg = cfg or ShardConfig()
+    dist = _dist()
+    world = dist.get_world_size() if dist else 1
+    t_start = time.perf_counter()
+    _, n, m = fileio.total_genotype_bytes(paths.geno)
+    if prepare_fn is None:
+        ctx, t_prep, _ = _load_prepare(paths)
+    else:
+        t0 = time.perf_counter()
+        ctx = prepare_fn(paths)
+        t_prep = time.perf_counter() - t0
+    s = stream_shard(paths, ctx, cfg, solve_fn=solve_fn)
     return RunSummary(
-        mode="sharded", n=n, m=m, p=p, m_blk=m_blk, np_=world, threads=1, t_prepare=t_prep,
-        t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io,
-        t_total=time.perf_counter() - t_start,
-        bytes_read=sum(s["bytes_read"] for s in allst),
-        bytes_written=sum(s["bytes_written"] for s in allst),
-        buffer_regions=2, gpus=world, t_device=max(s["t_dev"] for s in allst),
-        snps_per_s=m / t_max if t_max > 0 else 0.0)
+        mode="sharded", n=n, m=m, p=ctx.p, m_blk=s.m_blk, np_=world, threads=1,
+        t_prepare=t_prep, t_compute=s.t_compute, t_io_wait=s.t_io_wait,
+        t_total=time.perf_counter() - t_start, bytes_read=s.bytes_read,
+        bytes_written=s.bytes_written, buffer_regions=2, gpus=world, t_device=s.t_device,
+        snps_per_s=s.snps_per_s)

@@ -1,0 +1,60 @@
+"""GPU: the distributed (config-4) engine with the sm_100a kernels on one rank (grid 1x1; the
+multi-rank communication logic is covered over gloo in tests/test_distgrid_gloo.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, make_spd, write_golden_dataset
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_dist_factor_inverse_pack(gpu):
+    from scipy.linalg import cholesky, solve_triangular
+
+    from paper_1304_2272_b200 import distgrid, kernel
+
+    n, nb = 1000, 256
+    M = make_spd(n, 3)
+    ops = distgrid.DeviceOps()
+    lay = distgrid.BlockCyclic(n, nb, distgrid.grid_create(1), 0)
+    A, B = distgrid.local_from_global(M, lay, ops)
+    distgrid.dist_potrf_inv(A, B, lay, ops)
+    L = distgrid.gather_matrix(A, lay, ops)
+    Li = distgrid.gather_matrix(B, lay, ops)
+    Lr = cholesky(M, lower=True)
+    Lir = solve_triangular(Lr, np.eye(n), lower=True)
+    assert np.max(np.abs(L - Lr)) <= 1e-13 * np.max(np.abs(Lr))
+    assert np.max(np.abs(Li - Lir)) <= 1e-12 * np.max(np.abs(Lir))
+    P = distgrid.assemble_packed_inverse(B, lay, ops)
+    _, _, P1 = kernel._potrf_device(M)
+    assert P.shape == P1.shape
+    assert float((P - P1).abs().max()) <= 1e-12 * float(P1.abs().max())
+
+
+def test_device_dist_not_pd(gpu):
+    from paper_1304_2272_b200 import distgrid
+    from paper_1304_2272_b200.errors import NotPositiveDefinite
+
+    M = make_spd(600, 4)
+    M[450, 450] = -1.0
+    ops = distgrid.DeviceOps()
+    lay = distgrid.BlockCyclic(600, 128, distgrid.grid_create(1), 0)
+    A, B = distgrid.local_from_global(M, lay, ops)
+    with pytest.raises(NotPositiveDefinite) as e:
+        distgrid.dist_potrf_inv(A, B, lay, ops)
+    assert e.value.pivot_index == 450
+
+
+@pytest.mark.parametrize("case", ["baseline_p4", "degenerate"])
+def test_run_dist_end_to_end(gpu, tmp_path, case):
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import distgrid, fileio
+
+    g = golden(case)
+    paths = write_golden_dataset(tmp_path, g)
+    s = distgrid.run_dist(paths, distgrid.DistConfig(m_blk=257, nb=128))
+    assert s.mode == "dist" and s.np_ == 1
+    pay = fileio.read_matrix(paths.out, "GWAB")
+    rel, mism = O.compare(pay.betas, g["beta"])
+    assert mism == 0 and rel <= 1e-9
