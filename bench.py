@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-dtype", choices=["f64", "i8"], default="f64")
+    ap.add_argument("--resident", choices=["f64", "i8"], default=None,
+                    help="genotype storage in HBM (default: FP64 if it fits, else int8)")
     return ap.parse_args()
 
 
@@ -168,16 +170,27 @@ def run_ours(args):
     d = ctx._dev
     M = Md.cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     del Md
-    X = torch.empty((m, np_), dtype=torch.float64, device=dev)
-    X[:, n:].zero_()
-    G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
+    # genotypes resident in HBM: FP64 (config 1) when they fit, else int8 {0,1,2} dosages widened
+    # block by block inside the step (config 2/3 storage format)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    resident = args.resident or ("f64" if 8 * m * np_ < 0.6 * free_b else "i8")
     first_marker = rank * m
-    for j0 in range(0, m, m_blk):
-        cnt = min(m_blk, m - j0)
-        datagen.genotypes_device(spec, first_marker + j0, cnt, out=G)
-        check(lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(X[j0:]), np_,
-                                  _capi.stream_handle()), "widen")
-    del G
+    if resident == "f64":
+        X = torch.empty((m, np_), dtype=torch.float64, device=dev)
+        X[:, n:].zero_()
+        G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
+        for j0 in range(0, m, m_blk):
+            cnt = min(m_blk, m - j0)
+            datagen.genotypes_device(spec, first_marker + j0, cnt, out=G)
+            check(lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(X[j0:]), np_,
+                                      _capi.stream_handle()), "widen")
+        del G
+        Gres, xin = None, None
+    else:
+        Gres = datagen.genotypes_device(spec, first_marker, m)          # (m, n) int8
+        xin = torch.empty((m_blk, np_), dtype=torch.float64, device=dev)
+        xin[:, n:].zero_()
+        X = None
     xbar = torch.empty((m_blk, np_), dtype=torch.float64, device=dev)
     beta = torch.empty((m, p), dtype=torch.float64, device=dev)
     status = torch.empty((m,), dtype=torch.int32, device=dev)
@@ -191,7 +204,14 @@ def run_ours(args):
         for i, (f, c) in enumerate(plan):
             if record:
                 ev_pairs[i][0].record(stream)
-            rc = lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(X[f]), np_, ptr(xbar), np_,
+            if X is not None:
+                src = X[f]
+            else:
+                rc0 = lib.gg_widen_i8_f64(n, c, ptr(Gres[f]), n, ptr(xin), np_, sh)
+                if rc0:
+                    raise RuntimeError(_capi.last_error())
+                src = xin
+            rc = lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(src), np_, ptr(xbar), np_,
                                               sh)
             if record:
                 ev_pairs[i][1].record(stream)
@@ -243,14 +263,15 @@ def run_ours(args):
     # ---- e2e through the public stream API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist if use_dist else None,
-                      pipeline)
+        e2e = run_e2e(args, ctx, X if X is not None else Gres, n, m, world, rank, dev, np, torch,
+                      dist if use_dist else None, pipeline)
 
     # ---- CPU baseline + sampled parity on rank 0 at N = 1 -----------------------------------
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, parity = run_cpu_baseline(M, XL, y, X, n, beta, status, np)
+        cpu, parity = run_cpu_baseline(M, XL, y, X if X is not None else Gres, n, beta, status,
+                                       np)
 
     if rank == 0:
         line = {
@@ -264,8 +285,10 @@ def run_ours(args):
                             f"over all m SNPs",
                 "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": m_blk,
                 "blocks_per_step": len(plan), "parallelism": f"snp-shard x{world}",
-                "l2": "inputs larger than L2 (FP64 genotypes resident in HBM: "
-                      f"{m * np_ * 8 / 1e9:.1f} GB per GPU)",
+                "resident": resident,
+                "l2": "inputs larger than L2 (genotypes resident in HBM: "
+                      f"{m * (np_ * 8 if resident == 'f64' else n) / 1e9:.1f} GB per GPU, "
+                      f"{'FP64' if resident == 'f64' else 'int8, widened per block in the step'})",
                 "t_prepare_s": round(t_prepare, 4),
                 "prepare_device_ms": round(prepare_ms_device, 2),
                 "t_generate_M_s": round(t_gen_m, 2),
@@ -281,7 +304,7 @@ def run_ours(args):
                 "peak_source": FP64_PEAK_SOURCE,
                 "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
             },
-            "gpu_launches": 2 * len(plan) * args.steps,
+            "gpu_launches": (2 if resident == "f64" else 3) * len(plan) * args.steps,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -306,15 +329,16 @@ def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
             dtype = "i8"
     except ImportError:
         pass
+    src = X[:, :n] if X.dtype == torch.float64 else X           # (m, n) FP64 view or int8
     try:
-        if dtype == "f64":
+        if dtype == "f64" and X.dtype == torch.float64:
             host_t = torch.empty((m, n), dtype=torch.float64).pin_memory()
-            host_t.copy_(X[:, :n])
+            host_t.copy_(src)
         else:
-            raise RuntimeError("int8 requested")
+            raise RuntimeError("int8 host genotypes")
     except RuntimeError:
         host_t = torch.empty((m, n), dtype=torch.int8).pin_memory()
-        host_t.copy_(X[:, :n].to(torch.int8))
+        host_t.copy_(src.to(torch.int8))
     Xh = host_t.numpy().T                     # n x m, Fortran-ordered view of pinned memory
     int8 = Xh.dtype == np.int8
     engine = pipeline.StreamEngine(ctx, args.block_snps, int8=int8)
@@ -359,7 +383,7 @@ def run_cpu_baseline(M, XL, y, X, n, beta, status, np):
     from oracle import gls_ref as O
 
     S = CPU_SAMPLE_SNPS
-    Xs = X[:S, :n].cpu().numpy().T.copy(order="F")
+    Xs = X[:S, :n].double().cpu().numpy().T.copy(order="F")
     t0 = time.perf_counter()
     octx = O.gls_prepare(M, XL, y)
     t_prep = time.perf_counter() - t0

@@ -184,8 +184,8 @@ int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s) {
     set_error("dgemm: op(B)=B^T needs an even column count");
     return GG_EDIM;
   }
-  if ((a.flags & GEMM_C_LOWER) && a.N != a.M) {
-    set_error("dgemm: lower-only output needs a square C");
+  if ((a.flags & GEMM_C_LOWER) && a.N > a.M) {
+    set_error("dgemm: lower-only output needs N <= M (C anchored on the diagonal)");
     return GG_EDIM;
   }
   if (a.M == 0 || a.N == 0) return GG_OK;

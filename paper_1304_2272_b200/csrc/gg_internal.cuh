@@ -31,7 +31,8 @@ inline int pad_rows(int n) { return ((n + GG_TILE - 1) / GG_TILE) * GG_TILE; }
 enum GemmFlags : int {
   GEMM_A_LOWER = 1,   // A lower triangular: row tile mt only needs k < (mt+1)*BM
   GEMM_B_LOWER = 2,   // op(B) lower triangular (k >= n): column tile nt needs k >= nt*BN
-  GEMM_C_LOWER = 4,   // only tiles on/below the diagonal are computed (SYRK)
+  GEMM_C_LOWER = 4,   // only tiles on/below the diagonal are computed (SYRK; C's origin on
+                      // the diagonal, N <= M)
 };
 
 struct GemmArgs {

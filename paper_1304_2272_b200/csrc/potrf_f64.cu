@@ -21,6 +21,7 @@ namespace gg {
 namespace {
 
 constexpr int NB = 128;
+constexpr int OUTER = 4 * NB;   // outer block width of the two-level Cholesky
 constexpr int LEAF_THREADS = 512;
 constexpr size_t LEAF_SMEM = 0;   // register-resident leaf (static shared only)
 
@@ -311,33 +312,58 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
     cudaEventElapsedTime(&ms, a, b);
     acc += ms;
   };
-  for (int k = 0; k < np; k += NB) {
-    if (timing) cudaEventRecord(ev[0], s);
-    leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
-    GG_LAUNCH_CHECK("potrf leaf_kernel");
-    lap(t_leaf, ev[0], ev[1]);
-    const int rem = np - k - NB;
+  // Two-level right-looking blocking: outer block columns of OUTER (= 4 leaves); inside one,
+  // leaf + panel + an update restricted to the outer block's columns; after it, one trailing
+  // SYRK of depth OUTER (4x the arithmetic intensity of a depth-128 update).
+  for (int K0 = 0; K0 < np; K0 += OUTER) {
+    const int w = (np - K0 < OUTER) ? (np - K0) : OUTER;
+    for (int k = K0; k < K0 + w; k += NB) {
+      if (timing) cudaEventRecord(ev[0], s);
+      leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
+      GG_LAUNCH_CHECK("potrf leaf_kernel");
+      lap(t_leaf, ev[0], ev[1]);
+      const int rem = np - k - NB;          // rows below this leaf
+      if (rem <= 0) break;
+      const int rem_in = K0 + w - k - NB;   // columns of the outer block right of this leaf
+      // P = A21 Dinv^T (all rows below), written back into L's column block
+      GemmArgs pan{};
+      pan.M = rem; pan.N = NB; pan.K = NB;
+      pan.A = L + (k + NB) + (long long)k * ldp; pan.lda = ldp;
+      pan.B = Linv + k + (long long)k * ldp; pan.ldb = ldp;
+      pan.C = P; pan.ldc = np;
+      pan.alpha = 1.0; pan.beta = 0.0; pan.flags = 0; pan.abort_flag = &hdr->info;
+      int rc = launch_dgemm(pan, true, s);
+      if (rc != GG_OK) return rc;
+      GG_CUDA_TRY(cudaMemcpy2DAsync(L + (k + NB) + (long long)k * ldp,
+                                    (size_t)ldp * sizeof(double), P, (size_t)np * sizeof(double),
+                                    (size_t)rem * sizeof(double), NB, cudaMemcpyDeviceToDevice, s));
+      lap(t_pan, ev[1], ev[2]);
+      if (rem_in > 0) {
+        // update only the outer block's remaining columns: A[k+NB:, k+NB:K0+w] -= P P[:rem_in]^T
+        GemmArgs upd{};
+        upd.M = rem; upd.N = rem_in; upd.K = NB;
+        upd.A = P; upd.lda = np;
+        upd.B = P; upd.ldb = np;
+        upd.C = L + (k + NB) + (long long)(k + NB) * ldp; upd.ldc = ldp;
+        upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
+        rc = launch_dgemm(upd, true, s);
+        if (rc != GG_OK) return rc;
+      }
+      lap(t_upd, ev[2], ev[3]);
+    }
+    const int rem = np - K0 - w;
     if (rem <= 0) break;
-    GemmArgs pan{};
-    pan.M = rem; pan.N = NB; pan.K = NB;
-    pan.A = L + (k + NB) + (long long)k * ldp; pan.lda = ldp;
-    pan.B = Linv + k + (long long)k * ldp; pan.ldb = ldp;
-    pan.C = P; pan.ldc = np;
-    pan.alpha = 1.0; pan.beta = 0.0; pan.flags = 0; pan.abort_flag = &hdr->info;
-    int rc = launch_dgemm(pan, true, s);
-    if (rc != GG_OK) return rc;
-    lap(t_pan, ev[1], ev[2]);
+    if (timing) cudaEventRecord(ev[2], s);
+    // trailing SYRK of depth w: A22 -= L21 L21^T, L21 = L[K0+w:, K0:K0+w] (read in place;
+    // disjoint from the updated region), lower tiles only
     GemmArgs upd{};
-    upd.M = rem; upd.N = rem; upd.K = NB;
-    upd.A = P; upd.lda = np;
-    upd.B = P; upd.ldb = np;
-    upd.C = L + (k + NB) + (long long)(k + NB) * ldp; upd.ldc = ldp;
+    upd.M = rem; upd.N = rem; upd.K = w;
+    upd.A = L + (K0 + w) + (long long)K0 * ldp; upd.lda = ldp;
+    upd.B = L + (K0 + w) + (long long)K0 * ldp; upd.ldb = ldp;
+    upd.C = L + (K0 + w) + (long long)(K0 + w) * ldp; upd.ldc = ldp;
     upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
-    rc = launch_dgemm(upd, true, s);
+    int rc = launch_dgemm(upd, true, s);
     if (rc != GG_OK) return rc;
-    GG_CUDA_TRY(cudaMemcpy2DAsync(L + (k + NB) + (long long)k * ldp, (size_t)ldp * sizeof(double), P,
-                                  (size_t)np * sizeof(double), (size_t)rem * sizeof(double), NB,
-                                  cudaMemcpyDeviceToDevice, s));
     lap(t_upd, ev[2], ev[3]);
   }
   if (timing) cudaEventRecord(ev[0], s);
