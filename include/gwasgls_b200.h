@@ -111,6 +111,27 @@ int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double*
 int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
                                   const double* Bloc, int ldloc, double* LinvP, void* stream);
 
+/* ---- The int8 tensor-core TRSM for dosage blocks ------------------------------------------
+ * Dosages are exact int8, so X = L^-1 G runs on tcgen05.mma.kind::i8 with the inverse split
+ * error-free into gg_i8_slices() int8 slices per row:
+ *     Linv[i,k] = 2^expo[i] * sum_s a_s[i,k] 2^(-7 s)      (truncation residual < 2^(expo-56))
+ * Each slice product is an exact int32 integer; the slices are recombined in FP64 in a fixed
+ * order (per-column results independent of the column's position).
+ *   gg_slice_inverse_i8 : row-major inverse LinvT (see gg_trsm_lower_rm_f64) -> slices
+ *                         (gg_inverse_slices_bytes(n) bytes, [slice][row][k]) + expo (np ints).
+ *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg); *bad_dev |= 1 if
+ *                         any value is not an integer in [-127, 127] (device flag).
+ *   gg_trsm_lower_i8    : X (np x nrhs FP64, ldx) = L^-1 G for int8 G (n x nrhs, ldg a multiple
+ *                         of 16, 16-byte aligned).                                            */
+int gg_i8_slices(void);
+size_t gg_inverse_slices_bytes(int n);
+int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
+                        void* stream);
+int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
+                     int* bad_dev, void* stream);
+int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
+                     long long ldg, double* X, int ldx, void* stream);
+
 /* Square transpose (np x np, np a multiple of 32): T = A^T (column-major both).
  * Turns the Linv produced by gg_potrf_f64 into the LinvT operand above.              */
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream);

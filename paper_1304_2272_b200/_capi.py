@@ -38,6 +38,11 @@ SIGNATURES = {
     "gg_pack_lower_f64": (_i, [_i, _vp, _i, _i, _vp, _vp]),
     "gg_pack_lower_blockcyclic_f64": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "gg_trsm_lower_packed_f64": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp]),
+    "gg_i8_slices": (_i, []),
+    "gg_inverse_slices_bytes": (_sz, [_i]),
+    "gg_slice_inverse_i8": (_i, [_i, _vp, _i, _vp, _vp, _vp]),
+    "gg_narrow_f64_i8": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),
+    "gg_trsm_lower_i8": (_i, [_i, _i, _vp, _vp, _vp, _ll, _vp, _i, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
     "gg_widen_i8_f64": (_i, [_i, _i, _vp, _ll, _vp, _i, _vp]),

@@ -123,6 +123,40 @@ int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double*
   return gg::trsm_packed_run(n, nrhs, LinvP, B, ldb, X, ldx, as_stream(stream));
 }
 
+int gg_i8_slices(void) { return gg::i8_slices(); }
+
+size_t gg_inverse_slices_bytes(int n) { return n < 1 ? 0 : gg::inverse_slices_bytes(n); }
+
+int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
+                        void* stream) {
+  if (n < 1 || LinvT == nullptr || slices == nullptr || expo == nullptr) {
+    gg::set_error("slice_inverse: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::slice_inverse_run(n, LinvT, ldp, reinterpret_cast<signed char*>(slices), expo,
+                               as_stream(stream));
+}
+
+int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
+                     int* bad_dev, void* stream) {
+  if (n < 1 || X == nullptr || G == nullptr || bad_dev == nullptr) {
+    gg::set_error("narrow: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::narrow_run(n, cnt, X, ldx, reinterpret_cast<signed char*>(G), ldg, bad_dev,
+                        as_stream(stream));
+}
+
+int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
+                     long long ldg, double* X, int ldx, void* stream) {
+  if (n < 1 || nrhs < 0 || slices == nullptr || expo == nullptr || G == nullptr || X == nullptr) {
+    gg::set_error("trsm_i8: null pointer or bad size");
+    return GG_EARG;
+  }
+  return gg::trsm_i8_run(n, nrhs, reinterpret_cast<const signed char*>(slices), expo,
+                         reinterpret_cast<const signed char*>(G), ldg, X, ldx, as_stream(stream));
+}
+
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream) {
   if (A == nullptr || T == nullptr || A == T) {
     gg::set_error("transpose: null or aliased pointers");

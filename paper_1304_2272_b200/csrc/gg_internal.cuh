@@ -68,6 +68,16 @@ int pack_lower_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const doubl
                       double* P, cudaStream_t s);
 int transpose_square_run(int np, const double* A, int lda, double* T, int ldt, cudaStream_t s);
 
+// ---- int8 tensor-core TRSM with the sliced inverse (trsm_i8.cu) -----------------------------
+int i8_slices();
+size_t inverse_slices_bytes(int n);
+int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
+                      cudaStream_t s);
+int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
+               int* bad, cudaStream_t s);
+int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
+                long long ldg, double* X, int ldx, cudaStream_t s);
+
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------
 int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
              int ldxl, const double* ybar, double* dots, cudaStream_t s);

@@ -1,0 +1,470 @@
+// Streamed TRSM on the 5th-generation tensor cores: Xbar = Linv * G for int8 dosage blocks G,
+// with the FP64 inverse split error-free into S int8 slices (Ozaki-style splitting).
+//
+// Genotype dosages {0,1,2} are exact int8.  Each row i of Linv is written as
+//     Linv[i,k] = 2^e_i * sum_{s=1..S} a_s[i,k] * 2^(-7 s),   a_s int8 in [-127, 127]
+// (truncation residual < 2^(e_i - 7 S); S = 8 -> 56 bits, finer than FP64's 53), so
+//     Xbar[i,j] = 2^e_i * sum_s 2^(-7 s) * C_s[i,j],   C_s = sum_k a_s[i,k] G[k,j]
+// where every C_s is an EXACT int32 integer product (|C_s| <= 127*2*n < 2^31 for n < 8.4e6)
+// computed by tcgen05.mma.kind::i8.  The S terms are recombined in FP64 in a fixed order, so
+// a column's result never depends on its position (bitwise permutation invariance).
+//
+// Kernel (persistent, one CTA per SM, warp-specialised, 6 warps):
+//   warp 0  TMA producer: A = genotype tile (128 SNPs x 128 k, int8, 128B swizzle, OOB rows of
+//           k >= n zero-filled) and B = the S slices of 32 inverse rows (3-D box 128 k x 32 rows
+//           x S slices) into a 4-stage mbarrier ring (48 KB / stage);
+//   warp 1  MMA issuer (one lane): D[128 SNPs x (S*32)] += A . B^T, 4 x K=32 per stage, int32
+//           accumulators in TMEM, double-buffered (2 x 256 columns), tcgen05.commit to mbarriers;
+//   warps 2-5  epilogue: tcgen05.ld each SNP's S x 32 accumulators, recombine in FP64, scale by
+//           2^e_i, store 32 consecutive rows of the SNP's Xbar column (256 contiguous bytes).
+// Tiles = (32-row blocks of Linv) x (128-SNP column tiles); row block rb needs k < 32 (rb+1).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "gg_internal.cuh"
+
+namespace gg {
+namespace {
+
+constexpr int S = 8;                       // int8 slices of the inverse
+constexpr int TM = 128;                    // SNPs per tile (MMA M)
+constexpr int TR = 32;                     // inverse rows per tile
+constexpr int TN = S * TR;                 // MMA N = 256
+constexpr int TK = 128;                    // k per pipeline stage (4 MMAs of K = 32)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = TM * TK;           // 16 KB
+constexpr int B_BYTES = TN * TK;           // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 6 * 32;
+constexpr int ACC_COLS = TN;               // int32 columns per accumulator buffer
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+
+struct I8Args {
+  int N;            // SNP columns
+  int num_rb;       // np / 32
+  int num_nt;       // ceil(N / 128)
+  double* X;        // Xbar, column-major, leading dimension ldx
+  long long ldx;
+  const int* expo;  // e_i per inverse row (np)
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// K-major, 128-byte-swizzled shared-memory matrix descriptor (rows of 128 B, 8-row groups
+// 1024 B apart): start >> 4, LBO = 1, SBO = 1024 >> 4, version 1 (sm_100), layout SWIZZLE_128B.
+__device__ __forceinline__ unsigned long long smem_desc(unsigned saddr) {
+  return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// instruction descriptor: D s32, A/B signed int8, both K-major, N = TN, M = TM
+constexpr unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
+                           ((unsigned)(TM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(unsigned d_tmem, unsigned long long a, unsigned long long b,
+                                       unsigned accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(unsigned bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
+  rb = num_rb - 1 - t / num_nt;   // heavy row blocks first; a row block's SNP tiles together
+  nt = t % num_nt;
+}
+__device__ __forceinline__ int tile_of(int r, int b, int G) {
+  return r * G + ((r & 1) ? (G - 1 - b) : b);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    trsm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   I8Args a) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 4);
+  const unsigned sbase = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars);
+  const unsigned empty0 = smem_u32(bars + STAGES);
+  const unsigned accf0 = smem_u32(bars + 2 * STAGES);       // accumulator full  [2]
+  const unsigned acce0 = smem_u32(bars + 2 * STAGES + 2);   // accumulator empty [2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4 * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {   // TMEM: 2 accumulator buffers x 256 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const unsigned tmem_base = *tmem_slot;
+
+  const int total = a.num_rb * a.num_nt;
+  const int G = gridDim.x, bidx = blockIdx.x;
+
+  if (warp == 0) {
+    // ---------------------------------- TMA producer ----------------------------------------
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int r = 0;; ++r) {
+        const int t = tile_of(r, bidx, G);
+        if (t >= total) break;
+        int rb, nt;
+        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+        const int nk = (rb + 4) / 4;   // ceil(32 (rb+1) / 128)
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const unsigned fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          const unsigned dA = sbase + stage * STAGE_BYTES;
+          tma_2d(dA, &tmA, fb, kt * TK, nt * TM);
+          tma_3d(dA + A_BYTES, &tmB, fb, kt * TK, rb * TR, 0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------- MMA issuer ------------------------------------------
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int it = 0;
+      for (int r = 0;; ++r, ++it) {
+        const int t = tile_of(r, bidx, G);
+        if (t >= total) break;
+        int rb, nt;
+        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+        const int nk = (rb + 4) / 4;
+        const int ab = it & 1;
+        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);   // epilogue drained this buffer
+        fence_after();
+        const unsigned d_tmem = tmem_base + ab * ACC_COLS;
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(full0 + 8 * stage, phase);
+          fence_after();
+          const unsigned sa = sbase + stage * STAGE_BYTES;
+          const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TK / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-byte units
+            mma_i8(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(empty0 + 8 * stage);        // smem stage free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(accf0 + 8 * ab);              // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---------------------------------- epilogue (warps 2..5) -------------------------------
+    const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
+    const int m = quarter * 32 + lane;          // SNP within the tile
+    int it = 0;
+    for (int r = 0;; ++r, ++it) {
+      const int t = tile_of(r, bidx, G);
+      if (t >= total) break;
+      int rb, nt;
+      tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+      const int ab = it & 1;
+      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
+      fence_after();
+      double acc[TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
+      const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
+      // smallest slice first: acc = sum_s C_s 2^(-7 s), s = S..1
+#pragma unroll 1
+      for (int s = S - 1; s >= 0; --s) {
+        int v[32];
+        tmem_ld32(taddr + s * TR, v);
+        const double w = exp2(-7.0 * (s + 1));
+#pragma unroll
+        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], w, acc[i]);
+      }
+      fence_before();
+      mbar_arrive(acce0 + 8 * ab);
+      const int col = nt * TM + m;
+      if (col < a.N) {
+        const int row0 = rb * TR;
+        double* dst = a.X + (long long)col * a.ldx + row0;
+#pragma unroll
+        for (int i = 0; i < TR; i += 2) {
+          const double2 o = make_double2(ldexp(acc[i], a.expo[row0 + i]),
+                                         ldexp(acc[i + 1], a.expo[row0 + i + 1]));
+          *reinterpret_cast<double2*>(dst + i) = o;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+  }
+}
+
+// ---- inverse slicing ---------------------------------------------------------------------------
+// LinvT: row-major inverse (element (i, k) at LinvT[k + i*ld]); one CTA per row.
+__global__ void slice_rows_kernel(int np, const double* __restrict__ LinvT, long long ld,
+                                  signed char* __restrict__ Sl, int* __restrict__ expo) {
+  const int i = blockIdx.x;
+  const double* row = LinvT + (long long)i * ld;
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int k = threadIdx.x; k <= i && k < np; k += blockDim.x) mx = fmax(mx, fabs(row[k]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  mx = red[0];
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);   // mx = f * 2^e, f in [0.5, 1)  ->  |row| < 2^e
+  if (threadIdx.x == 0) expo[i] = e;
+  const long long plane = (long long)np * np;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    double v = (k <= i) ? ldexp(row[k], -e) : 0.0;   // |v| < 1, exact power-of-2 scaling
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double t = v * 128.0;                     // exact
+      const double q = trunc(t);                      // |q| <= 127
+      Sl[s * plane + (long long)i * np + k] = (signed char)(int)q;
+      v = t - q;                                      // exact remainder, |v| < 1
+    }
+  }
+}
+
+// FP64 dosages -> int8 (exactness check: integers in [-127, 127]); padding rows not written.
+__global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long long ldx,
+                              signed char* __restrict__ G, long long ldg, int* __restrict__ bad) {
+  const long long total = (long long)n * cnt;
+  int local_bad = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n);
+    const long long j = e / n;
+    const double v = X[i + j * ldx];
+    const bool ok = (v == trunc(v)) && fabs(v) <= 127.0;
+    local_bad |= ok ? 0 : 1;
+    G[i + j * ldg] = ok ? (signed char)(int)v : 0;
+  }
+  if (local_bad) atomicOr(bad, 1);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_i8() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int encode(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
+           const cuuint64_t* strides, const cuuint32_t* box) {
+  auto fn = encode_fn_i8();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return GG_ECUDA;
+  }
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (int8) failed (code " + std::to_string((int)r) + ")");
+    return GG_ECUDA;
+  }
+  return GG_OK;
+}
+
+int sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace
+
+int i8_slices() { return S; }
+
+size_t inverse_slices_bytes(int n) {
+  const size_t np = (size_t)pad_rows(n);
+  return (size_t)S * np * np;
+}
+
+int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
+                      cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (ldp < np) {
+    set_error("slice_inverse: ld must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, LinvT, ldp, Sl, expo);
+  GG_LAUNCH_CHECK("slice_rows_kernel");
+  return GG_OK;
+}
+
+int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
+               int* bad, cudaStream_t s) {
+  if (ldx < n || ldg < n) {
+    set_error("narrow: leading dimensions too small");
+    return GG_EDIM;
+  }
+  if (cnt <= 0) return GG_OK;
+  long long grid = ((long long)n * cnt + 255) / 256;
+  if (grid > 148LL * 32) grid = 148LL * 32;
+  narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, bad);
+  GG_LAUNCH_CHECK("narrow_kernel");
+  return GG_OK;
+}
+
+int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
+                long long ldg, double* X, int ldx, cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (ldx < np || ldg < n || (ldg % 16) != 0) {
+    set_error("trsm_i8: ldx >= gg_pad(n), ldg >= n and ldg a multiple of 16 required");
+    return GG_EDIM;
+  }
+  if (nrhs <= 0) return GG_OK;
+  if ((reinterpret_cast<uintptr_t>(Sl) | reinterpret_cast<uintptr_t>(G) |
+       reinterpret_cast<uintptr_t>(X)) & 15) {
+    set_error("trsm_i8: operands must be 16-byte aligned");
+    return GG_EARG;
+  }
+  CUtensorMap mA, mB;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)nrhs};   // k beyond n: TMA zero fill
+    cuuint64_t strides[1] = {(cuuint64_t)ldg};
+    cuuint32_t box[2] = {TK, TM};
+    int rc = encode(&mA, 2, G, dims, strides, box);
+    if (rc != GG_OK) return rc;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
+    cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
+    cuuint32_t box[3] = {TK, TR, S};
+    int rc = encode(&mB, 3, Sl, dims, strides, box);
+    if (rc != GG_OK) return rc;
+  }
+  I8Args a;
+  a.N = nrhs;
+  a.num_rb = np / TR;
+  a.num_nt = (nrhs + TM - 1) / TM;
+  a.X = X;
+  a.ldx = ldx;
+  a.expo = expo;
+  const int tiles = a.num_rb * a.num_nt;
+  int grid = sms();
+  if (grid > tiles) grid = tiles;
+  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)SMEM_BYTES));
+  trsm_i8_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
+  GG_LAUNCH_CHECK("trsm_i8_kernel");
+  return GG_OK;
+}
+
+}  // namespace gg
