@@ -37,6 +37,12 @@ UNIT = "SNPs/s"
 FP64_PEAK_TFLOPS = 37.09
 FP64_PEAK_SOURCE = ("measured: DMMA m8n8k4 sustained 37.09 TF/s @1965 MHz, tools/fp64_peak.cu "
                     "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry")
+# int8 tensor-core peak (the int8 TRSM's roofline): measured with tools/i8_peak.cu on this pool's
+# B200 (tcgen05.mma.cta_group::1.kind::i8 M128 N256 K32 back to back on every SM).
+I8_PEAK_TOPS = 4428.7
+I8_PEAK_SOURCE = ("measured: tcgen05.mma.kind::i8 M128 N256 K32 back to back on 148 SMs, 4428.7 "
+                  "TOPS (tools/i8_peak.cu, profiles/r01_i8_peak.log); MEASURED_PEAKS.json has no "
+                  "int8 entry")
 CPU_SAMPLE_SNPS = 4096
 REF_SAMPLE_SNPS = 2048
 
@@ -53,6 +59,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-dtype", choices=["f64", "i8"], default="f64")
+    ap.add_argument("--trsm", choices=["i8", "dmma"], default="i8",
+                    help="TRSM engine: int8 tensor cores with the sliced inverse (default) or "
+                         "the FP64 DMMA kernel")
     ap.add_argument("--resident", choices=["f64", "i8"], default=None,
                     help="genotype storage in HBM (default: FP64 if it fits, else int8)")
     return ap.parse_args()
@@ -114,9 +123,9 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def load_traffic():
+def load_traffic(engine):
     """Per-launch DRAM bytes of the TRSM kernel from the committed ncu --set full summary."""
-    path = os.path.join(REPO, "profiles", "ncu_trsm_summary.json")
+    path = os.path.join(REPO, "profiles", f"ncu_trsm_{engine}_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -136,6 +145,7 @@ def run_ours(args):
 
     from paper_1304_2272_b200 import _capi, datagen, kernel, pipeline
     from paper_1304_2272_b200._capi import check, ptr
+    from paper_1304_2272_b200._device import alloc_cols
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -170,11 +180,14 @@ def run_ours(args):
     d = ctx._dev
     M = Md.cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     del Md
-    # genotypes resident in HBM: FP64 (config 1) when they fit, else int8 {0,1,2} dosages widened
-    # block by block inside the step (config 2/3 storage format)
+    # genotypes resident in HBM: FP64 (config 1) when they fit, else int8 {0,1,2} dosages (the
+    # config 2/3 storage format)
     free_b, _ = torch.cuda.mem_get_info(dev)
     resident = args.resident or ("f64" if 8 * m * np_ < 0.6 * free_b else "i8")
+    use_i8 = args.trsm == "i8" and d.slices is not None
+    n16 = -(-n // 16) * 16
     first_marker = rank * m
+    X = Gres = None
     if resident == "f64":
         X = torch.empty((m, np_), dtype=torch.float64, device=dev)
         X[:, n:].zero_()
@@ -185,13 +198,14 @@ def run_ours(args):
             check(lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(X[j0:]), np_,
                                       _capi.stream_handle()), "widen")
         del G
-        Gres, xin = None, None
     else:
-        Gres = datagen.genotypes_device(spec, first_marker, m)          # (m, n) int8
-        xin = torch.empty((m_blk, np_), dtype=torch.float64, device=dev)
-        xin[:, n:].zero_()
-        X = None
-    xbar = torch.empty((m_blk, np_), dtype=torch.float64, device=dev)
+        Gres = datagen.genotypes_device(spec, first_marker, m, ld=n16)   # (m, n16) int8
+    g8 = torch.empty((m_blk, n16), dtype=torch.int8, device=dev) if (use_i8 and X is not None) \
+        else None
+    xin = alloc_cols(m_blk, np_) if (not use_i8 and X is None) else None
+    xbar = alloc_cols(m_blk, np_, zero=False) if not use_i8 else None
+    P = torch.empty(int(lib.gg_partials_bytes(n, m_blk, q)) // 8, dtype=torch.float64, device=dev)
+    bad = torch.zeros((1,), dtype=torch.int32, device=dev)
     beta = torch.empty((m, p), dtype=torch.float64, device=dev)
     status = torch.empty((m,), dtype=torch.int32, device=dev)
     plan = pipeline.block_plan(m, m_blk).blocks
@@ -199,27 +213,48 @@ def run_ours(args):
     sh = _capi.C.c_void_p(stream.cuda_stream)
     ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in plan]
+    launches_per_block = 0
 
     def step(record):
+        nonlocal launches_per_block
         for i, (f, c) in enumerate(plan):
-            if record:
-                ev_pairs[i][0].record(stream)
-            if X is not None:
-                src = X[f]
+            rc = 0
+            nl = 0
+            if use_i8:
+                if X is not None:            # FP64 dosages -> int8 (exactness flag checked after)
+                    rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8), n16, ptr(bad), sh)
+                    G, ldg, nl = g8, n16, nl + 1
+                else:
+                    G, ldg = Gres[f:], n16
+                if record:
+                    ev_pairs[i][0].record(stream)
+                rc |= lib.gg_trsm_lower_i8_partials(n, c, ptr(d.slices), ptr(d.expo), ptr(G), ldg,
+                                                    q, ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0,
+                                                    None, 0, sh)
+                if record:
+                    ev_pairs[i][1].record(stream)
+                rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
+                                                  ptr(beta[f]), ptr(status[f]), None, ptr(P), sh)
+                nl += 2
             else:
-                rc0 = lib.gg_widen_i8_f64(n, c, ptr(Gres[f]), n, ptr(xin), np_, sh)
-                if rc0:
-                    raise RuntimeError(_capi.last_error())
-                src = xin
-            rc = lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(src), np_, ptr(xbar), np_,
-                                              sh)
-            if record:
-                ev_pairs[i][1].record(stream)
-            rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(xbar), np_, ptr(d.XLy), np_, ptr(d.ybar),
-                                          ptr(d.S_TL), ptr(d.b_T), ptr(beta[f]), ptr(status[f]),
-                                          None, sh)
+                if X is not None:
+                    src = X[f]
+                else:
+                    rc |= lib.gg_widen_i8_f64(n, c, ptr(Gres[f]), n16, ptr(xin), np_, sh)
+                    src, nl = xin, nl + 1
+                if record:
+                    ev_pairs[i][0].record(stream)
+                rc |= lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(src), np_, ptr(xbar),
+                                                   np_, sh)
+                if record:
+                    ev_pairs[i][1].record(stream)
+                rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(xbar), np_, ptr(d.XLy), np_,
+                                              ptr(d.ybar), ptr(d.S_TL), ptr(d.b_T), ptr(beta[f]),
+                                              ptr(status[f]), None, ptr(P), sh)
+                nl += 3          # TRSM + partials + reduce/solve
             if rc:
                 raise RuntimeError(_capi.last_error())
+            launches_per_block = nl
         return None
 
     def barrier():
@@ -239,12 +274,10 @@ def run_ours(args):
     t_start.record(stream)
     for k in range(args.steps):
         step(True)
-        if k == 0:
-            pass
     t_end.record(stream)
     torch.cuda.synchronize()
-    for a, b in ev_pairs:
-        trsm_ms += a.elapsed_time(b)     # last step's per-launch times
+    for a_ev, b_ev in ev_pairs:
+        trsm_ms += a_ev.elapsed_time(b_ev)     # last step's per-launch times
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     barrier()
@@ -252,13 +285,43 @@ def run_ours(args):
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
+    if int(bad.item()) != 0:
+        raise RuntimeError("non-integer dosages reached the int8 path")
     ok_all = bool((status >= 0).sum().item() == 0)
     snps_per_step_total = m * world
     value = snps_per_step_total * args.steps / (elapsed_ms / 1e3)
+    traffic_full, ncu = load_traffic("i8" if use_i8 else "dmma")
     flops_per_step = float(n) * n * m
-    trsm_tflops = flops_per_step / (trsm_ms / 1e3) / 1e12
+    trsm_tflops = flops_per_step / (trsm_ms / 1e3) / 1e12          # FP64-equivalent rate
     step_tflops = flops_per_step * args.steps / (elapsed_ms / 1e3) / 1e12
-    traffic_full, ncu = load_traffic()
+    if use_i8:
+        slices = int(lib.gg_i8_slices())
+        tops = slices * flops_per_step / (trsm_ms / 1e3) / 1e12     # int8 ops: S slices x n^2
+        roofline = {
+            "bound": "tensor",
+            "kernel": "trsm_i8_kernel (persistent TMA + tcgen05.mma.kind::i8 TRSM, fused "
+                      "reductions; inverse split into int8 slices)",
+            "achieved": round(tops, 1), "peak": I8_PEAK_TOPS, "unit": "TOPS",
+            "frac": round(tops / I8_PEAK_TOPS, 4),
+            "traffic": traffic_full,
+            "algorithmic_unit": f"{slices} slices x n^2 int8 ops per SNP (exact int32 products of "
+                                "the sliced inverse with the dosages) x SNPs per launch",
+            "peak_source": I8_PEAK_SOURCE,
+            "fp64_equivalent_tflops": round(trsm_tflops, 2),
+            "fp64_equivalent_vs_dmma_peak": round(trsm_tflops / FP64_PEAK_TFLOPS, 3),
+            "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
+        }
+    else:
+        roofline = {
+            "bound": "tensor",
+            "kernel": "trsm_tma_kernel (persistent TMA + DMMA TRSM, Xbar = Linv*X)",
+            "achieved": round(trsm_tflops, 3), "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": round(trsm_tflops / FP64_PEAK_TFLOPS, 4),
+            "traffic": traffic_full,
+            "algorithmic_unit": "n^2 FLOP per SNP (LAPACK dtrsm count) x SNPs per launch",
+            "peak_source": FP64_PEAK_SOURCE,
+            "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
+        }
 
     # ---- e2e through the public stream API with host buffers --------------------------------
     e2e = None
@@ -295,16 +358,8 @@ def run_ours(args):
                 "step_fp64_tflops": round(step_tflops, 3),
                 "all_snps_ok": ok_all,
             },
-            "roofline": {
-                "bound": "tensor", "kernel": "trsm_tma_kernel (persistent TMA + DMMA TRSM, Xbar = Linv*X)",
-                "achieved": round(trsm_tflops, 3), "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": round(trsm_tflops / FP64_PEAK_TFLOPS, 4),
-                "traffic": traffic_full,
-                "algorithmic_unit": "n^2 FLOP per SNP (LAPACK dtrsm count) x SNPs per launch",
-                "peak_source": FP64_PEAK_SOURCE,
-                "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
-            },
-            "gpu_launches": (2 if resident == "f64" else 3) * len(plan) * args.steps,
+            "roofline": roofline,
+            "gpu_launches": launches_per_block * len(plan) * args.steps,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -43,6 +43,7 @@ extern "C" {
 
 #define GG_TILE 128      /* row padding unit = GEMM tile edge                    */
 #define GG_PMAX 20       /* largest p supported by the small-system solver       */
+#define GG_DOT_BLOCK 32  /* rows per partial sum of the canonical reduction order */
 
 /* Library identification / errors. */
 const char* gg_version(void);
@@ -132,6 +133,21 @@ int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, 
 int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
                      long long ldg, double* X, int ldx, void* stream);
 
+/* The same kernel with the per-SNP reductions fused into its TMEM epilogue: writes the
+ * canonical-order partial dots P (gg_partials_bytes(n, cnt, q) bytes; Xbar against XLbar (q
+ * columns, ld gg_pad(n)) and ybar) and, if X != NULL, Xbar itself.  gate != NULL: the kernel
+ * runs only if *gate == gate_value (device-side path selection).
+ * gg_gls_reduce_solve_f64 then sums the partials in order and solves each SNP's p x p system
+ * (the second half of gg_gls_epilogue_f64).                                                    */
+size_t gg_partials_bytes(int n, int cnt, int q);
+int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* expo,
+                              const int8_t* G, long long ldg, int q, const double* XLbar,
+                              const double* ybar, double* P, double* X, int ldx, const int* gate,
+                              int gate_value, void* stream);
+int gg_gls_reduce_solve_f64(int n, int cnt, int q, const double* P, const double* S_TL,
+                            const double* b_T, double* beta, int* status, double* sinv,
+                            void* stream);
+
 /* Square transpose (np x np, np a multiple of 32): T = A^T (column-major both).
  * Turns the Linv produced by gg_potrf_f64 into the LinvT operand above.              */
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream);
@@ -155,11 +171,12 @@ int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, i
  * dots[j*(q+2) + k] = sum_i Xbar[i,j]*XLbar[i,k]  (k < q)      (kernel.py:266-267)
  * dots[j*(q+2) + q] = sum_i Xbar[i,j]^2                          (kernel.py:268)
  * dots[j*(q+2)+q+1] = sum_i Xbar[i,j]*ybar[i]                    (kernel.py:269)
- * One fixed summation order for every column (replaces _column_sums,
- * kernel.py:260-270, and kernel.gram, kernel.py:124-131).                          */
+ * One fixed summation order for every column: FMA chains over blocks of GG_DOT_BLOCK rows,
+ * block sums strided over 32 lanes then an xor butterfly (replaces _column_sums,
+ * kernel.py:260-270, and kernel.gram, kernel.py:124-131).                               */
 int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                     const double* XLbar, int ldxl, const double* ybar, double* dots,
-                    void* stream);
+                    void* work, void* stream);   /* work: gg_partials_bytes(n, cnt, q) bytes */
 
 /* Batched small SPD solve (replaces kernel.cholesky_solve_batch, kernel.py:138-208):
  * S (batch x p x p, row-major per system), rhs (batch x p) -> x (batch x p; NaN rows
@@ -176,18 +193,23 @@ int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs,
 int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                         const double* XLbar, int ldxl, const double* ybar,
                         const double* S_TL, const double* b_T, double* beta, int* status,
-                        double* sinv, void* stream);
+                        double* sinv, void* work, void* stream);   /* work: as gg_gls_dots_f64 */
 
-/* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342):
- * [widen int8 ->] TRSM (packed inverse LinvP, see gg_trsm_lower_packed_f64) -> fused
- * epilogue.  XLbar has leading dimension gg_pad(n).  Exactly one of X64 (np rows,
- * ldx) / G8 (n rows, ldg) is non-NULL.  xbar_work: np x cnt FP64 scratch (ld = np),
- * x64_work: np x cnt FP64 scratch used only for the int8 path (may be NULL otherwise). */
-int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP,
-                     const double* XLbar, const double* ybar, const double* S_TL,
-                     const double* b_T, const double* X64, int ldx, const int8_t* G8,
-                     long long ldg, double* x64_work, double* xbar_work, double* beta,
-                     int* status, double* sinv, void* stream);
+/* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342).
+ * Paths (all selected without a host synchronisation):
+ *   slices given, G8 (int8 dosages) : int8 tensor-core TRSM with the per-SNP reductions fused
+ *                                     into its TMEM epilogue (Xbar never written) -> solve;
+ *   slices given, X64 (FP64)        : device narrowing; exact integers in [-127,127] take the
+ *                                     int8 path, otherwise the FP64 DMMA TRSM (LinvP) runs;
+ *   no slices                       : [widen int8 ->] FP64 DMMA TRSM (LinvP) -> reductions.
+ * Then the batched p x p solve.  XLbar has leading dimension gg_pad(n).  work: at least
+ * gg_gls_block_workspace_bytes(n, q, cnt, input_int8, have_slices) bytes of device memory.   */
+size_t gg_gls_block_workspace_bytes(int n, int q, int cnt, int input_int8, int have_slices);
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* slices,
+                     const int* expo, const double* XLbar, const double* ybar,
+                     const double* S_TL, const double* b_T, const double* X64, int ldx,
+                     const int8_t* G8, long long ldg, void* work, double* beta, int* status,
+                     double* sinv, void* stream);
 
 /* ---- Stream plumbing ----------------------------------------------------------------
  * Pitched asynchronous copy (host<->device or device<->device) on `stream`; used by the

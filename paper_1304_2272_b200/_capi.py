@@ -43,14 +43,19 @@ SIGNATURES = {
     "gg_slice_inverse_i8": (_i, [_i, _vp, _i, _vp, _vp, _vp]),
     "gg_narrow_f64_i8": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),
     "gg_trsm_lower_i8": (_i, [_i, _i, _vp, _vp, _vp, _ll, _vp, _i, _vp]),
+    "gg_partials_bytes": (_sz, [_i, _i, _i]),
+    "gg_trsm_lower_i8_partials": (_i, [_i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp, _i,
+                                       _vp, _i, _vp]),
+    "gg_gls_reduce_solve_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
     "gg_widen_i8_f64": (_i, [_i, _i, _vp, _ll, _vp, _i, _vp]),
-    "gg_gls_dots_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp]),
+    "gg_gls_dots_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp]),
     "gg_small_spd_solve_f64": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gg_gls_epilogue_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp,
-                                 _vp]),
-    "gg_gls_block_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _ll, _vp,
+                                 _vp, _vp]),
+    "gg_gls_block_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
+    "gg_gls_block_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _ll,
                               _vp, _vp, _vp, _vp, _vp]),
     "gg_memcpy2d_async": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _i, _vp]),
     "gg_gen_genotypes_i8": (_i, [_ull, _i, _i, _i, _ll, _ll, _i, _d, _d, _vp, _ll, _vp, _i,

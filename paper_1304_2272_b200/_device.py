@@ -95,6 +95,8 @@ class DeviceContext:
     XLy: object        # (q + 1, np): whitened covariates, then whitened phenotype
     S_TL: object       # (q * q,) row-major
     b_T: object        # (q,)
+    slices: object = None   # int8 slices of the inverse ([S][np][np]) for the tensor-core TRSM
+    expo: object = None     # per-row power-of-two exponents of the slices (np int32)
 
     @property
     def p(self):
@@ -132,25 +134,30 @@ class BlockWorkspace:
         torch = _torch()
         self.dctx = dctx
         self.m_blk = int(m_blk)
+        self.int8_input = bool(int8_input)
         p = dctx.p
         dev = _capi.device()
-        self.xbar = alloc_cols(self.m_blk, dctx.np_, zero=False)
-        self.x64 = alloc_cols(self.m_blk, dctx.np_, zero=False) if int8_input else None
+        have_slices = dctx.slices is not None
+        nbytes = int(_capi.lib().gg_gls_block_workspace_bytes(
+            dctx.n, dctx.q, self.m_blk, 1 if int8_input else 0, 1 if have_slices else 0))
+        self.work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.beta = torch.empty((self.m_blk, p), dtype=torch.float64, device=dev)
         self.status = torch.empty((self.m_blk,), dtype=torch.int32, device=dev)
         self.sinv = (torch.empty((self.m_blk, p * (p + 1) // 2), dtype=torch.float64, device=dev)
                      if emit_s_inv else None)
 
     def run(self, cnt, X64=None, ldx=0, G8=None, ldg=0, stream=None):
-        """TRSM + fused epilogue for ``cnt`` columns already resident on the device."""
+        """TRSM + reductions + small solves for ``cnt`` columns already on the device."""
         d = self.dctx
         if cnt > self.m_blk:
             raise ValueError("block larger than the workspace")
-        if d.LinvP is None:
+        if d.LinvP is None and d.slices is None:
             raise ValueError("context has no device factor (prepared from host fields only)")
+        if (G8 is not None) != self.int8_input:
+            raise ValueError("input kind does not match the workspace")
         s = stream_handle() if stream is None else stream
         rc = _capi.lib().gg_gls_block_f64(
-            d.n, d.q, int(cnt), ptr(d.LinvP), ptr(d.XLy), ptr(d.ybar), ptr(d.S_TL),
-            ptr(d.b_T), ptr(X64), int(ldx), ptr(G8), int(ldg), ptr(self.x64), ptr(self.xbar),
-            ptr(self.beta), ptr(self.status), ptr(self.sinv), s)
+            d.n, d.q, int(cnt), ptr(d.LinvP), ptr(d.slices), ptr(d.expo), ptr(d.XLy),
+            ptr(d.ybar), ptr(d.S_TL), ptr(d.b_T), ptr(X64), int(ldx), ptr(G8), int(ldg),
+            ptr(self.work), ptr(self.beta), ptr(self.status), ptr(self.sinv), s)
         check(rc, "gg_gls_block_f64")

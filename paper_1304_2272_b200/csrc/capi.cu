@@ -24,6 +24,9 @@ int cuda_fail(cudaError_t e, const char* what) {
 using gg::pad_rows;
 
 static inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+static inline const signed char* slices_as(const int8_t* p) {
+  return reinterpret_cast<const signed char*>(p);
+}
 
 extern "C" {
 
@@ -157,6 +160,37 @@ int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, con
                          reinterpret_cast<const signed char*>(G), ldg, X, ldx, as_stream(stream));
 }
 
+size_t gg_partials_bytes(int n, int cnt, int q) {
+  return (n < 1 || cnt < 1 || q < 0) ? 0 : gg::partials_bytes(n, cnt, q);
+}
+
+int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* expo,
+                              const int8_t* G, long long ldg, int q, const double* XLbar,
+                              const double* ybar, double* P, double* X, int ldx, const int* gate,
+                              int gate_value, void* stream) {
+  if (n < 1 || cnt < 0 || slices == nullptr || expo == nullptr || G == nullptr || P == nullptr ||
+      ybar == nullptr || (q > 0 && XLbar == nullptr) || q < 0 || q > GG_PMAX - 1) {
+    gg::set_error("trsm_i8_partials: null pointer or bad size");
+    return GG_EARG;
+  }
+  return gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo,
+                               reinterpret_cast<const signed char*>(G), ldg, X, ldx, q, XLbar,
+                               pad_rows(n), ybar, P, gate, gate_value, as_stream(stream));
+}
+
+int gg_gls_reduce_solve_f64(int n, int cnt, int q, const double* P, const double* S_TL,
+                            const double* b_T, double* beta, int* status, double* sinv,
+                            void* stream) {
+  if (n < 1 || P == nullptr || beta == nullptr || status == nullptr || q < 0 || q > GG_PMAX - 1 ||
+      (q > 0 && (S_TL == nullptr || b_T == nullptr))) {
+    gg::set_error("reduce_solve: null pointer or bad size");
+    return GG_EARG;
+  }
+  if (cnt <= 0) return GG_OK;
+  return gg::reduce_solve_run(n, cnt, q, P, nullptr, S_TL, b_T, beta, status, sinv,
+                              as_stream(stream));
+}
+
 int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void* stream) {
   if (A == nullptr || T == nullptr || A == T) {
     gg::set_error("transpose: null or aliased pointers");
@@ -192,12 +226,14 @@ int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, i
 }
 
 int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
-                    int ldxl, const double* ybar, double* dots, void* stream) {
-  if (Xbar == nullptr || ybar == nullptr || dots == nullptr || (q > 0 && XLbar == nullptr)) {
+                    int ldxl, const double* ybar, double* dots, void* work, void* stream) {
+  if (Xbar == nullptr || ybar == nullptr || dots == nullptr || work == nullptr ||
+      (q > 0 && XLbar == nullptr)) {
     gg::set_error("dots: null pointer");
     return GG_EARG;
   }
-  return gg::dots_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, dots, as_stream(stream));
+  return gg::dots_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, dots,
+                      static_cast<double*>(work), as_stream(stream));
 }
 
 int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs, double* x,
@@ -211,47 +247,117 @@ int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs,
 
 int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                         int ldxl, const double* ybar, const double* S_TL, const double* b_T,
-                        double* beta, int* status, double* sinv, void* stream) {
+                        double* beta, int* status, double* sinv, void* work, void* stream) {
   if (Xbar == nullptr || ybar == nullptr || beta == nullptr || status == nullptr ||
-      (q > 0 && (XLbar == nullptr || S_TL == nullptr || b_T == nullptr))) {
+      work == nullptr || (q > 0 && (XLbar == nullptr || S_TL == nullptr || b_T == nullptr))) {
     gg::set_error("epilogue: null pointer");
     return GG_EARG;
   }
   return gg::epilogue_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, S_TL, b_T, beta, status, sinv,
-                          as_stream(stream));
+                          static_cast<double*>(work), as_stream(stream));
 }
 
-int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const double* XLbar,
-                     const double* ybar, const double* S_TL, const double* b_T, const double* X64,
-                     int ldx, const int8_t* G8, long long ldg, double* x64_work, double* xbar_work,
-                     double* beta, int* status, double* sinv, void* stream) {
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct BlockWs {
+  int* flag;
+  double* P;
+  signed char* g8;
+  double* x64;
+  double* xbar;
+  size_t bytes;
+};
+
+// Workspace layout of gg_gls_block_f64 (what each input kind / path needs).
+static BlockWs block_ws(int n, int q, int cnt, int input_int8, int have_slices, char* base) {
+  const size_t np = (size_t)pad_rows(n), n16 = (size_t)((n + 15) / 16 * 16);
+  BlockWs w{};
+  size_t off = 256;   // flag
+  w.flag = reinterpret_cast<int*>(base);
+  w.P = reinterpret_cast<double*>(base + off);
+  off += align256(gg::partials_bytes(n, cnt, q));
+  const bool need_g8 = have_slices;                              // narrowed / re-pitched dosages
+  const bool need_x64 = !have_slices && input_int8;              // widened dosages (DMMA path)
+  const bool need_xbar = !(have_slices && input_int8);           // DMMA result
+  w.g8 = need_g8 ? reinterpret_cast<signed char*>(base + off) : nullptr;
+  if (need_g8) off += align256(n16 * cnt);
+  w.x64 = need_x64 ? reinterpret_cast<double*>(base + off) : nullptr;
+  if (need_x64) off += align256(np * cnt * sizeof(double));
+  w.xbar = need_xbar ? reinterpret_cast<double*>(base + off) : nullptr;
+  if (need_xbar) off += align256(np * cnt * sizeof(double));
+  w.bytes = off;
+  return w;
+}
+
+size_t gg_gls_block_workspace_bytes(int n, int q, int cnt, int input_int8, int have_slices) {
+  if (n < 1 || cnt < 1) return 256;
+  return block_ws(n, q, cnt, input_int8, have_slices, nullptr).bytes;
+}
+
+int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* slices,
+                     const int* expo, const double* XLbar, const double* ybar, const double* S_TL,
+                     const double* b_T, const double* X64, int ldx, const int8_t* G8,
+                     long long ldg, void* work, double* beta, int* status, double* sinv,
+                     void* stream) {
   cudaStream_t s = as_stream(stream);
   if ((X64 == nullptr) == (G8 == nullptr)) {
     gg::set_error("gls_block: exactly one of X64 / G8 must be given");
     return GG_EARG;
   }
-  if (xbar_work == nullptr || LinvP == nullptr) {
-    gg::set_error("gls_block: null workspace / LinvP");
+  const bool have_slices = slices != nullptr && expo != nullptr;
+  if (work == nullptr || (LinvP == nullptr && !(have_slices && G8 != nullptr))) {
+    gg::set_error("gls_block: null workspace / inverse");
     return GG_EARG;
   }
-  const int np = pad_rows(n);
-  if (cnt <= 0) return GG_OK;
-  const double* xin = X64;
-  int ldin = ldx;
-  if (G8 != nullptr) {
-    if (x64_work == nullptr) {
-      gg::set_error("gls_block: int8 input needs x64_work");
-      return GG_EARG;
-    }
-    int rc = gg::widen_run(n, cnt, G8, ldg, x64_work, np, s);
-    if (rc != GG_OK) return rc;
-    xin = x64_work;
-    ldin = np;
+  if (q < 0 || q > GG_PMAX - 1) {
+    gg::set_error("gls_block: need 0 <= q <= 19");
+    return GG_EARG;
   }
-  int rc = gg::trsm_packed_run(n, cnt, LinvP, xin, ldin, xbar_work, np, s);
+  if (cnt <= 0) return GG_OK;
+  const int np = pad_rows(n);
+  const long long n16 = (n + 15) / 16 * 16;
+  const BlockWs w = block_ws(n, q, cnt, G8 != nullptr, have_slices, static_cast<char*>(work));
+  int rc = GG_OK;
+  if (have_slices) {
+    const signed char* g = reinterpret_cast<const signed char*>(G8);
+    long long lg = ldg;
+    if (G8 != nullptr) {
+      if (ldg % 16 != 0 || (reinterpret_cast<uintptr_t>(G8) & 15)) {   // re-pitch for TMA
+        GG_CUDA_TRY(cudaMemcpy2DAsync(w.g8, n16, G8, ldg, n, cnt, cudaMemcpyDeviceToDevice, s));
+        g = w.g8;
+        lg = n16;
+      }
+      rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q, XLbar, np,
+                                 ybar, w.P, nullptr, 0, s);
+    } else {
+      // FP64 dosages: narrow on the device; exact integers take the int8 tensor-core path, any
+      // other value sends the whole block down the FP64 DMMA path (selected on the device: both
+      // kernels are queued, the one whose gate does not match exits at once; no host sync).
+      GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
+      rc = gg::narrow_run(n, cnt, X64, ldx, w.g8, n16, w.flag, s);
+      if (rc == GG_OK)
+        rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, w.g8, n16, nullptr, 0, q,
+                                   XLbar, np, ybar, w.P, w.flag, 0, s);
+      if (rc == GG_OK && LinvP != nullptr) {
+        rc = gg::trsm_packed_gated_run(n, cnt, LinvP, X64, ldx, w.xbar, np, w.flag, 1, s);
+        if (rc == GG_OK)
+          rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
+      }
+    }
+  } else {
+    const double* xin = X64;
+    int ldin = ldx;
+    if (G8 != nullptr) {
+      rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);
+      xin = w.x64;
+      ldin = np;
+    }
+    if (rc == GG_OK) rc = gg::trsm_packed_run(n, cnt, LinvP, xin, ldin, w.xbar, np, s);
+    if (rc == GG_OK)
+      rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, nullptr, 0);
+  }
   if (rc != GG_OK) return rc;
-  return gg::epilogue_run(n, cnt, q, xbar_work, np, XLbar, np, ybar, S_TL, b_T, beta, status,
-                          sinv, s);
+  return gg::reduce_solve_run(n, cnt, q, w.P, nullptr, S_TL, b_T, beta, status, sinv, s);
 }
 
 int gg_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,

@@ -62,6 +62,8 @@ int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const doubl
                       double* X, int ldx, cudaStream_t s);
 int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int ldb, double* X,
                     int ldx, cudaStream_t s);
+int trsm_packed_gated_run(int n, int nrhs, const double* LinvP, const double* B, int ldb,
+                          double* X, int ldx, const int* gate, int gate_value, cudaStream_t s);
 size_t packed_lower_elems(int n);
 int pack_lower_run(int n, const double* A, int lda, int row_major, double* P, cudaStream_t s);
 int pack_lower_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
@@ -77,17 +79,27 @@ int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, l
                int* bad, cudaStream_t s);
 int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
                 long long ldg, double* X, int ldx, cudaStream_t s);
+int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
+                      const signed char* G, long long ldg, double* X, int ldx, int q,
+                      const double* XL, int ldxl, const double* y, double* P, const int* gate,
+                      int gate_value, cudaStream_t s);
 
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------
 int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
-             int ldxl, const double* ybar, double* dots, cudaStream_t s);
+             int ldxl, const double* ybar, double* dots, double* P, cudaStream_t s);
 int small_solve_run(int batch, int p, const double* S, const double* rhs, double* x,
                     int* status, double* sinv, cudaStream_t s);
 int epilogue_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                  int ldxl, const double* ybar, const double* S_TL, const double* b_T,
-                 double* beta, int* status, double* sinv, cudaStream_t s);
+                 double* beta, int* status, double* sinv, double* P, cudaStream_t s);
 int widen_run(int n, int cnt, const int8_t* G, long long ldg, double* X, int ldx,
               cudaStream_t s);
+size_t partials_bytes(int n, int cnt, int q);
+int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+                 int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
+                 int gate_value);
+int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,
+                     const double* b_T, double* beta, int* status, double* sinv, cudaStream_t s);
 
 // ---- generator (datagen.cu) -----------------------------------------------------------
 int gen_genotypes_run(unsigned long long seed, int stream_maf, int stream_geno, int n,

@@ -7,26 +7,22 @@
 //   cholesky_solve_batch  kernel.py:138-208   pivot rule d > p*eps*max|S| and finite,
 //                                             placeholder pivot 1.0, NaN for failed systems,
 //                                             optional packed S^-1 (np.tril_indices order)
-// The reductions use ONE summation order for every column (lane-strided FMA chains followed by
-// an xor butterfly), so a column's sums do not depend on its position in the block, and
-// gram(XLbar) computed with the same kernel is bitwise consistent with S_BL/S_BR for a SNP
-// column equal to a covariate column (the degenerate-SNP case, tests/conftest.py:29-41).
+// Canonical reduction order (shared with the fused epilogue of the int8 TRSM, trsm_i8.cu):
+//   partial_rb = FMA chain over the 32 rows of row block rb, in order;
+//   lane_l     = sum of partial_rb for rb = l, l+32, l+64, ... in order (l = 0..31);
+//   dot        = xor-butterfly sum of the 32 lane values (identical on every lane).
+// Every column uses this order whatever its position, and gram(XLbar) / S_TL / b_T are formed
+// the same way, so a SNP column equal to a covariate column yields an exactly singular S (the
+// degenerate-SNP case, tests/conftest.py:29-41).  Two kernels: partials (per column and row
+// block; or written directly by the int8 TRSM epilogue) and reduce+solve (per column).
 #include "gg_internal.cuh"
 
 namespace gg {
 namespace {
 
 constexpr double EPS = 2.220446049250313e-16;   // 2^-52 (kernel.py:28)
-constexpr int DOT_WARPS = 8;
-constexpr int DOT_COLS_PER_WARP = 2;
-constexpr int DOT_CHUNK = GG_TILE;   // rows of XLbar / ybar staged per step (np is a multiple)
 constexpr int QMAX = GG_PMAX - 1;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+constexpr int RB = GG_DOT_BLOCK;   // rows per partial (np is a multiple)
 
 // ---- small SPD solve, mirroring cholesky_solve_batch operation by operation -------------
 // S, L: p x p row-major local arrays (stride PM).  Products and differences are rounded
@@ -108,105 +104,119 @@ __device__ int small_spd_solve(int p, const double* S, const double* rhs, double
 }
 
 // ---- reductions ----------------------------------------------------------------------------
-// Each warp owns DOT_COLS_PER_WARP columns; XLbar/ybar row chunks are staged once per CTA in
-// shared memory and reused by its 8 warps.  Lane l accumulates rows l, l+32, l+64, ... in order.
-template <int QM>
-__device__ __forceinline__ void dots_accumulate(int np, int cnt, int q, int col0,
-                                                const double* __restrict__ X, long long ldx,
-                                                const double* __restrict__ XL, long long ldxl,
-                                                const double* __restrict__ y, double* sm,
-                                                double (&acc)[DOT_COLS_PER_WARP][QM + 2]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 0; c < DOT_COLS_PER_WARP; ++c)
-#pragma unroll
-    for (int k = 0; k < QM + 2; ++k) acc[c][k] = 0.0;
-  for (int r0 = 0; r0 < np; r0 += DOT_CHUNK) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (q + 1) * DOT_CHUNK; idx += blockDim.x) {
-      const int k = idx / DOT_CHUNK, r = idx % DOT_CHUNK;
-      sm[idx] = (k < q) ? XL[(long long)k * ldxl + r0 + r] : y[r0 + r];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < DOT_COLS_PER_WARP; ++c) {
-      const int col = col0 + c;
-      if (col >= cnt) continue;
-      const double* xc = X + (long long)col * ldx + r0;
-#pragma unroll 4
-      for (int u = 0; u < DOT_CHUNK / 32; ++u) {
-        const int r = lane + 32 * u;
-        const double xv = xc[r];
-#pragma unroll
-        for (int k = 0; k < QM; ++k)
-          if (k < q) acc[c][k] = fma(xv, sm[k * DOT_CHUNK + r], acc[c][k]);
-        acc[c][QM] = fma(xv, xv, acc[c][QM]);
-        acc[c][QM + 1] = fma(xv, sm[q * DOT_CHUNK + r], acc[c][QM + 1]);
-      }
-    }
+// partials[(rb * cnt + col) * (q+2) + k]: k < q -> x.XL[:,k], q -> x.x, q+1 -> x.y over the
+// 32-row block rb (layout shared with the fused epilogue of trsm_i8.cu).
+// CTA = 8 warps = 8 columns x 32 row blocks (1024 rows): XL/y rows staged once per CTA, each
+// warp stages its column's 1024 values (coalesced, padded against bank conflicts) and lane l
+// computes row block l's partial with one sequential FMA chain per output.
+constexpr int PRB = 32;               // row blocks per CTA (one per lane)
+constexpr int PROWS = PRB * RB;       // 1024 rows
+template <int QM, int PCOLS>          // PCOLS columns per CTA (one per warp)
+__global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
+    int nrb, int cnt, int q, const double* __restrict__ X, long long ldx,
+    const double* __restrict__ XL, long long ldxl, const double* __restrict__ y,
+    double* __restrict__ P, const int* gate, int gate_value) {
+  if (gate != nullptr && *gate != gate_value) return;
+  extern __shared__ double sm[];
+  constexpr int LDP = PROWS + PRB;                   // padded: row r at r + r / RB
+  double* sv = sm;                                   // (q+1) x LDP: XL columns, then y
+  double* sx = sm + (size_t)(q + 1) * LDP;           // PCOLS x LDP: the warps' columns
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb0 = blockIdx.y * PRB;
+  const long long r0 = (long long)rb0 * RB;
+  const int nrows = min(PROWS, (nrb - rb0) * RB);
+  for (int idx = threadIdx.x; idx < (q + 1) * nrows; idx += blockDim.x) {
+    const int k = idx / nrows, r = idx % nrows;
+    sv[k * LDP + r + r / RB] = (k < q) ? XL[k * ldxl + r0 + r] : y[r0 + r];
   }
+  const int col = blockIdx.x * PCOLS + warp;
+  double* mx = sx + warp * LDP;
+  if (col < cnt) {
+    const double* xc = X + (long long)col * ldx + r0;
+    for (int r = lane; r < nrows; r += 32) mx[r + r / RB] = xc[r];
+  }
+  __syncthreads();
+  const int rb = rb0 + lane;
+  if (col >= cnt || rb >= nrb) return;
+  const double* xr = mx + lane * (RB + 1);
+  double acc[QM + 2];
 #pragma unroll
-  for (int c = 0; c < DOT_COLS_PER_WARP; ++c)
+  for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
+  for (int i = 0; i < RB; ++i) {
+    const double xv = xr[i];
+    const int r = lane * (RB + 1) + i;
 #pragma unroll
-    for (int k = 0; k < QM + 2; ++k) acc[c][k] = warp_sum(acc[c][k]);
+    for (int k = 0; k < QM; ++k)
+      if (k < q) acc[k] = fma(xv, sv[k * LDP + r], acc[k]);
+    acc[QM] = fma(xv, xv, acc[QM]);
+    acc[QM + 1] = fma(xv, sv[q * LDP + r], acc[QM + 1]);
+  }
+  double* out = P + ((long long)rb * cnt + col) * (q + 2);
+#pragma unroll
+  for (int k = 0; k < QM; ++k)
+    if (k < q) out[k] = acc[k];
+  out[q] = acc[QM];
+  out[q + 1] = acc[QM + 1];
 }
 
-template <int QM>
-__global__ void __launch_bounds__(DOT_WARPS * 32) dots_kernel(
-    int np, int cnt, int q, const double* __restrict__ X, long long ldx,
-    const double* __restrict__ XL, long long ldxl, const double* __restrict__ y,
-    double* __restrict__ dots) {
-  extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col0 = (blockIdx.x * DOT_WARPS + warp) * DOT_COLS_PER_WARP;
-  double acc[DOT_COLS_PER_WARP][QM + 2];
-  dots_accumulate<QM>(np, cnt, q, col0, X, ldx, XL, ldxl, y, sm, acc);
+// One warp per column: lane l sums the partials of row blocks l, l+32, l+64, ... in order, an
+// xor butterfly combines the lanes (every lane ends with the same, position-independent value),
+// then (if S_TL given) lane 0 assembles S = [[S_TL, S_BL^T], [S_BL, S_BR]], rhs = [b_T, b_B] and
+// solves.  This fixes the cross-block part of the canonical order.
+__device__ __forceinline__ double warp_allsum(double v) {
 #pragma unroll
-  for (int c = 0; c < DOT_COLS_PER_WARP; ++c) {
-    const int col = col0 + c;
-    if (col >= cnt || lane != c) continue;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int QM, int PM>
+__global__ void __launch_bounds__(256) reduce_solve_kernel(
+    int nrb, int cnt, int q, const double* __restrict__ P, double* __restrict__ dots,
+    const double* __restrict__ S_TL, const double* __restrict__ b_T, double* __restrict__ beta,
+    int* __restrict__ status, double* __restrict__ sinv) {
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (col >= cnt) return;
+  double acc[QM + 2];
+#pragma unroll
+  for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
+  const long long stride = (long long)cnt * (q + 2);
+  for (int rb = lane; rb < nrb; rb += 32) {
+    const double* pp = P + rb * stride + (long long)col * (q + 2);
+#pragma unroll
+    for (int k = 0; k < QM; ++k)
+      if (k < q) acc[k] = acc[k] + pp[k];
+    acc[QM] = acc[QM] + pp[q];
+    acc[QM + 1] = acc[QM + 1] + pp[q + 1];
+  }
+#pragma unroll
+  for (int k = 0; k < QM + 2; ++k) acc[k] = warp_allsum(acc[k]);
+  if (lane != 0) return;
+  if (dots != nullptr) {
     double* out = dots + (long long)col * (q + 2);
 #pragma unroll
     for (int k = 0; k < QM; ++k)
-      if (k < q) out[k] = acc[c][k];
-    out[q] = acc[c][QM];
-    out[q + 1] = acc[c][QM + 1];
+      if (k < q) out[k] = acc[k];
+    out[q] = acc[QM];
+    out[q + 1] = acc[QM + 1];
   }
-}
-
-// Fused: reductions + assembly + small solve.  Lane c of each warp solves column col0 + c.
-template <int QM, int PM>
-__global__ void __launch_bounds__(DOT_WARPS * 32) epilogue_kernel(
-    int np, int cnt, int q, const double* __restrict__ X, long long ldx,
-    const double* __restrict__ XL, long long ldxl, const double* __restrict__ y,
-    const double* __restrict__ S_TL, const double* __restrict__ b_T, double* __restrict__ beta,
-    int* __restrict__ status, double* __restrict__ sinv) {
-  extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col0 = (blockIdx.x * DOT_WARPS + warp) * DOT_COLS_PER_WARP;
-  double acc[DOT_COLS_PER_WARP][QM + 2];
-  dots_accumulate<QM>(np, cnt, q, col0, X, ldx, XL, ldxl, y, sm, acc);
+  if (beta == nullptr) return;
   const int p = q + 1;
+  double S[PM * PM], rhs[PM], x[PM];
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) S[i * PM + j] = S_TL[i * q + j];
 #pragma unroll
-  for (int c = 0; c < DOT_COLS_PER_WARP; ++c) {
-    const int col = col0 + c;
-    if (col >= cnt || lane != c) continue;
-    double S[PM * PM], rhs[PM], x[PM];
-    for (int i = 0; i < q; ++i)
-      for (int j = 0; j < q; ++j) S[i * PM + j] = S_TL[i * q + j];
-#pragma unroll
-    for (int k = 0; k < QM; ++k)
-      if (k < q) {
-        S[q * PM + k] = acc[c][k];
-        S[k * PM + q] = acc[c][k];
-        rhs[k] = b_T[k];
-      }
-    S[q * PM + q] = acc[c][QM];
-    rhs[q] = acc[c][QM + 1];
-    double* so = sinv ? sinv + (long long)col * (p * (p + 1) / 2) : nullptr;
-    status[col] = small_spd_solve<PM>(p, S, rhs, x, so);
-    for (int i = 0; i < p; ++i) beta[(long long)col * p + i] = x[i];
-  }
+  for (int k = 0; k < QM; ++k)
+    if (k < q) {
+      S[q * PM + k] = acc[k];
+      S[k * PM + q] = acc[k];
+      rhs[k] = b_T[k];
+    }
+  S[q * PM + q] = acc[QM];
+  rhs[q] = acc[QM + 1];
+  double* so = sinv ? sinv + (long long)col * (p * (p + 1) / 2) : nullptr;
+  status[col] = small_spd_solve<PM>(p, S, rhs, x, so);
+  for (int i = 0; i < p; ++i) beta[(long long)col * p + i] = x[i];
 }
 
 template <int PM>
@@ -236,11 +246,6 @@ __global__ void widen_kernel(int n, int np, int cnt, const int8_t* __restrict__ 
   }
 }
 
-size_t dot_smem(int q) { return (size_t)(q + 1) * DOT_CHUNK * sizeof(double); }
-int dot_grid(int cnt) {
-  return (cnt + DOT_WARPS * DOT_COLS_PER_WARP - 1) / (DOT_WARPS * DOT_COLS_PER_WARP);
-}
-
 int check_ld(int n, int ldx, int ldxl) {
   const int np = pad_rows(n);
   if (ldx < np || ldxl < np) {
@@ -252,8 +257,52 @@ int check_ld(int n, int ldx, int ldxl) {
 
 }  // namespace
 
+template <int QM, int PC>
+static int launch_partials(int nrb, int cnt, int q, const double* Xbar, int ldx,
+                           const double* XLbar, int ldxl, const double* ybar, double* P,
+                           cudaStream_t s, const int* gate, int gate_value) {
+  dim3 grid((cnt + PC - 1) / PC, (nrb + PRB - 1) / PRB);
+  const size_t sm = (size_t)(q + 1 + PC) * (PROWS + PRB) * sizeof(double);
+  GG_CUDA_TRY(cudaFuncSetAttribute(partials_kernel<QM, PC>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  partials_kernel<QM, PC><<<grid, PC * 32, sm, s>>>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P,
+                                                    gate, gate_value);
+  GG_LAUNCH_CHECK("partials_kernel");
+  return GG_OK;
+}
+
+int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
+                 int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
+                 int gate_value) {
+  const int nrb = pad_rows(n) / RB;
+  if (q <= 3) return launch_partials<3, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  if (q <= 7) return launch_partials<7, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  return launch_partials<QMAX, 4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+}
+
+int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,
+                     const double* b_T, double* beta, int* status, double* sinv, cudaStream_t s) {
+  const int nrb = pad_rows(n) / RB;
+  const int threads = 256, grid = (cnt + 7) / 8;
+  if (q <= 3)
+    reduce_solve_kernel<3, 4><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T, beta,
+                                                       status, sinv);
+  else if (q <= 7)
+    reduce_solve_kernel<7, 8><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T, beta,
+                                                       status, sinv);
+  else
+    reduce_solve_kernel<QMAX, GG_PMAX><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
+                                                               beta, status, sinv);
+  GG_LAUNCH_CHECK("reduce_solve_kernel");
+  return GG_OK;
+}
+
+size_t partials_bytes(int n, int cnt, int q) {
+  return (size_t)(pad_rows(n) / RB) * (size_t)cnt * (size_t)(q + 2) * sizeof(double);
+}
+
 int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar, int ldxl,
-             const double* ybar, double* dots, cudaStream_t s) {
+             const double* ybar, double* dots, double* P, cudaStream_t s) {
   if (q < 0 || q > QMAX || n < 1) {
     set_error("dots: need 0 <= q <= 19 and n >= 1");
     return GG_EARG;
@@ -261,27 +310,15 @@ int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* X
   if (cnt <= 0) return GG_OK;
   int rc = check_ld(n, ldx, q > 0 ? ldxl : pad_rows(n));
   if (rc != GG_OK) return rc;
-  const int np = pad_rows(n);
-  const size_t sm = dot_smem(q);
-  if (q <= 3) {
-    dots_kernel<3><<<dot_grid(cnt), DOT_WARPS * 32, sm, s>>>(np, cnt, q, Xbar, ldx, XLbar, ldxl,
-                                                            ybar, dots);
-  } else if (q <= 7) {
-    dots_kernel<7><<<dot_grid(cnt), DOT_WARPS * 32, sm, s>>>(np, cnt, q, Xbar, ldx, XLbar, ldxl,
-                                                            ybar, dots);
-  } else {
-    GG_CUDA_TRY(cudaFuncSetAttribute(dots_kernel<QMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sm));
-    dots_kernel<QMAX><<<dot_grid(cnt), DOT_WARPS * 32, sm, s>>>(np, cnt, q, Xbar, ldx, XLbar,
-                                                               ldxl, ybar, dots);
-  }
-  GG_LAUNCH_CHECK("dots_kernel");
-  return GG_OK;
+  rc = partials_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, nullptr, 0);
+  if (rc == GG_OK)
+    rc = reduce_solve_run(n, cnt, q, P, dots, nullptr, nullptr, nullptr, nullptr, nullptr, s);
+  return rc;
 }
 
 int epilogue_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                  int ldxl, const double* ybar, const double* S_TL, const double* b_T,
-                 double* beta, int* status, double* sinv, cudaStream_t s) {
+                 double* beta, int* status, double* sinv, double* P, cudaStream_t s) {
   if (q < 0 || q > QMAX || n < 1) {
     set_error("epilogue: need 0 <= q <= 19 and n >= 1");
     return GG_EARG;
@@ -289,23 +326,10 @@ int epilogue_run(int n, int cnt, int q, const double* Xbar, int ldx, const doubl
   if (cnt <= 0) return GG_OK;
   int rc = check_ld(n, ldx, q > 0 ? ldxl : pad_rows(n));
   if (rc != GG_OK) return rc;
-  const int np = pad_rows(n);
-  const size_t sm = dot_smem(q);
-  const int grid = dot_grid(cnt);
-  if (q <= 3) {
-    epilogue_kernel<3, 4><<<grid, DOT_WARPS * 32, sm, s>>>(np, cnt, q, Xbar, ldx, XLbar, ldxl, ybar,
-                                                           S_TL, b_T, beta, status, sinv);
-  } else if (q <= 7) {
-    epilogue_kernel<7, 8><<<grid, DOT_WARPS * 32, sm, s>>>(np, cnt, q, Xbar, ldx, XLbar, ldxl, ybar,
-                                                           S_TL, b_T, beta, status, sinv);
-  } else {
-    GG_CUDA_TRY(cudaFuncSetAttribute(epilogue_kernel<QMAX, GG_PMAX>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    epilogue_kernel<QMAX, GG_PMAX><<<grid, DOT_WARPS * 32, sm, s>>>(
-        np, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, S_TL, b_T, beta, status, sinv);
-  }
-  GG_LAUNCH_CHECK("epilogue_kernel");
-  return GG_OK;
+  rc = partials_run(n, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, nullptr, 0);
+  if (rc == GG_OK)
+    rc = reduce_solve_run(n, cnt, q, P, nullptr, S_TL, b_T, beta, status, sinv, s);
+  return rc;
 }
 
 int small_solve_run(int batch, int p, const double* S, const double* rhs, double* x, int* status,

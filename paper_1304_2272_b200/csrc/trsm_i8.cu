@@ -46,9 +46,18 @@ struct I8Args {
   int N;            // SNP columns
   int num_rb;       // np / 32
   int num_nt;       // ceil(N / 128)
-  double* X;        // Xbar, column-major, leading dimension ldx
+  double* X;        // Xbar, column-major, leading dimension ldx (nullptr: not materialised)
   long long ldx;
   const int* expo;  // e_i per inverse row (np)
+  // fused epilogue reductions (canonical order of gls_epilogue.cu): partial dots of each SNP's
+  // 32-row block against XLbar (q columns, ld ldxl) and ybar -> P[(rb*N + col)*(q+2) + k]
+  int q;
+  const double* XL;
+  long long ldxl;
+  const double* y;
+  double* P;        // nullptr: no partials
+  const int* gate;  // device flag: the kernel runs only if *gate == gate_value (nullptr: always)
+  int gate_value;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -163,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned accf0 = smem_u32(bars + 2 * STAGES);       // accumulator full  [2]
   const unsigned acce0 = smem_u32(bars + 2 * STAGES + 2);   // accumulator empty [2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.gate != nullptr && *a.gate != a.gate_value) return;   // device-side path selection
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -277,14 +287,33 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_before();
       mbar_arrive(acce0 + 8 * ab);
       const int col = nt * TM + m;
-      if (col < a.N) {
-        const int row0 = rb * TR;
-        double* dst = a.X + (long long)col * a.ldx + row0;
+      const int row0 = rb * TR;
 #pragma unroll
-        for (int i = 0; i < TR; i += 2) {
-          const double2 o = make_double2(ldexp(acc[i], a.expo[row0 + i]),
-                                         ldexp(acc[i + 1], a.expo[row0 + i + 1]));
-          *reinterpret_cast<double2*>(dst + i) = o;
+      for (int i = 0; i < TR; ++i) acc[i] = ldexp(acc[i], a.expo[row0 + i]);   // exact
+      if (col < a.N) {
+        if (a.X != nullptr) {
+          double* dst = a.X + (long long)col * a.ldx + row0;
+#pragma unroll
+          for (int i = 0; i < TR; i += 2)
+            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
+        }
+        if (a.P != nullptr) {
+          double* pp = a.P + ((long long)rb * a.N + col) * (a.q + 2);
+          for (int k = 0; k < a.q; ++k) {
+            const double* xl = a.XL + k * a.ldxl + row0;
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
+            pp[k] = sum;
+          }
+          double sxx = 0.0, sxy = 0.0;
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            sxx = fma(acc[i], acc[i], sxx);
+            sxy = fma(acc[i], a.y[row0 + i], sxy);
+          }
+          pp[a.q] = sxx;
+          pp[a.q + 1] = sxy;
         }
       }
     }
@@ -424,8 +453,16 @@ int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, l
 
 int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
                 long long ldg, double* X, int ldx, cudaStream_t s) {
+  return trsm_i8_fused_run(n, nrhs, Sl, expo, G, ldg, X, ldx, 0, nullptr, 0, nullptr, nullptr,
+                           nullptr, 0, s);
+}
+
+int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
+                      const signed char* G, long long ldg, double* X, int ldx, int q,
+                      const double* XL, int ldxl, const double* y, double* P, const int* gate,
+                      int gate_value, cudaStream_t s) {
   const int np = pad_rows(n);
-  if (ldx < np || ldg < n || (ldg % 16) != 0) {
+  if ((X != nullptr && ldx < np) || ldg < n || (ldg % 16) != 0 || (P != nullptr && ldxl < np)) {
     set_error("trsm_i8: ldx >= gg_pad(n), ldg >= n and ldg a multiple of 16 required");
     return GG_EDIM;
   }
@@ -457,6 +494,13 @@ int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const s
   a.X = X;
   a.ldx = ldx;
   a.expo = expo;
+  a.q = q;
+  a.XL = XL;
+  a.ldxl = ldxl;
+  a.y = y;
+  a.P = P;
+  a.gate = gate;
+  a.gate_value = gate_value;
   const int tiles = a.num_rb * a.num_nt;
   int grid = sms();
   if (grid > tiles) grid = tiles;

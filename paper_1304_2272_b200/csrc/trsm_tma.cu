@@ -41,6 +41,8 @@ struct TrsmArgs {
   int num_nt;     // ceil(N / 128)
   double* C;
   long long ldc;
+  const int* gate;   // run only if *gate == gate_value (nullptr: always)
+  int gate_value;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned empty0 = smem_u32(bars + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.gate != nullptr && *a.gate != a.gate_value) return;   // device-side path selection
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -413,8 +416,10 @@ static int make_packed_map(CUtensorMap* map, const double* base, long long ntile
 
 template <bool PACKED>
 static int launch_trsm(const CUtensorMap& mA, const CUtensorMap& mB, int np, int nrhs, double* X,
-                       int ldx, cudaStream_t s) {
+                       int ldx, cudaStream_t s, const int* gate = nullptr, int gate_value = 0) {
   TrsmArgs a;
+  a.gate = gate;
+  a.gate_value = gate_value;
   a.N = nrhs;
   a.num_mt = np / BM;
   a.num_nt = (nrhs + BN - 1) / BN;
@@ -432,6 +437,11 @@ static int launch_trsm(const CUtensorMap& mA, const CUtensorMap& mB, int np, int
 
 int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int ldb, double* X,
                     int ldx, cudaStream_t s) {
+  return trsm_packed_gated_run(n, nrhs, LinvP, B, ldb, X, ldx, nullptr, 0, s);
+}
+
+int trsm_packed_gated_run(int n, int nrhs, const double* LinvP, const double* B, int ldb,
+                          double* X, int ldx, const int* gate, int gate_value, cudaStream_t s) {
   const int np = pad_rows(n);
   if (ldb < np || ldx < np) {
     set_error("trsm: leading dimensions must be >= gg_pad(n)");
@@ -449,7 +459,7 @@ int trsm_packed_run(int n, int nrhs, const double* LinvP, const double* B, int l
   if (rc != GG_OK) return rc;
   rc = make_kmajor_map(&mB, B, np, nrhs, ldb);
   if (rc != GG_OK) return rc;
-  return launch_trsm<true>(mA, mB, np, nrhs, X, ldx, s);
+  return launch_trsm<true>(mA, mB, np, nrhs, X, ldx, s, gate, gate_value);
 }
 
 int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,

@@ -203,6 +203,40 @@ def _pack_lower(Linv_colmajor, n):
     return P
 
 
+def _slice_inverse(Linv_colmajor, n):
+    """int8 slices + exponents of the inverse (operands of the tensor-core TRSM)."""
+    torch = __import__("torch")
+    from ._device import transpose_square
+
+    LinvT = transpose_square(Linv_colmajor)
+    sl = torch.empty(int(_capi.lib().gg_inverse_slices_bytes(n)), dtype=torch.int8,
+                     device=LinvT.device)
+    expo = torch.empty(LinvT.shape[0], dtype=torch.int32, device=LinvT.device)
+    check(_capi.lib().gg_slice_inverse_i8(n, ptr(LinvT), LinvT.shape[1], ptr(sl), ptr(expo),
+                                          stream_handle()), "gg_slice_inverse_i8")
+    del LinvT
+    return sl, expo
+
+
+def _int8_exact(col):
+    return bool(np.all(np.isfinite(col)) and np.all(col == np.trunc(col))
+                and np.all(np.abs(col) <= 127))
+
+
+def _trsm_i8_device(slices, expo, n, A):
+    """X = L^-1 A for a host matrix of int8-exact columns, on the tensor-core path."""
+    torch = __import__("torch")
+    n16 = -(-n // 16) * 16
+    A = np.asarray(A)
+    G = torch.zeros((A.shape[1], n16), dtype=torch.int8)
+    G[:, :n] = torch.from_numpy(np.ascontiguousarray(A.T).astype(np.int8))
+    G = G.to(slices.device)
+    X = alloc_cols(A.shape[1], pad(n))
+    check(_capi.lib().gg_trsm_lower_i8(n, A.shape[1], ptr(slices), ptr(expo), ptr(G), n16, ptr(X),
+                                       pad(n), stream_handle()), "gg_trsm_lower_i8")
+    return X
+
+
 def _potrf_device(M, keep_square_inverse=False):
     """Device Cholesky + inverse of the n x n matrix M (host array, or CUDA tensor read
     row-major); returns (n, L_dev, LinvP_dev) with the inverse in the packed tile-major layout
@@ -297,10 +331,12 @@ def _dots_device(Xd, n, cnt, XLd, q, yd):
     """dots (cnt x (q+2)) of the device columns Xd against XLd (q columns) and yd."""
     torch = __import__("torch")
     out = torch.empty((max(cnt, 1), q + 2), dtype=torch.float64, device=Xd.device)
+    work = torch.empty(max(int(_capi.lib().gg_partials_bytes(n, max(cnt, 1), q)), 8),
+                       dtype=torch.uint8, device=Xd.device)
     check(_capi.lib().gg_gls_dots_f64(n, cnt, q, ptr(Xd), Xd.shape[1],
                                       ptr(XLd) if q > 0 else None,
                                       XLd.shape[1] if q > 0 else pad(n), ptr(yd), ptr(out),
-                                      stream_handle()), "gg_gls_dots_f64")
+                                      ptr(work), stream_handle()), "gg_gls_dots_f64")
     return out[:cnt]
 
 
@@ -372,13 +408,17 @@ def solve_small_spd(S, rhs):
 # the GLS sweep
 # ---------------------------------------------------------------------------------------------
 
-def gls_prepare(M, XL, y):
+def gls_prepare(M, XL, y, int8_split=True):
     """Hoist all marker-independent work (kernel.py:233-257): factor M (device Cholesky +
     inverse, kept resident), whiten XL and y with the same TRSM kernel as the SNP blocks, and
     form S_TL and b_T with the same reduction kernel as the per-SNP sums.
 
     M may also be a CUDA float64 tensor (n, n) already resident on the device (row-major, as a
-    C-contiguous array would be): the factorisation then reads it in place, no host round trip."""
+    C-contiguous array would be): the factorisation then reads it in place, no host round trip.
+
+    int8_split (default) also stores the inverse as int8 slices so that dosage blocks run on
+    the int8 tensor cores (exact integer products, FP64 recombination); False keeps only the
+    FP64 DMMA TRSM."""
     torch = __import__("torch")
     if not (isinstance(M, torch.Tensor) and M.is_cuda and M.dtype == torch.float64):
         M = np.ascontiguousarray(M, dtype=np.float64)
@@ -392,11 +432,13 @@ def gls_prepare(M, XL, y):
     q = XL.shape[1]
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
-    _, L, LinvP = _potrf_device(M)
-    return prepare_from_inverse(LinvP, n, XL, y, L=L)
+    _, L, LinvP, Linv = _potrf_device(M, keep_square_inverse=True)
+    slices, expo = _slice_inverse(Linv, n) if int8_split else (None, None)
+    del Linv
+    return prepare_from_inverse(LinvP, n, XL, y, L=L, slices=slices, expo=expo)
 
 
-def prepare_from_inverse(LinvP, n, XL, y, L=None):
+def prepare_from_inverse(LinvP, n, XL, y, L=None, slices=None, expo=None):
     """The marker-independent tail of gls_prepare (kernel.py:246-257) given the packed inverse:
     whiten [X_L | y] with the streamed TRSM kernel, S_TL = gram(X_L bar) and b_T with the
     per-SNP reduction kernel, SPD check of S_TL.  Shared by gls_prepare and the distributed
@@ -408,6 +450,15 @@ def prepare_from_inverse(LinvP, n, XL, y, L=None):
     np_ = pad(n)
     RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
     XLy = _trsm_device(LinvP, n, RHS, q + 1)
+    if slices is not None:
+        # covariate columns that are exact small integers (the intercept) are whitened by the
+        # same tensor-core kernel as the dosage blocks, so a SNP equal to such a column gives
+        # an exactly singular S (degenerate-SNP fixture)
+        ints = [j for j in range(q) if _int8_exact(XL[:, j])]
+        if ints:
+            Xi = _trsm_i8_device(slices, expo, n, XL[:, ints])
+            for c, j in enumerate(ints):
+                XLy[j].copy_(Xi[c])
     dev = XLy.device
     dots = _dots_device(XLy, n, q, XLy, q, XLy[q]) if q > 0 else None
     if q > 0:
@@ -434,7 +485,7 @@ def prepare_from_inverse(LinvP, n, XL, y, L=None):
     XLbar = np.asfortranarray(host[:, :q])
     ybar = np.ascontiguousarray(host[:, q])
     dctx = DeviceContext(n=n, np_=np_, q=q, L=L, LinvP=LinvP, XLy=XLy, S_TL=S_TL_d.reshape(-1),
-                         b_T=b_T_d)
+                         b_T=b_T_d, slices=slices, expo=expo)
     return PreparedContext(L=None, XLbar=XLbar, ybar=ybar, S_TL=S_TL, b_T=b_T, _dev=dctx)
 
 
@@ -466,6 +517,7 @@ def device_context(ctx, need_factor=False):
 def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv=False):
     """Per-marker assembly and solve for already-whitened columns Xbar (n x count)
     (kernel.py:273-312); the fused device epilogue.  Returns a list of SnpResult."""
+    torch = __import__("torch")
     d = device_context(ctx)
     Xbar = np.asarray(Xbar, dtype=np.float64)
     if Xbar.ndim != 2 or Xbar.shape[0] != d.n:
@@ -474,9 +526,11 @@ def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv
     ws = BlockWorkspace(d, max(cnt, 1), emit_s_inv=emit_s_inv)
     if cnt:
         Xd = upload_cols(Xbar, ld=d.np_)
+        work = torch.empty(int(_capi.lib().gg_partials_bytes(d.n, cnt, d.q)), dtype=torch.uint8,
+                           device=Xd.device)
         check(_capi.lib().gg_gls_epilogue_f64(
             d.n, cnt, d.q, ptr(Xd), d.np_, ptr(d.XLy), d.np_, ptr(d.ybar), ptr(d.S_TL),
-            ptr(d.b_T), ptr(ws.beta), ptr(ws.status), ptr(ws.sinv), stream_handle()),
+            ptr(d.b_T), ptr(ws.beta), ptr(ws.status), ptr(ws.sinv), ptr(work), stream_handle()),
             "gg_gls_epilogue_f64")
     return list(_collect(ws, cnt, first_index, global_indices, emit_s_inv).results)
 
@@ -493,8 +547,9 @@ def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
     int8 = blk.data.dtype == np.int8
     ws = BlockWorkspace(d, cnt, emit_s_inv=emit_s_inv, int8_input=int8)
     if int8:
-        G = upload_cols(blk.data, ld=d.n)
-        ws.run(cnt, G8=G, ldg=d.n)
+        n16 = -(-d.n // 16) * 16
+        G = upload_cols(blk.data, ld=n16)
+        ws.run(cnt, G8=G, ldg=n16)
     else:
         X = upload_cols(np.asarray(blk.data, dtype=np.float64), ld=d.np_)
         ws.run(cnt, X64=X, ldx=d.np_)

@@ -156,7 +156,8 @@ class StreamEngine:
         self.int8 = bool(int8)
         self.emit_s_inv = bool(emit_s_inv)
         d = self.d
-        self.ld_in = d.n if self.int8 else d.np_
+        # int8 dosage rows pitched to 16 bytes (TMA operand of the tensor-core TRSM)
+        self.ld_in = (-(-d.n // 16) * 16) if self.int8 else d.np_
         dt = torch.int8 if self.int8 else torch.float64
         self.ws = [BlockWorkspace(d, self.m_blk, emit_s_inv, self.int8) for _ in range(self.REGIONS)]
         self.dev_in = [alloc_cols(self.m_blk, self.ld_in, dtype=dt) for _ in range(self.REGIONS)]

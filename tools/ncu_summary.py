@@ -26,6 +26,9 @@ KEYS = [
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__t_sector_hit_rate.pct",
@@ -97,17 +100,22 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--cnt", type=int, default=8192)
+    ap.add_argument("--engine", choices=["dmma", "i8"], default="i8")
     args = ap.parse_args()
     os.makedirs(PROFILES, exist_ok=True)
     if args.rep:
         ks = kernels(args.rep)
         with open(os.path.join(PROFILES, f"{args.tag}_ncu_kernels.json"), "w") as f:
             json.dump({"source": os.path.basename(args.rep), "kernels": ks}, f, indent=1)
-        trsm = [k for k in ks if "trsm" in k["kernel"] or "dgemm" in k["kernel"]]
+        trsm = [k for k in ks if ("trsm_i8" in k["kernel"]) == (args.engine == "i8")
+                and ("trsm" in k["kernel"] or "dgemm" in k["kernel"])]
         if trsm:
             k = trsm[0]
             rd, wr = k.get("dram__bytes_read.sum"), k.get("dram__bytes_write.sum")
-            algo = 8.0 * (args.n * args.cnt * 2 + args.n * args.n / 2)
+            if args.engine == "i8":   # int8 dosages in, S=8 int8 slices of the triangle, partials out
+                algo = args.n * args.cnt + 8 * args.n * args.n / 2 + 8.0 * 5 * args.cnt * args.n / 32
+            else:                     # FP64 block in, packed FP64 triangle, FP64 Xbar out
+                algo = 8.0 * (args.n * args.cnt * 2 + args.n * args.n / 2)
             summ = {
                 "source": f"profiles/{args.tag}_ncu_kernels.json ({os.path.basename(args.rep)}, "
                           "ncu --set full --clock-control none)",
@@ -119,7 +127,7 @@ def main():
                 "dmma_pipe_active_pct": k.get(
                     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
             }
-            with open(os.path.join(PROFILES, "ncu_trsm_summary.json"), "w") as f:
+            with open(os.path.join(PROFILES, f"ncu_trsm_{args.engine}_summary.json"), "w") as f:
                 json.dump(summ, f, indent=1)
             print(json.dumps(summ, indent=1))
     if args.launches:

@@ -67,16 +67,38 @@ def main():
     for _ in range(2):
         check(lib.gg_trsm_lower_packed_f64(n, args.cnt, ptr(d.LinvP), ptr(X), np_, ptr(xbar), np_, s), "trsm")
     torch.cuda.synchronize()
+    # int8 tensor-core path (the production path for dosage blocks)
+    n16 = -(-n // 16) * 16
+    G16 = datagen.genotypes_device(spec, 0, args.cnt, ld=n16)
+    P = torch.empty(int(lib.gg_partials_bytes(n, args.cnt, d.q)) // 8, dtype=torch.float64,
+                    device="cuda")
+    for rep in range(args.reps + 1):
+        a, b, c = ev(), ev(), ev()
+        if rep > 0:
+            torch.cuda.nvtx.range_push("hot")
+        a.record()
+        check(lib.gg_trsm_lower_i8_partials(n, args.cnt, ptr(d.slices), ptr(d.expo), ptr(G16), n16,
+                                            d.q, ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0, None, 0,
+                                            s), "trsm_i8")
+        b.record()
+        check(lib.gg_gls_reduce_solve_f64(n, args.cnt, d.q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
+                                          ptr(beta), ptr(st), None, s), "reduce")
+        c.record()
+        if rep > 0:
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        fl = float(n) * n * args.cnt
+        print(f"i8 rep {rep}: trsm+partials {a.elapsed_time(b):.3f} ms = "
+              f"{fl / a.elapsed_time(b) / 1e9:.1f} TF/s FP64-equivalent; reduce+solve "
+              f"{b.elapsed_time(c):.3f} ms")
     for rep in range(args.reps):
         a, b, c = ev(), ev(), ev()
-        torch.cuda.nvtx.range_push("hot")
         a.record()
         check(lib.gg_trsm_lower_packed_f64(n, args.cnt, ptr(d.LinvP), ptr(X), np_, ptr(xbar), np_, s), "trsm")
         b.record()
         check(lib.gg_gls_epilogue_f64(n, args.cnt, d.q, ptr(xbar), np_, ptr(d.XLy), np_, ptr(d.ybar),
-                                      ptr(d.S_TL), ptr(d.b_T), ptr(beta), ptr(st), None, s), "epi")
+                                      ptr(d.S_TL), ptr(d.b_T), ptr(beta), ptr(st), None, ptr(P), s), "epi")
         c.record()
-        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         t_trsm = a.elapsed_time(b)
         t_epi = b.elapsed_time(c)
