@@ -58,7 +58,6 @@ def parse_args():
     ap.add_argument("--block-snps", type=int, default=8192)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-dtype", choices=["f64", "i8"], default="f64")
     ap.add_argument("--trsm", choices=["i8", "dmma"], default="i8",
                     help="TRSM engine: int8 tensor cores with the sliced inverse (default) or "
                          "the FP64 DMMA kernel")
@@ -234,7 +233,7 @@ def run_ours(args):
                 if record:
                     ev_pairs[i][1].record(stream)
                 rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
-                                                  ptr(beta[f]), ptr(status[f]), None, ptr(P), sh)
+                                                  ptr(beta[f]), ptr(status[f]), None, sh)
                 nl += 2
             else:
                 if X is not None:
@@ -374,51 +373,53 @@ def run_ours(args):
 
 
 def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
-    """Same metric through pipeline.solve_array with host genotypes: every step H2D-copies all
-    m markers from pinned host memory (double-buffered, copy stream) and reads the results back."""
-    dtype = args.e2e_dtype
-    try:   # FP64 host genotypes need m*n*8 pinned bytes per rank; keep well inside host RAM
-        import psutil
+    """Same metric through the public stream API, pipeline.solve_array, with the genotypes in
+    pinned host memory: every step H2D-copies all m markers (copy stream, double-buffered) and
+    reads every block's results back.  Primary: int8 dosages on the host (the GWAI / config-2
+    storage format, n bytes per SNP); also reported: FP64 host genotypes (8 n bytes per SNP,
+    PCIe-bound) when host memory allows."""
+    src = X[:, :n] if X.dtype == torch.float64 else X[:, :n]
+    out = {}
+    for dtype in ("i8", "f64"):
+        if dtype == "f64":
+            try:   # FP64 host genotypes need m*n*8 pinned bytes per rank
+                import psutil
 
-        if world * m * n * 8 > 0.5 * psutil.virtual_memory().available:
-            dtype = "i8"
-    except ImportError:
-        pass
-    src = X[:, :n] if X.dtype == torch.float64 else X           # (m, n) FP64 view or int8
-    try:
-        if dtype == "f64" and X.dtype == torch.float64:
-            host_t = torch.empty((m, n), dtype=torch.float64).pin_memory()
-            host_t.copy_(src)
-        else:
-            raise RuntimeError("int8 host genotypes")
-    except RuntimeError:
-        host_t = torch.empty((m, n), dtype=torch.int8).pin_memory()
-        host_t.copy_(src.to(torch.int8))
-    Xh = host_t.numpy().T                     # n x m, Fortran-ordered view of pinned memory
-    int8 = Xh.dtype == np.int8
-    engine = pipeline.StreamEngine(ctx, args.block_snps, int8=int8)
-    res = pipeline.solve_array(ctx, Xh, engine=engine)      # warm-up
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    h0, d0 = engine.h2d_bytes, engine.d2h_bytes
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        res = pipeline.solve_array(ctx, Xh, engine=engine)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    ok = bool(np.all(res.ok))
-    del host_t
-    return {"value": round(m * world * args.steps / dt, 1), "unit": UNIT,
+                if world * m * n * 8 > 0.5 * psutil.virtual_memory().available:
+                    continue
+            except ImportError:
+                pass
+        engine = pipeline.StreamEngine(ctx, args.block_snps, int8=dtype == "i8")
+        tdt = torch.int8 if dtype == "i8" else torch.float64
+        host_t = torch.empty((m, n), dtype=tdt).pin_memory()
+        host_t.copy_(src.to(tdt))
+        Xh = host_t.numpy().T                 # n x m, Fortran-ordered view of pinned memory
+        res = pipeline.solve_array(ctx, Xh, engine=engine)      # warm-up
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        h0, d0 = engine.h2d_bytes, engine.d2h_bytes
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = pipeline.solve_array(ctx, Xh, engine=engine)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        out[dtype] = {
+            "value": round(m * world * args.steps / dt, 1), "unit": UNIT,
             "h2d_bytes_per_step": int((engine.h2d_bytes - h0) // args.steps),
             "d2h_bytes_per_step": int((engine.d2h_bytes - d0) // args.steps),
             "api": "paper_1304_2272_b200.pipeline.solve_array (pinned host "
-                   f"{'int8' if int8 else 'FP64'} genotypes, double-buffered H2D)",
-            "all_snps_ok": ok}
+                   f"{'int8' if dtype == 'i8' else 'FP64'} genotypes, double-buffered H2D)",
+            "all_snps_ok": bool(np.all(res.ok))}
+        del host_t, engine, Xh
+    e2e = dict(out["i8"])
+    if "f64" in out:
+        e2e["fp64_host"] = out["f64"]
+    return e2e
 
 
 def _blas_threads():

@@ -80,12 +80,33 @@ def load_library(path=LIB_PATH):
     return lib
 
 
+class _CheckedLib:
+    """Arity-checked view of the library: ctypes forwards surplus arguments to a C function
+    silently (the last one would be taken as the stream); refuse them instead."""
+
+    def __init__(self, cdll):
+        self._cdll = cdll
+
+    def __getattr__(self, name):
+        fn = getattr(self._cdll, name)
+        want = len(SIGNATURES[name][1]) if name in SIGNATURES else None
+
+        def call(*args):
+            if want is not None and len(args) != want:
+                raise TypeError(f"{name} takes {want} arguments ({len(args)} given)")
+            return fn(*args)
+
+        call.__name__ = name
+        setattr(self, name, call)
+        return call
+
+
 def lib():
     global _lib
     if _lib is None:
         with _lock:
             if _lib is None:
-                _lib = load_library()
+                _lib = _CheckedLib(load_library())
     return _lib
 
 

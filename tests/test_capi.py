@@ -62,3 +62,25 @@ def test_sm100a_code_in_library():
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "DMMA" in out, "FP64 tensor-core (DMMA) instructions missing from the GEMM"
+
+
+def test_every_ctypes_call_matches_declared_arity():
+    """A C-ABI call with an extra or missing argument passes garbage as the stream pointer; catch
+    it statically for every call site in the package, bench and tools."""
+    import ast
+
+    from paper_1304_2272_b200 import _capi
+
+    files = ["bench.py", "__graft_entry__.py"]
+    for d in ("paper_1304_2272_b200", "tools", "tests"):
+        files += [os.path.join(d, f) for f in os.listdir(os.path.join(REPO, d)) if f.endswith(".py")]
+    bad = []
+    for f in files:
+        tree = ast.parse(open(os.path.join(REPO, f)).read())
+        for node in ast.walk(tree):
+            if (isinstance(node, ast.Call) and isinstance(node.func, ast.Attribute)
+                    and node.func.attr in _capi.SIGNATURES):
+                want = len(_capi.SIGNATURES[node.func.attr][1])
+                if len(node.args) != want:
+                    bad.append((f, node.lineno, node.func.attr, len(node.args), want))
+    assert not bad, bad

@@ -1,0 +1,118 @@
+"""GPU: the int8 tensor-core TRSM path (inverse split into int8 slices, exact int32 products,
+FP64 recombination) against the FP64 DMMA path and the oracle; its fused reductions against the
+standalone ones; device-side fallback for non-integer FP64 blocks."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, make_spd, maxnorm
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K(gpu):
+    from paper_1304_2272_b200 import kernel
+
+    return kernel
+
+
+def _betas(rb):
+    return np.array([r.beta for r in rb.results])
+
+
+@pytest.mark.parametrize("n,cnt", [(37, 5), (300, 257), (1000, 129), (1001, 300)])
+def test_i8_trsm_matches_dmma(K, n, cnt):
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._capi import ptr, stream_handle
+    from paper_1304_2272_b200._device import alloc_cols, upload_cols
+
+    M = make_spd(n, n)
+    _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+    sl, expo = K._slice_inverse(Linv, n)
+    G = np.random.default_rng(n).integers(0, 3, (n, cnt))
+    np_ = _capi.pad(n)
+    Xd = K._trsm_device(LinvP, n, upload_cols(G.astype(float), ld=np_), cnt)
+    Xi = K._trsm_i8_device(sl, expo, n, G)
+    torch.cuda.synchronize()
+    ref = Xd[:, :n].cpu().numpy()
+    got = Xi[:, :n].cpu().numpy()
+    colrel = np.max(np.abs(got - ref), axis=1) / np.max(np.abs(ref), axis=1)
+    assert colrel.max() <= 1e-13, colrel.max()
+    assert bool((Xi[:, n:] == 0).all())
+    # bitwise column-permutation invariance of the tensor-core path
+    perm = np.random.default_rng(1).permutation(cnt)
+    Xp = K._trsm_i8_device(sl, expo, n, G[:, perm]).cpu().numpy()
+    assert np.array_equal(Xp, Xi.cpu().numpy()[perm])
+
+
+@pytest.mark.parametrize("case", ["seed42", "baseline_p4", "baseline_p8", "degenerate"])
+def test_i8_and_dmma_paths_agree_with_reference(K, case):
+    from oracle import gls_ref as O
+
+    g = golden(case)
+    X = g["G"].astype(float)
+    ctx8 = K.gls_prepare(g["M"], g["XL"], g["y"])
+    ctx64 = K.gls_prepare(g["M"], g["XL"], g["y"], int8_split=False)
+    assert ctx8._dev.slices is not None and ctx64._dev.slices is None
+    b8 = _betas(K.gls_solve_block(ctx8, K.SnpBlock(0, X)))
+    b64 = _betas(K.gls_solve_block(ctx64, K.SnpBlock(0, X)))
+    for b in (b8, b64):
+        rel, mism = O.compare(b, g["beta"])
+        assert mism == 0 and rel <= 1e-9, rel
+    rel, mism = O.compare(b8, b64)
+    assert mism == 0 and rel <= 1e-12
+
+
+def test_fused_reductions_equal_standalone(K):
+    """The TRSM epilogue's fused partial dots give the same bits as the standalone reductions
+    applied to the same Xbar (one canonical order)."""
+    g = golden("baseline_p4")
+    ctx = K.gls_prepare(g["M"], g["XL"], g["y"])
+    G = g["G"][:, :300]
+    fused = _betas(K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(G))))
+    n = g["M"].shape[0]
+    Xbar = K._trsm_i8_device(ctx._dev.slices, ctx._dev.expo, n, G)[:, :n].cpu().numpy().T
+    res = K.solve_whitened_block(ctx, Xbar, 0)
+    assert np.array_equal(np.array([r.beta for r in res]), fused)
+
+
+def test_non_integer_block_falls_back_to_dmma(K):
+    """FP64 blocks are narrowed on the device; any non-integer value routes the block through
+    the FP64 DMMA TRSM (chosen on the device, no host sync).  Results match the oracle."""
+    from oracle import gls_ref as O
+
+    rng = np.random.default_rng(3)
+    n = 200
+    M = make_spd(n, 5)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 2))])
+    y = rng.standard_normal(n)
+    Xint = rng.integers(0, 3, (n, 40)).astype(float)
+    Xmix = Xint.copy()
+    Xmix[7, 3] = 0.5                              # one non-integer dosage
+    Xbig = Xint.copy()
+    Xbig[0, 0] = 300.0                            # out of int8 range
+    ctx = K.gls_prepare(M, XL, y)
+    octx = O.gls_prepare(M, XL, y)
+    for X in (Xint, Xmix, Xbig):
+        got = _betas(K.gls_solve_block(ctx, K.SnpBlock(0, X)))
+        ref, ok = O.gls_solve_block(octx, X)
+        rel, mism = O.compare(got, ref)
+        assert mism == 0 and rel <= 1e-11, rel
+
+
+def test_intercept_duplicate_exactly_singular(K):
+    """A SNP equal to the intercept: whitened by the same tensor-core kernel as X_L[:,0] and
+    reduced in the same order, S is exactly singular and the SNP is flagged degenerate."""
+    rng = np.random.default_rng(9)
+    n = 150
+    M = make_spd(n, 2)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 2))])
+    ctx = K.gls_prepare(M, XL, rng.standard_normal(n))
+    X = rng.integers(0, 3, (n, 10)).astype(np.int8)
+    X[:, 4] = 1
+    rb = K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(X)))
+    st = [r.status for r in rb.results]
+    assert st[4] == "degenerate" and st.count("degenerate") == 1
