@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -148,6 +149,11 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// 2^e as a double for |e| < 1022 (exact; built from the exponent bits, no libm call)
+__device__ __forceinline__ double pow2(int e) {
+  return __longlong_as_double((long long)(1023 + e) << 52);
 }
 
 __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int s = S - 1; s >= 0; --s) {
         int v[32];
         tmem_ld32(taddr + s * TR, v);
-        const double w = exp2(-7.0 * (s + 1));
+        const double w = pow2(-7 * (s + 1));
 #pragma unroll
         for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], w, acc[i]);
       }
@@ -289,7 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int col = nt * TM + m;
       const int row0 = rb * TR;
 #pragma unroll
-      for (int i = 0; i < TR; ++i) acc[i] = ldexp(acc[i], a.expo[row0 + i]);   // exact
+      for (int i = 0; i < TR; ++i) acc[i] *= pow2(a.expo[row0 + i]);   // exact power-of-two scale
       if (col < a.N) {
         if (a.X != nullptr) {
           double* dst = a.X + (long long)col * a.ldx + row0;
@@ -321,6 +327,240 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+  }
+}
+
+// ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
+// A cluster of 2 CTAs on a TPC computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs issued
+// by the leader: each CTA stages its own 128 SNPs (A) and HALF of the slices (B is split along N:
+// CTA0 slices 0..3, CTA1 slices 4..7), so per-SM staging traffic drops by a third and 6 stages fit
+// in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
+// commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
+// threads release the accumulator on the leader's "accumulator empty" barrier.
+constexpr int P_STAGES = 6;
+constexpr int P_SLICES = S / 2;
+constexpr int P_B_BYTES = P_SLICES * TR * TK;        // 16 KB
+constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 32 KB
+constexpr size_t P_SMEM_BYTES = size_t(P_STAGES) * P_STAGE_BYTES + 1024 + 256;
+constexpr unsigned IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
+                            ((unsigned)(2 * TM >> 4) << 24);
+constexpr unsigned PEER_MASK = 0xFEFFFFFFu;          // clear the CTA-rank bit: the leader's copy
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" :::
+                   "memory");
+}
+__device__ __forceinline__ void tma_2d_pair(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_pair(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(unsigned d_tmem, unsigned long long a,
+                                            unsigned long long b, unsigned accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(unsigned bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    trsm_i8_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, I8Args a) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + P_STAGES * P_STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * P_STAGES + 4);
+  const unsigned sbase = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars);
+  const unsigned empty0 = smem_u32(bars + P_STAGES);
+  const unsigned accf0 = smem_u32(bars + 2 * P_STAGES);
+  const unsigned acce0 = smem_u32(bars + 2 * P_STAGES + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rank = cluster_rank();
+  const bool leader = rank == 0;
+  if (a.gate != nullptr && *a.gate != a.gate_value) return;   // uniform over the grid
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 2 * 4 * 32);   // both CTAs' epilogue threads (leader's copy used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const unsigned tmem_base = *tmem_slot;
+
+  const int num_pp = (a.num_nt + 1) / 2;          // 256-SNP tile pairs
+  const int total = a.num_rb * num_pp;
+  const int G = gridDim.x / 2, cid = blockIdx.x / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int r = 0;; ++r) {
+        const int t = tile_of(r, cid, G);
+        if (t >= total) break;
+        int rb, pp;
+        tile_coords(t, a.num_rb, num_pp, rb, pp);
+        const int nt = 2 * pp + (int)rank;
+        const int nk = (rb + 4) / 4;
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const unsigned fb = full0 + 8 * stage;
+          if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
+          const unsigned dA = sbase + stage * P_STAGE_BYTES;
+          tma_2d_pair(dA, &tmA, fb & PEER_MASK, kt * TK, nt * TM);
+          tma_3d_pair(dA + A_BYTES, &tmB, fb & PEER_MASK, kt * TK, rb * TR, (int)rank * P_SLICES);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      int stage = 0;
+      unsigned phase = 0;
+      int it = 0;
+      for (int r = 0;; ++r, ++it) {
+        const int t = tile_of(r, cid, G);
+        if (t >= total) break;
+        int rb, pp;
+        tile_coords(t, a.num_rb, num_pp, rb, pp);
+        const int nk = (rb + 4) / 4;
+        const int ab = it & 1;
+        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);
+        fence_after();
+        const unsigned d_tmem = tmem_base + ab * ACC_COLS;
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(full0 + 8 * stage, phase);
+          fence_after();
+          const unsigned sa = sbase + stage * P_STAGE_BYTES;
+          const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TK / 32; ++kk)
+            mma_i8_pair(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_pair(empty0 + 8 * stage);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(accf0 + 8 * ab);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    int it = 0;
+    for (int r = 0;; ++r, ++it) {
+      const int t = tile_of(r, cid, G);
+      if (t >= total) break;
+      int rb, pp;
+      tile_coords(t, a.num_rb, num_pp, rb, pp);
+      const int nt = 2 * pp + (int)rank;
+      const int ab = it & 1;
+      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
+      fence_after();
+      double acc[TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
+      const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
+#pragma unroll 1
+      for (int s = S - 1; s >= 0; --s) {
+        int v[32];
+        tmem_ld32(taddr + s * TR, v);
+        const double w = pow2(-7 * (s + 1));
+#pragma unroll
+        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], w, acc[i]);
+      }
+      fence_before();
+      mbar_arrive_cluster((acce0 + 8 * ab) & PEER_MASK);
+      const int col = nt * TM + m;
+      const int row0 = rb * TR;
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] *= pow2(a.expo[row0 + i]);
+      if (col < a.N) {
+        if (a.X != nullptr) {
+          double* dst = a.X + (long long)col * a.ldx + row0;
+#pragma unroll
+          for (int i = 0; i < TR; i += 2)
+            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
+        }
+        if (a.P != nullptr) {
+          double* ppo = a.P + ((long long)rb * a.N + col) * (a.q + 2);
+          for (int k = 0; k < a.q; ++k) {
+            const double* xl = a.XL + k * a.ldxl + row0;
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
+            ppo[k] = sum;
+          }
+          double sxx = 0.0, sxy = 0.0;
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            sxx = fma(acc[i], acc[i], sxx);
+            sxy = fma(acc[i], a.y[row0 + i], sxy);
+          }
+          ppo[a.q] = sxx;
+          ppo[a.q + 1] = sxy;
+        }
+      }
+    }
+  }
+  fence_before();
+  cluster_sync();   // every MMA retired and every remote arrival delivered before freeing TMEM
+  fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
                  "r"(2 * ACC_COLS)
                  : "memory");
   }
@@ -501,6 +741,36 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.P = P;
   a.gate = gate;
   a.gate_value = gate_value;
+  const char* pair_env = getenv("GG_I8_PAIR");
+  const bool pair = !(pair_env != nullptr && pair_env[0] == '0');
+  if (pair) {
+    CUtensorMap mB2;
+    cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
+    cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
+    cuuint32_t box[3] = {TK, TR, P_SLICES};
+    int rc = encode(&mB2, 3, Sl, dims, strides, box);
+    if (rc != GG_OK) return rc;
+    const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
+    int clusters = sms() / 2;
+    if (clusters > pairs) clusters = pairs;
+    GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_pair_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)P_SMEM_BYTES));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = P_SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB2, a));
+    return GG_OK;
+  }
   const int tiles = a.num_rb * a.num_nt;
   int grid = sms();
   if (grid > tiles) grid = tiles;
