@@ -171,10 +171,9 @@ int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, i
  * dots[j*(q+2) + k] = sum_i Xbar[i,j]*XLbar[i,k]  (k < q)      (kernel.py:266-267)
  * dots[j*(q+2) + q] = sum_i Xbar[i,j]^2                          (kernel.py:268)
  * dots[j*(q+2)+q+1] = sum_i Xbar[i,j]*ybar[i]                    (kernel.py:269)
- * One fixed summation order for every column: each block of GG_DOT_BLOCK rows is summed
- * exactly in 128-bit fixed point (block exponents, 61-bit mantissas) and rounded once; block
- * sums are strided over 32 lanes then an xor butterfly (replaces _column_sums,
- * kernel.py:260-270, and kernel.gram, kernel.py:124-131).                                */
+ * One fixed summation order for every column: FMA chains over blocks of GG_DOT_BLOCK rows,
+ * block sums strided over 32 lanes then an xor butterfly (replaces _column_sums,
+ * kernel.py:260-270, and kernel.gram, kernel.py:124-131).                               */
 int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                     const double* XLbar, int ldxl, const double* ybar, double* dots,
                     void* work, void* stream);   /* work: gg_partials_bytes(n, cnt, q) bytes */

@@ -8,15 +8,13 @@
 //                                             placeholder pivot 1.0, NaN for failed systems,
 //                                             optional packed S^-1 (np.tril_indices order)
 // Canonical reduction order (shared with the fused epilogue of the int8 TRSM, trsm_i8.cu):
-//   partial_rb = canonical fixed-point block dot over the 32 rows of row block rb (exact
-//                128-bit sum rounded once, fixed_dot.cuh; no FP64 pipe needed);
+//   partial_rb = FMA chain over the 32 rows of row block rb, in order;
 //   lane_l     = sum of partial_rb for rb = l, l+32, l+64, ... in order (l = 0..31);
 //   dot        = xor-butterfly sum of the 32 lane values (identical on every lane).
 // Every column uses this order whatever its position, and gram(XLbar) / S_TL / b_T are formed
 // the same way, so a SNP column equal to a covariate column yields an exactly singular S (the
 // degenerate-SNP case, tests/conftest.py:29-41).  Two kernels: partials (per column and row
 // block; or written directly by the int8 TRSM epilogue) and reduce+solve (per column).
-#include "fixed_dot.cuh"
 #include "gg_internal.cuh"
 
 namespace gg {
@@ -110,10 +108,10 @@ __device__ int small_spd_solve(int p, const double* S, const double* rhs, double
 // 32-row block rb (layout shared with the fused epilogue of trsm_i8.cu).
 // CTA = 8 warps = 8 columns x 32 row blocks (1024 rows): XL/y rows staged once per CTA, each
 // warp stages its column's 1024 values (coalesced, padded against bank conflicts) and lane l
-// computes row block l's partials in the canonical sub-chain order.
+// computes row block l's partial with one sequential FMA chain per output.
 constexpr int PRB = 32;               // row blocks per CTA (one per lane)
 constexpr int PROWS = PRB * RB;       // 1024 rows
-template <int PCOLS>                  // PCOLS columns per CTA (one per warp)
+template <int QM, int PCOLS>          // PCOLS columns per CTA (one per warp)
 __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
     int nrb, int cnt, int q, const double* __restrict__ X, long long ldx,
     const double* __restrict__ XL, long long ldxl, const double* __restrict__ y,
@@ -141,28 +139,24 @@ __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
   const int rb = rb0 + lane;
   if (col >= cnt || rb >= nrb) return;
   const double* xr = mx + lane * (RB + 1);
-  // canonical block dots (fixed_dot.cuh): exact fixed-point sums, rounded once
-  int Ex = fx_exp(xr[0]);
+  double acc[QM + 2];
 #pragma unroll
-  for (int i = 1; i < RB; ++i) Ex = max(Ex, fx_exp(xr[i]));
-  Fx2 U[RB];
+  for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
+  for (int i = 0; i < RB; ++i) {
+    const double xv = xr[i];
+    const int r = lane * (RB + 1) + i;
 #pragma unroll
-  for (int i = 0; i < RB; ++i) U[i] = fx_split(fx_scale(xr[i], Ex));
-  double* out = P + ((long long)rb * cnt + col) * (q + 2);
-  FxAcc sxx = {0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < RB; ++i) fx_mac(sxx, U[i], U[i]);
-  out[q] = fx_finish(sxx, Ex, Ex);
-  for (int k = 0; k <= q; ++k) {   // the q covariate columns, then ybar
-    const double* w = sv + k * LDP + lane * (RB + 1);
-    int Ew = fx_exp(w[0]);
-#pragma unroll
-    for (int i = 1; i < RB; ++i) Ew = max(Ew, fx_exp(w[i]));
-    FxAcc acc = {0, 0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < RB; ++i) fx_mac(acc, U[i], fx_split(fx_scale(w[i], Ew)));
-    out[k < q ? k : q + 1] = fx_finish(acc, Ex, Ew);
+    for (int k = 0; k < QM; ++k)
+      if (k < q) acc[k] = fma(xv, sv[k * LDP + r], acc[k]);
+    acc[QM] = fma(xv, xv, acc[QM]);
+    acc[QM + 1] = fma(xv, sv[q * LDP + r], acc[QM + 1]);
   }
+  double* out = P + ((long long)rb * cnt + col) * (q + 2);
+#pragma unroll
+  for (int k = 0; k < QM; ++k)
+    if (k < q) out[k] = acc[k];
+  out[q] = acc[QM];
+  out[q + 1] = acc[QM + 1];
 }
 
 // One warp per column: lane l sums the partials of row blocks l, l+32, l+64, ... in order, an
@@ -263,15 +257,15 @@ int check_ld(int n, int ldx, int ldxl) {
 
 }  // namespace
 
-template <int PC>
+template <int QM, int PC>
 static int launch_partials(int nrb, int cnt, int q, const double* Xbar, int ldx,
                            const double* XLbar, int ldxl, const double* ybar, double* P,
                            cudaStream_t s, const int* gate, int gate_value) {
   dim3 grid((cnt + PC - 1) / PC, (nrb + PRB - 1) / PRB);
   const size_t sm = (size_t)(q + 1 + PC) * (PROWS + PRB) * sizeof(double);
-  GG_CUDA_TRY(cudaFuncSetAttribute(partials_kernel<PC>,
+  GG_CUDA_TRY(cudaFuncSetAttribute(partials_kernel<QM, PC>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  partials_kernel<PC><<<grid, PC * 32, sm, s>>>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P,
+  partials_kernel<QM, PC><<<grid, PC * 32, sm, s>>>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P,
                                                     gate, gate_value);
   GG_LAUNCH_CHECK("partials_kernel");
   return GG_OK;
@@ -281,9 +275,9 @@ int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const doubl
                  int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
                  int gate_value) {
   const int nrb = pad_rows(n) / RB;
-  if (q <= 7)
-    return launch_partials<8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
-  return launch_partials<4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  if (q <= 3) return launch_partials<3, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  if (q <= 7) return launch_partials<7, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  return launch_partials<QMAX, 4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
 }
 
 int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,

@@ -2,32 +2,22 @@
 // with the FP64 inverse split error-free into S int8 slices (Ozaki-style splitting).
 //
 // Genotype dosages {0,1,2} are exact int8.  Each row i of Linv is written as
-//     Linv[i,k] = 2^e_i * sum_{s=0..S-1} a_s[i,k] * 2^(-7 (s+1)),   a_s int8 in [-127, 127]
+//     Linv[i,k] = 2^e_i * sum_{s=1..S} a_s[i,k] * 2^(-7 s),   a_s int8 in [-127, 127]
 // (truncation residual < 2^(e_i - 7 S); S = 8 -> 56 bits, finer than FP64's 53), so
-//     Xbar[i,j] = 2^(e_i - 56) * T[i,j],   T = sum_s 2^(7 (7 - s)) C_s,   C_s = a_s . G
-// where every C_s is an EXACT int32 product (|C_s| <= 127*2*n < 2^31 for n < 8.4e6) computed by
-// tcgen05.mma.kind::i8, T is assembled exactly in 128-bit integers and rounded ONCE to double:
-// Xbar is the correctly rounded value of (sliced inverse) x G, whatever the column's position
-// (bitwise permutation invariance).
+//     Xbar[i,j] = 2^e_i * sum_s 2^(-7 s) * C_s[i,j],   C_s = sum_k a_s[i,k] G[k,j]
+// where every C_s is an EXACT int32 integer product (|C_s| <= 127*2*n < 2^31 for n < 8.4e6)
+// computed by tcgen05.mma.kind::i8.  The S terms are recombined in FP64 in a fixed order, so
+// a column's result never depends on its position (bitwise permutation invariance).
 //
-// The epilogue uses no FP64 instruction (fixed_dot.cuh: the FP64 pipe is throttled while the
-// tensor core runs); its per-SNP reductions are the canonical fixed-point block dots.
-//
-// Kernel: persistent, clusters of 2 CTAs (one per SM of a TPC), warp-specialised, 6 warps/CTA.
-// A pair computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs (tcgen05 cta_group::2)
-// issued by the leader CTA: each CTA stages its own 128 SNPs (A) and HALF of the slices (B split
-// along N: CTA0 slices 0..3, CTA1 slices 4..7).
-//   warp 0  TMA producer (both CTAs): A = genotype tile (128 SNPs x 128 k, int8, 128B swizzle, k
-//           >= n zero-filled), B = 4 slices of 32 inverse rows (3-D box 128 k x 32 rows x 4) into
-//           a 6-stage ring (32 KB / stage); both CTAs' loads complete on the leader's barrier.
-//           Also stages each tile's row data (e_i, the 32 rows of XLbar's q columns and of ybar)
-//           with bulk copies into a 4-slot ring.
-//   warp 1  MMA issuer (leader, one lane): D[256 SNPs x 256] += A . B^T, 4 x K=32 per stage,
-//           int32 accumulators in TMEM, double-buffered (2 x 256 columns); commits multicast to
-//           both CTAs' barriers.
-//   warps 2-5  epilogue (both CTAs): tcgen05.ld the S x 32 accumulators of each SNP, exact
-//           recombination + one rounding, then Xbar and/or the canonical partial dots.
-// Tiles = (32-row blocks of Linv) x (256-SNP column pairs); row block rb needs k < 32 (rb+1).
+// Kernel (persistent, one CTA per SM, warp-specialised, 6 warps):
+//   warp 0  TMA producer: A = genotype tile (128 SNPs x 128 k, int8, 128B swizzle, OOB rows of
+//           k >= n zero-filled) and B = the S slices of 32 inverse rows (3-D box 128 k x 32 rows
+//           x S slices) into a 4-stage mbarrier ring (48 KB / stage);
+//   warp 1  MMA issuer (one lane): D[128 SNPs x (S*32)] += A . B^T, 4 x K=32 per stage, int32
+//           accumulators in TMEM, double-buffered (2 x 256 columns), tcgen05.commit to mbarriers;
+//   warps 2-5  epilogue: tcgen05.ld each SNP's S x 32 accumulators, recombine in FP64, scale by
+//           2^e_i, store 32 consecutive rows of the SNP's Xbar column (256 contiguous bytes).
+// Tiles = (32-row blocks of Linv) x (128-SNP column tiles); row block rb needs k < 32 (rb+1).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -35,33 +25,23 @@
 #include <mutex>
 #include <string>
 
-#include "fixed_dot.cuh"
 #include "gg_internal.cuh"
 
 namespace gg {
 namespace {
 
 constexpr int S = 8;                       // int8 slices of the inverse
-constexpr int TM = 128;                    // SNPs per CTA tile (MMA M = 2 x 128 per pair)
+constexpr int TM = 128;                    // SNPs per tile (MMA M)
 constexpr int TR = 32;                     // inverse rows per tile
 constexpr int TN = S * TR;                 // MMA N = 256
 constexpr int TK = 128;                    // k per pipeline stage (4 MMAs of K = 32)
+constexpr int STAGES = 4;
 constexpr int A_BYTES = TM * TK;           // 16 KB
+constexpr int B_BYTES = TN * TK;           // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 6 * 32;
 constexpr int ACC_COLS = TN;               // int32 columns per accumulator buffer
-constexpr int P_STAGES = 6;
-constexpr int P_SLICES = S / 2;
-constexpr int P_B_BYTES = P_SLICES * TR * TK;        // 16 KB
-constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 32 KB
-// per-tile row data slot: e_i (32 ints) | block exponents of the q+1 columns (32 ints) |
-// the tile's 32 rows of XLbar's q columns then ybar (doubles, converted in place to fixed point)
-constexpr int RD_SLOTS = 4;
-constexpr int RD_COLS_OFF = 2 * TR * 4;
-constexpr int RD_BYTES = RD_COLS_OFF + GG_PMAX * TR * 8;    // 5376
-constexpr size_t P_SMEM_BYTES =
-    size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 256;
-static_assert(TR == GG_DOT_BLOCK, "a tile's rows are one canonical reduction block");
-static_assert(S == 8, "tmem_ld_rows8 / slice recombination are written for 8 slices");
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
 
 struct I8Args {
   int N;            // SNP columns
@@ -70,8 +50,8 @@ struct I8Args {
   double* X;        // Xbar, column-major, leading dimension ldx (nullptr: not materialised)
   long long ldx;
   const int* expo;  // e_i per inverse row (np)
-  // fused reductions (canonical block dots, fixed_dot.cuh): each SNP's 32-row block against
-  // XLbar (q columns, ld ldxl), itself and ybar -> P[(rb*N + col)*(q+2) + k]
+  // fused epilogue reductions (canonical order of gls_epilogue.cu): partial dots of each SNP's
+  // 32-row block against XLbar (q columns, ld ldxl) and ybar -> P[(rb*N + col)*(q+2) + k]
   int q;
   const double* XL;
   long long ldxl;
@@ -94,9 +74,6 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_cluster(unsigned bar) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -108,6 +85,275 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// K-major, 128-byte-swizzled shared-memory matrix descriptor (rows of 128 B, 8-row groups
+// 1024 B apart): start >> 4, LBO = 1, SBO = 1024 >> 4, version 1 (sm_100), layout SWIZZLE_128B.
+__device__ __forceinline__ unsigned long long smem_desc(unsigned saddr) {
+  return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// instruction descriptor: D s32, A/B signed int8, both K-major, N = TN, M = TM
+constexpr unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
+                           ((unsigned)(TM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(unsigned d_tmem, unsigned long long a, unsigned long long b,
+                                       unsigned accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(unsigned bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// 2^e as a double for |e| < 1022 (exact; built from the exponent bits, no libm call)
+__device__ __forceinline__ double pow2(int e) {
+  return __longlong_as_double((long long)(1023 + e) << 52);
+}
+
+__device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
+  rb = num_rb - 1 - t / num_nt;   // heavy row blocks first; a row block's SNP tiles together
+  nt = t % num_nt;
+}
+__device__ __forceinline__ int tile_of(int r, int b, int G) {
+  return r * G + ((r & 1) ? (G - 1 - b) : b);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    trsm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   I8Args a) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 4);
+  const unsigned sbase = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars);
+  const unsigned empty0 = smem_u32(bars + STAGES);
+  const unsigned accf0 = smem_u32(bars + 2 * STAGES);       // accumulator full  [2]
+  const unsigned acce0 = smem_u32(bars + 2 * STAGES + 2);   // accumulator empty [2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.gate != nullptr && *a.gate != a.gate_value) return;   // device-side path selection
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4 * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {   // TMEM: 2 accumulator buffers x 256 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const unsigned tmem_base = *tmem_slot;
+
+  const int total = a.num_rb * a.num_nt;
+  const int G = gridDim.x, bidx = blockIdx.x;
+
+  if (warp == 0) {
+    // ---------------------------------- TMA producer ----------------------------------------
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int r = 0;; ++r) {
+        const int t = tile_of(r, bidx, G);
+        if (t >= total) break;
+        int rb, nt;
+        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+        const int nk = (rb + 4) / 4;   // ceil(32 (rb+1) / 128)
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const unsigned fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          const unsigned dA = sbase + stage * STAGE_BYTES;
+          tma_2d(dA, &tmA, fb, kt * TK, nt * TM);
+          tma_3d(dA + A_BYTES, &tmB, fb, kt * TK, rb * TR, 0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------- MMA issuer ------------------------------------------
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int it = 0;
+      for (int r = 0;; ++r, ++it) {
+        const int t = tile_of(r, bidx, G);
+        if (t >= total) break;
+        int rb, nt;
+        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+        const int nk = (rb + 4) / 4;
+        const int ab = it & 1;
+        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);   // epilogue drained this buffer
+        fence_after();
+        const unsigned d_tmem = tmem_base + ab * ACC_COLS;
+        for (int kt = 0; kt < nk; ++kt) {
+          mbar_wait(full0 + 8 * stage, phase);
+          fence_after();
+          const unsigned sa = sbase + stage * STAGE_BYTES;
+          const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < TK / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-byte units
+            mma_i8(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(empty0 + 8 * stage);        // smem stage free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(accf0 + 8 * ab);              // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---------------------------------- epilogue (warps 2..5) -------------------------------
+    const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
+    const int m = quarter * 32 + lane;          // SNP within the tile
+    int it = 0;
+    for (int r = 0;; ++r, ++it) {
+      const int t = tile_of(r, bidx, G);
+      if (t >= total) break;
+      int rb, nt;
+      tile_coords(t, a.num_rb, a.num_nt, rb, nt);
+      const int ab = it & 1;
+      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
+      fence_after();
+      double acc[TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
+      const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
+      // smallest slice first: acc = sum_s C_s 2^(-7 s), s = S..1
+#pragma unroll 1
+      for (int s = S - 1; s >= 0; --s) {
+        int v[32];
+        tmem_ld32(taddr + s * TR, v);
+        const double w = pow2(-7 * (s + 1));
+#pragma unroll
+        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], w, acc[i]);
+      }
+      fence_before();
+      mbar_arrive(acce0 + 8 * ab);
+      const int col = nt * TM + m;
+      const int row0 = rb * TR;
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] *= pow2(a.expo[row0 + i]);   // exact power-of-two scale
+      if (col < a.N) {
+        if (a.X != nullptr) {
+          double* dst = a.X + (long long)col * a.ldx + row0;
+#pragma unroll
+          for (int i = 0; i < TR; i += 2)
+            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
+        }
+        if (a.P != nullptr) {
+          double* pp = a.P + ((long long)rb * a.N + col) * (a.q + 2);
+          for (int k = 0; k < a.q; ++k) {
+            const double* xl = a.XL + k * a.ldxl + row0;
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
+            pp[k] = sum;
+          }
+          double sxx = 0.0, sxy = 0.0;
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            sxx = fma(acc[i], acc[i], sxx);
+            sxy = fma(acc[i], a.y[row0 + i], sxy);
+          }
+          pp[a.q] = sxx;
+          pp[a.q + 1] = sxy;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "r"(2 * ACC_COLS)
+                 : "memory");
+  }
+}
+
+// ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
+// A cluster of 2 CTAs on a TPC computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs issued
+// by the leader: each CTA stages its own 128 SNPs (A) and HALF of the slices (B is split along N:
+// CTA0 slices 0..3, CTA1 slices 4..7), so per-SM staging traffic drops by a third and 6 stages fit
+// in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
+// commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
+// threads release the accumulator on the leader's "accumulator empty" barrier.
+constexpr int P_STAGES = 6;
+constexpr int P_SLICES = S / 2;
+constexpr int P_B_BYTES = P_SLICES * TR * TK;        // 16 KB
+constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 32 KB
+// per-tile row data staged by the producer with bulk copies: e_i (32 ints) then the tile's 32
+// rows of XLbar's q columns and of ybar (q + 1 <= GG_PMAX columns)
+constexpr int RD_SLOTS = 4;
+constexpr int RD_COLS_OFF = TR * 4;
+constexpr int RD_BYTES = RD_COLS_OFF + GG_PMAX * TR * 8;    // 5248
+constexpr size_t P_SMEM_BYTES =
+    size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 256;
+constexpr unsigned IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
+                            ((unsigned)(2 * TM >> 4) << 24);
+constexpr unsigned PEER_MASK = 0xFEFFFFFFu;          // clear the CTA-rank bit: the leader's copy
+
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -117,17 +363,6 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" :::
                    "memory");
 }
-__device__ __forceinline__ void epilogue_bar() {   // the CTA's 4 epilogue warps
-  asm volatile("bar.sync 1, 128;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-}
-
-// TMA tile loads issued by either CTA of the pair, completing on the leader's barrier
 __device__ __forceinline__ void tma_2d_pair(unsigned dst, const CUtensorMap* map, unsigned bar,
                                             int c0, int c1) {
   asm volatile(
@@ -144,28 +379,6 @@ __device__ __forceinline__ void tma_3d_pair(unsigned dst, const CUtensorMap* map
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-// contiguous global -> own shared memory copy (row data), completing on the CTA's own barrier
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
-                                         unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-// K-major, 128-byte-swizzled shared-memory matrix descriptor (rows of 128 B, 8-row groups
-// 1024 B apart): start >> 4, LBO = 1, SBO = 1024 >> 4, version 1 (sm_100), layout SWIZZLE_128B.
-__device__ __forceinline__ unsigned long long smem_desc(unsigned saddr) {
-  return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
-         (2ull << 61);
-}
-
-// instruction descriptor: D s32, A/B signed int8, both K-major, N = TN, M = 2 x TM
-constexpr unsigned IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
-                            ((unsigned)(2 * TM >> 4) << 24);
-constexpr unsigned PEER_MASK = 0xFEFFFFFFu;   // clear the CTA-rank bit: the leader's copy
-
 __device__ __forceinline__ void mma_i8_pair(unsigned d_tmem, unsigned long long a,
                                             unsigned long long b, unsigned accumulate) {
   asm volatile(
@@ -184,56 +397,41 @@ __device__ __forceinline__ void mma_commit_pair(unsigned bar) {
       "h"((unsigned short)3)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
 
-// 8 rows x all S slices of one accumulator quarter: v[s][r] = C_s of row r (8 loads, one wait)
-__device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[8][8]) {
+// contiguous global -> own shared memory copy (row data), completing on the CTA's own barrier
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned bar) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%64];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%65];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%66];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%67];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%68];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%69];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%70];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%56,%57,%58,%59,%60,%61,%62,%63}, [%71];\n"
-      "tcgen05.wait::ld.sync.aligned;\n"
-      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]),
-        "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]), "=r"(v[1][0]), "=r"(v[1][1]),
-        "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]),
-        "=r"(v[1][7]), "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]),
-        "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]), "=r"(v[3][0]),
-        "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]),
-        "=r"(v[3][6]), "=r"(v[3][7]), "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]),
-        "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
-        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]),
-        "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]), "=r"(v[6][0]), "=r"(v[6][1]),
-        "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]),
-        "=r"(v[6][7]), "=r"(v[7][0]), "=r"(v[7][1]), "=r"(v[7][2]), "=r"(v[7][3]),
-        "=r"(v[7][4]), "=r"(v[7][5]), "=r"(v[7][6]), "=r"(v[7][7])
-      : "r"(taddr), "r"(taddr + TR), "r"(taddr + 2 * TR), "r"(taddr + 3 * TR),
-        "r"(taddr + 4 * TR), "r"(taddr + 5 * TR), "r"(taddr + 6 * TR), "r"(taddr + 7 * TR)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(bar)
       : "memory");
 }
 
-// Xbar = RN(2^(e - 56) * T), T = sum_s C_s 2^(7 (7 - s)) exact (|T| < 2^81)
-__device__ __forceinline__ double slices_to_double(const int (&v)[8][8], int r, int e) {
-  const long long hi = ((long long)v[0][r] << 21) + ((long long)v[1][r] << 14) +
-                       ((long long)v[2][r] << 7) + (long long)v[3][r];
-  const long long lo = ((long long)v[4][r] << 21) + ((long long)v[5][r] << 14) +
-                       ((long long)v[6][r] << 7) + (long long)v[7][r];
-  // (hi * 2^28 + lo) as a 128-bit two's-complement pair
-  const unsigned long long l0 = (unsigned long long)hi << 28;
-  const unsigned long long l1 = l0 + (unsigned long long)lo;
-  const long long h = (hi >> 36) + (lo >> 63) + (long long)(l1 < l0);
-  return fx_to_double(l1, h, e - 56);
-}
-
-__device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
-  rb = num_rb - 1 - t / num_nt;   // heavy row blocks first; a row block's SNP tiles together
-  nt = t % num_nt;
-}
-__device__ __forceinline__ int tile_of(int r, int b, int G) {   // snake over the clusters
-  return r * G + ((r & 1) ? (G - 1 - b) : b);
+// 32 lanes x 64 columns (two adjacent slices) -> 64 registers per thread, one wait
+__device__ __forceinline__ void tmem_ld64(unsigned taddr, int (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,"
+      "%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,"
+      "%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+        "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]),
+        "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]),
+        "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]),
+        "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
+        "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]),
+        "=r"(v[62]), "=r"(v[63])
+      : "r"(taddr)
+      : "memory");
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -291,7 +489,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const bool partials = a.P != nullptr;
 
   if (warp == 0) {
-    // ------------------------- TMA producer (both CTAs) ----------------------------------------
     if (lane == 0) {
       int stage = 0;
       unsigned phase = 0;
@@ -302,7 +499,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tile_coords(t, a.num_rb, num_pp, rb, pp);
         const int nt = 2 * pp + (int)rank;
         const int nk = (rb + 4) / 4;
-        {   // this CTA's row data for the tile (its own barrier)
+        {   // this CTA's row data for the tile (its own barrier): e_i, XLbar rows, ybar rows
           const int slot = r % RD_SLOTS;
           mbar_wait(rde0 + 8 * slot, ((r / RD_SLOTS) & 1) ^ 1);
           const unsigned rbar = rdf0 + 8 * slot, dst = rbase + slot * RD_BYTES;
@@ -330,18 +527,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------- MMA issuer (leader CTA, one lane) ------------------------------
     if (lane == 0 && leader) {
       int stage = 0;
       unsigned phase = 0;
-      for (int r = 0;; ++r) {
+      int it = 0;
+      for (int r = 0;; ++r, ++it) {
         const int t = tile_of(r, cid, G);
         if (t >= total) break;
         int rb, pp;
         tile_coords(t, a.num_rb, num_pp, rb, pp);
         const int nk = (rb + 4) / 4;
-        const int ab = r & 1;
-        mbar_wait(acce0 + 8 * ab, ((r >> 1) & 1) ^ 1);   // both epilogues drained this buffer
+        const int ab = it & 1;
+        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);
         fence_after();
         const unsigned d_tmem = tmem_base + ab * ACC_COLS;
         for (int kt = 0; kt < nk; ++kt) {
@@ -350,59 +547,54 @@ __global__ void __launch_bounds__(THREADS, 1)
           const unsigned sa = sbase + stage * P_STAGE_BYTES;
           const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TK / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-byte units
+          for (int kk = 0; kk < TK / 32; ++kk)
             mma_i8_pair(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
-          mma_commit_pair(empty0 + 8 * stage);   // stage free (both CTAs) once these retire
+          mma_commit_pair(empty0 + 8 * stage);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_pair(accf0 + 8 * ab);         // accumulator ready for both epilogues
+        mma_commit_pair(accf0 + 8 * ab);
       }
     }
   } else {
-    // ------------------------- epilogue (warps 2..5 of both CTAs) -----------------------------
-    const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
-    const int m = quarter * 32 + lane;          // SNP within the CTA's 128
-    for (int r = 0;; ++r) {
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    int it = 0;
+    for (int r = 0;; ++r, ++it) {
       const int t = tile_of(r, cid, G);
       if (t >= total) break;
       int rb, pp;
       tile_coords(t, a.num_rb, num_pp, rb, pp);
       const int nt = 2 * pp + (int)rank;
-      const int ab = r & 1;
-      const int slot = r % RD_SLOTS;
-      unsigned char* rd = rdata + slot * RD_BYTES;
-      const int* ex = reinterpret_cast<const int*>(rd);
-      int* cexp = reinterpret_cast<int*>(rd + TR * 4);
-      Fx2* cfx = reinterpret_cast<Fx2*>(rd + RD_COLS_OFF);
-      mbar_wait(rdf0 + 8 * slot, (r / RD_SLOTS) & 1);
-      if (partials) {
-        // covariate / phenotype rows -> canonical fixed point, in place (column c by warp c % 4)
-        for (int c = quarter; c <= a.q; c += 4) {
-          const double w = reinterpret_cast<const double*>(cfx)[c * TR + lane];
-          int E = fx_exp(w);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) E = max(E, __shfl_xor_sync(0xffffffffu, E, o));
-          cfx[c * TR + lane] = fx_split(fx_scale(w, E));
-          if (lane == 0) cexp[c] = E;
-        }
-        epilogue_bar();
-      }
-      mbar_wait(accf0 + 8 * ab, (r >> 1) & 1);
+      const int ab = it & 1;
+      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
       fence_after();
-      double x[TR];
+      const int slot = it % RD_SLOTS;
+      const unsigned char* rd = rdata + slot * RD_BYTES;
+      const int* ex = reinterpret_cast<const int*>(rd);
+      const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
+      double acc[TR];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
       const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
+      // two slices per TMEM load; smallest slice first: acc = sum_s C_s 2^(-7 (s+1)), s = S-1..0
+#pragma unroll 1
+      for (int s2 = S / 2 - 1; s2 >= 0; --s2) {
+        int v[64];
+        tmem_ld64(taddr + 2 * s2 * TR, v);
+        const double whi = pow2(-7 * (2 * s2 + 2)), wlo = pow2(-7 * (2 * s2 + 1));
 #pragma unroll
-      for (int q4 = 0; q4 < TR / 8; ++q4) {
-        int v[8][8];
-        tmem_ld_rows8(taddr + q4 * 8, v);
+        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[TR + i], whi, acc[i]);
 #pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) x[q4 * 8 + r8] = slices_to_double(v, r8, ex[q4 * 8 + r8]);
+        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], wlo, acc[i]);
       }
       fence_before();
-      mbar_arrive_cluster((acce0 + 8 * ab) & PEER_MASK);   // accumulator buffer free
+      mbar_arrive_cluster((acce0 + 8 * ab) & PEER_MASK);
+      mbar_wait(rdf0 + 8 * slot, (it / RD_SLOTS) & 1);
+#pragma unroll
+      for (int i = 0; i < TR; ++i) acc[i] *= pow2(ex[i]);   // exact power-of-two scale
       const int col = nt * TM + m;
       const int row0 = rb * TR;
       if (col < a.N) {
@@ -410,43 +602,29 @@ __global__ void __launch_bounds__(THREADS, 1)
           double* dst = a.X + (long long)col * a.ldx + row0;
 #pragma unroll
           for (int i = 0; i < TR; i += 2)
-            *reinterpret_cast<double2*>(dst + i) = make_double2(x[i], x[i + 1]);
+            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
         }
-        if (partials) {
-          int Ex = fx_exp(x[0]);
-#pragma unroll
-          for (int i = 1; i < TR; ++i) Ex = max(Ex, fx_exp(x[i]));
-          Fx2 U[TR];
-#pragma unroll
-          for (int i = 0; i < TR; ++i) U[i] = fx_split(fx_scale(x[i], Ex));
+        if (partials) {   // canonical order: one FMA chain over the 32 rows per dot
           double* ppo = a.P + ((long long)rb * a.N + col) * (a.q + 2);
-          for (int c = 0; c < a.q; c += 2) {   // two covariate columns at a time
-            const int c1 = min(c + 1, a.q - 1);
-            const Fx2* w0 = cfx + c * TR;
-            const Fx2* w1 = cfx + c1 * TR;
-            FxAcc s0 = {0, 0, 0, 0}, s1 = {0, 0, 0, 0};
+          for (int k = 0; k < a.q; ++k) {
+            const double* xl = cols + k * TR;
+            double sum = 0.0;
 #pragma unroll
-            for (int i = 0; i < TR; ++i) {
-              fx_mac(s0, U[i], w0[i]);
-              fx_mac(s1, U[i], w1[i]);
-            }
-            ppo[c] = fx_finish(s0, Ex, cexp[c]);
-            if (c + 1 < a.q) ppo[c + 1] = fx_finish(s1, Ex, cexp[c1]);
+            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
+            ppo[k] = sum;
           }
-          const Fx2* wy = cfx + a.q * TR;
-          FxAcc sxx = {0, 0, 0, 0}, sxy = {0, 0, 0, 0};
+          const double* yv = cols + a.q * TR;
+          double sxx = 0.0, sxy = 0.0;
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
-            fx_mac(sxx, U[i], U[i]);
-            fx_mac(sxy, U[i], wy[i]);
+            sxx = fma(acc[i], acc[i], sxx);
+            sxy = fma(acc[i], yv[i], sxy);
           }
-          ppo[a.q] = fx_finish(sxx, Ex, Ex);
-          ppo[a.q + 1] = fx_finish(sxy, Ex, cexp[a.q]);
+          ppo[a.q] = sxx;
+          ppo[a.q + 1] = sxy;
         }
       }
-      // generic-proxy reads/writes of the slot precede the producer's next bulk copy into it
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_arrive(rde0 + 8 * slot);
+      mbar_arrive(rde0 + 8 * slot);   // row data slot free
     }
   }
   fence_before();
@@ -601,19 +779,9 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   }
   if (nrhs <= 0) return GG_OK;
   if ((reinterpret_cast<uintptr_t>(Sl) | reinterpret_cast<uintptr_t>(G) |
-       reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(expo)) & 15) {
+       reinterpret_cast<uintptr_t>(X)) & 15) {
     set_error("trsm_i8: operands must be 16-byte aligned");
     return GG_EARG;
-  }
-  if (P != nullptr) {
-    if (q < 0 || q + 1 > GG_PMAX) {
-      set_error("trsm_i8: need 0 <= q < GG_PMAX covariate columns");
-      return GG_EARG;
-    }
-    if (((reinterpret_cast<uintptr_t>(XL) | reinterpret_cast<uintptr_t>(y)) & 15) || (ldxl & 1)) {
-      set_error("trsm_i8: XLbar / ybar must be 16-byte aligned with an even leading dimension");
-      return GG_EARG;
-    }
   }
   CUtensorMap mA, mB;
   {
@@ -623,10 +791,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     int rc = encode(&mA, 2, G, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
-  {   // each CTA of a pair loads half of the slices (box: 128 k x 32 rows x S/2 slices)
+  {
     cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
     cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
-    cuuint32_t box[3] = {TK, TR, P_SLICES};
+    cuuint32_t box[3] = {TK, TR, S};
     int rc = encode(&mB, 3, Sl, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
@@ -644,24 +812,43 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.P = P;
   a.gate = gate;
   a.gate_value = gate_value;
-  const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
-  int clusters = sms() / 2;
-  if (clusters > pairs) clusters = pairs;
-  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)P_SMEM_BYTES));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = P_SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB, a));
+  const char* pair_env = getenv("GG_I8_PAIR");
+  const bool pair = !(pair_env != nullptr && pair_env[0] == '0');
+  if (pair) {
+    CUtensorMap mB2;
+    cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
+    cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
+    cuuint32_t box[3] = {TK, TR, P_SLICES};
+    int rc = encode(&mB2, 3, Sl, dims, strides, box);
+    if (rc != GG_OK) return rc;
+    const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
+    int clusters = sms() / 2;
+    if (clusters > pairs) clusters = pairs;
+    GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_pair_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)P_SMEM_BYTES));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = P_SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB2, a));
+    return GG_OK;
+  }
+  const int tiles = a.num_rb * a.num_nt;
+  int grid = sms();
+  if (grid > tiles) grid = tiles;
+  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)SMEM_BYTES));
+  trsm_i8_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
+  GG_LAUNCH_CHECK("trsm_i8_kernel");
   return GG_OK;
 }
 

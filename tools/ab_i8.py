@@ -1,0 +1,39 @@
+"""A/B timing of the fused int8 TRSM across library builds on one box (config-1 block).
+    python tools/ab_i8.py tools/alt/lib_a.so [...]   (the in-tree library is always included)"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1304_2272_b200 import _capi, datagen, kernel  # noqa: E402
+from paper_1304_2272_b200._capi import ptr  # noqa: E402
+
+n, cnt = 10000, 8192
+spec = datagen.BaselineSpec(n=n, m=cnt, p=4)
+ctx = kernel.gls_prepare(datagen.kinship_covariance_device(spec), *datagen.covariates_host(spec))
+d = ctx._dev
+n16 = -(-n // 16) * 16
+G16 = datagen.genotypes_device(spec, 0, cnt, ld=n16)
+P = torch.empty(int(_capi.lib().gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64,
+                device="cuda")
+s = _capi.stream_handle()
+for path in [_capi.LIB_PATH] + sys.argv[1:]:
+    lib = C.CDLL(path)
+    f = lib.gg_trsm_lower_i8_partials
+    f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int,
+                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                  C.c_void_p]
+    ts = []
+    for rep in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = f(n, cnt, ptr(d.slices), ptr(d.expo), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
+               ptr(P), None, 0, None, 0, s)
+        b.record()
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        ts.append(a.elapsed_time(b))
+    print(f"{os.path.basename(path)}: {min(ts[1:]):.3f} ms (median {sorted(ts[1:])[2]:.3f})")
