@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -35,13 +36,9 @@ constexpr int TM = 128;                    // SNPs per tile (MMA M)
 constexpr int TR = 32;                     // inverse rows per tile
 constexpr int TN = S * TR;                 // MMA N = 256
 constexpr int TK = 128;                    // k per pipeline stage (4 MMAs of K = 32)
-constexpr int STAGES = 4;
 constexpr int A_BYTES = TM * TK;           // 16 KB
-constexpr int B_BYTES = TN * TK;           // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int THREADS = 6 * 32;
+constexpr int THREADS = 10 * 32;   // producer, MMA, two epilogue groups of 4 warps
 constexpr int ACC_COLS = TN;               // int32 columns per accumulator buffer
-constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
 
 struct I8Args {
   int N;            // SNP columns
@@ -59,6 +56,7 @@ struct I8Args {
   double* P;        // nullptr: no partials
   const int* gate;  // device flag: the kernel runs only if *gate == gate_value (nullptr: always)
   int gate_value;
+  int* tile_counter;  // zeroed before the launch: clusters take tiles dynamically, heavy first
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -85,22 +83,6 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_2d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
-                                       int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
-                                       int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 
 // K-major, 128-byte-swizzled shared-memory matrix descriptor (rows of 128 B, 8-row groups
 // 1024 B apart): start >> 4, LBO = 1, SBO = 1024 >> 4, version 1 (sm_100), layout SWIZZLE_128B.
@@ -109,46 +91,11 @@ __device__ __forceinline__ unsigned long long smem_desc(unsigned saddr) {
          (2ull << 61);
 }
 
-// instruction descriptor: D s32, A/B signed int8, both K-major, N = TN, M = TM
-constexpr unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
-                           ((unsigned)(TM >> 4) << 24);
-
-__device__ __forceinline__ void mma_i8(unsigned d_tmem, unsigned long long a, unsigned long long b,
-                                       unsigned accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(unsigned bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   bar)
-               : "memory");
-}
 __device__ __forceinline__ void fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-}
-
-// 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread
-__device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
 // 2^e as a double for |e| < 1022 (exact; built from the exponent bits, no libm call)
@@ -159,177 +106,6 @@ __device__ __forceinline__ double pow2(int e) {
 __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
   rb = num_rb - 1 - t / num_nt;   // heavy row blocks first; a row block's SNP tiles together
   nt = t % num_nt;
-}
-__device__ __forceinline__ int tile_of(int r, int b, int G) {
-  return r * G + ((r & 1) ? (G - 1 - b) : b);
-}
-
-__global__ void __launch_bounds__(THREADS, 1)
-    trsm_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   I8Args a) {
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 4);
-  const unsigned sbase = smem_u32(smem);
-  const unsigned full0 = smem_u32(bars);
-  const unsigned empty0 = smem_u32(bars + STAGES);
-  const unsigned accf0 = smem_u32(bars + 2 * STAGES);       // accumulator full  [2]
-  const unsigned acce0 = smem_u32(bars + 2 * STAGES + 2);   // accumulator empty [2]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (a.gate != nullptr && *a.gate != a.gate_value) return;   // device-side path selection
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, 4 * 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 1) {   // TMEM: 2 accumulator buffers x 256 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(2 * ACC_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const unsigned tmem_base = *tmem_slot;
-
-  const int total = a.num_rb * a.num_nt;
-  const int G = gridDim.x, bidx = blockIdx.x;
-
-  if (warp == 0) {
-    // ---------------------------------- TMA producer ----------------------------------------
-    if (lane == 0) {
-      int stage = 0;
-      unsigned phase = 0;
-      for (int r = 0;; ++r) {
-        const int t = tile_of(r, bidx, G);
-        if (t >= total) break;
-        int rb, nt;
-        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
-        const int nk = (rb + 4) / 4;   // ceil(32 (rb+1) / 128)
-        for (int kt = 0; kt < nk; ++kt) {
-          mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          const unsigned fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, STAGE_BYTES);
-          const unsigned dA = sbase + stage * STAGE_BYTES;
-          tma_2d(dA, &tmA, fb, kt * TK, nt * TM);
-          tma_3d(dA + A_BYTES, &tmB, fb, kt * TK, rb * TR, 0);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------------------------- MMA issuer ------------------------------------------
-    if (lane == 0) {
-      int stage = 0;
-      unsigned phase = 0;
-      int it = 0;
-      for (int r = 0;; ++r, ++it) {
-        const int t = tile_of(r, bidx, G);
-        if (t >= total) break;
-        int rb, nt;
-        tile_coords(t, a.num_rb, a.num_nt, rb, nt);
-        const int nk = (rb + 4) / 4;
-        const int ab = it & 1;
-        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);   // epilogue drained this buffer
-        fence_after();
-        const unsigned d_tmem = tmem_base + ab * ACC_COLS;
-        for (int kt = 0; kt < nk; ++kt) {
-          mbar_wait(full0 + 8 * stage, phase);
-          fence_after();
-          const unsigned sa = sbase + stage * STAGE_BYTES;
-          const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < TK / 32; ++kk)   // K = 32 bytes per MMA: +2 in 16-byte units
-            mma_i8(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(empty0 + 8 * stage);        // smem stage free once these MMAs retire
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        mma_commit(accf0 + 8 * ab);              // accumulator ready for the epilogue
-      }
-    }
-  } else {
-    // ---------------------------------- epilogue (warps 2..5) -------------------------------
-    const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
-    const int m = quarter * 32 + lane;          // SNP within the tile
-    int it = 0;
-    for (int r = 0;; ++r, ++it) {
-      const int t = tile_of(r, bidx, G);
-      if (t >= total) break;
-      int rb, nt;
-      tile_coords(t, a.num_rb, a.num_nt, rb, nt);
-      const int ab = it & 1;
-      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
-      fence_after();
-      double acc[TR];
-#pragma unroll
-      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
-      const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
-      // smallest slice first: acc = sum_s C_s 2^(-7 s), s = S..1
-#pragma unroll 1
-      for (int s = S - 1; s >= 0; --s) {
-        int v[32];
-        tmem_ld32(taddr + s * TR, v);
-        const double w = pow2(-7 * (s + 1));
-#pragma unroll
-        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], w, acc[i]);
-      }
-      fence_before();
-      mbar_arrive(acce0 + 8 * ab);
-      const int col = nt * TM + m;
-      const int row0 = rb * TR;
-#pragma unroll
-      for (int i = 0; i < TR; ++i) acc[i] *= pow2(a.expo[row0 + i]);   // exact power-of-two scale
-      if (col < a.N) {
-        if (a.X != nullptr) {
-          double* dst = a.X + (long long)col * a.ldx + row0;
-#pragma unroll
-          for (int i = 0; i < TR; i += 2)
-            *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
-        }
-        if (a.P != nullptr) {
-          double* pp = a.P + ((long long)rb * a.N + col) * (a.q + 2);
-          for (int k = 0; k < a.q; ++k) {
-            const double* xl = a.XL + k * a.ldxl + row0;
-            double sum = 0.0;
-#pragma unroll
-            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
-            pp[k] = sum;
-          }
-          double sxx = 0.0, sxy = 0.0;
-#pragma unroll
-          for (int i = 0; i < TR; ++i) {
-            sxx = fma(acc[i], acc[i], sxx);
-            sxy = fma(acc[i], a.y[row0 + i], sxy);
-          }
-          pp[a.q] = sxx;
-          pp[a.q + 1] = sxy;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
-                 "r"(2 * ACC_COLS)
-                 : "memory");
-  }
 }
 
 // ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
@@ -349,7 +125,11 @@ constexpr int RD_SLOTS = 4;
 constexpr int RD_COLS_OFF = TR * 4;
 constexpr int RD_BYTES = RD_COLS_OFF + GG_PMAX * TR * 8;    // 5248
 constexpr size_t P_SMEM_BYTES =
-    size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 256;
+    size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 512;
+// dynamic tile queue: TQ slots; readers per slot: leader MMA + peer producer + one epilogue
+// group (4 warps) in each CTA
+constexpr int TQ = 8;
+constexpr int TQ_READERS = 2 + 2 * 4;
 constexpr unsigned IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
                             ((unsigned)(2 * TM >> 4) << 24);
 constexpr unsigned PEER_MASK = 0xFEFFFFFFu;          // clear the CTA-rank bit: the leader's copy
@@ -397,6 +177,33 @@ __device__ __forceinline__ void mma_commit_pair(unsigned bar) {
       "h"((unsigned short)3)
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_acq_cluster(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITQ_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITQ_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// the same shared-memory offset in the other CTA of the pair
+__device__ __forceinline__ unsigned mapa_peer(unsigned saddr) {
+  unsigned r, peer;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  peer = r ^ 1u;
+  unsigned out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(saddr), "r"(peer));
+  return out;
+}
+__device__ __forceinline__ void st_cluster_s32(unsigned addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_release(unsigned bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
@@ -442,7 +249,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* rdata = smem + P_STAGES * P_STAGE_BYTES;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(rdata + RD_SLOTS * RD_BYTES);
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS);
+  int* tq = reinterpret_cast<int*>(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS + 2 * TQ);   // tiles
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tq + TQ);
   const unsigned sbase = smem_u32(smem);
   const unsigned rbase = smem_u32(rdata);
   const unsigned full0 = smem_u32(bars);
@@ -451,6 +259,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned acce0 = smem_u32(bars + 2 * P_STAGES + 2);
   const unsigned rdf0 = smem_u32(bars + 2 * P_STAGES + 4);              // row data full  [4]
   const unsigned rde0 = smem_u32(bars + 2 * P_STAGES + 4 + RD_SLOTS);   // row data empty [4]
+  const unsigned tqf0 = smem_u32(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS);   // tile posted [TQ]
+  const unsigned tqe0 = tqf0 + 8 * TQ;                                        // tile read   [TQ]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned rank = cluster_rank();
   const bool leader = rank == 0;
@@ -469,6 +279,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(rdf0 + 8 * b, 1);
       mbar_init(rde0 + 8 * b, 4 * 32);
     }
+    for (int b = 0; b < TQ; ++b) {
+      mbar_init(tqf0 + 8 * b, 1);
+      mbar_init(tqe0 + 8 * b, TQ_READERS);   // leader's copy used
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -485,16 +299,47 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int num_pp = (a.num_nt + 1) / 2;          // 256-SNP tile pairs
   const int total = a.num_rb * num_pp;
-  const int G = gridDim.x / 2, cid = blockIdx.x / 2;
   const bool partials = a.P != nullptr;
+  const unsigned peer_tq = mapa_peer(smem_u32(tq));
+  // r-th tile of this cluster (-1: none left).  The leader's producer takes tiles from the global
+  // counter and posts them to both CTAs' queues; every other role reads its CTA's copy.
+  auto tile_at = [&](int r) -> int {
+    const int slot = r % TQ;
+    mbar_wait_acq_cluster(tqf0 + 8 * slot, (r / TQ) & 1);
+    return *reinterpret_cast<volatile int*>(tq + slot);
+  };
+  auto tile_read = [&](int r) {   // this reader is done with queue slot r % TQ
+    mbar_arrive_cluster((tqe0 + 8 * (r % TQ)) & PEER_MASK);
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       unsigned phase = 0;
       for (int r = 0;; ++r) {
-        const int t = tile_of(r, cid, G);
-        if (t >= total) break;
+        int t;
+        if (leader) {   // take the next tile (heavy first) and post it to both CTAs
+          const int slot = r % TQ;
+          mbar_wait(tqe0 + 8 * slot, ((r / TQ) & 1) ^ 1);
+          t = atomicAdd(a.tile_counter, 1);
+          if (t >= total) t = -1;
+          tq[slot] = t;
+          st_cluster_s32(peer_tq + 4 * slot, t);
+          mbar_arrive(tqf0 + 8 * slot);
+          mbar_arrive_remote_release(mapa_peer(tqf0 + 8 * slot));
+          if (t < 0) {   // the other epilogue group reads the next slot: end it there too
+            const int s2 = (r + 1) % TQ;
+            mbar_wait(tqe0 + 8 * s2, (((r + 1) / TQ) & 1) ^ 1);
+            tq[s2] = -1;
+            st_cluster_s32(peer_tq + 4 * s2, -1);
+            mbar_arrive(tqf0 + 8 * s2);
+            mbar_arrive_remote_release(mapa_peer(tqf0 + 8 * s2));
+          }
+        } else {
+          t = tile_at(r);
+          tile_read(r);
+        }
+        if (t < 0) break;
         int rb, pp;
         tile_coords(t, a.num_rb, num_pp, rb, pp);
         const int nt = 2 * pp + (int)rank;
@@ -532,8 +377,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       unsigned phase = 0;
       int it = 0;
       for (int r = 0;; ++r, ++it) {
-        const int t = tile_of(r, cid, G);
-        if (t >= total) break;
+        const int t = tile_at(r);
+        tile_read(r);
+        if (t < 0) break;
         int rb, pp;
         tile_coords(t, a.num_rb, num_pp, rb, pp);
         const int nk = (rb + 4) / 4;
@@ -559,12 +405,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
+    const int group = (warp - 2) >> 2;         // group g drains accumulator buffer g
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;
-    int it = 0;
-    for (int r = 0;; ++r, ++it) {
-      const int t = tile_of(r, cid, G);
-      if (t >= total) break;
+    for (int r = group;; r += 2) {
+      const int it = r;
+      const int t = tile_at(r);
+      __syncwarp();
+      if (lane == 0) tile_read(r);
+      if (t < 0) break;
       int rb, pp;
       tile_coords(t, a.num_rb, num_pp, rb, pp);
       const int nt = 2 * pp + (int)rank;
@@ -721,6 +570,30 @@ int encode(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
   return GG_OK;
 }
 
+// A zeroed int per launch for the dynamic tile scheduler: a ring of counters per device, each
+// cleared on the launch stream just before use.
+int* tile_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<int, int*> bufs;
+  static unsigned next = 0;
+  constexpr unsigned RING = 4096;
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  int*& buf = bufs[dev];
+  if (buf == nullptr && cudaMalloc(&buf, RING * sizeof(int)) != cudaSuccess) {
+    buf = nullptr;
+    set_error("trsm_i8: cannot allocate the tile counters");
+    return nullptr;
+  }
+  int* p = buf + (next++ % RING);
+  if (cudaMemsetAsync(p, 0, sizeof(int), s) != cudaSuccess) {
+    set_error("trsm_i8: cannot clear the tile counter");
+    return nullptr;
+  }
+  return p;
+}
+
 int sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -791,10 +664,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     int rc = encode(&mA, 2, G, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
-  {
+  {   // each CTA of a pair loads half of the slices (box: 128 k x 32 rows x S/2 slices)
     cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
     cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
-    cuuint32_t box[3] = {TK, TR, S};
+    cuuint32_t box[3] = {TK, TR, P_SLICES};
     int rc = encode(&mB, 3, Sl, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
@@ -812,15 +685,9 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.P = P;
   a.gate = gate;
   a.gate_value = gate_value;
-  const char* pair_env = getenv("GG_I8_PAIR");
-  const bool pair = !(pair_env != nullptr && pair_env[0] == '0');
-  if (pair) {
-    CUtensorMap mB2;
-    cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
-    cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
-    cuuint32_t box[3] = {TK, TR, P_SLICES};
-    int rc = encode(&mB2, 3, Sl, dims, strides, box);
-    if (rc != GG_OK) return rc;
+  a.tile_counter = tile_counter(s);
+  if (a.tile_counter == nullptr) return GG_ECUDA;
+  {
     const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
     int clusters = sms() / 2;
     if (clusters > pairs) clusters = pairs;
@@ -839,17 +706,9 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB2, a));
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB, a));
     return GG_OK;
   }
-  const int tiles = a.num_rb * a.num_nt;
-  int grid = sms();
-  if (grid > tiles) grid = tiles;
-  GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)SMEM_BYTES));
-  trsm_i8_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(mA, mB, a);
-  GG_LAUNCH_CHECK("trsm_i8_kernel");
-  return GG_OK;
 }
 
 }  // namespace gg
