@@ -218,26 +218,33 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
       : "memory");
 }
 
-// 32 lanes x 64 columns (two adjacent slices) -> 64 registers per thread, one wait
-__device__ __forceinline__ void tmem_ld64(unsigned taddr, int (&v)[64]) {
+// 8 rows x all S slices of one accumulator quarter: v[s][r] = C_s of row r (8 loads, one wait)
+__device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[8][8]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,"
-      "%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,"
-      "%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%65];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%66];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%67];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%68];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%69];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%70];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%56,%57,%58,%59,%60,%61,%62,%63}, [%71];\n"
       "tcgen05.wait::ld.sync.aligned;\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
-        "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]),
-        "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]),
-        "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]),
-        "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
-        "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]),
-        "=r"(v[62]), "=r"(v[63])
-      : "r"(taddr)
+      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]),
+        "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]), "=r"(v[1][0]), "=r"(v[1][1]),
+        "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]),
+        "=r"(v[1][7]), "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]),
+        "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]), "=r"(v[3][0]),
+        "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]),
+        "=r"(v[3][6]), "=r"(v[3][7]), "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]),
+        "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
+        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]),
+        "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]), "=r"(v[6][0]), "=r"(v[6][1]),
+        "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]),
+        "=r"(v[6][7]), "=r"(v[7][0]), "=r"(v[7][1]), "=r"(v[7][2]), "=r"(v[7][3]),
+        "=r"(v[7][4]), "=r"(v[7][5]), "=r"(v[7][6]), "=r"(v[7][7])
+      : "r"(taddr), "r"(taddr + TR), "r"(taddr + 2 * TR), "r"(taddr + 3 * TR),
+        "r"(taddr + 4 * TR), "r"(taddr + 5 * TR), "r"(taddr + 6 * TR), "r"(taddr + 7 * TR)
       : "memory");
 }
 
@@ -424,26 +431,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       const unsigned char* rd = rdata + slot * RD_BYTES;
       const int* ex = reinterpret_cast<const int*>(rd);
       const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
+      // X = RN(T 2^(e_i - 56)), T = sum_s C_s 2^(7 (7 - s)): the two exact int64 halves
+      // hi = C_0..C_3, lo = C_4..C_7 (|hi|, |lo| < 2^53 since |C_s| < 2^31) are converted
+      // exactly and combined with ONE rounding (4 FP64 instructions per element: the FP64 pipe
+      // is throttled while the tensor core runs)
+      mbar_wait(rdf0 + 8 * slot, (it / RD_SLOTS) & 1);
       double acc[TR];
-#pragma unroll
-      for (int i = 0; i < TR; ++i) acc[i] = 0.0;
       const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
-      // two slices per TMEM load; smallest slice first: acc = sum_s C_s 2^(-7 (s+1)), s = S-1..0
-#pragma unroll 1
-      for (int s2 = S / 2 - 1; s2 >= 0; --s2) {
-        int v[64];
-        tmem_ld64(taddr + 2 * s2 * TR, v);
-        const double whi = pow2(-7 * (2 * s2 + 2)), wlo = pow2(-7 * (2 * s2 + 1));
 #pragma unroll
-        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[TR + i], whi, acc[i]);
+      for (int q4 = 0; q4 < TR / 8; ++q4) {
+        int v[8][8];
+        tmem_ld_rows8(taddr + q4 * 8, v);
 #pragma unroll
-        for (int i = 0; i < TR; ++i) acc[i] = fma((double)v[i], wlo, acc[i]);
+        for (int r8 = 0; r8 < 8; ++r8) {
+          const long long hi = (((long long)v[0][r8] * 128 + v[1][r8]) * 128 + v[2][r8]) * 128 +
+                               v[3][r8];
+          const long long lo = (((long long)v[4][r8] * 128 + v[5][r8]) * 128 + v[6][r8]) * 128 +
+                               v[7][r8];
+          const int e = ex[q4 * 8 + r8];
+          acc[q4 * 8 + r8] = fma((double)hi, pow2(e - 28), (double)lo * pow2(e - 56));
+        }
       }
       fence_before();
       mbar_arrive_cluster((acce0 + 8 * ab) & PEER_MASK);
-      mbar_wait(rdf0 + 8 * slot, (it / RD_SLOTS) & 1);
-#pragma unroll
-      for (int i = 0; i < TR; ++i) acc[i] *= pow2(ex[i]);   // exact power-of-two scale
       const int col = nt * TM + m;
       const int row0 = rb * TR;
       if (col < a.N) {
