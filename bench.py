@@ -298,8 +298,8 @@ def run_ours(args):
         tops = slices * flops_per_step / (trsm_ms / 1e3) / 1e12     # int8 ops: S slices x n^2
         roofline = {
             "bound": "tensor",
-            "kernel": "trsm_i8_kernel (persistent TMA + tcgen05.mma.kind::i8 TRSM, fused "
-                      "reductions; inverse split into int8 slices)",
+            "kernel": "trsm_i8_pair_kernel (persistent CTA-pair TMA + tcgen05.mma.kind::i8 TRSM, "
+                      "fused reductions; inverse split into int8 slices)",
             "achieved": round(tops, 1), "peak": I8_PEAK_TOPS, "unit": "TOPS",
             "frac": round(tops / I8_PEAK_TOPS, 4),
             "traffic": traffic_full,

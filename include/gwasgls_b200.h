@@ -116,12 +116,14 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
  * Dosages are exact int8, so X = L^-1 G runs on tcgen05.mma.kind::i8 with the inverse split
  * error-free into gg_i8_slices() int8 slices per row:
  *     Linv[i,k] = 2^expo[i] * sum_s a_s[i,k] 2^(-7 s)      (truncation residual < 2^(expo-56))
- * Each slice product is an exact int32 integer; the slices are recombined in FP64 in a fixed
- * order (per-column results independent of the column's position).
+ * Each slice product is an exact int32 integer; the eight are combined exactly into two int64
+ * halves and rounded once to double (correctly rounded; per-column results independent of the
+ * column's position).
  *   gg_slice_inverse_i8 : row-major inverse LinvT (see gg_trsm_lower_rm_f64) -> slices
  *                         (gg_inverse_slices_bytes(n) bytes, [slice][row][k]) + expo (np ints).
- *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg); *bad_dev |= 1 if
- *                         any value is not an integer in [-127, 127] (device flag).
+ *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg; with ldg a multiple
+ *                         of 16 the rows up to the next multiple of 16 are zeroed); *bad_dev |= 1
+ *                         if any value is not an integer in [-127, 127] (device flag).
  *   gg_trsm_lower_i8    : X (np x nrhs FP64, ldx) = L^-1 G for int8 G (n x nrhs, ldg a multiple
  *                         of 16, 16-byte aligned).                                            */
 int gg_i8_slices(void);
