@@ -169,36 +169,62 @@ __device__ __forceinline__ double warp_allsum(double v) {
   return v;
 }
 
+// 32 columns per CTA.  Warp w sums, for every column at once (coalesced loads of consecutive
+// columns' partials), the row blocks of lane slots l = w, w+8, w+16, w+24 -- exactly lane l's
+// share of the canonical order -- into shared memory; warp 0 then applies the xor-butterfly tree
+// (t_l <- t_l + t_(l^o), o = 16 .. 1) per column and value, and solves.
 template <int QM, int PM>
 __global__ void __launch_bounds__(256) reduce_solve_kernel(
     int nrb, int cnt, int q, const double* __restrict__ P, double* __restrict__ dots,
     const double* __restrict__ S_TL, const double* __restrict__ b_T, double* __restrict__ beta,
     int* __restrict__ status, double* __restrict__ sinv) {
-  const int lane = threadIdx.x & 31;
-  const int col = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (col >= cnt) return;
-  double acc[QM + 2];
-#pragma unroll
-  for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
+  extern __shared__ double sh[];   // [32 lane slots][32 columns][QM + 2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 32 + lane;
   const long long stride = (long long)cnt * (q + 2);
-  for (int rb = lane; rb < nrb; rb += 32) {
-    const double* pp = P + rb * stride + (long long)col * (q + 2);
+  for (int l = warp; l < 32; l += 8) {
+    double acc[QM + 2];
 #pragma unroll
-    for (int k = 0; k < QM; ++k)
-      if (k < q) acc[k] = acc[k] + pp[k];
-    acc[QM] = acc[QM] + pp[q];
-    acc[QM + 1] = acc[QM + 1] + pp[q + 1];
+    for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
+    if (col < cnt) {
+      for (int rb = l; rb < nrb; rb += 32) {
+        const double* pp = P + rb * stride + (long long)col * (q + 2);
+#pragma unroll
+        for (int k = 0; k < QM; ++k)
+          if (k < q) acc[k] = acc[k] + pp[k];
+        acc[QM] = acc[QM] + pp[q];
+        acc[QM + 1] = acc[QM + 1] + pp[q + 1];
+      }
+    }
+    double* dst = sh + (l * 32 + lane) * (QM + 2);
+#pragma unroll
+    for (int k = 0; k < QM + 2; ++k) dst[k] = acc[k];
   }
+  __syncthreads();
+  if (warp != 0 || col >= cnt) return;
+  double tot[QM + 2];
+#pragma unroll 1
+  for (int k = 0; k < QM + 2; ++k) {
+    double t[32];
 #pragma unroll
-  for (int k = 0; k < QM + 2; ++k) acc[k] = warp_allsum(acc[k]);
-  if (lane != 0) return;
+    for (int l = 0; l < 32; ++l) t[l] = sh[(l * 32 + lane) * (QM + 2) + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double u[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) u[l] = t[l] + t[l ^ o];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) t[l] = u[l];
+    }
+    tot[k] = t[0];
+  }
   if (dots != nullptr) {
     double* out = dots + (long long)col * (q + 2);
 #pragma unroll
     for (int k = 0; k < QM; ++k)
-      if (k < q) out[k] = acc[k];
-    out[q] = acc[QM];
-    out[q + 1] = acc[QM + 1];
+      if (k < q) out[k] = tot[k];
+    out[q] = tot[QM];
+    out[q + 1] = tot[QM + 1];
   }
   if (beta == nullptr) return;
   const int p = q + 1;
@@ -208,12 +234,12 @@ __global__ void __launch_bounds__(256) reduce_solve_kernel(
 #pragma unroll
   for (int k = 0; k < QM; ++k)
     if (k < q) {
-      S[q * PM + k] = acc[k];
-      S[k * PM + q] = acc[k];
+      S[q * PM + k] = tot[k];
+      S[k * PM + q] = tot[k];
       rhs[k] = b_T[k];
     }
-  S[q * PM + q] = acc[QM];
-  rhs[q] = acc[QM + 1];
+  S[q * PM + q] = tot[QM];
+  rhs[q] = tot[QM + 1];
   double* so = sinv ? sinv + (long long)col * (p * (p + 1) / 2) : nullptr;
   status[col] = small_spd_solve<PM>(p, S, rhs, x, so);
   for (int i = 0; i < p; ++i) beta[(long long)col * p + i] = x[i];
@@ -280,21 +306,25 @@ int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const doubl
   return launch_partials<QMAX, 4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
 }
 
+template <int QM, int PM>
+static int launch_reduce(int nrb, int cnt, int q, const double* P, double* dots,
+                         const double* S_TL, const double* b_T, double* beta, int* status,
+                         double* sinv, cudaStream_t s) {
+  const size_t sm = (size_t)32 * 32 * (QM + 2) * sizeof(double);
+  GG_CUDA_TRY(cudaFuncSetAttribute(reduce_solve_kernel<QM, PM>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  reduce_solve_kernel<QM, PM><<<(cnt + 31) / 32, 256, sm, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
+                                                                beta, status, sinv);
+  GG_LAUNCH_CHECK("reduce_solve_kernel");
+  return GG_OK;
+}
+
 int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,
                      const double* b_T, double* beta, int* status, double* sinv, cudaStream_t s) {
   const int nrb = pad_rows(n) / RB;
-  const int threads = 256, grid = (cnt + 7) / 8;
-  if (q <= 3)
-    reduce_solve_kernel<3, 4><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T, beta,
-                                                       status, sinv);
-  else if (q <= 7)
-    reduce_solve_kernel<7, 8><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T, beta,
-                                                       status, sinv);
-  else
-    reduce_solve_kernel<QMAX, GG_PMAX><<<grid, threads, 0, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
-                                                               beta, status, sinv);
-  GG_LAUNCH_CHECK("reduce_solve_kernel");
-  return GG_OK;
+  if (q <= 3) return launch_reduce<3, 4>(nrb, cnt, q, P, dots, S_TL, b_T, beta, status, sinv, s);
+  if (q <= 7) return launch_reduce<7, 8>(nrb, cnt, q, P, dots, S_TL, b_T, beta, status, sinv, s);
+  return launch_reduce<QMAX, GG_PMAX>(nrb, cnt, q, P, dots, S_TL, b_T, beta, status, sinv, s);
 }
 
 size_t partials_bytes(int n, int cnt, int q) {
