@@ -123,10 +123,15 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
  *                         (gg_inverse_slices_bytes(n) bytes, [slice][row][k]) + expo (np ints).
  *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg; with ldg a multiple
  *                         of 16 the rows up to the next multiple of 16 are zeroed); *bad_dev |= 1
- *                         if any value is not an integer in [-127, 127] (device flag).
+ *                         if any value is not an integer with |v| <= gg_i8_value_bound(n).
  *   gg_trsm_lower_i8    : X (np x nrhs FP64, ldx) = L^-1 G for int8 G (n x nrhs, ldg a multiple
  *                         of 16, 16-byte aligned).                                            */
 int gg_i8_slices(void);
+/* Largest |value| of an int8 operand for which the int32 slice products stay exact at this n:
+ * min(127, floor((2^31 - 1) / (127 n))) -- 127 up to n = 133,144; genotype dosages (<= 2) are
+ * exact for n < 8.4e6.  gg_narrow_f64_i8 and gg_gls_block_f64 enforce it (larger values take the
+ * FP64 path); callers of gg_trsm_lower_i8* must respect it.                                  */
+int gg_i8_value_bound(int n);
 size_t gg_inverse_slices_bytes(int n);
 int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
                         void* stream);

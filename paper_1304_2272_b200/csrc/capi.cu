@@ -128,6 +128,8 @@ int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double*
 
 int gg_i8_slices(void) { return gg::i8_slices(); }
 
+int gg_i8_value_bound(int n) { return gg::i8_value_bound(n); }
+
 size_t gg_inverse_slices_bytes(int n) { return n < 1 ? 0 : gg::inverse_slices_bytes(n); }
 
 int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
@@ -276,9 +278,11 @@ static BlockWs block_ws(int n, int q, int cnt, int input_int8, int have_slices, 
   w.flag = reinterpret_cast<int*>(base);
   w.P = reinterpret_cast<double*>(base + off);
   off += align256(gg::partials_bytes(n, cnt, q));
+  // int8 input at n > 133,144: values beyond gg_i8_value_bound(n) take the DMMA path
+  const bool i8_guard = have_slices && input_int8 && gg::i8_value_bound(n) < 127;
   const bool need_g8 = have_slices;                              // narrowed / re-pitched dosages
-  const bool need_x64 = !have_slices && input_int8;              // widened dosages (DMMA path)
-  const bool need_xbar = !(have_slices && input_int8);           // DMMA result
+  const bool need_x64 = (!have_slices && input_int8) || i8_guard;   // widened dosages (DMMA)
+  const bool need_xbar = !(have_slices && input_int8) || i8_guard;  // DMMA result
   w.g8 = need_g8 ? reinterpret_cast<signed char*>(base + off) : nullptr;
   if (need_g8) off += align256(n16 * cnt);
   w.x64 = need_x64 ? reinterpret_cast<double*>(base + off) : nullptr;
@@ -327,8 +331,26 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
         g = w.g8;
         lg = n16;
       }
-      rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q, XLbar, np,
-                                 ybar, w.P, nullptr, 0, s);
+      if (gg::i8_value_bound(n) >= 127) {
+        rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q, XLbar,
+                                   np, ybar, w.P, nullptr, 0, s);
+      } else {
+        // large n: values beyond the exact-int32 bound send the block down the DMMA path
+        if (LinvP == nullptr) {
+          gg::set_error("gls_block: n > 133144 with int8 input needs LinvP (value-range fallback)");
+          return GG_EARG;
+        }
+        GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
+        rc = gg::range_i8_run(n, cnt, g, lg, w.flag, s);
+        if (rc == GG_OK)
+          rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q,
+                                     XLbar, np, ybar, w.P, w.flag, 0, s);
+        if (rc == GG_OK) rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);
+        if (rc == GG_OK)
+          rc = gg::trsm_packed_gated_run(n, cnt, LinvP, w.x64, np, w.xbar, np, w.flag, 1, s);
+        if (rc == GG_OK)
+          rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
+      }
     } else {
       // FP64 dosages: narrow on the device; exact integers take the int8 tensor-core path, any
       // other value sends the whole block down the FP64 DMMA path (selected on the device: both

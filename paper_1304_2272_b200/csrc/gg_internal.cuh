@@ -75,6 +75,8 @@ int i8_slices();
 size_t inverse_slices_bytes(int n);
 int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
                       cudaStream_t s);
+int i8_value_bound(int n);
+int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, cudaStream_t s);
 int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
                int* bad, cudaStream_t s);
 int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,

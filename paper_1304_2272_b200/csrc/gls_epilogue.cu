@@ -159,15 +159,10 @@ __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
   out[q + 1] = acc[QM + 1];
 }
 
-// One warp per column: lane l sums the partials of row blocks l, l+32, l+64, ... in order, an
-// xor butterfly combines the lanes (every lane ends with the same, position-independent value),
-// then (if S_TL given) lane 0 assembles S = [[S_TL, S_BL^T], [S_BL, S_BR]], rhs = [b_T, b_B] and
-// solves.  This fixes the cross-block part of the canonical order.
-__device__ __forceinline__ double warp_allsum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+// Cross-block part of the canonical order: "lane" l sums the partials of row blocks l, l+32,
+// l+64, ... in order, then an xor butterfly combines the 32 lane sums (the value a warp reduction
+// v += shfl_xor(v, o), o = 16 .. 1, leaves on every lane); then (if S_TL is given) the SNP's
+// S = [[S_TL, S_BL^T], [S_BL, S_BR]], rhs = [b_T, b_B] is assembled and solved.
 
 // 32 columns per CTA.  Warp w sums, for every column at once (coalesced loads of consecutive
 // columns' partials), the row blocks of lane slots l = w, w+8, w+16, w+24 -- exactly lane l's

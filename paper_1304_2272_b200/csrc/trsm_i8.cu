@@ -535,7 +535,8 @@ __global__ void slice_rows_kernel(int np, const double* __restrict__ LinvT, long
 // are written as zero when ldg is a multiple of 16.  One thread converts 16 consecutive rows of a
 // column: 8 x 16-byte loads, one 16-byte store (HBM-bound: 8 B read + 1 B written per dosage).
 __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long long ldx,
-                              signed char* __restrict__ G, long long ldg, int* __restrict__ bad) {
+                              signed char* __restrict__ G, long long ldg, double gmax,
+                              int* __restrict__ bad) {
   const int chunks = (n + 15) / 16;                  // 16-row chunks per column
   const long long total = (long long)chunks * cnt;
   const bool vec = ((ldx & 1) == 0) && ((ldg & 15) == 0);
@@ -555,7 +556,7 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const double v = vv[u];
-          const bool ok = (v == trunc(v)) && fabs(v) <= 127.0;
+          const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
           local_bad |= ok ? 0 : 1;
           const int f = 2 * h + u;
           w[f >> 2] |= (unsigned)((ok ? (int)v : 0) & 0xff) << (8 * (f & 3));
@@ -565,7 +566,7 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
 #pragma unroll 1
       for (int f = 0; f < 16 && r0 + f < n; ++f) {
         const double v = col[f];
-        const bool ok = (v == trunc(v)) && fabs(v) <= 127.0;
+        const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
         local_bad |= ok ? 0 : 1;
         w[f >> 2] |= (unsigned)((ok ? (int)v : 0) & 0xff) << (8 * (f & 3));
       }
@@ -579,6 +580,21 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
     }
   }
   if (__any_sync(0xffffffffu, local_bad != 0) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// int8 dosages: *bad |= 1 if any |g| exceeds gmax (the exact-int32 bound for this n).
+__global__ void range_i8_kernel(int n, int cnt, const signed char* __restrict__ G, long long ldg,
+                                int gmax, int* __restrict__ bad) {
+  const long long total = (long long)n * cnt;
+  bool b = false;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / n;
+    const int i = (int)(e - j * n);
+    const int g = G[j * ldg + i];
+    b |= (g > gmax) || (g < -gmax);
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_i8() {
@@ -664,6 +680,22 @@ int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int*
   return GG_OK;
 }
 
+// Largest |dosage| for which every slice product 127 |g| n stays below 2^31 (exact int32).
+int i8_value_bound(int n) {
+  if (n < 1) return 127;
+  const long long b = 2147483647LL / (127LL * (long long)n);
+  return b >= 127 ? 127 : (int)b;
+}
+
+int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, cudaStream_t s) {
+  if (cnt <= 0 || i8_value_bound(n) >= 127) return GG_OK;
+  long long grid = ((long long)n * cnt + 255) / 256;
+  if (grid > 148LL * 16) grid = 148LL * 16;
+  range_i8_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, G, ldg, i8_value_bound(n), bad);
+  GG_LAUNCH_CHECK("range_i8_kernel");
+  return GG_OK;
+}
+
 int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
                int* bad, cudaStream_t s) {
   if (ldx < n || ldg < n) {
@@ -673,7 +705,7 @@ int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, l
   if (cnt <= 0) return GG_OK;
   long long grid = ((long long)((n + 15) / 16) * cnt + 255) / 256;
   if (grid > 148LL * 16) grid = 148LL * 16;
-  narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, bad);
+  narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, (double)i8_value_bound(n), bad);
   GG_LAUNCH_CHECK("narrow_kernel");
   return GG_OK;
 }

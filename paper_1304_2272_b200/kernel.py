@@ -219,8 +219,11 @@ def _slice_inverse(Linv_colmajor, n):
 
 
 def _int8_exact(col):
+    """Integer values the int8 tensor-core path computes exactly at this n (the int32 bound of
+    gg_i8_value_bound: 127 up to n = 133,144)."""
+    bound = _capi.lib().gg_i8_value_bound(len(col))
     return bool(np.all(np.isfinite(col)) and np.all(col == np.trunc(col))
-                and np.all(np.abs(col) <= 127))
+                and np.all(np.abs(col) <= bound))
 
 
 def _trsm_i8_device(slices, expo, n, A):

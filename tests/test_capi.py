@@ -49,6 +49,9 @@ def test_host_only_entry_points():
     assert lib.gg_pad(1) == 128 and lib.gg_pad(128) == 128 and lib.gg_pad(129) == 256
     assert lib.gg_potrf_workspace_bytes(10000) >= 8 * 10112 * 128
     assert lib.gg_trtri_workspace_bytes(10000) > 0
+    # exact-int32 bound of the int8 path: 127 up to n = 133,144, then shrinking
+    assert lib.gg_i8_value_bound(10000) == 127 and lib.gg_i8_value_bound(133144) == 127 and lib.gg_i8_value_bound(133145) == 126
+    assert lib.gg_i8_value_bound(150000) == 2147483647 // (127 * 150000) == 112
     # argument validation happens before any device work
     rc = lib.gg_trsm_lower_f64(0, 1, None, 128, None, 128, None, 128, None)
     assert rc == _capi.GG_EARG
