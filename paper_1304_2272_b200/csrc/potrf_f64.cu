@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long
         return;
       }
       const double piv = sqrt(d);
+      const double rpiv = 1.0 / piv;          // scale by the reciprocal, as dpotf2's DSCAL does
       double* col = sh.col[j & 1];
       const int bj = j >> 4;
       if (ty == (j & 15)) {                   // owners of column j
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long
             if (b != bj) continue;
             const int r = tx + 32 * a;
             if (r > j) {
-              v[a][b] = v[a][b] / piv;
+              v[a][b] = v[a][b] * rpiv;
               col[r] = v[a][b];
             } else if (r == j) {
               v[a][b] = piv;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long
           if (a != ai) continue;
           const int c = ty + 16 * b;
           if (c < i) {
-            v[a][b] = v[a][b] / lii;
+            v[a][b] = v[a][b] * inv_ii;
             sh.rowx[c] = v[a][b];
           } else if (c == i) {
             v[a][b] = inv_ii;
