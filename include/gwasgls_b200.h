@@ -120,7 +120,16 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
  * halves and rounded once to double (correctly rounded; per-column results independent of the
  * column's position).
  *   gg_slice_inverse_i8 : row-major inverse LinvT (see gg_trsm_lower_rm_f64) -> slices
- *                         (gg_inverse_slices_bytes(n) bytes, [slice][row][k]) + expo (np ints).
+ *                         (gg_inverse_slices_bytes(n) bytes) + expo (np ints).  Slices are
+ *                         tile-packed: the lower triangle of 128 x 128 tiles (row tile mt, k
+ *                         tile kt <= mt) at tile index mt (mt+1)/2 + kt, each [slice][row][k]
+ *                         int8 (128 KB): 4 np^2 + O(np) bytes.
+ *   gg_slice_packed_inverse_i8 : the same from the packed FP64 inverse of gg_pack_lower_f64.
+ *   gg_row_exponents_blockcyclic / gg_slice_blockcyclic_i8 : the distributed form -- each rank
+ *                         computes its rows' exponents over its blocks (INT_MIN where it owns
+ *                         nothing; a MAX all-reduce gives expo), then writes the slices of the
+ *                         elements it owns with zeros elsewhere (a SUM all-reduce of the int8
+ *                         buffers over disjoint supports is exact).
  *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg; with ldg a multiple
  *                         of 16 the rows up to the next multiple of 16 are zeroed); *bad_dev |= 1
  *                         if any value is not an integer with |v| <= gg_i8_value_bound(n).
@@ -135,6 +144,13 @@ int gg_i8_value_bound(int n);
 size_t gg_inverse_slices_bytes(int n);
 int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
                         void* stream);
+int gg_slice_packed_inverse_i8(int n, const double* LinvP, int8_t* slices, int* expo,
+                               void* stream);
+int gg_row_exponents_blockcyclic(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                                 const double* Bloc, int ldloc, int* expo, void* stream);
+int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                            const double* Bloc, int ldloc, const int* expo, int8_t* slices,
+                            void* stream);
 int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
                      int* bad_dev, void* stream);
 int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,

@@ -40,6 +40,9 @@ SIGNATURES = {
     "gg_trsm_lower_packed_f64": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp]),
     "gg_i8_slices": (_i, []),
     "gg_i8_value_bound": (_i, [_i]),
+    "gg_slice_packed_inverse_i8": (_i, [_i, _vp, _vp, _vp, _vp]),
+    "gg_row_exponents_blockcyclic": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
+    "gg_slice_blockcyclic_i8": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp]),
     "gg_inverse_slices_bytes": (_sz, [_i]),
     "gg_slice_inverse_i8": (_i, [_i, _vp, _i, _vp, _vp, _vp]),
     "gg_narrow_f64_i8": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),

@@ -142,6 +142,37 @@ int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int
                                as_stream(stream));
 }
 
+int gg_slice_packed_inverse_i8(int n, const double* LinvP, int8_t* slices, int* expo,
+                               void* stream) {
+  if (n < 1 || LinvP == nullptr || slices == nullptr || expo == nullptr) {
+    gg::set_error("slice_packed_inverse: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::slice_packed_run(n, LinvP, reinterpret_cast<signed char*>(slices), expo,
+                              as_stream(stream));
+}
+
+int gg_row_exponents_blockcyclic(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                                 const double* Bloc, int ldloc, int* expo, void* stream) {
+  if (n < 1 || Bloc == nullptr || expo == nullptr) {
+    gg::set_error("row_exponents_blockcyclic: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::row_exponents_bc_run(n, nb, grid_r, grid_c, prow, pcol, Bloc, ldloc, expo,
+                                  as_stream(stream));
+}
+
+int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
+                            const double* Bloc, int ldloc, const int* expo, int8_t* slices,
+                            void* stream) {
+  if (n < 1 || Bloc == nullptr || expo == nullptr || slices == nullptr) {
+    gg::set_error("slice_blockcyclic: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::slice_bc_run(n, nb, grid_r, grid_c, prow, pcol, Bloc, ldloc, expo,
+                          reinterpret_cast<signed char*>(slices), as_stream(stream));
+}
+
 int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
                      int* bad_dev, void* stream) {
   if (n < 1 || X == nullptr || G == nullptr || bad_dev == nullptr) {

@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -151,12 +152,13 @@ __device__ __forceinline__ void tma_2d_pair(unsigned dst, const CUtensorMap* map
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void tma_3d_pair(unsigned dst, const CUtensorMap* map, unsigned bar,
-                                            int c0, int c1, int c2) {
+__device__ __forceinline__ void tma_4d_pair(unsigned dst, const CUtensorMap* map, unsigned bar,
+                                            int c0, int c1, int c2, int c3) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void mma_i8_pair(unsigned d_tmem, unsigned long long a,
@@ -370,7 +372,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
           const unsigned dA = sbase + stage * P_STAGE_BYTES;
           tma_2d_pair(dA, &tmA, fb & PEER_MASK, kt * TK, nt * TM);
-          tma_3d_pair(dA + A_BYTES, &tmB, fb & PEER_MASK, kt * TK, rb * TR, (int)rank * P_SLICES);
+          tma_4d_pair(dA + A_BYTES, &tmB, fb & PEER_MASK, 0, (rb & 3) * TR, (int)rank * P_SLICES,
+                      (rb >> 2) * ((rb >> 2) + 1) / 2 + kt);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -497,35 +500,84 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---- inverse slicing ---------------------------------------------------------------------------
-// LinvT: row-major inverse (element (i, k) at LinvT[k + i*ld]); one CTA per row.
-__global__ void slice_rows_kernel(int np, const double* __restrict__ LinvT, long long ld,
-                                  signed char* __restrict__ Sl, int* __restrict__ expo) {
+// Slices are stored tile-packed: the lower triangle of 128 x 128 tiles (row tile mt, k tile kt,
+// kt <= mt) at tile index mt (mt+1)/2 + kt, each tile [slice 8][row 128][k 128] int8 (128 KB), so
+// the slices take S/2 bytes per element of the triangle (4 np^2 + O(np) bytes) -- 90 GB at
+// n = 1.5e5, where a square layout would not fit a GPU.
+constexpr int ST = 128;                                  // slice tile edge
+constexpr long long ST_BYTES = (long long)S * ST * ST;   // 128 KB
+
+__host__ __device__ inline long long slice_tiles(int np) {
+  const long long nt = np / ST;
+  return nt * (nt + 1) / 2;
+}
+__device__ __forceinline__ long long slice_offset(int i, int k, int s) {   // k <= diag tile end
+  const long long mt = i / ST, kt = k / ST;
+  return (mt * (mt + 1) / 2 + kt) * ST_BYTES + (long long)s * ST * ST + (long long)(i % ST) * ST +
+         (k % ST);
+}
+
+// Element sources for the slicing kernels: row-major square inverse, packed FP64 inverse
+// (trsm_tma.cu layout), and one rank's share of a 2D block-cyclic inverse (0 where not owned).
+struct SrcRowMajor {
+  const double* A;
+  long long ld;
+  __device__ double operator()(int i, int k) const { return A[(long long)i * ld + k]; }
+};
+struct SrcPacked {
+  const double* P;
+  __device__ double operator()(int i, int k) const {
+    const long long mt = i / 128;
+    return P[(4 * mt * (mt + 1) + k / 16) * 2048 + (i % 128) * 16 + (k % 16)];
+  }
+};
+struct SrcBlockCyclic {
+  const double* B;
+  long long ldl;
+  int nb, gr, gc, pr, pc;
+  __device__ double operator()(int i, int k) const {
+    const int I = i / nb, J = k / nb;
+    if (I % gr != pr || J % gc != pc) return 0.0;
+    const long long li = (long long)(I / gr) * nb + i % nb, lk = (long long)(J / gc) * nb + k % nb;
+    return B[li + lk * ldl];
+  }
+};
+
+// Row exponents: e_i with max_k |Linv[i,k]| < 2^e_i (INT_MIN when the row has no nonzero here:
+// the distributed form takes a MAX over ranks).  One CTA per row.
+template <class Src>
+__global__ void row_exponent_kernel(int np, Src src, int* __restrict__ expo) {
   const int i = blockIdx.x;
-  const double* row = LinvT + (long long)i * ld;
   __shared__ double red[32];
   double mx = 0.0;
-  for (int k = threadIdx.x; k <= i && k < np; k += blockDim.x) mx = fmax(mx, fabs(row[k]));
+  for (int k = threadIdx.x; k <= i && k < np; k += blockDim.x) mx = fmax(mx, fabs(src(i, k)));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    mx = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (threadIdx.x == 0) red[0] = mx;
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x / 32); ++w) mx = fmax(mx, red[w]);
+    int e = INT_MIN;
+    if (mx > 0.0) frexp(mx, &e);   // mx = f 2^e, f in [0.5, 1)  ->  |row| < 2^e
+    expo[i] = e;
   }
-  __syncthreads();
-  mx = red[0];
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);   // mx = f * 2^e, f in [0.5, 1)  ->  |row| < 2^e
-  if (threadIdx.x == 0) expo[i] = e;
-  const long long plane = (long long)np * np;
-  for (int k = threadIdx.x; k < np; k += blockDim.x) {
-    double v = (k <= i) ? ldexp(row[k], -e) : 0.0;   // |v| < 1, exact power-of-2 scaling
+}
+
+// Slices of row i for k < (i/128 + 1) * 128 (zero above the diagonal) given e_i:
+// v = Linv[i,k] 2^-e_i (|v| < 1, exact), then a_s = trunc(128 v), v = 128 v - a_s (exact).
+template <class Src>
+__global__ void slice_rows_kernel(int np, Src src, const int* __restrict__ expo,
+                                  signed char* __restrict__ Sl) {
+  const int i = blockIdx.x;
+  const int e = expo[i];
+  const int kend = (i / ST + 1) * ST;
+  for (int k = threadIdx.x; k < kend; k += blockDim.x) {
+    double v = (k <= i) ? src(i, k) : 0.0;
+    v = (v != 0.0) ? ldexp(v, -e) : 0.0;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double t = v * 128.0;                     // exact
       const double q = trunc(t);                      // |q| <= 127
-      Sl[s * plane + (long long)i * np + k] = (signed char)(int)q;
+      Sl[slice_offset(i, k, s)] = (signed char)(int)q;
       v = t - q;                                      // exact remainder, |v| < 1
     }
   }
@@ -618,7 +670,7 @@ int encode(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
     set_error("cuTensorMapEncodeTiled unavailable from the driver");
     return GG_ECUDA;
   }
-  cuuint32_t estr[3] = {1, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -663,10 +715,7 @@ int sms() {
 
 int i8_slices() { return S; }
 
-size_t inverse_slices_bytes(int n) {
-  const size_t np = (size_t)pad_rows(n);
-  return (size_t)S * np * np;
-}
+size_t inverse_slices_bytes(int n) { return (size_t)slice_tiles(pad_rows(n)) * ST_BYTES; }
 
 int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
                       cudaStream_t s) {
@@ -675,7 +724,46 @@ int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int*
     set_error("slice_inverse: ld must be >= gg_pad(n)");
     return GG_EDIM;
   }
-  slice_rows_kernel<<<np, 256, 0, s>>>(np, LinvT, ldp, Sl, expo);
+  SrcRowMajor src{LinvT, ldp};
+  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
+  GG_LAUNCH_CHECK("row_exponent_kernel");
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
+  GG_LAUNCH_CHECK("slice_rows_kernel");
+  return GG_OK;
+}
+
+int slice_packed_run(int n, const double* LinvP, signed char* Sl, int* expo, cudaStream_t s) {
+  const int np = pad_rows(n);
+  SrcPacked src{LinvP};
+  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
+  GG_LAUNCH_CHECK("row_exponent_kernel");
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
+  GG_LAUNCH_CHECK("slice_rows_kernel");
+  return GG_OK;
+}
+
+int row_exponents_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
+                         int* expo, cudaStream_t s) {
+  if (nb < 1 || gr < 1 || gc < 1 || pr < 0 || pr >= gr || pc < 0 || pc >= gc) {
+    set_error("row_exponents_blockcyclic: bad grid");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  SrcBlockCyclic src{B, ldl, nb, gr, gc, pr, pc};
+  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
+  GG_LAUNCH_CHECK("row_exponent_kernel");
+  return GG_OK;
+}
+
+int slice_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
+                 const int* expo, signed char* Sl, cudaStream_t s) {
+  if (nb < 1 || gr < 1 || gc < 1 || pr < 0 || pr >= gr || pc < 0 || pc >= gc) {
+    set_error("slice_blockcyclic: bad grid");
+    return GG_EARG;
+  }
+  const int np = pad_rows(n);
+  SrcBlockCyclic src{B, ldl, nb, gr, gc, pr, pc};
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
   GG_LAUNCH_CHECK("slice_rows_kernel");
   return GG_OK;
 }
@@ -739,11 +827,12 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     int rc = encode(&mA, 2, G, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
-  {   // each CTA of a pair loads half of the slices (box: 128 k x 32 rows x S/2 slices)
-    cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)np, (cuuint64_t)S};
-    cuuint64_t strides[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
-    cuuint32_t box[3] = {TK, TR, P_SLICES};
-    int rc = encode(&mB, 3, Sl, dims, strides, box);
+  {   // tile-packed slices; each CTA of a pair loads 4 of the 8 slices of 32 rows x 128 k
+    cuuint64_t dims[4] = {(cuuint64_t)ST, (cuuint64_t)ST, (cuuint64_t)S,
+                          (cuuint64_t)slice_tiles(np)};
+    cuuint64_t strides[3] = {(cuuint64_t)ST, (cuuint64_t)ST * ST, (cuuint64_t)ST_BYTES};
+    cuuint32_t box[4] = {TK, TR, P_SLICES, 1};
+    int rc = encode(&mB, 4, Sl, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
   I8Args a;

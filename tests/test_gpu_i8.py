@@ -116,3 +116,57 @@ def test_intercept_duplicate_exactly_singular(K):
     rb = K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(X)))
     st = [r.status for r in rb.results]
     assert st[4] == "degenerate" and st.count("degenerate") == 1
+
+
+@pytest.mark.parametrize("n", [300, 1001])
+def test_slices_from_packed_and_block_cyclic_sources(K, n):
+    """The tile-packed slices are identical whether cut from the row-major inverse, the packed
+    FP64 inverse, or assembled from a 2x2 block-cyclic distribution (row exponents MAX-reduced,
+    per-rank slices with zeros elsewhere SUM-reduced) -- the config-4 construction."""
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._capi import ptr, stream_handle
+
+    lib = _capi.lib()
+    s = stream_handle()
+    M = make_spd(n, n + 1)
+    _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+    sl_ref, ex_ref = K._slice_inverse(Linv, n)
+    np_ = _capi.pad(n)
+    sl = torch.empty_like(sl_ref)
+    ex = torch.empty_like(ex_ref)
+    assert lib.gg_slice_packed_inverse_i8(n, ptr(LinvP), ptr(sl), ptr(ex), s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(ex, ex_ref) and torch.equal(sl, sl_ref)
+    # 2x2 block-cyclic, nb = 128: local blocks of each "rank" from the full column-major inverse
+    nb, gr, gc = 128, 2, 2
+    Linv_h = Linv[:np_, :np_].cpu().numpy()          # (cols, rows): Linv_h[k, i] = Linv[i, k]
+    nbk = np_ // nb
+    exps, slcs = [], []
+    for pr in range(gr):
+        for pc in range(gc):
+            rows = [I for I in range(nbk) if I % gr == pr]
+            cols = [J for J in range(nbk) if J % gc == pc]
+            loc = np.zeros((len(cols) * nb, len(rows) * nb))   # column-major local (cols, rows)
+            for a_, I in enumerate(rows):
+                for b_, J in enumerate(cols):
+                    loc[b_ * nb:(b_ + 1) * nb, a_ * nb:(a_ + 1) * nb] = \
+                        Linv_h[J * nb:(J + 1) * nb, I * nb:(I + 1) * nb]
+            B = torch.from_numpy(loc).cuda()
+            e = torch.empty_like(ex)
+            assert lib.gg_row_exponents_blockcyclic(n, nb, gr, gc, pr, pc, ptr(B),
+                                                    len(rows) * nb, ptr(e), s) == 0
+            exps.append(e)
+            slcs.append((B, rows))
+    emax = torch.stack(exps).max(dim=0).values
+    torch.cuda.synchronize()
+    assert torch.equal(emax, ex_ref)
+    total = torch.zeros(sl_ref.numel(), dtype=torch.int32, device="cuda")
+    for (B, rows), (pr, pc) in zip(slcs, [(0, 0), (0, 1), (1, 0), (1, 1)]):
+        part = torch.full_like(sl_ref, 7)
+        assert lib.gg_slice_blockcyclic_i8(n, nb, gr, gc, pr, pc, ptr(B), len(rows) * nb,
+                                           ptr(emax), ptr(part), s) == 0
+        total += part.to(torch.int32)
+    torch.cuda.synchronize()
+    assert torch.equal(total.to(torch.int8), sl_ref) and int(total.abs().max()) <= 127
