@@ -43,6 +43,7 @@ extern "C" {
 
 #define GG_TILE 128      /* row padding unit = GEMM tile edge                    */
 #define GG_PMAX 20       /* largest p supported by the small-system solver       */
+#define GG_STATUS_INVALID (-2) /* per-SNP status: block not computable on the chosen path */
 #define GG_DOT_BLOCK 32  /* rows per partial sum of the canonical reduction order */
 
 /* Library identification / errors. */
@@ -225,6 +226,8 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
  *   slices given, X64 (FP64)        : device narrowing; exact integers in [-127,127] take the
  *                                     int8 path, otherwise the FP64 DMMA TRSM (LinvP) runs;
  *   no slices                       : [widen int8 ->] FP64 DMMA TRSM (LinvP) -> reductions.
+ * Without LinvP (slices only: the config-4 form) a block the int8 path cannot compute exactly
+ * gets status GG_STATUS_INVALID and NaN coefficients for every SNP.
  * Then the batched p x p solve.  XLbar has leading dimension gg_pad(n).  work: at least
  * gg_gls_block_workspace_bytes(n, q, cnt, input_int8, have_slices) bytes of device memory.   */
 size_t gg_gls_block_workspace_bytes(int n, int q, int cnt, int input_int8, int have_slices);

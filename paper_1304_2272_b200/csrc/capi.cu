@@ -340,7 +340,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
     return GG_EARG;
   }
   const bool have_slices = slices != nullptr && expo != nullptr;
-  if (work == nullptr || (LinvP == nullptr && !(have_slices && G8 != nullptr))) {
+  if (work == nullptr || (LinvP == nullptr && !have_slices)) {
     gg::set_error("gls_block: null workspace / inverse");
     return GG_EARG;
   }
@@ -353,6 +353,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
   const long long n16 = (n + 15) / 16 * 16;
   const BlockWs w = block_ws(n, q, cnt, G8 != nullptr, have_slices, static_cast<char*>(work));
   int rc = GG_OK;
+  bool invalid_gate = false;
   if (have_slices) {
     const signed char* g = reinterpret_cast<const signed char*>(G8);
     long long lg = ldg;
@@ -367,20 +368,20 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
                                    np, ybar, w.P, nullptr, 0, s);
       } else {
         // large n: values beyond the exact-int32 bound send the block down the DMMA path
-        if (LinvP == nullptr) {
-          gg::set_error("gls_block: n > 133144 with int8 input needs LinvP (value-range fallback)");
-          return GG_EARG;
-        }
+        // (or, without an FP64 inverse, mark it invalid)
         GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
         rc = gg::range_i8_run(n, cnt, g, lg, w.flag, s);
         if (rc == GG_OK)
           rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q,
                                      XLbar, np, ybar, w.P, w.flag, 0, s);
-        if (rc == GG_OK) rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);
-        if (rc == GG_OK)
-          rc = gg::trsm_packed_gated_run(n, cnt, LinvP, w.x64, np, w.xbar, np, w.flag, 1, s);
-        if (rc == GG_OK)
-          rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
+        if (rc == GG_OK && LinvP != nullptr) {
+          rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);
+          if (rc == GG_OK)
+            rc = gg::trsm_packed_gated_run(n, cnt, LinvP, w.x64, np, w.xbar, np, w.flag, 1, s);
+          if (rc == GG_OK)
+            rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
+        }
+        invalid_gate = LinvP == nullptr;
       }
     } else {
       // FP64 dosages: narrow on the device; exact integers take the int8 tensor-core path, any
@@ -396,6 +397,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
         if (rc == GG_OK)
           rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
       }
+      invalid_gate = LinvP == nullptr;   // non-integer dosages and no FP64 inverse
     }
   } else {
     const double* xin = X64;
@@ -410,7 +412,9 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
       rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, nullptr, 0);
   }
   if (rc != GG_OK) return rc;
-  return gg::reduce_solve_run(n, cnt, q, w.P, nullptr, S_TL, b_T, beta, status, sinv, s);
+  rc = gg::reduce_solve_run(n, cnt, q, w.P, nullptr, S_TL, b_T, beta, status, sinv, s);
+  if (rc == GG_OK && invalid_gate) rc = gg::mark_invalid_run(cnt, q + 1, w.flag, 1, beta, status, s);
+  return rc;
 }
 
 int gg_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,

@@ -105,6 +105,8 @@ size_t partials_bytes(int n, int cnt, int q);
 int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                  int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
                  int gate_value);
+int mark_invalid_run(int cnt, int p, const int* gate, int gate_value, double* beta, int* status,
+                     cudaStream_t s);
 int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,
                      const double* b_T, double* beta, int* status, double* sinv, cudaStream_t s);
 

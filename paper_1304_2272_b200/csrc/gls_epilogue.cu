@@ -256,6 +256,20 @@ __global__ void small_solve_kernel(int batch, int p, const double* __restrict__ 
   for (int i = 0; i < p; ++i) x[(long long)b * p + i] = xo[i];
 }
 
+// Block-level rejection (device-side): if *gate == gate_value every SNP of the block gets
+// status GG_STATUS_INVALID and NaN coefficients (values the selected path cannot compute exactly
+// and no FP64 inverse to fall back on).
+__global__ void mark_invalid_kernel(int cnt, int p, const int* __restrict__ gate, int gate_value,
+                                    double* __restrict__ beta, int* __restrict__ status) {
+  if (*gate != gate_value) return;
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)cnt * p;
+       e += (long long)gridDim.x * blockDim.x) {
+    beta[e] = qnan;
+    if (e % p == 0) status[e / p] = GG_STATUS_INVALID;
+  }
+}
+
 __global__ void widen_kernel(int n, int np, int cnt, const int8_t* __restrict__ G, long long ldg,
                              double* __restrict__ X, long long ldx) {
   const long long total = (long long)np * cnt;
@@ -311,6 +325,15 @@ static int launch_reduce(int nrb, int cnt, int q, const double* P, double* dots,
   reduce_solve_kernel<QM, PM><<<(cnt + 31) / 32, 256, sm, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
                                                                 beta, status, sinv);
   GG_LAUNCH_CHECK("reduce_solve_kernel");
+  return GG_OK;
+}
+
+int mark_invalid_run(int cnt, int p, const int* gate, int gate_value, double* beta, int* status,
+                     cudaStream_t s) {
+  if (cnt <= 0) return GG_OK;
+  const int grid = (int)(((long long)cnt * p + 255) / 256 > 1184 ? 1184 : ((long long)cnt * p + 255) / 256);
+  mark_invalid_kernel<<<grid, 256, 0, s>>>(cnt, p, gate, gate_value, beta, status);
+  GG_LAUNCH_CHECK("mark_invalid_kernel");
   return GG_OK;
 }
 

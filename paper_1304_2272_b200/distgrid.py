@@ -147,6 +147,12 @@ def _allreduce(t, dist):
     return t
 
 
+def _allreduce_max(t, dist):
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t
+
+
 def _broadcast(t, src, dist):
     if dist is not None:
         dist.broadcast(t, src)
@@ -218,6 +224,36 @@ def assemble_packed_inverse(B, layout, ops, dist=None):
     """Replicate the packed tile-major inverse on every rank from the block-cyclic shares."""
     P = ops.pack_blockcyclic(B, layout)
     return _allreduce(P, dist)
+
+
+def assemble_slices(B, layout, ops, dist=None):
+    """Replicated int8 slices + row exponents of the inverse from the block-cyclic shares: each
+    rank takes its rows' exponents over its blocks (MAX all-reduce), then cuts the slices of the
+    elements it owns with zeros elsewhere (SUM all-reduce of int8 over disjoint supports: exact).
+    Needs 4 np^2 bytes per rank (90 GB at n = 1.5e5) and no replicated FP64 inverse."""
+    expo = ops.row_exponents(B, layout)
+    _allreduce_max(expo, dist)
+    S = ops.slice_blockcyclic(B, layout, expo)
+    return _allreduce(S, dist), expo
+
+
+def whiten_blockcyclic(B, layout, ops, RHS, dist=None):
+    """[X_L | y] bar = L^-1 [X_L | y] from the block-cyclic inverse: one local GEMM of this
+    rank's blocks against the rows of RHS it needs, scattered to global rows and summed over
+    ranks (FP64 all-reduce).  RHS: host (n x k).  Returns a replicated (k, n_pad) tensor."""
+    n, k = RHS.shape
+    full = np.zeros((layout.n_pad, k))
+    full[:n] = RHS                       # padding rows zero (the inverse is identity there)
+    cols = layout.global_rows(layout.col_blocks)
+    rows = layout.global_rows(layout.row_blocks)
+    Y = ops.zeros(k, layout.n_pad)
+    if len(rows) and len(cols):
+        Xloc = ops.from_host(full[cols])                     # (n_loc x k)
+        Yloc = ops.empty(k, layout.m_loc)
+        ops.gemm(Yloc, 0, 0, layout.m_loc, k, B, 0, 0, Xloc, 0, 0, layout.n_loc, 1.0, 0.0,
+                 trans_b=False)
+        ops.scatter_cols_rows(Y, rows, Yloc)
+    return _allreduce(Y, dist)
 
 
 def gather_matrix(D, layout, ops, dist=None):
@@ -318,6 +354,28 @@ class DeviceOps:
                 if I < J:
                     A[jl * nb:(jl + 1) * nb, il * nb:(il + 1) * nb].zero_()
 
+    def row_exponents(self, B, layout):
+        torch, capi = self.torch, self.capi
+        e = torch.empty(layout.n_pad, dtype=torch.int32, device=self.dev)
+        ldl = max(B.shape[1], 1)
+        rc = capi.lib().gg_row_exponents_blockcyclic(
+            layout.n, layout.nb, layout.grid.r, layout.grid.c, layout.pr, layout.pc,
+            capi.ptr(B) if B.numel() else capi.ptr(e), ldl, capi.ptr(e), capi.stream_handle())
+        capi.check(rc, "gg_row_exponents_blockcyclic")
+        return e
+
+    def slice_blockcyclic(self, B, layout, expo):
+        torch, capi = self.torch, self.capi
+        S = torch.empty(int(capi.lib().gg_inverse_slices_bytes(layout.n)), dtype=torch.int8,
+                        device=self.dev)
+        ldl = max(B.shape[1], 1)
+        rc = capi.lib().gg_slice_blockcyclic_i8(
+            layout.n, layout.nb, layout.grid.r, layout.grid.c, layout.pr, layout.pc,
+            capi.ptr(B) if B.numel() else capi.ptr(S), ldl, capi.ptr(expo), capi.ptr(S),
+            capi.stream_handle())
+        capi.check(rc, "gg_slice_blockcyclic_i8")
+        return S
+
     def pack_blockcyclic(self, B, layout):
         torch, capi = self.torch, self.capi
         P = torch.empty(int(capi.lib().gg_packed_lower_bytes(layout.n)) // 8,
@@ -340,6 +398,8 @@ class DistConfig:
     m_blk: int = 8192
     emit_s_inv: bool = False
     nb: int = DEFAULT_NB
+    int8: bool = True                  # replicate the int8 slices (dosage blocks on tcgen05)
+    fp64_inverse: bool | None = None   # replicate the packed FP64 inverse (None: if it fits)
 
 
 def run_dist(paths, cfg=None, ops=None, sweep=True):
@@ -364,11 +424,23 @@ def run_dist(paths, cfg=None, ops=None, sweep=True):
     layout = BlockCyclic(n, cfg.nb, grid, rank)
     A, B = local_from_gwam(paths.cov, layout, ops)
     dist_potrf_inv(A, B, layout, ops, dist)
-    LinvP = assemble_packed_inverse(B, layout, ops, dist)
-    del B
+    if sweep:
+        A = None                           # L itself is not needed by the sweep
     XL = fileio.read_matrix(paths.covariates, "GWAC")
     y = fileio.read_matrix(paths.pheno, "GWAY")
-    ctx = kernel.prepare_from_inverse(LinvP, n, XL, y)
+    slices, expo = assemble_slices(B, layout, ops, dist) if cfg.int8 else (None, None)
+    fp64 = cfg.fp64_inverse
+    if fp64 is None:   # the same decision on every rank (same n, same device class)
+        fp64 = _packed_inverse_fits(layout.n, ops)
+    if fp64 or slices is None:
+        LinvP = assemble_packed_inverse(B, layout, ops, dist)
+        del B
+        ctx = kernel.prepare_from_inverse(LinvP, n, XL, y, slices=slices, expo=expo)
+    else:   # config-4 sizes: no replicated FP64 inverse; whiten from the block-cyclic one
+        LinvP = None
+        XLy = whiten_blockcyclic(B, layout, ops, np.column_stack([XL, np.ravel(y)]), dist)
+        del B
+        ctx = kernel.prepare_from_inverse(None, n, XL, y, slices=slices, expo=expo, XLy=XLy)
     t_prepare = time.perf_counter() - t_start
     if not sweep:
         return ctx, (A, layout)
@@ -379,7 +451,19 @@ def run_dist(paths, cfg=None, ops=None, sweep=True):
         t_total=time.perf_counter() - t_start, bytes_read=s.bytes_read,
         bytes_written=s.bytes_written, buffer_regions=2, gpus=world, t_device=s.t_device,
         snps_per_s=s.snps_per_s,
-        peak_resident_est=8 * (layout.m_loc * layout.n_loc * 2 + LinvP.numel()))
+        peak_resident_est=8 * layout.m_loc * layout.n_loc * 2
+        + (8 * LinvP.numel() if LinvP is not None else 0)
+        + (slices.numel() if slices is not None else 0))
+
+
+def _packed_inverse_fits(n, ops):
+    """Room for the replicated packed FP64 inverse (4 np^2 doubles) next to the slices."""
+    torch = getattr(ops, "torch", None)
+    if torch is None or not torch.cuda.is_available():
+        return True
+    from . import _capi
+    free, _ = torch.cuda.mem_get_info(_capi.device())
+    return int(_capi.lib().gg_packed_lower_bytes(n)) < 0.6 * free
 
 
 def env_rank():

@@ -29,7 +29,7 @@ from ._device import (
     upload_cols,
     upload_square_identity_padded,
 )
-from .errors import DimensionMismatch, NotPositiveDefinite, RankDeficientCovariates
+from .errors import DeviceError, DimensionMismatch, NotPositiveDefinite, RankDeficientCovariates
 
 EPS = 2.0 ** -52   # kernel.py:28
 
@@ -82,7 +82,7 @@ class _LazyResults:
     def _one(self, k):
         a = self._a
         gidx = a.first_index + k if a.global_indices is None else int(a.global_indices[k])
-        if a.status[k] < 0:
+        if a.status[k] == -1:
             return SnpResult(snp_index=gidx, beta=a.beta[k],
                              s_inv=a.sinv[k] if a.sinv is not None else None, status="ok")
         return SnpResult(snp_index=gidx, beta=np.full(a.beta.shape[1], np.nan), s_inv=None,
@@ -122,13 +122,20 @@ class ResultArrays:
     sinv: np.ndarray | None = None
     global_indices: np.ndarray | None = None
 
+    def __post_init__(self):
+        if np.any(self.status == STATUS_INVALID):
+            raise DeviceError(
+                "block holds dosages the int8 tensor-core path cannot compute exactly and the "
+                "context has no FP64 inverse to fall back on (distributed engine: use "
+                "DistConfig(fp64_inverse=True))")
+
     @property
     def count(self):
         return self.beta.shape[0]
 
     @property
     def ok(self):
-        return self.status < 0
+        return self.status == -1
 
 
 @dataclass
@@ -216,6 +223,27 @@ def _slice_inverse(Linv_colmajor, n):
                                           stream_handle()), "gg_slice_inverse_i8")
     del LinvT
     return sl, expo
+
+
+def _slices_fit(n):
+    """Room for the int8 slices (4 np^2 bytes) next to what is already resident."""
+    torch = __import__("torch")
+    free, _ = torch.cuda.mem_get_info(_capi.device())
+    return int(_capi.lib().gg_inverse_slices_bytes(n)) < 0.8 * free
+
+
+def _slice_packed(LinvP, n):
+    """int8 slices + exponents from the packed FP64 inverse."""
+    torch = __import__("torch")
+    sl = torch.empty(int(_capi.lib().gg_inverse_slices_bytes(n)), dtype=torch.int8,
+                     device=LinvP.device)
+    expo = torch.empty(pad(n), dtype=torch.int32, device=LinvP.device)
+    check(_capi.lib().gg_slice_packed_inverse_i8(n, ptr(LinvP), ptr(sl), ptr(expo),
+                                                 stream_handle()), "gg_slice_packed_inverse_i8")
+    return sl, expo
+
+
+STATUS_INVALID = -2   # GG_STATUS_INVALID (include/gwasgls_b200.h)
 
 
 def _int8_exact(col):
@@ -438,21 +466,29 @@ def gls_prepare(M, XL, y, int8_split=True):
     _, L, LinvP, Linv = _potrf_device(M, keep_square_inverse=True)
     slices, expo = _slice_inverse(Linv, n) if int8_split else (None, None)
     del Linv
-    return prepare_from_inverse(LinvP, n, XL, y, L=L, slices=slices, expo=expo)
+    return prepare_from_inverse(LinvP, n, XL, y, L=L, slices=slices, expo=expo,
+                                int8_split=int8_split)
 
 
-def prepare_from_inverse(LinvP, n, XL, y, L=None, slices=None, expo=None):
-    """The marker-independent tail of gls_prepare (kernel.py:246-257) given the packed inverse:
+def prepare_from_inverse(LinvP, n, XL, y, L=None, slices=None, expo=None, XLy=None,
+                         int8_split=True):
+    """The marker-independent tail of gls_prepare (kernel.py:246-257) given the inverse:
     whiten [X_L | y] with the streamed TRSM kernel, S_TL = gram(X_L bar) and b_T with the
     per-SNP reduction kernel, SPD check of S_TL.  Shared by gls_prepare and the distributed
-    engine (whose factor exists only block-cyclically, so L may be None)."""
+    engine, whose factor exists only block-cyclically (L None); at config-4 sizes that engine
+    also has no replicated FP64 inverse (LinvP None) and passes the whitened [X_L | y] (XLy,
+    device, (q + 1, gg_pad(n))) it formed itself plus the int8 slices, and without LinvP no
+    slices are cut here (slices come from the caller)."""
     torch = __import__("torch")
     XL = np.asarray(XL, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64).ravel()
     q = XL.shape[1]
     np_ = pad(n)
-    RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
-    XLy = _trsm_device(LinvP, n, RHS, q + 1)
+    if XLy is None:
+        RHS = upload_cols(np.column_stack([XL, y]), ld=np_)
+        XLy = _trsm_device(LinvP, n, RHS, q + 1)
+    if int8_split and slices is None and LinvP is not None and _slices_fit(n):
+        slices, expo = _slice_packed(LinvP, n)
     if slices is not None:
         # covariate columns that are exact small integers (the intercept) are whitened by the
         # same tensor-core kernel as the dosage blocks, so a SNP equal to such a column gives
@@ -504,16 +540,20 @@ def _collect(ws, cnt, first_index, global_indices, emit_s_inv):
 def device_context(ctx, need_factor=False):
     """Device half of any PreparedContext-like object (ours, or the reference's dataclass built
     by a caller such as run_dist, distgrid.py:385).  Built from the host fields on first use and
-    cached on the object; with ``need_factor`` the row-major inverse is derived from ``ctx.L``."""
+    cached on the object; with ``need_factor`` the inverse is derived from ``ctx.L`` unless the
+    context already carries one (packed FP64 or, in the distributed config-4 form, only the int8
+    slices: blocks that need FP64 then come back invalid)."""
     d = getattr(ctx, "_dev", None)
     if d is None:
         d = DeviceContext.from_host(ctx.XLbar, ctx.ybar, ctx.S_TL, ctx.b_T)
         ctx._dev = d
-    if need_factor and d.LinvP is None:
+    if need_factor and d.LinvP is None and d.slices is None:
         L = np.asarray(ctx.L, dtype=np.float64)
         if L.ndim != 2 or L.shape != (d.n, d.n):
             raise DimensionMismatch("context has no usable Cholesky factor for the TRSM")
         _, d.LinvP = _trtri_device(L)
+        if d.slices is None and _slices_fit(d.n):   # dosage blocks then take the int8 path
+            d.slices, d.expo = _slice_packed(d.LinvP, d.n)
     return d
 
 

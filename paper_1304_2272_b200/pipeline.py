@@ -150,7 +150,7 @@ class StreamEngine:
 
         self.torch = torch
         self.d = ctx._dev
-        if self.d is None or self.d.LinvP is None:
+        if self.d is None or (self.d.LinvP is None and self.d.slices is None):
             raise ConfigError("StreamEngine needs a device-prepared context")
         self.m_blk = int(m_blk)
         self.int8 = bool(int8)

@@ -8,6 +8,42 @@ from scipy.linalg import solve_triangular
 from scipy.linalg.lapack import dpotrf
 
 
+INT_MIN = -2 ** 31
+
+
+def slice_offsets(i, k, np_):
+    """Byte offsets of element (i, k) in the tile-packed slice layout, one per slice."""
+    mt, kt = i // 128, k // 128
+    base = (mt * (mt + 1) // 2 + kt) * 131072 + (i % 128) * 128 + (k % 128)
+    return base[..., None] + 16384 * np.arange(8)
+
+
+def slices_dense(Linv_rows, expo, np_):
+    """Tile-packed int8 slices of a dense lower-triangular inverse given row exponents (the
+    restatement of slice_rows_kernel, used as the CPU ops' implementation and the check)."""
+    nt = np_ // 128
+    out = np.zeros(nt * (nt + 1) // 2 * 131072, dtype=np.int8)
+    for i in range(np_):
+        kend = (i // 128 + 1) * 128
+        k = np.arange(kend)
+        v = np.where(k <= i, Linv_rows(i, kend), 0.0)
+        v = np.where(v != 0.0, np.ldexp(v, -int(expo[i])), 0.0)
+        q = np.empty((kend, 8))
+        for s in range(8):
+            t = v * 128.0
+            q[:, s] = np.trunc(t)
+            v = t - q[:, s]
+        out[slice_offsets(i, k, np_)] = q.astype(np.int8)
+    return out
+
+
+def row_exponents_dense(rows_abs_max):
+    e = np.full(rows_abs_max.shape, INT_MIN, dtype=np.int32)
+    nz = rows_abs_max > 0
+    e[nz] = np.frexp(rows_abs_max[nz])[1]
+    return e
+
+
 def pack_lower_dense(Dense, n):
     """Packed tile-major layout of the lower triangle of a dense (>= np x np) matrix."""
     np_ = -(-n // 128) * 128
@@ -82,6 +118,23 @@ class CpuOps:
             for il, I in enumerate(layout.row_blocks):
                 if I < J:
                     A[jl * nb:(jl + 1) * nb, il * nb:(il + 1) * nb].zero_()
+
+    def _full_share(self, B, layout):
+        full = np.zeros((layout.n_pad, layout.n_pad))
+        rows = layout.global_rows(layout.row_blocks)
+        cols = layout.global_rows(layout.col_blocks)
+        if len(rows) and len(cols):
+            full[np.ix_(rows, cols)] = self.to_host(B)
+        return full
+
+    def row_exponents(self, B, layout):
+        full = np.tril(self._full_share(B, layout))
+        return torch.from_numpy(row_exponents_dense(np.abs(full).max(axis=1)))
+
+    def slice_blockcyclic(self, B, layout, expo):
+        full = np.tril(self._full_share(B, layout))
+        S = slices_dense(lambda i, kend: full[i, :kend], expo.numpy(), layout.n_pad)
+        return torch.from_numpy(S)
 
     def pack_blockcyclic(self, B, layout):
         full = np.zeros((layout.n_pad, layout.n_pad))

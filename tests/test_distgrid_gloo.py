@@ -58,7 +58,10 @@ def _body(rank, world, n, nb, bad_pivot, q, dist):
     L = distgrid.gather_matrix(A, lay, ops, dist)
     Li = distgrid.gather_matrix(B, lay, ops, dist)
     P = distgrid.assemble_packed_inverse(B, lay, ops, dist).numpy()
-    q.put((rank, "ok", (L, Li, P)))
+    S, e = distgrid.assemble_slices(B, lay, ops, dist)
+    RHS = np.random.default_rng(3).standard_normal((n, 3))
+    W = distgrid.whiten_blockcyclic(B, lay, ops, RHS, dist)
+    q.put((rank, "ok", (L, Li, P, S.numpy(), e.numpy(), ops.to_host(W), RHS)))
 
 
 def _run(world, n, nb, bad_pivot=None):
@@ -109,13 +112,27 @@ def test_dist_cholesky_inverse_and_packed_assembly(world):
     Lr = cholesky(M, lower=True)
     Lir = solve_triangular(Lr, np.eye(n), lower=True)
     Pr = pack_lower_dense(Lir, n)
-    for rank, kind, (L, Li, P) in out:
+    from dist_cpu_ops import row_exponents_dense, slices_dense
+
+    np_ = -(-n // 128) * 128
+    for rank, kind, (L, Li, P, S, e, W, RHS) in out:
         assert kind == "ok"
         assert np.max(np.abs(L - Lr)) <= 1e-13 * np.max(np.abs(Lr))
         assert np.all(np.triu(L, 1) == 0)
         assert np.max(np.abs(Li - Lir)) <= 1e-12 * np.max(np.abs(Lir))
         assert np.max(np.abs(P - Pr)) <= 1e-12 * np.max(np.abs(Pr))
         assert np.array_equal(P, out[0][2][2])          # identical replica on every rank
+        # int8 slices: MAX-reduced exponents and SUM-reduced per-rank slices equal the slices
+        # of the gathered inverse (what one GPU would cut), identical on every rank
+        Lg = np.eye(np_)
+        Lg[:n, :n] = np.tril(Li)
+        ex = row_exponents_dense(np.abs(Lg).max(axis=1))
+        assert np.array_equal(e, ex)
+        assert np.array_equal(S, slices_dense(lambda i, kend: Lg[i, :kend], ex, np_))
+        assert np.array_equal(S, out[0][2][3])
+        # whitening from the block-cyclic inverse
+        Wr = Lir @ RHS
+        assert np.max(np.abs(W[:n] - Wr)) <= 1e-12 * np.max(np.abs(Wr)) and not W[n:].any()
 
 
 def test_dist_not_positive_definite_global_pivot():

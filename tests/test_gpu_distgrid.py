@@ -46,15 +46,38 @@ def test_device_dist_not_pd(gpu):
     assert e.value.pivot_index == 450
 
 
+@pytest.mark.parametrize("fp64_inverse", [None, False])
 @pytest.mark.parametrize("case", ["baseline_p4", "degenerate"])
-def test_run_dist_end_to_end(gpu, tmp_path, case):
+def test_run_dist_end_to_end(gpu, tmp_path, case, fp64_inverse):
+    """Both forms of the distributed prepare: replicated packed FP64 inverse + slices, and the
+    config-4 form (slices only, [X_L | y] whitened from the block-cyclic inverse)."""
     from oracle import gls_ref as O
     from paper_1304_2272_b200 import distgrid, fileio
 
     g = golden(case)
     paths = write_golden_dataset(tmp_path, g)
-    s = distgrid.run_dist(paths, distgrid.DistConfig(m_blk=257, nb=128))
+    s = distgrid.run_dist(paths, distgrid.DistConfig(m_blk=257, nb=128, fp64_inverse=fp64_inverse))
     assert s.mode == "dist" and s.np_ == 1
     pay = fileio.read_matrix(paths.out, "GWAB")
     rel, mism = O.compare(pay.betas, g["beta"])
     assert mism == 0 and rel <= 1e-9
+
+
+def test_slices_only_context_rejects_non_integer_blocks(gpu):
+    """Without an FP64 inverse a non-integer block cannot be computed: every SNP of the block is
+    marked invalid on the device and the host raises (no silent wrong numbers)."""
+    from paper_1304_2272_b200 import kernel
+    from paper_1304_2272_b200.errors import DeviceError
+
+    rng = np.random.default_rng(2)
+    n = 200
+    M = make_spd(n, 5)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 2))])
+    ctx = kernel.gls_prepare(M, XL, rng.standard_normal(n))
+    ctx._dev.LinvP = None
+    X = rng.integers(0, 3, (n, 20)).astype(float)
+    ok = kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X))
+    assert all(r.status in ("ok", "degenerate") for r in ok.results)
+    X[5, 3] = 0.25
+    with pytest.raises(DeviceError):
+        kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X))
