@@ -170,3 +170,59 @@ def test_slices_from_packed_and_block_cyclic_sources(K, n):
         total += part.to(torch.int32)
     torch.cuda.synchronize()
     assert torch.equal(total.to(torch.int8), sl_ref) and int(total.abs().max()) <= 127
+
+
+def test_dynamic_scheduler_stress_deterministic(K):
+    """Many launches of the tile-queue kernel with ragged shapes (1 .. 2 SNP tiles, partial row
+    blocks): every repeat is bitwise identical to the first (no scheduling race, no hang)."""
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._capi import ptr, stream_handle
+
+    lib = _capi.lib()
+    s = stream_handle()
+    rng = np.random.default_rng(11)
+    for n, cnts in ((130, (1, 7, 255, 256, 257, 513)), (1000, (33, 300))):
+        M = make_spd(n, n + 3)
+        XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 2))])
+        ctx = K.gls_prepare(M, XL, rng.standard_normal(n))
+        d = ctx._dev
+        n16 = -(-n // 16) * 16
+        for cnt in cnts:
+            G = torch.zeros((cnt, n16), dtype=torch.int8)
+            G[:, :n] = torch.from_numpy(rng.integers(0, 3, (cnt, n)).astype(np.int8))
+            G = G.cuda()
+            P = torch.empty(int(lib.gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64,
+                            device="cuda")
+            ref = None
+            for rep in range(40):
+                assert lib.gg_trsm_lower_i8_partials(n, cnt, ptr(d.slices), ptr(d.expo), ptr(G),
+                                                     n16, d.q, ptr(d.XLy), ptr(d.ybar), ptr(P),
+                                                     None, 0, None, 0, s) == 0
+                if rep == 0:
+                    ref = P.clone()
+            torch.cuda.synchronize()
+            assert torch.equal(P, ref), (n, cnt)
+
+
+@pytest.mark.parametrize("p", [2, 8, 20])
+def test_i8_path_all_covariate_counts(K, p):
+    """The fused epilogue's partial dots for p = 2, 8, 20 (q = 1, 7, 19: the
+    three reduction variants) against the oracle."""
+    from oracle import gls_ref as O
+
+    rng = np.random.default_rng(50 + p)
+    n = 333
+    M = make_spd(n, p)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, p - 2))]) if p >= 2 \
+        else np.zeros((n, 0))
+    y = rng.standard_normal(n)
+    G = rng.integers(0, 3, (n, 70)).astype(np.int8)
+    ctx = K.gls_prepare(M, XL, y)
+    assert ctx._dev.slices is not None
+    rb = K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(G)), emit_s_inv=True)
+    got = _betas(rb)
+    ref, ok = O.gls_solve_block(O.gls_prepare(M, XL, y), G.astype(float))
+    rel, mism = O.compare(got, ref)
+    assert mism == 0 and rel <= 1e-10, rel
