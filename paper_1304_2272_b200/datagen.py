@@ -203,9 +203,10 @@ class DatasetPaths:
                    geno=os.path.join(out_dir, "genotypes.gwai" if int8 else "genotypes.gwax"))
 
 
-def write_dataset(spec, out_dir, int8=False, M=None, chunk=4096):
+def write_dataset(spec, out_dir, int8=False, M=None, chunk=4096, device=False):
     """Write GWAM/GWAC/GWAY and the genotype file (GWAX FP64 or GWAI int8), streaming the
-    genotypes in column chunks so m may exceed host memory."""
+    genotypes in column chunks so m may exceed host memory (``device``: generate the chunks
+    with the bit-identical device generator)."""
     os.makedirs(out_dir, exist_ok=True)
     paths = DatasetPaths.in_dir(out_dir, int8=int8)
     if M is None:
@@ -219,7 +220,10 @@ def write_dataset(spec, out_dir, int8=False, M=None, chunk=4096):
         f.write(fileio.pack_header(kind, (spec.n, spec.m)))
         for j0 in range(0, spec.m, chunk):
             cnt = min(chunk, spec.m - j0)
-            g = genotypes_host(spec.seed, spec.n, spec.m, j0, cnt, spec.maf)
+            if device:
+                g = genotypes_device(spec, j0, cnt).cpu().numpy().T
+            else:
+                g = genotypes_host(spec.seed, spec.n, spec.m, j0, cnt, spec.maf)
             arr = g if int8 else g.astype(np.float64, order="F")
             f.write(arr.tobytes(order="F"))
     return paths

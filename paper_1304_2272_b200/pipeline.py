@@ -122,13 +122,33 @@ class SolveConfig:
         return int(env) if env else None
 
 
+def _read_cov_device(path):
+    """GWAM -> device: parallel preads into pinned memory, one H2D copy, and the reader's
+    symmetry / finiteness checks (fileio.py:153-157) done on the device."""
+    import torch
+
+    from .errors import AsymmetricCovariance
+
+    n = fileio.read_dims(path, "GWAM")[0]
+    host = torch.empty(8 * n * n, dtype=torch.uint8).pin_memory()
+    got = fileio.pread_into(path, fileio.header_size("GWAM"), memoryview(host.numpy()))
+    if got < 8 * n * n:
+        raise fileio.TruncatedFile(f"expected {8 * n * n} payload bytes, got {got}")
+    Md = host.view(torch.float64).reshape(n, n).to(_capi.device(), non_blocking=True)
+    if not bool(torch.equal(Md, Md.T)):
+        raise AsymmetricCovariance("covariance file is not exactly symmetric")
+    if not bool(torch.isfinite(Md).all()):
+        raise AsymmetricCovariance("covariance file has non-finite entries")
+    return Md
+
+
 def _load_prepare(paths):
     t0 = time.perf_counter()
-    M = fileio.read_matrix(paths.cov, "GWAM")
+    Md = _read_cov_device(paths.cov)
     XL = fileio.read_matrix(paths.covariates, "GWAC")
     y = fileio.read_matrix(paths.pheno, "GWAY")
-    ctx = kernel.gls_prepare(M, XL, y)
-    return ctx, time.perf_counter() - t0, M.nbytes
+    ctx = kernel.gls_prepare(Md, XL, y)
+    return ctx, time.perf_counter() - t0, Md.numel() * 8
 
 
 # ---------------------------------------------------------------------------------------------
