@@ -2,8 +2,8 @@
 //
 // Replaces kernel.cholesky_spd (reference kernel.py:92-109: LAPACK dpotrf lower, clean=1).
 // Per 128-column block k:
-//   leaf     : one CTA factors the 128x128 diagonal block in shared memory (pivot rule of
-//              LAPACK dpotf2: fail iff a_jj <= 0 or NaN) and inverts it in place
+//   leaf     : one CTA factors the 128x128 diagonal block in shared memory, blocked by 32
+//              (pivot rule of LAPACK dpotf2: fail iff a_jj <= 0 or NaN) and inverts it
 //              (Dinv_k = L_kk^-1, written to the diagonal block of Linv);
 //   panel    : L21 = A21 * Dinv_k^T                 (DMMA GEMM, op(B) = B^T)
 //   trailing : A22 -= L21 * L21^T, lower tiles only  (DMMA GEMM, K = 128)
@@ -23,7 +23,6 @@ namespace {
 constexpr int NB = 128;
 constexpr int OUTER = 4 * NB;   // outer block width of the two-level Cholesky
 constexpr int LEAF_THREADS = 512;
-constexpr size_t LEAF_SMEM = 0;   // register-resident leaf (static shared only)
 
 struct PotrfHeader {
   int info;                      // 0 = ok, else failing pivot + 1
@@ -67,155 +66,156 @@ __global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long 
   }
 }
 
-// Register-resident 128 x 128 leaf.  512 threads; thread (tx = tid % 32, ty = tid / 32) owns
-// the 32 elements (r, c) = (tx + 32a, ty + 16b), a < 4, b < 8, in v[a][b] (lower part only; the
-// upper part is kept zero).  Shared memory holds only the broadcast vectors of each step.
-struct LeafShared {
-  double col[2][NB];   // scaled column j of L (phase 1), double-buffered by step parity
-  double rowx[NB];     // final row i of the inverse (phase 2)
-  double colL[NB];     // column i of L, staged before the in-place overwrite (phase 2)
-  double diag[NB];     // pivots L_jj
-  double d;            // current pivot candidate
-};
+// Blocked 128 x 128 leaf in shared memory (b = 32 sub-blocks; 512 threads).  Factor:
+// for each diagonal sub-block J one warp factors it (right-looking, dpotf2 pivot rule: fail
+// iff a_jj <= 0 or NaN, scaling by the reciprocal pivot as dpotf2's DSCAL does) and inverts
+// it (T_J = L_JJ^-1); then all threads form the panel L_IJ = A_IJ T_J^T and update the
+// trailing lower part.  Inverse: X_JJ = T_J, X_IJ = -T_I sum_{K=J}^{I-1} L_IK X_KJ.  ~16 block
+// barriers instead of two per column.
+constexpr int LB = 32;                  // sub-block edge
+constexpr int LDS = NB + 1;             // padded smem row stride (conflict-free columns)
+constexpr size_t LEAF2_SMEM = (size_t)(NB * LDS + 2 * 4 * LB * LB) * sizeof(double) + 16;
 
-// FACTOR = true : factor the diagonal block at (k0, k0) of A in place (lower, upper zeroed,
-//                 dpotf2 pivot rule: fail iff a_jj <= 0 or NaN), then write its inverse to Dinv.
-//                 One CTA; the blocks are processed in order by the host loop.
-// FACTOR = false: blockIdx.x selects diagonal block b; only invert it (triangular inverse of a
-//                 caller-supplied L).  All blocks in parallel.
+// warp: factor the 32 x 32 diagonal sub-block at (j0, j0) of S in place; returns the failing
+// local column (0..31) or -1.  Lane i owns row j0 + i.
+__device__ int warp_factor32(double* S, int j0, int lane) {
+  for (int j = 0; j < LB; ++j) {
+    const double d = S[(j0 + j) * LDS + j0 + j];
+    if (!(d > 0.0)) return j;                      // uniform: every lane read the same d
+    const double piv = sqrt(d), rp = 1.0 / piv;
+    __syncwarp();
+    if (lane == j) S[(j0 + j) * LDS + j0 + j] = piv;
+    if (lane > j) S[(j0 + lane) * LDS + j0 + j] *= rp;
+    __syncwarp();
+    if (lane > j) {
+      const double l = S[(j0 + lane) * LDS + j0 + j];
+      for (int c = j + 1; c <= lane; ++c)
+        S[(j0 + lane) * LDS + j0 + c] -= l * S[(j0 + c) * LDS + j0 + j];
+    }
+    __syncwarp();
+  }
+  return -1;
+}
+
+// warp: T = L^-1 for the 32 x 32 lower sub-block at (j0, j0) of S; T row-major 32 x 32 (upper
+// part zero).  Lane c computes column c by forward substitution (multiplying by 1/L_ii).
+__device__ void warp_inverse32(const double* S, int j0, double* T, int lane) {
+  const int c = lane;
+  for (int i = 0; i < c; ++i) T[i * LB + c] = 0.0;
+  T[c * LB + c] = 1.0 / S[(j0 + c) * LDS + j0 + c];
+  for (int i = c + 1; i < LB; ++i) {
+    double acc = 0.0;
+    for (int k = c; k < i; ++k) acc += S[(j0 + i) * LDS + j0 + k] * T[k * LB + c];
+    T[i * LB + c] = -acc * (1.0 / S[(j0 + i) * LDS + j0 + i]);
+  }
+  __syncwarp();
+}
+
 template <bool FACTOR>
-__global__ void __launch_bounds__(LEAF_THREADS) leaf_kernel(double* A, long long ld, double* Dinv,
-                                                            long long ldi, int k0, int* info) {
-  __shared__ LeafShared sh;
+__global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long long ld,
+                                                             double* Dinv, long long ldi, int k0,
+                                                             int* info) {
+  extern __shared__ double lsm[];
+  double* S = lsm;                          // 128 x 128 row-major (ld LDS): the block, then L
+  double* T = lsm + NB * LDS;               // 4 x (32 x 32): T_J = L_JJ^-1
+  double* W = T + 4 * LB * LB;              // 4 x (32 x 32): scratch of the inverse phase
+  int* fail = reinterpret_cast<int*>(W + 4 * LB * LB);
   if (info != nullptr && *info != 0) return;
   if (!FACTOR) k0 = blockIdx.x * NB;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* Ab = A + k0 + (long long)k0 * ld;
-  double v[4][8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = tx + 32 * a, c = ty + 16 * b;
-      v[a][b] = (r >= c) ? Ab[r + (long long)c * ld] : 0.0;
-    }
-
+  for (int e = tid; e < NB * NB; e += blockDim.x) {   // column-major global -> row-major smem
+    const int r = e % NB, c = e / NB;
+    S[r * LDS + c] = (r >= c) ? Ab[r + (long long)c * ld] : 0.0;
+  }
+  if (tid == 0) *fail = -1;
+  __syncthreads();
   if (FACTOR) {
-    // ---- phase 1: right-looking Cholesky --------------------------------------------------
-    if (tx == 0 && ty == 0) sh.d = v[0][0];
-    __syncthreads();
-    for (int j = 0; j < NB; ++j) {
-      const double d = sh.d;
-      if (!(d > 0.0)) {                       // uniform decision
-        if (tid == 0) *info = k0 + j + 1;
-        return;
-      }
-      const double piv = sqrt(d);
-      const double rpiv = 1.0 / piv;          // scale by the reciprocal, as dpotf2's DSCAL does
-      double* col = sh.col[j & 1];
-      const int bj = j >> 4;
-      if (ty == (j & 15)) {                   // owners of column j
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            if (b != bj) continue;
-            const int r = tx + 32 * a;
-            if (r > j) {
-              v[a][b] = v[a][b] * rpiv;
-              col[r] = v[a][b];
-            } else if (r == j) {
-              v[a][b] = piv;
-              sh.diag[j] = piv;
-            }
-          }
+    for (int J = 0; J < NB / LB; ++J) {
+      const int j0 = J * LB;
+      double* TJ = T + J * LB * LB;
+      if (warp == 0) {
+        const int f = warp_factor32(S, j0, lane);
+        if (f >= 0) {
+          if (lane == 0) *fail = j0 + f;
+        } else {
+          warp_inverse32(S, j0, TJ, lane);
+        }
       }
       __syncthreads();
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int r = tx + 32 * a;
-        if (r <= j) continue;
-        const double lr = col[r];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const int c = ty + 16 * b;
-          if (c > j && c <= r) {
-            v[a][b] = v[a][b] - lr * col[c];
-            if (r == j + 1 && c == j + 1) sh.d = v[a][b];   // next pivot candidate
-          }
-        }
+      if (*fail >= 0) {
+        if (tid == 0) *info = k0 + *fail + 1;
+        return;
+      }
+      const int r0 = j0 + LB, rows = NB - r0;
+      if (rows <= 0) break;
+      // panel: L_IJ = A_IJ T_J^T   (rows r0.., columns j0..j0+31); each thread some (r, c)
+      for (int e = tid; e < rows * LB; e += blockDim.x) {
+        const int r = r0 + e / LB, c = e % LB;
+        double acc = 0.0;
+        for (int k = 0; k <= c; ++k) acc += S[r * LDS + j0 + k] * TJ[c * LB + k];
+        W[e] = acc;
+      }
+      __syncthreads();
+      for (int e = tid; e < rows * LB; e += blockDim.x) S[(r0 + e / LB) * LDS + j0 + e % LB] = W[e];
+      __syncthreads();
+      // trailing update of the lower part: S[r][c] -= sum_j L[r][j0+j] L[c][j0+j], c <= r
+      for (int e = tid; e < rows * rows; e += blockDim.x) {
+        const int r = r0 + e / rows, c = r0 + e % rows;
+        if (c > r) continue;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < LB; ++j) acc += S[r * LDS + j0 + j] * S[c * LDS + j0 + j];
+        S[r * LDS + c] -= acc;
       }
       __syncthreads();
     }
     double* Aw = A + k0 + (long long)k0 * ld;
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int r = tx + 32 * a, c = ty + 16 * b;
-        Aw[r + (long long)c * ld] = (r >= c) ? v[a][b] : 0.0;
-      }
+    for (int e = tid; e < NB * NB; e += blockDim.x) {
+      const int r = e % NB, c = e / NB;
+      Aw[r + (long long)c * ld] = (r >= c) ? S[r * LDS + c] : 0.0;
+    }
   } else {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (tx + 32 * a == ty + 16 * b) sh.diag[tx + 32 * a] = v[a][b];
+    if (warp < NB / LB) warp_inverse32(S, warp * LB, T + warp * LB * LB, lane);
     __syncthreads();
   }
-
-  // ---- phase 2: in-place inverse (row-oriented forward substitution on X = I) -------------
-  for (int i = 0; i < NB; ++i) {
-    const double lii = sh.diag[i];
-    const double inv_ii = 1.0 / lii;
-    const int ai = i >> 5, bi = i >> 4;
-    if (ty == (i & 15)) {                     // stage column i of L (rows > i)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (b == bi && tx + 32 * a > i) sh.colL[tx + 32 * a] = v[a][b];
-    }
-    if (tx == (i & 31)) {                     // finalize row i of X
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (a != ai) continue;
-          const int c = ty + 16 * b;
-          if (c < i) {
-            v[a][b] = v[a][b] * inv_ii;
-            sh.rowx[c] = v[a][b];
-          } else if (c == i) {
-            v[a][b] = inv_ii;
-            sh.rowx[c] = inv_ii;
-          }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = tx + 32 * a;
-      if (r <= i) continue;
-      const double lri = sh.colL[r];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int c = ty + 16 * b;
-        if (c < i) v[a][b] = v[a][b] - lri * sh.rowx[c];
-        else if (c == i) v[a][b] = -(lri * inv_ii);
-      }
-    }
-    __syncthreads();
-  }
+  // ---- inverse: X_IJ = -T_I sum_{K=J}^{I-1} L_IK X_KJ, block rows I = 1..3 in order; X is
+  // kept in the lower blocks of S (S's L_IK for K < I is read before X_IK overwrites it:
+  // each block row I first computes all its W_IJ, then writes)
   double* Db = Dinv + k0 + (long long)k0 * ldi;
-#pragma unroll
-  for (int b = 0; b < 8; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = tx + 32 * a, c = ty + 16 * b;
-      Db[r + (long long)c * ldi] = (r >= c) ? v[a][b] : 0.0;
+  for (int I = 1; I < NB / LB; ++I) {
+    // W_IJ = sum_{K=J}^{I-1} L_IK X_KJ for J < I   (X_KK = T_K; X_KJ, K > J, from S)
+    for (int e = tid; e < I * LB * LB; e += blockDim.x) {
+      const int J = e / (LB * LB), rr = (e / LB) % LB, cc = e % LB;
+      double acc = 0.0;
+      for (int K = J; K < I; ++K)
+        for (int k = 0; k < LB; ++k) {
+          const double x = (K == J) ? T[J * LB * LB + k * LB + cc]
+                                    : S[(K * LB + k) * LDS + J * LB + cc];
+          acc += S[(I * LB + rr) * LDS + K * LB + k] * x;
+        }
+      W[e] = acc;
     }
+    __syncthreads();
+    for (int e = tid; e < I * LB * LB; e += blockDim.x) {
+      const int J = e / (LB * LB), rr = (e / LB) % LB, cc = e % LB;
+      double acc = 0.0;
+      for (int k = 0; k <= rr; ++k) acc += T[I * LB * LB + rr * LB + k] * W[J * LB * LB + k * LB + cc];
+      S[(I * LB + rr) * LDS + J * LB + cc] = -acc;   // X_IJ (L_IJ no longer needed)
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e % NB, c = e / NB;
+    const int I = r / LB, J = c / LB;
+    double v;
+    if (r < c) v = 0.0;
+    else if (I == J) v = T[I * LB * LB + (r % LB) * LB + (c % LB)];
+    else v = S[r * LDS + c];
+    Db[r + (long long)c * ldi] = v;
+  }
 }
+
 
 int grid_for(long long total) {
   long long g = (total + 255) / 256;
@@ -299,6 +299,8 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   GG_LAUNCH_CHECK("nonfinite_kernel");
   init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, rs, cs, L, Linv, ldp);
   GG_LAUNCH_CHECK("init_factor_kernel");
+  GG_CUDA_TRY(cudaFuncSetAttribute(leaf2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)LEAF2_SMEM));
   // optional phase timing (GG_POTRF_TIMING=1): leaf / panel / trailing / inverse, to stderr
   const bool timing = getenv("GG_POTRF_TIMING") != nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -320,8 +322,8 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
     const int w = (np - K0 < OUTER) ? (np - K0) : OUTER;
     for (int k = K0; k < K0 + w; k += NB) {
       if (timing) cudaEventRecord(ev[0], s);
-      leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
-      GG_LAUNCH_CHECK("potrf leaf_kernel");
+      leaf2_kernel<true><<<1, LEAF_THREADS, LEAF2_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
+      GG_LAUNCH_CHECK("potrf leaf2_kernel");
       lap(t_leaf, ev[0], ev[1]);
       const int rem = np - k - NB;          // rows below this leaf
       if (rem <= 0) break;
@@ -412,8 +414,10 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
   double* T = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
   zero_square_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(np, Linv, ldp);
   GG_LAUNCH_CHECK("zero_square_kernel");
-  // leaf_kernel<false> only reads L; the const_cast never results in a write.
-  leaf_kernel<false><<<np / NB, LEAF_THREADS, LEAF_SMEM, s>>>(const_cast<double*>(L), ldl, Linv,
+  GG_CUDA_TRY(cudaFuncSetAttribute(leaf2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)LEAF2_SMEM));
+  // leaf2_kernel<false> only reads L; the const_cast never results in a write.
+  leaf2_kernel<false><<<np / NB, LEAF_THREADS, LEAF2_SMEM, s>>>(const_cast<double*>(L), ldl, Linv,
                                                                ldp, 0, nullptr);
   GG_LAUNCH_CHECK("trtri leaf_kernel");
   long long tr, tc;
