@@ -77,37 +77,57 @@ constexpr int LDS = NB + 1;             // padded smem row stride (conflict-free
 constexpr size_t LEAF2_SMEM = (size_t)(NB * LDS + 2 * 4 * LB * LB) * sizeof(double) + 16;
 
 // warp: factor the 32 x 32 diagonal sub-block at (j0, j0) of S in place; returns the failing
-// local column (0..31) or -1.  Lane i owns row j0 + i.
+// local column (0..31) or -1.  Lane i keeps row i in registers; the column being eliminated is
+// broadcast with shuffles (no shared-memory round trips inside the 32 steps).
 __device__ int warp_factor32(double* S, int j0, int lane) {
-  for (int j = 0; j < LB; ++j) {
-    const double d = S[(j0 + j) * LDS + j0 + j];
-    if (!(d > 0.0)) return j;                      // uniform: every lane read the same d
+  double r[LB];
+#pragma unroll
+  for (int c = 0; c < LB; ++c) r[c] = S[(j0 + lane) * LDS + j0 + c];
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < LB; ++j) {   // fully unrolled (r stays in registers): no early exit
+    double d = __shfl_sync(0xffffffffu, r[j], j);
+    if (fail < 0 && !(d > 0.0)) fail = j;        // uniform: every lane sees the same d
+    if (fail >= 0) d = 1.0;                      // keep the arithmetic finite past a failure
     const double piv = sqrt(d), rp = 1.0 / piv;
-    __syncwarp();
-    if (lane == j) S[(j0 + j) * LDS + j0 + j] = piv;
-    if (lane > j) S[(j0 + lane) * LDS + j0 + j] *= rp;
-    __syncwarp();
-    if (lane > j) {
-      const double l = S[(j0 + lane) * LDS + j0 + j];
-      for (int c = j + 1; c <= lane; ++c)
-        S[(j0 + lane) * LDS + j0 + c] -= l * S[(j0 + c) * LDS + j0 + j];
+    if (lane == j) r[j] = piv;
+    else if (lane > j) r[j] = r[j] * rp;         // dpotf2's DSCAL by the reciprocal pivot
+#pragma unroll
+    for (int c = j + 1; c < LB; ++c) {
+      const double lc = __shfl_sync(0xffffffffu, r[j], c);
+      if (lane >= c) r[c] -= r[j] * lc;
     }
-    __syncwarp();
   }
-  return -1;
+#pragma unroll
+  for (int c = 0; c < LB; ++c) S[(j0 + lane) * LDS + j0 + c] = r[c];
+  __syncwarp();
+  return fail;
 }
 
 // warp: T = L^-1 for the 32 x 32 lower sub-block at (j0, j0) of S; T row-major 32 x 32 (upper
-// part zero).  Lane c computes column c by forward substitution (multiplying by 1/L_ii).
+// part zero).  Lane c computes column c by forward substitution in registers, multiplying by the
+// reciprocal diagonal (shuffled from the lane that owns it).
 __device__ void warp_inverse32(const double* S, int j0, double* T, int lane) {
+  const double rdiag = 1.0 / S[(j0 + lane) * LDS + j0 + lane];
   const int c = lane;
-  for (int i = 0; i < c; ++i) T[i * LB + c] = 0.0;
-  T[c * LB + c] = 1.0 / S[(j0 + c) * LDS + j0 + c];
-  for (int i = c + 1; i < LB; ++i) {
-    double acc = 0.0;
-    for (int k = c; k < i; ++k) acc += S[(j0 + i) * LDS + j0 + k] * T[k * LB + c];
-    T[i * LB + c] = -acc * (1.0 / S[(j0 + i) * LDS + j0 + i]);
+  double t[LB];
+#pragma unroll
+  for (int i = 0; i < LB; ++i) {
+    const double ri = __shfl_sync(0xffffffffu, rdiag, i);
+    if (i < c) {
+      t[i] = 0.0;
+    } else if (i == c) {
+      t[i] = ri;
+    } else {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= c) acc += S[(j0 + i) * LDS + j0 + k] * t[k];
+      t[i] = -acc * ri;
+    }
   }
+#pragma unroll
+  for (int i = 0; i < LB; ++i) T[i * LB + c] = t[i];
   __syncwarp();
 }
 
@@ -163,10 +183,15 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
       for (int e = tid; e < rows * rows; e += blockDim.x) {
         const int r = r0 + e / rows, c = r0 + e % rows;
         if (c > r) continue;
-        double acc = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < LB; ++j) acc += S[r * LDS + j0 + j] * S[c * LDS + j0 + j];
-        S[r * LDS + c] -= acc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: latency-bound CTA
+#pragma unroll
+        for (int j = 0; j < LB; j += 4) {
+          a0 += S[r * LDS + j0 + j] * S[c * LDS + j0 + j];
+          a1 += S[r * LDS + j0 + j + 1] * S[c * LDS + j0 + j + 1];
+          a2 += S[r * LDS + j0 + j + 2] * S[c * LDS + j0 + j + 2];
+          a3 += S[r * LDS + j0 + j + 3] * S[c * LDS + j0 + j + 3];
+        }
+        S[r * LDS + c] -= (a0 + a1) + (a2 + a3);
       }
       __syncthreads();
     }
@@ -187,14 +212,18 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
     // W_IJ = sum_{K=J}^{I-1} L_IK X_KJ for J < I   (X_KK = T_K; X_KJ, K > J, from S)
     for (int e = tid; e < I * LB * LB; e += blockDim.x) {
       const int J = e / (LB * LB), rr = (e / LB) % LB, cc = e % LB;
-      double acc = 0.0;
+      double a0 = 0.0, a1 = 0.0;
       for (int K = J; K < I; ++K)
-        for (int k = 0; k < LB; ++k) {
-          const double x = (K == J) ? T[J * LB * LB + k * LB + cc]
-                                    : S[(K * LB + k) * LDS + J * LB + cc];
-          acc += S[(I * LB + rr) * LDS + K * LB + k] * x;
+#pragma unroll 8
+        for (int k = 0; k < LB; k += 2) {
+          const double x0 = (K == J) ? T[J * LB * LB + k * LB + cc]
+                                     : S[(K * LB + k) * LDS + J * LB + cc];
+          const double x1 = (K == J) ? T[J * LB * LB + (k + 1) * LB + cc]
+                                     : S[(K * LB + k + 1) * LDS + J * LB + cc];
+          a0 += S[(I * LB + rr) * LDS + K * LB + k] * x0;
+          a1 += S[(I * LB + rr) * LDS + K * LB + k + 1] * x1;
         }
-      W[e] = acc;
+      W[e] = a0 + a1;
     }
     __syncthreads();
     for (int e = tid; e < I * LB * LB; e += blockDim.x) {
