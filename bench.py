@@ -199,8 +199,14 @@ def run_ours(args):
         del G
     else:
         Gres = datagen.genotypes_device(spec, first_marker, m, ld=n16)   # (m, n16) int8
-    g8 = torch.empty((m_blk, n16), dtype=torch.int8, device=dev) if (use_i8 and X is not None) \
-        else None
+    # FP64-resident dosages are narrowed to int8 on a side stream, one block ahead, into a double
+    # buffer: the HBM-bound narrow of block i+1 runs beside the tensor-core TRSM of block i
+    g8s = [torch.empty((m_blk, n16), dtype=torch.int8, device=dev) for _ in range(2)] \
+        if (use_i8 and X is not None) else None
+    side = torch.cuda.Stream(device=dev) if g8s is not None else None
+    narrow_done = [torch.cuda.Event() for _ in range(2)]
+    trsm_done = [torch.cuda.Event() for _ in range(2)]
+    trsm_started = [False, False]
     xin = alloc_cols(m_blk, np_) if (not use_i8 and X is None) else None
     xbar = alloc_cols(m_blk, np_, zero=False) if not use_i8 else None
     P = torch.empty(int(lib.gg_partials_bytes(n, m_blk, q)) // 8, dtype=torch.float64, device=dev)
@@ -221,8 +227,15 @@ def run_ours(args):
             nl = 0
             if use_i8:
                 if X is not None:            # FP64 dosages -> int8 (exactness flag checked after)
-                    rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8), n16, ptr(bad), sh)
-                    G, ldg, nl = g8, n16, nl + 1
+                    slot = i % 2
+                    with torch.cuda.stream(side):
+                        if trsm_started[slot]:          # buffer free once its last TRSM is done
+                            side.wait_event(trsm_done[slot])
+                        rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8s[slot]), n16,
+                                                   ptr(bad), _capi.C.c_void_p(side.cuda_stream))
+                        narrow_done[slot].record(side)
+                    stream.wait_event(narrow_done[slot])
+                    G, ldg, nl = g8s[slot], n16, nl + 1
                 else:
                     G, ldg = Gres[f:], n16
                 if record:
@@ -232,6 +245,9 @@ def run_ours(args):
                                                     None, 0, sh)
                 if record:
                     ev_pairs[i][1].record(stream)
+                if X is not None:
+                    trsm_done[i % 2].record(stream)
+                    trsm_started[i % 2] = True
                 rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
                                                   ptr(beta[f]), ptr(status[f]), None, sh)
                 nl += 2
