@@ -87,3 +87,33 @@ def test_every_ctypes_call_matches_declared_arity():
                 if len(node.args) != want:
                     bad.append((f, node.lineno, node.func.attr, len(node.args), want))
     assert not bad, bad
+
+
+def test_argument_validation_without_a_gpu():
+    """Every compute entry point validates its arguments before touching the device: bad sizes,
+    null pointers and bad leading dimensions return GG_EARG / GG_EDIM with a message (this runs
+    on the CPU box; no kernel is launched)."""
+    from paper_1304_2272_b200 import _capi
+
+    lib = _capi.load_library()
+    EARG, EDIM = _capi.GG_EARG, _capi.GG_EDIM
+    V = None
+    cases = [
+        (lib.gg_potrf_f64, (0, V, 1, 0, V, V, 128, V, V, V), EARG),
+        (lib.gg_trtri_lower_f64, (0, V, 128, V, 128, V, V), EARG),
+        (lib.gg_trsm_lower_i8, (0, 1, V, V, V, 16, V, 128, V), EARG),
+        (lib.gg_trsm_lower_i8_partials, (10, 1, V, V, V, 16, 3, V, V, V, V, 0, V, 0, V), EARG),
+        (lib.gg_gls_reduce_solve_f64, (10, 1, 3, V, V, V, V, V, V, V), EARG),
+        (lib.gg_gls_block_f64, (10, 3, 1, V, V, V, V, V, V, V, V, 0, V, 0, V, V, V, V, V), EARG),
+        (lib.gg_slice_inverse_i8, (0, V, 128, V, V, V), EARG),
+        (lib.gg_slice_packed_inverse_i8, (0, V, V, V, V), EARG),
+        (lib.gg_row_exponents_blockcyclic, (10, 128, 1, 1, 0, 0, V, 128, V, V), EARG),
+        (lib.gg_slice_blockcyclic_i8, (10, 128, 1, 1, 0, 0, V, 128, V, V, V), EARG),
+        (lib.gg_narrow_f64_i8, (0, 1, V, 1, V, 1, V, V), EARG),
+        (lib.gg_small_spd_solve_f64, (1, 0, V, V, V, V, V, V), EARG),
+        (lib.gg_gls_dots_f64, (10, 1, 25, V, 128, V, 128, V, V, V, V), EARG),
+    ]
+    for fn, args, want in cases:
+        rc = fn(*args)
+        assert rc in (want, EDIM), (fn.__name__, rc)
+        assert lib.gg_last_error(), fn.__name__
