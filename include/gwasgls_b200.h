@@ -115,22 +115,30 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
 
 /* ---- The int8 tensor-core TRSM for dosage blocks ------------------------------------------
  * Dosages are exact int8, so X = L^-1 G runs on tcgen05.mma.kind::i8 with the inverse split
- * error-free into gg_i8_slices() int8 slices per row:
- *     Linv[i,k] = 2^expo[i] * sum_s a_s[i,k] 2^(-7 s)      (truncation residual < 2^(expo-56))
- * Each slice product is an exact int32 integer; the eight are combined exactly into two int64
- * halves and rounded once to double (correctly rounded; per-column results independent of the
- * column's position).
+ * error-free into gg_i8_slices() (= 7) int8 slices per row plus an integer diagonal head:
+ *     Linv[i,k] = 2^e_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  |a_s| <= 127
+ * with e_i = max(e_off_i, e_diag_i - 20) (|Linv[i,k]| < 2^e_off_i over k < i, |Linv_ii| <
+ * 2^e_diag_i), |h_i| < 2^20: the truncation residual is < 2^(e_i - 49), i.e. 49 bits below the
+ * row's largest off-diagonal entry and >= 53 bits below its largest entry whenever the diagonal
+ * is >= 16x the off-diagonal maximum (kinship-type covariances).  Each slice product is an exact
+ * int32 integer; the head term h_i g_i and the seven products are combined exactly into two
+ * int64 halves and rounded once to double (correctly rounded; per-column results independent of
+ * the column's position).
+ * Slice metadata ("expo" below): gg_slice_meta_ints(n) = 2 np ints, e_i (np) then h_i (np).
  *   gg_slice_inverse_i8 : row-major inverse LinvT (see gg_trsm_lower_rm_f64) -> slices
- *                         (gg_inverse_slices_bytes(n) bytes) + expo (np ints).  Slices are
- *                         tile-packed: the lower triangle of 128 x 128 tiles (row tile mt, k
- *                         tile kt <= mt) at tile index mt (mt+1)/2 + kt, each [slice][row][k]
- *                         int8 (128 KB): 4 np^2 + O(np) bytes.
+ *                         (gg_inverse_slices_bytes(n) bytes) + metadata.  Slices are tile-packed:
+ *                         the lower triangle of 128 x 128 tiles (row tile mt, k tile kt <= mt)
+ *                         at tile index mt (mt+1)/2 + kt, each [slice][row][k] int8 (112 KB):
+ *                         3.5 np^2 + O(np) bytes.
  *   gg_slice_packed_inverse_i8 : the same from the packed FP64 inverse of gg_pack_lower_f64.
- *   gg_row_exponents_blockcyclic / gg_slice_blockcyclic_i8 : the distributed form -- each rank
- *                         computes its rows' exponents over its blocks (INT_MIN where it owns
- *                         nothing; a MAX all-reduce gives expo), then writes the slices of the
- *                         elements it owns with zeros elsewhere (a SUM all-reduce of the int8
- *                         buffers over disjoint supports is exact).
+ *   gg_row_exponents_blockcyclic / gg_slice_meta_i8 / gg_slice_blockcyclic_i8 : the distributed
+ *                         form -- each rank computes [e_off | e_diag] (2 np ints) over the blocks
+ *                         it owns (INT_MIN where it owns nothing); after a MAX all-reduce
+ *                         gg_slice_meta_i8 turns them into the metadata (heads zeroed); each rank
+ *                         then writes the slices of the elements it owns (zeros elsewhere) and
+ *                         the heads of the diagonals it owns.  SUM all-reduces of the int8 slices
+ *                         and of the heads (metadata ints np .. 2np) over disjoint supports are
+ *                         exact and give the single-GPU result.
  *   gg_narrow_f64_i8    : FP64 dosages (n x cnt, ldx) -> int8 (n x cnt, ldg; with ldg a multiple
  *                         of 16 the rows up to the next multiple of 16 are zeroed); *bad_dev |= 1
  *                         if any value is not an integer with |v| <= gg_i8_value_bound(n).
@@ -147,10 +155,12 @@ int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int
                         void* stream);
 int gg_slice_packed_inverse_i8(int n, const double* LinvP, int8_t* slices, int* expo,
                                void* stream);
+size_t gg_slice_meta_ints(int n);
 int gg_row_exponents_blockcyclic(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
-                                 const double* Bloc, int ldloc, int* expo, void* stream);
+                                 const double* Bloc, int ldloc, int* ex2, void* stream);
+int gg_slice_meta_i8(int n, const int* ex2, int* expo, void* stream);
 int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
-                            const double* Bloc, int ldloc, const int* expo, int8_t* slices,
+                            const double* Bloc, int ldloc, int* expo, int8_t* slices,
                             void* stream);
 int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
                      int* bad_dev, void* stream);

@@ -44,6 +44,8 @@ SIGNATURES = {
     "gg_row_exponents_blockcyclic": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "gg_slice_blockcyclic_i8": (_i, [_i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp, _vp]),
     "gg_inverse_slices_bytes": (_sz, [_i]),
+    "gg_slice_meta_ints": (_sz, [_i]),
+    "gg_slice_meta_i8": (_i, [_i, _vp, _vp, _vp]),
     "gg_slice_inverse_i8": (_i, [_i, _vp, _i, _vp, _vp, _vp]),
     "gg_narrow_f64_i8": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),
     "gg_trsm_lower_i8": (_i, [_i, _i, _vp, _vp, _vp, _ll, _vp, _i, _vp]),

@@ -95,8 +95,8 @@ class DeviceContext:
     XLy: object        # (q + 1, np): whitened covariates, then whitened phenotype
     S_TL: object       # (q * q,) row-major
     b_T: object        # (q,)
-    slices: object = None   # int8 slices of the inverse ([S][np][np]) for the tensor-core TRSM
-    expo: object = None     # per-row power-of-two exponents of the slices (np int32)
+    slices: object = None   # int8 slices of the inverse (tile-packed) for the tensor-core TRSM
+    expo: object = None     # slice metadata: row exponents, diagonal heads (2 np int32)
 
     @property
     def p(self):

@@ -152,18 +152,28 @@ int gg_slice_packed_inverse_i8(int n, const double* LinvP, int8_t* slices, int* 
                               as_stream(stream));
 }
 
+size_t gg_slice_meta_ints(int n) { return n < 1 ? 0 : gg::slice_meta_ints(n); }
+
 int gg_row_exponents_blockcyclic(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
-                                 const double* Bloc, int ldloc, int* expo, void* stream) {
-  if (n < 1 || Bloc == nullptr || expo == nullptr) {
+                                 const double* Bloc, int ldloc, int* ex2, void* stream) {
+  if (n < 1 || Bloc == nullptr || ex2 == nullptr) {
     gg::set_error("row_exponents_blockcyclic: null pointer or n < 1");
     return GG_EARG;
   }
-  return gg::row_exponents_bc_run(n, nb, grid_r, grid_c, prow, pcol, Bloc, ldloc, expo,
+  return gg::row_exponents_bc_run(n, nb, grid_r, grid_c, prow, pcol, Bloc, ldloc, ex2,
                                   as_stream(stream));
 }
 
+int gg_slice_meta_i8(int n, const int* ex2, int* expo, void* stream) {
+  if (n < 1 || ex2 == nullptr || expo == nullptr) {
+    gg::set_error("slice_meta: null pointer or n < 1");
+    return GG_EARG;
+  }
+  return gg::slice_meta_run(n, ex2, expo, as_stream(stream));
+}
+
 int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int pcol,
-                            const double* Bloc, int ldloc, const int* expo, int8_t* slices,
+                            const double* Bloc, int ldloc, int* expo, int8_t* slices,
                             void* stream) {
   if (n < 1 || Bloc == nullptr || expo == nullptr || slices == nullptr) {
     gg::set_error("slice_blockcyclic: null pointer or n < 1");

@@ -76,11 +76,13 @@ size_t inverse_slices_bytes(int n);
 int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
                       cudaStream_t s);
 int i8_value_bound(int n);
-int slice_packed_run(int n, const double* LinvP, signed char* Sl, int* expo, cudaStream_t s);
+int slice_packed_run(int n, const double* LinvP, signed char* Sl, int* meta, cudaStream_t s);
+size_t slice_meta_ints(int n);
 int row_exponents_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
-                         int* expo, cudaStream_t s);
+                         int* ex2, cudaStream_t s);
+int slice_meta_run(int n, const int* ex2, int* meta, cudaStream_t s);
 int slice_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
-                 const int* expo, signed char* Sl, cudaStream_t s);
+                 int* meta, signed char* Sl, cudaStream_t s);
 int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, cudaStream_t s);
 int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
                int* bad, cudaStream_t s);

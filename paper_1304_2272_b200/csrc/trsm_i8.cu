@@ -1,23 +1,28 @@
 // Streamed TRSM on the 5th-generation tensor cores: Xbar = Linv * G for int8 dosage blocks G,
-// with the FP64 inverse split error-free into S int8 slices (Ozaki-style splitting).
+// with the FP64 inverse split error-free into int8 slices (Ozaki-style splitting).
 //
 // Genotype dosages {0,1,2} are exact int8.  Each row i of Linv is written as
-//     Linv[i,k] = 2^e_i * sum_{s=1..S} a_s[i,k] * 2^(-7 s),   a_s int8 in [-127, 127]
-// (truncation residual < 2^(e_i - 7 S); S = 8 -> 56 bits, finer than FP64's 53), so
-//     Xbar[i,j] = 2^e_i * sum_s 2^(-7 s) * C_s[i,j],   C_s = sum_k a_s[i,k] G[k,j]
-// where every C_s is an EXACT int32 integer product (|C_s| <= 127*2*n < 2^31 for n < 8.4e6)
-// computed by tcgen05.mma.kind::i8.  The S terms are recombined in FP64 in a fixed order, so
-// a column's result never depends on its position (bitwise permutation invariance).
+//     Linv[i,k] = 2^e_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  a_s in [-127, 127]
+// (integer diagonal head |h_i| < 2^20, e_i >= e(diagonal) - 20; truncation residual
+// < 2^(e_i - 49), see "inverse slicing" below), so
+//     Xbar[i,j] = 2^(e_i - 49) ( h_i G[i,j] 2^49 + sum_s 2^(7 (6 - s)) C_s[i,j] ),
+//     C_s = sum_k a_s[i,k] G[k,j]
+// where every C_s is an EXACT int32 product (|C_s| <= 127 * 127 n < 2^31 up to n = 133,144;
+// dosages <= 2 up to 8.4e6) computed by tcgen05.mma.kind::i8; the bracket is assembled as two
+// exact int64 halves and rounded once, so a column's result never depends on its position.
 //
-// Kernel (persistent, one CTA per SM, warp-specialised, 6 warps):
-//   warp 0  TMA producer: A = genotype tile (128 SNPs x 128 k, int8, 128B swizzle, OOB rows of
-//           k >= n zero-filled) and B = the S slices of 32 inverse rows (3-D box 128 k x 32 rows
-//           x S slices) into a 4-stage mbarrier ring (48 KB / stage);
-//   warp 1  MMA issuer (one lane): D[128 SNPs x (S*32)] += A . B^T, 4 x K=32 per stage, int32
-//           accumulators in TMEM, double-buffered (2 x 256 columns), tcgen05.commit to mbarriers;
-//   warps 2-5  epilogue: tcgen05.ld each SNP's S x 32 accumulators, recombine in FP64, scale by
-//           2^e_i, store 32 consecutive rows of the SNP's Xbar column (256 contiguous bytes).
-// Tiles = (32-row blocks of Linv) x (128-SNP column tiles); row block rb needs k < 32 (rb+1).
+// Kernel (persistent, CTA pairs with cta_group::2, one CTA per SM, 10 warps):
+//   warp 0  producer: A = 128 SNPs x 128 k int8 per CTA (TMA, 128B swizzle, k >= n zero-filled),
+//           B = this CTA's half of the 7 x 32 slice rows of the tile (tile-packed slices), into a
+//           6-stage mbarrier ring (30 KB / stage); per-tile row data (e_i, h_i, XLbar/ybar rows)
+//           by bulk copies into 4 slots; pulls tiles heavy-first from a global atomic counter and
+//           posts them to a per-cluster tile queue;
+//   warp 1  MMA issuer (leader CTA, one lane): D[256 SNPs x 224] += A . B^T over the pair,
+//           int32 accumulators in TMEM, double-buffered (2 x 256 columns);
+//   warps 2-9  two epilogue groups (one per accumulator buffer): tcgen05.ld each SNP's 7 x 32
+//           accumulators, recombine, store the SNP's 32 Xbar rows and/or the fused per-SNP partial
+//           dots against XLbar / ybar (canonical order of gls_epilogue.cu).
+// Tiles = (32-row blocks of Linv) x (256-SNP column pairs); row block rb needs k < 32 (rb+1).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,14 +37,16 @@
 namespace gg {
 namespace {
 
-constexpr int S = 8;                       // int8 slices of the inverse
+constexpr int S = 7;                       // int8 slices of the inverse (+ a diagonal head)
 constexpr int TM = 128;                    // SNPs per tile (MMA M)
 constexpr int TR = 32;                     // inverse rows per tile
-constexpr int TN = S * TR;                 // MMA N = 256
+constexpr int TN = S * TR;                 // MMA N = 224
 constexpr int TK = 128;                    // k per pipeline stage (4 MMAs of K = 32)
 constexpr int A_BYTES = TM * TK;           // 16 KB
 constexpr int THREADS = 10 * 32;   // producer, MMA, two epilogue groups of 4 warps
-constexpr int ACC_COLS = TN;               // int32 columns per accumulator buffer
+constexpr int ACC_COLS = 256;              // TMEM columns per accumulator buffer (TN used)
+static_assert(S == 7, "tmem_ld_rows8 and the hi/lo recombination are written for 7 slices");
+constexpr int HEAD_BITS = 20;              // e'_i >= e(diagonal) - HEAD_BITS: |h_i| < 2^20
 
 struct I8Args {
   int N;            // SNP columns
@@ -47,7 +54,10 @@ struct I8Args {
   int num_nt;       // ceil(N / 128)
   double* X;        // Xbar, column-major, leading dimension ldx (nullptr: not materialised)
   long long ldx;
-  const int* expo;  // e_i per inverse row (np)
+  const int* expo;  // slice metadata: e'_i per inverse row (np), then the heads h_i (np)
+  const signed char* G;   // the dosages (for the head term h_i g_i of the diagonal)
+  long long ldg;
+  int n;
   // fused epilogue reductions (canonical order of gls_epilogue.cu): partial dots of each SNP's
   // 32-row block against XLbar (q columns, ld ldxl) and ybar -> P[(rb*N + col)*(q+2) + k]
   int q;
@@ -117,13 +127,13 @@ __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& 
 // commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
 // threads release the accumulator on the leader's "accumulator empty" barrier.
 constexpr int P_STAGES = 6;
-constexpr int P_SLICES = S / 2;
-constexpr int P_B_BYTES = P_SLICES * TR * TK;        // 16 KB
-constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 32 KB
+constexpr int P_B_ROWS = TN / 2;                    // 112 slice rows per CTA of the pair
+constexpr int P_B_BYTES = P_B_ROWS * TK;             // 14 KB
+constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 30 KB
 // per-tile row data staged by the producer with bulk copies: e_i (32 ints) then the tile's 32
 // rows of XLbar's q columns and of ybar (q + 1 <= GG_PMAX columns)
 constexpr int RD_SLOTS = 4;
-constexpr int RD_COLS_OFF = TR * 4;
+constexpr int RD_COLS_OFF = 2 * TR * 4;   // e'_i, then the diagonal heads h_i
 constexpr int RD_BYTES = RD_COLS_OFF + GG_PMAX * TR * 8;    // 5248
 constexpr size_t P_SMEM_BYTES =
     size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 512;
@@ -220,39 +230,32 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
       : "memory");
 }
 
-// 8 rows x all S slices of one accumulator quarter: v[s][r] = C_s of row r (8 loads, one wait)
-__device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[8][8]) {
+// 8 rows x all S slices of one accumulator quarter: v[s][r] = C_s of row r (7 loads, one wait)
+__device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[S][8]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%64];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%65];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%66];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%67];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%68];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%69];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%70];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%56,%57,%58,%59,%60,%61,%62,%63}, [%71];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%56];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%57];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%58];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%59];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%60];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%61];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%62];\n"
       "tcgen05.wait::ld.sync.aligned;\n"
-      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]),
-        "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]), "=r"(v[1][0]), "=r"(v[1][1]),
-        "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]),
-        "=r"(v[1][7]), "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]),
-        "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]), "=r"(v[3][0]),
-        "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]),
-        "=r"(v[3][6]), "=r"(v[3][7]), "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]),
-        "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
-        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]),
-        "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]), "=r"(v[6][0]), "=r"(v[6][1]),
-        "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]),
-        "=r"(v[6][7]), "=r"(v[7][0]), "=r"(v[7][1]), "=r"(v[7][2]), "=r"(v[7][3]),
-        "=r"(v[7][4]), "=r"(v[7][5]), "=r"(v[7][6]), "=r"(v[7][7])
-      : "r"(taddr), "r"(taddr + TR), "r"(taddr + 2 * TR), "r"(taddr + 3 * TR),
-        "r"(taddr + 4 * TR), "r"(taddr + 5 * TR), "r"(taddr + 6 * TR), "r"(taddr + 7 * TR)
+      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]),
+        "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]), "=r"(v[1][7]),
+        "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]), "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]),
+        "=r"(v[3][0]), "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]), "=r"(v[3][6]), "=r"(v[3][7]),
+        "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]), "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
+        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]), "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]),
+        "=r"(v[6][0]), "=r"(v[6][1]), "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]), "=r"(v[6][7])
+      : "r"(taddr + 0 * TR), "r"(taddr + 1 * TR), "r"(taddr + 2 * TR), "r"(taddr + 3 * TR), "r"(taddr + 4 * TR), "r"(taddr + 5 * TR), "r"(taddr + 6 * TR)
       : "memory");
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     trsm_i8_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, I8Args a) {
+                        const __grid_constant__ CUtensorMap tmB3,
+                        const __grid_constant__ CUtensorMap tmB1, I8Args a) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -358,8 +361,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(rde0 + 8 * slot, ((r / RD_SLOTS) & 1) ^ 1);
           const unsigned rbar = rdf0 + 8 * slot, dst = rbase + slot * RD_BYTES;
           const int row0 = rb * TR;
-          mbar_expect_tx(rbar, TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0));
+          mbar_expect_tx(rbar, 2 * TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0));
           bulk_g2s(dst, a.expo + row0, TR * 4, rbar);
+          bulk_g2s(dst + TR * 4, a.expo + a.num_rb * TR + row0, TR * 4, rbar);
           if (partials) {
             for (int c = 0; c < a.q; ++c)
               bulk_g2s(dst + RD_COLS_OFF + c * TR * 8, a.XL + c * a.ldxl + row0, TR * 8, rbar);
@@ -372,8 +376,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
           const unsigned dA = sbase + stage * P_STAGE_BYTES;
           tma_2d_pair(dA, &tmA, fb & PEER_MASK, kt * TK, nt * TM);
-          tma_4d_pair(dA + A_BYTES, &tmB, fb & PEER_MASK, 0, (rb & 3) * TR, (int)rank * P_SLICES,
-                      (rb >> 2) * ((rb >> 2) + 1) / 2 + kt);
+          // this CTA's 112 slice rows: CTA0 = slices 0-2 + rows 0-15 of slice 3,
+          // CTA1 = rows 16-31 of slice 3 + slices 4-6 (accumulator column = 32 s + row)
+          const int tile = (rb >> 2) * ((rb >> 2) + 1) / 2 + kt, r0 = (rb & 3) * TR;
+          if (rank == 0) {
+            tma_4d_pair(dA + A_BYTES, &tmB3, fb & PEER_MASK, 0, r0, 0, tile);
+            tma_4d_pair(dA + A_BYTES + 3 * TR * TK, &tmB1, fb & PEER_MASK, 0, r0, 3, tile);
+          } else {
+            tma_4d_pair(dA + A_BYTES, &tmB1, fb & PEER_MASK, 0, r0 + TR / 2, 3, tile);
+            tma_4d_pair(dA + A_BYTES + (TR / 2) * TK, &tmB3, fb & PEER_MASK, 0, r0, 4, tile);
+          }
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -427,6 +439,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       int rb, pp;
       tile_coords(t, a.num_rb, num_pp, rb, pp);
       const int nt = 2 * pp + (int)rank;
+      const int col_g = nt * TM + m, row0_g = rb * TR;
+      // this SNP's dosages on the tile's rows (the head term; rows >= n are zero), loaded before
+      // the accumulator wait so their latency hides behind it
+      int gq[TR / 4];
+      {
+        const signed char* gp = a.G + (long long)(col_g < a.N ? col_g : 0) * a.ldg + row0_g;
+        if (col_g < a.N && row0_g + TR <= a.n) {
+          const int4 w0 = *reinterpret_cast<const int4*>(gp);
+          const int4 w1 = *reinterpret_cast<const int4*>(gp + 16);
+          gq[0] = w0.x; gq[1] = w0.y; gq[2] = w0.z; gq[3] = w0.w;
+          gq[4] = w1.x; gq[5] = w1.y; gq[6] = w1.z; gq[7] = w1.w;
+        } else {
+#pragma unroll
+          for (int w = 0; w < TR / 4; ++w) {
+            int v = 0;
+            for (int b = 0; b < 4; ++b) {
+              const int rr = row0_g + 4 * w + b;
+              const int g = (col_g < a.N && rr < a.n) ? (int)gp[4 * w + b] : 0;
+              v |= (g & 0xff) << (8 * b);
+            }
+            gq[w] = v;
+          }
+        }
+      }
       const int ab = it & 1;
       mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
       fence_after();
@@ -434,25 +470,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       const unsigned char* rd = rdata + slot * RD_BYTES;
       const int* ex = reinterpret_cast<const int*>(rd);
       const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
-      // X = RN(T 2^(e_i - 56)), T = sum_s C_s 2^(7 (7 - s)): the two exact int64 halves
-      // hi = C_0..C_3, lo = C_4..C_7 (|hi|, |lo| < 2^53 since |C_s| < 2^31) are converted
-      // exactly and combined with ONE rounding (4 FP64 instructions per element: the FP64 pipe
-      // is throttled while the tensor core runs)
+      // X = RN(2^(e'_i - 49) T), T = h_i g_i 2^49 + sum_s C_s 2^(7 (6 - s)): the two exact int64
+      // halves hi = h g 2^21 + C_0 2^14 + C_1 2^7 + C_2 and lo = C_3 2^21 + ... + C_6 (both
+      // < 2^53) are converted exactly and combined with ONE rounding (4 FP64 instructions per
+      // element: the FP64 pipe is throttled while the tensor core runs)
       mbar_wait(rdf0 + 8 * slot, (it / RD_SLOTS) & 1);
+      const int* hd = reinterpret_cast<const int*>(rd + TR * 4);
       double acc[TR];
       const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
 #pragma unroll
       for (int q4 = 0; q4 < TR / 8; ++q4) {
-        int v[8][8];
+        int v[S][8];
         tmem_ld_rows8(taddr + q4 * 8, v);
 #pragma unroll
         for (int r8 = 0; r8 < 8; ++r8) {
-          const long long hi = (((long long)v[0][r8] * 128 + v[1][r8]) * 128 + v[2][r8]) * 128 +
-                               v[3][r8];
-          const long long lo = (((long long)v[4][r8] * 128 + v[5][r8]) * 128 + v[6][r8]) * 128 +
-                               v[7][r8];
-          const int e = ex[q4 * 8 + r8];
-          acc[q4 * 8 + r8] = fma((double)hi, pow2(e - 28), (double)lo * pow2(e - 56));
+          const int i = q4 * 8 + r8;
+          const int g = (int)(signed char)((gq[i >> 2] >> (8 * (i & 3))) & 0xff);
+          const long long hi = (long long)hd[i] * g * (1ll << 21) +
+                               (((long long)v[0][r8] * 128 + v[1][r8]) * 128 + v[2][r8]);
+          const long long lo = (((long long)v[3][r8] * 128 + v[4][r8]) * 128 + v[5][r8]) * 128 +
+                               v[6][r8];
+          const int e = ex[i];
+          acc[i] = fma((double)hi, pow2(e - 21), (double)lo * pow2(e - 49));
         }
       }
       fence_before();
@@ -500,12 +539,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---- inverse slicing ---------------------------------------------------------------------------
+// Row i of the inverse is split as
+//     Linv[i,k] = 2^e'_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  a_s in [-127, 127]
+// with e'_i = max(e_off_i, e_diag_i - HEAD_BITS) (|Linv[i,k]| < 2^e_off_i for k < i): the large
+// diagonal element gets an integer head h_i (|h_i| < 2^20, applied in the epilogue as h_i g_i),
+// everything else 7 slices = 49 bits below the row's largest off-diagonal entry (>= 53 bits below
+// the row maximum when the diagonal dominates it 16x, as in kinship covariances: ~30x).
 // Slices are stored tile-packed: the lower triangle of 128 x 128 tiles (row tile mt, k tile kt,
-// kt <= mt) at tile index mt (mt+1)/2 + kt, each tile [slice 8][row 128][k 128] int8 (128 KB), so
-// the slices take S/2 bytes per element of the triangle (4 np^2 + O(np) bytes) -- 90 GB at
-// n = 1.5e5, where a square layout would not fit a GPU.
+// kt <= mt) at tile index mt (mt+1)/2 + kt, each tile [slice 7][row 128][k 128] int8 (112 KB):
+// 3.5 np^2 + O(np) bytes (79 GB at n = 1.5e5, where a square layout would not fit a GPU).
+// Metadata ("expo" in the C-ABI): e'_i (np ints) then h_i (np ints).
 constexpr int ST = 128;                                  // slice tile edge
-constexpr long long ST_BYTES = (long long)S * ST * ST;   // 128 KB
+constexpr long long ST_BYTES = (long long)S * ST * ST;   // 112 KB
 
 __host__ __device__ inline long long slice_tiles(int np) {
   const long long nt = np / ST;
@@ -543,36 +588,59 @@ struct SrcBlockCyclic {
   }
 };
 
-// Row exponents: e_i with max_k |Linv[i,k]| < 2^e_i (INT_MIN when the row has no nonzero here:
-// the distributed form takes a MAX over ranks).  One CTA per row.
+__device__ __forceinline__ int exp_of(double mx) {   // |x| < 2^e, INT_MIN for 0
+  int e = INT_MIN;
+  if (mx > 0.0) frexp(mx, &e);
+  return e;
+}
+
+// Row exponents over what this source holds: out[i] = e_off_i (k < i), out[np + i] = e_diag_i
+// (INT_MIN where absent: the distributed form MAX-reduces them over ranks).  One CTA per row.
 template <class Src>
-__global__ void row_exponent_kernel(int np, Src src, int* __restrict__ expo) {
+__global__ void row_exponent_kernel(int np, Src src, int* __restrict__ out) {
   const int i = blockIdx.x;
   __shared__ double red[32];
   double mx = 0.0;
-  for (int k = threadIdx.x; k <= i && k < np; k += blockDim.x) mx = fmax(mx, fabs(src(i, k)));
+  for (int k = threadIdx.x; k < i && k < np; k += blockDim.x) mx = fmax(mx, fabs(src(i, k)));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x / 32); ++w) mx = fmax(mx, red[w]);
-    int e = INT_MIN;
-    if (mx > 0.0) frexp(mx, &e);   // mx = f 2^e, f in [0.5, 1)  ->  |row| < 2^e
-    expo[i] = e;
+    out[i] = exp_of(mx);
+    out[np + i] = exp_of(fabs(src(i, i)));
   }
 }
 
-// Slices of row i for k < (i/128 + 1) * 128 (zero above the diagonal) given e_i:
-// v = Linv[i,k] 2^-e_i (|v| < 1, exact), then a_s = trunc(128 v), v = 128 v - a_s (exact).
+// meta[i] = e'_i = max(e_off, e_diag - HEAD_BITS) from [e_off | e_diag]; meta[np + i] = 0 (the
+// heads are written by the slicing kernel).  In place is allowed.
+__global__ void slice_meta_kernel(int np, const int* ex2, int* meta) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const int eo = ex2[i], ed = ex2[np + i];
+    int e = ed == INT_MIN ? eo : (eo == INT_MIN ? ed - HEAD_BITS : max(eo, ed - HEAD_BITS));
+    if (e == INT_MIN) e = 0;   // all-zero row (not an inverse row; keeps the arithmetic finite)
+    meta[i] = e;
+    meta[np + i] = 0;
+  }
+}
+
+// Slices of row i for k < (i/128 + 1) * 128 (zero above the diagonal) given e'_i; the diagonal
+// splits into the head h_i (written to meta[np + i] by the thread that sees a nonzero Linv_ii)
+// and its fractional part, sliced like the other entries.  v in (-1, 1); every step is exact.
 template <class Src>
-__global__ void slice_rows_kernel(int np, Src src, const int* __restrict__ expo,
+__global__ void slice_rows_kernel(int np, Src src, int* __restrict__ meta,
                                   signed char* __restrict__ Sl) {
   const int i = blockIdx.x;
-  const int e = expo[i];
+  const int e = meta[i];
   const int kend = (i / ST + 1) * ST;
   for (int k = threadIdx.x; k < kend; k += blockDim.x) {
     double v = (k <= i) ? src(i, k) : 0.0;
     v = (v != 0.0) ? ldexp(v, -e) : 0.0;
+    if (k == i) {
+      const double h = trunc(v);
+      if (v != 0.0) meta[np + i] = (int)h;
+      v -= h;
+    }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double t = v * 128.0;                     // exact
@@ -716,54 +784,62 @@ int sms() {
 int i8_slices() { return S; }
 
 size_t inverse_slices_bytes(int n) { return (size_t)slice_tiles(pad_rows(n)) * ST_BYTES; }
+size_t slice_meta_ints(int n) { return 2 * (size_t)pad_rows(n); }
 
-int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* expo,
-                      cudaStream_t s) {
+template <class Src>
+static int slice_from(int n, Src src, signed char* Sl, int* meta, cudaStream_t s) {
   const int np = pad_rows(n);
-  if (ldp < np) {
+  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, meta);   // [e_off | e_diag] in place
+  GG_LAUNCH_CHECK("row_exponent_kernel");
+  slice_meta_kernel<<<(np + 255) / 256, 256, 0, s>>>(np, meta, meta);
+  GG_LAUNCH_CHECK("slice_meta_kernel");
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, meta, Sl);
+  GG_LAUNCH_CHECK("slice_rows_kernel");
+  return GG_OK;
+}
+
+int slice_inverse_run(int n, const double* LinvT, int ldp, signed char* Sl, int* meta,
+                      cudaStream_t s) {
+  if (ldp < pad_rows(n)) {
     set_error("slice_inverse: ld must be >= gg_pad(n)");
     return GG_EDIM;
   }
-  SrcRowMajor src{LinvT, ldp};
-  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
-  GG_LAUNCH_CHECK("row_exponent_kernel");
-  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
-  GG_LAUNCH_CHECK("slice_rows_kernel");
-  return GG_OK;
+  return slice_from(n, SrcRowMajor{LinvT, ldp}, Sl, meta, s);
 }
 
-int slice_packed_run(int n, const double* LinvP, signed char* Sl, int* expo, cudaStream_t s) {
-  const int np = pad_rows(n);
-  SrcPacked src{LinvP};
-  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
-  GG_LAUNCH_CHECK("row_exponent_kernel");
-  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
-  GG_LAUNCH_CHECK("slice_rows_kernel");
-  return GG_OK;
+int slice_packed_run(int n, const double* LinvP, signed char* Sl, int* meta, cudaStream_t s) {
+  return slice_from(n, SrcPacked{LinvP}, Sl, meta, s);
 }
 
 int row_exponents_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
-                         int* expo, cudaStream_t s) {
+                         int* ex2, cudaStream_t s) {
   if (nb < 1 || gr < 1 || gc < 1 || pr < 0 || pr >= gr || pc < 0 || pc >= gc) {
     set_error("row_exponents_blockcyclic: bad grid");
     return GG_EARG;
   }
   const int np = pad_rows(n);
   SrcBlockCyclic src{B, ldl, nb, gr, gc, pr, pc};
-  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, expo);
+  row_exponent_kernel<<<np, 256, 0, s>>>(np, src, ex2);
   GG_LAUNCH_CHECK("row_exponent_kernel");
   return GG_OK;
 }
 
+int slice_meta_run(int n, const int* ex2, int* meta, cudaStream_t s) {
+  const int np = pad_rows(n);
+  slice_meta_kernel<<<(np + 255) / 256, 256, 0, s>>>(np, ex2, meta);
+  GG_LAUNCH_CHECK("slice_meta_kernel");
+  return GG_OK;
+}
+
 int slice_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
-                 const int* expo, signed char* Sl, cudaStream_t s) {
+                 int* meta, signed char* Sl, cudaStream_t s) {
   if (nb < 1 || gr < 1 || gc < 1 || pr < 0 || pr >= gr || pc < 0 || pc >= gc) {
     set_error("slice_blockcyclic: bad grid");
     return GG_EARG;
   }
   const int np = pad_rows(n);
   SrcBlockCyclic src{B, ldl, nb, gr, gc, pr, pc};
-  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, expo, Sl);
+  slice_rows_kernel<<<np, 256, 0, s>>>(np, src, meta, Sl);
   GG_LAUNCH_CHECK("slice_rows_kernel");
   return GG_OK;
 }
@@ -827,12 +903,16 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     int rc = encode(&mA, 2, G, dims, strides, box);
     if (rc != GG_OK) return rc;
   }
-  {   // tile-packed slices; each CTA of a pair loads 4 of the 8 slices of 32 rows x 128 k
+  CUtensorMap mB1;
+  {   // tile-packed slices [tile][slice][row][k]: boxes of 3 slices x 32 rows and 1 slice x 16
     cuuint64_t dims[4] = {(cuuint64_t)ST, (cuuint64_t)ST, (cuuint64_t)S,
                           (cuuint64_t)slice_tiles(np)};
     cuuint64_t strides[3] = {(cuuint64_t)ST, (cuuint64_t)ST * ST, (cuuint64_t)ST_BYTES};
-    cuuint32_t box[4] = {TK, TR, P_SLICES, 1};
-    int rc = encode(&mB, 4, Sl, dims, strides, box);
+    cuuint32_t box3[4] = {TK, TR, 3, 1};
+    int rc = encode(&mB, 4, Sl, dims, strides, box3);
+    if (rc != GG_OK) return rc;
+    cuuint32_t box1[4] = {TK, TR / 2, 1, 1};
+    rc = encode(&mB1, 4, Sl, dims, strides, box1);
     if (rc != GG_OK) return rc;
   }
   I8Args a;
@@ -842,6 +922,9 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.X = X;
   a.ldx = ldx;
   a.expo = expo;
+  a.G = G;
+  a.ldg = ldg;
+  a.n = n;
   a.q = q;
   a.XL = XL;
   a.ldxl = ldxl;
@@ -870,7 +953,7 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB, a));
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB, mB1, a));
     return GG_OK;
   }
 }

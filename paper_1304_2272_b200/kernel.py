@@ -211,14 +211,16 @@ def _pack_lower(Linv_colmajor, n):
 
 
 def _slice_inverse(Linv_colmajor, n):
-    """int8 slices + exponents of the inverse (operands of the tensor-core TRSM)."""
+    """int8 slices + metadata (row exponents, diagonal heads) of the inverse: the operands of the
+    tensor-core TRSM."""
     torch = __import__("torch")
     from ._device import transpose_square
 
     LinvT = transpose_square(Linv_colmajor)
     sl = torch.empty(int(_capi.lib().gg_inverse_slices_bytes(n)), dtype=torch.int8,
                      device=LinvT.device)
-    expo = torch.empty(LinvT.shape[0], dtype=torch.int32, device=LinvT.device)
+    expo = torch.empty(int(_capi.lib().gg_slice_meta_ints(n)), dtype=torch.int32,
+                       device=LinvT.device)
     check(_capi.lib().gg_slice_inverse_i8(n, ptr(LinvT), LinvT.shape[1], ptr(sl), ptr(expo),
                                           stream_handle()), "gg_slice_inverse_i8")
     del LinvT
@@ -226,18 +228,19 @@ def _slice_inverse(Linv_colmajor, n):
 
 
 def _slices_fit(n):
-    """Room for the int8 slices (4 np^2 bytes) next to what is already resident."""
+    """Room for the int8 slices (3.5 np^2 bytes) next to what is already resident."""
     torch = __import__("torch")
     free, _ = torch.cuda.mem_get_info(_capi.device())
     return int(_capi.lib().gg_inverse_slices_bytes(n)) < 0.8 * free
 
 
 def _slice_packed(LinvP, n):
-    """int8 slices + exponents from the packed FP64 inverse."""
+    """int8 slices + metadata from the packed FP64 inverse."""
     torch = __import__("torch")
     sl = torch.empty(int(_capi.lib().gg_inverse_slices_bytes(n)), dtype=torch.int8,
                      device=LinvP.device)
-    expo = torch.empty(pad(n), dtype=torch.int32, device=LinvP.device)
+    expo = torch.empty(int(_capi.lib().gg_slice_meta_ints(n)), dtype=torch.int32,
+                       device=LinvP.device)
     check(_capi.lib().gg_slice_packed_inverse_i8(n, ptr(LinvP), ptr(sl), ptr(expo),
                                                  stream_handle()), "gg_slice_packed_inverse_i8")
     return sl, expo

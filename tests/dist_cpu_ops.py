@@ -11,37 +11,63 @@ from scipy.linalg.lapack import dpotrf
 INT_MIN = -2 ** 31
 
 
+S = 7              # int8 slices (trsm_i8.cu)
+HEAD_BITS = 20     # diagonal head width (trsm_i8.cu)
+TILE = S * 128 * 128
+
+
 def slice_offsets(i, k, np_):
     """Byte offsets of element (i, k) in the tile-packed slice layout, one per slice."""
     mt, kt = i // 128, k // 128
-    base = (mt * (mt + 1) // 2 + kt) * 131072 + (i % 128) * 128 + (k % 128)
-    return base[..., None] + 16384 * np.arange(8)
+    base = (mt * (mt + 1) // 2 + kt) * TILE + (i % 128) * 128 + (k % 128)
+    return base[..., None] + 16384 * np.arange(S)
 
 
-def slices_dense(Linv_rows, expo, np_):
-    """Tile-packed int8 slices of a dense lower-triangular inverse given row exponents (the
-    restatement of slice_rows_kernel, used as the CPU ops' implementation and the check)."""
+def _exp_of(x):
+    e = np.full(x.shape, INT_MIN, dtype=np.int64)
+    nz = x > 0
+    e[nz] = np.frexp(x[nz])[1]
+    return e
+
+
+def row_exponents_dense(full_tril):
+    """[e_off | e_diag] of a dense lower-triangular (np x np) matrix (row_exponent_kernel)."""
+    off = np.abs(np.tril(full_tril, -1)).max(axis=1)
+    return np.concatenate([_exp_of(off), _exp_of(np.abs(np.diag(full_tril)))]).astype(np.int32)
+
+
+def slice_meta_dense(ex2):
+    """Row exponents e' = max(e_off, e_diag - HEAD_BITS), heads zeroed (slice_meta_kernel)."""
+    np_ = len(ex2) // 2
+    eo, ed = ex2[:np_].astype(np.int64), ex2[np_:].astype(np.int64)
+    e = np.where(ed == INT_MIN, eo,
+                 np.where(eo == INT_MIN, ed - HEAD_BITS, np.maximum(eo, ed - HEAD_BITS)))
+    e = np.where(e == INT_MIN, 0, e)
+    return np.concatenate([e, np.zeros(np_, dtype=np.int64)]).astype(np.int32)
+
+
+def slices_dense(Linv_rows, meta, np_):
+    """Tile-packed int8 slices of a dense lower-triangular inverse given the metadata (the
+    restatement of slice_rows_kernel, used as the CPU ops' implementation and the check); the
+    heads of rows with a nonzero diagonal are written into meta[np_:] in place."""
     nt = np_ // 128
-    out = np.zeros(nt * (nt + 1) // 2 * 131072, dtype=np.int8)
+    out = np.zeros(nt * (nt + 1) // 2 * TILE, dtype=np.int8)
     for i in range(np_):
         kend = (i // 128 + 1) * 128
         k = np.arange(kend)
         v = np.where(k <= i, Linv_rows(i, kend), 0.0)
-        v = np.where(v != 0.0, np.ldexp(v, -int(expo[i])), 0.0)
-        q = np.empty((kend, 8))
-        for s in range(8):
+        v = np.where(v != 0.0, np.ldexp(v, -int(meta[i])), 0.0)
+        if v[i] != 0.0:
+            h = np.trunc(v[i])
+            meta[np_ + i] = int(h)
+            v[i] -= h
+        q = np.empty((kend, S))
+        for s in range(S):
             t = v * 128.0
             q[:, s] = np.trunc(t)
             v = t - q[:, s]
         out[slice_offsets(i, k, np_)] = q.astype(np.int8)
     return out
-
-
-def row_exponents_dense(rows_abs_max):
-    e = np.full(rows_abs_max.shape, INT_MIN, dtype=np.int32)
-    nz = rows_abs_max > 0
-    e[nz] = np.frexp(rows_abs_max[nz])[1]
-    return e
 
 
 def pack_lower_dense(Dense, n):
@@ -127,13 +153,24 @@ class CpuOps:
             full[np.ix_(rows, cols)] = self.to_host(B)
         return full
 
-    def row_exponents(self, B, layout):
-        full = np.tril(self._full_share(B, layout))
-        return torch.from_numpy(row_exponents_dense(np.abs(full).max(axis=1)))
+    def _tril_share(self, B, layout):
+        np_ = -(-layout.n // 128) * 128
+        full = self._full_share(B, layout)
+        out = np.zeros((np_, np_))
+        m = min(np_, full.shape[0])
+        out[:m, :m] = full[:m, :m]
+        return np.tril(out), np_
 
-    def slice_blockcyclic(self, B, layout, expo):
-        full = np.tril(self._full_share(B, layout))
-        S = slices_dense(lambda i, kend: full[i, :kend], expo.numpy(), layout.n_pad)
+    def row_exponents(self, B, layout):
+        full, _ = self._tril_share(B, layout)
+        return torch.from_numpy(row_exponents_dense(full))
+
+    def slice_meta(self, ex2, layout):
+        return torch.from_numpy(slice_meta_dense(ex2.numpy()))
+
+    def slice_blockcyclic(self, B, layout, meta):
+        full, np_ = self._tril_share(B, layout)
+        S = slices_dense(lambda i, kend: full[i, :kend], meta.numpy(), np_)
         return torch.from_numpy(S)
 
     def pack_blockcyclic(self, B, layout):

@@ -52,6 +52,10 @@ def test_host_only_entry_points():
     # exact-int32 bound of the int8 path: 127 up to n = 133,144, then shrinking
     assert lib.gg_i8_value_bound(10000) == 127 and lib.gg_i8_value_bound(133144) == 127 and lib.gg_i8_value_bound(133145) == 126
     assert lib.gg_i8_value_bound(150000) == 2147483647 // (127 * 150000) == 112
+    # 7 tile-packed slices (112 KB per 128 x 128 tile of the triangle) + 2 np metadata ints
+    assert lib.gg_i8_slices() == 7
+    assert lib.gg_inverse_slices_bytes(1000) == 36 * 7 * 128 * 128
+    assert lib.gg_slice_meta_ints(1000) == 2 * 1024
     # argument validation happens before any device work
     rc = lib.gg_trsm_lower_f64(0, 1, None, 128, None, 128, None, 128, None)
     assert rc == _capi.GG_EARG
@@ -109,6 +113,7 @@ def test_argument_validation_without_a_gpu():
         (lib.gg_slice_packed_inverse_i8, (0, V, V, V, V), EARG),
         (lib.gg_row_exponents_blockcyclic, (10, 128, 1, 1, 0, 0, V, 128, V, V), EARG),
         (lib.gg_slice_blockcyclic_i8, (10, 128, 1, 1, 0, 0, V, 128, V, V, V), EARG),
+        (lib.gg_slice_meta_i8, (10, V, V, V), EARG),
         (lib.gg_narrow_f64_i8, (0, 1, V, 1, V, 1, V, V), EARG),
         (lib.gg_small_spd_solve_f64, (1, 0, V, V, V, V, V, V), EARG),
         (lib.gg_gls_dots_f64, (10, 1, 25, V, 128, V, 128, V, V, V, V), EARG),

@@ -112,7 +112,7 @@ def test_dist_cholesky_inverse_and_packed_assembly(world):
     Lr = cholesky(M, lower=True)
     Lir = solve_triangular(Lr, np.eye(n), lower=True)
     Pr = pack_lower_dense(Lir, n)
-    from dist_cpu_ops import row_exponents_dense, slices_dense
+    from dist_cpu_ops import row_exponents_dense, slice_meta_dense, slices_dense
 
     np_ = -(-n // 128) * 128
     for rank, kind, (L, Li, P, S, e, W, RHS) in out:
@@ -122,13 +122,14 @@ def test_dist_cholesky_inverse_and_packed_assembly(world):
         assert np.max(np.abs(Li - Lir)) <= 1e-12 * np.max(np.abs(Lir))
         assert np.max(np.abs(P - Pr)) <= 1e-12 * np.max(np.abs(Pr))
         assert np.array_equal(P, out[0][2][2])          # identical replica on every rank
-        # int8 slices: MAX-reduced exponents and SUM-reduced per-rank slices equal the slices
-        # of the gathered inverse (what one GPU would cut), identical on every rank
+        # int8 slices: MAX-reduced exponents, SUM-reduced per-rank slices and heads equal what
+        # one GPU would cut from the gathered inverse, identical on every rank
         Lg = np.eye(np_)
         Lg[:n, :n] = np.tril(Li)
-        ex = row_exponents_dense(np.abs(Lg).max(axis=1))
-        assert np.array_equal(e, ex)
-        assert np.array_equal(S, slices_dense(lambda i, kend: Lg[i, :kend], ex, np_))
+        meta = slice_meta_dense(row_exponents_dense(Lg))
+        Sx = slices_dense(lambda i, kend: Lg[i, :kend], meta, np_)
+        assert np.array_equal(e, meta)
+        assert np.array_equal(S, Sx)
         assert np.array_equal(S, out[0][2][3])
         # whitening from the block-cyclic inverse
         Wr = Lir @ RHS

@@ -160,16 +160,22 @@ def test_slices_from_packed_and_block_cyclic_sources(K, n):
             exps.append(e)
             slcs.append((B, rows))
     emax = torch.stack(exps).max(dim=0).values
+    meta = torch.empty_like(ex)
+    assert lib.gg_slice_meta_i8(n, ptr(emax), ptr(meta), s) == 0
     torch.cuda.synchronize()
-    assert torch.equal(emax, ex_ref)
+    assert torch.equal(meta[:np_], ex_ref[:np_]) and not meta[np_:].any()
     total = torch.zeros(sl_ref.numel(), dtype=torch.int32, device="cuda")
+    heads = torch.zeros(np_, dtype=torch.int32, device="cuda")
     for (B, rows), (pr, pc) in zip(slcs, [(0, 0), (0, 1), (1, 0), (1, 1)]):
         part = torch.full_like(sl_ref, 7)
+        m = meta.clone()
         assert lib.gg_slice_blockcyclic_i8(n, nb, gr, gc, pr, pc, ptr(B), len(rows) * nb,
-                                           ptr(emax), ptr(part), s) == 0
+                                           ptr(m), ptr(part), s) == 0
         total += part.to(torch.int32)
+        heads += m[np_:]
     torch.cuda.synchronize()
     assert torch.equal(total.to(torch.int8), sl_ref) and int(total.abs().max()) <= 127
+    assert torch.equal(heads, ex_ref[np_:])
 
 
 def test_dynamic_scheduler_stress_deterministic(K):

@@ -1,4 +1,6 @@
-"""A/B timing of the fused int8 TRSM across library builds on one box (config-1 block).
+"""A/B timing of the fused int8 TRSM across library builds on one box (config-1 block).  Each
+library cuts its own slices from the packed FP64 inverse (so slice layouts may differ); the
+libraries are timed round-robin to cancel clock / power drift.
     python tools/ab_i8.py tools/alt/lib_a.so [...]   (the in-tree library is always included)"""
 import ctypes as C
 import os
@@ -20,20 +22,40 @@ G16 = datagen.genotypes_device(spec, 0, cnt, ld=n16)
 P = torch.empty(int(_capi.lib().gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64,
                 device="cuda")
 s = _capi.stream_handle()
+libs = []
 for path in [_capi.LIB_PATH] + sys.argv[1:]:
     lib = C.CDLL(path)
     f = lib.gg_trsm_lower_i8_partials
     f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int,
                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                   C.c_void_p]
-    ts = []
-    for rep in range(6):
+    lib.gg_inverse_slices_bytes.restype = C.c_size_t
+    lib.gg_inverse_slices_bytes.argtypes = [C.c_int]
+    lib.gg_slice_packed_inverse_i8.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_void_p]
+    sl = torch.empty(int(lib.gg_inverse_slices_bytes(n)), dtype=torch.int8, device="cuda")
+    meta = torch.zeros(2 * _capi.pad(n), dtype=torch.int32, device="cuda")
+    assert lib.gg_slice_packed_inverse_i8(n, ptr(d.LinvP), ptr(sl), ptr(meta), s) == 0
+    libs.append((os.path.basename(path), f, sl, meta, []))
+torch.cuda.synchronize()
+d.slices = None
+Pref = None
+for rep in range(8):
+    for name, f, sl, meta, ts in libs:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        rc = f(n, cnt, ptr(d.slices), ptr(d.expo), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
+        rc = f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
                ptr(P), None, 0, None, 0, s)
         b.record()
         torch.cuda.synchronize()
         assert rc == 0, rc
         ts.append(a.elapsed_time(b))
-    print(f"{os.path.basename(path)}: {min(ts[1:]):.3f} ms (median {sorted(ts[1:])[2]:.3f})")
+        if rep == 0:
+            if Pref is None:
+                Pref = P.clone()
+            else:   # partial dots of the candidates vs the in-tree library's
+                rel = float(((P - Pref).abs().max() / Pref.abs().max()))
+                print(f"{name}: max rel diff of partials vs in-tree {rel:.2e}")
+for name, f, sl, meta, ts in libs:
+    t = sorted(ts[1:])
+    print(f"{name}: {t[0]:.3f} ms (median {t[len(t) // 2]:.3f})")
