@@ -219,6 +219,7 @@ def run_ours(args):
     ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in plan]
     launches_per_block = 0
+    serial_narrow = os.environ.get("GG_BENCH_SERIAL_NARROW") == "1"
 
     def step(record):
         nonlocal launches_per_block
@@ -228,13 +229,18 @@ def run_ours(args):
             if use_i8:
                 if X is not None:            # FP64 dosages -> int8 (exactness flag checked after)
                     slot = i % 2
-                    with torch.cuda.stream(side):
-                        if trsm_started[slot]:          # buffer free once its last TRSM is done
-                            side.wait_event(trsm_done[slot])
+                    if serial_narrow:
                         rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8s[slot]), n16,
-                                                   ptr(bad), _capi.C.c_void_p(side.cuda_stream))
-                        narrow_done[slot].record(side)
-                    stream.wait_event(narrow_done[slot])
+                                                   ptr(bad), sh)
+                    else:
+                        with torch.cuda.stream(side):
+                            if trsm_started[slot]:      # buffer free once its last TRSM is done
+                                side.wait_event(trsm_done[slot])
+                            rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8s[slot]),
+                                                       n16, ptr(bad),
+                                                       _capi.C.c_void_p(side.cuda_stream))
+                            narrow_done[slot].record(side)
+                        stream.wait_event(narrow_done[slot])
                     G, ldg, nl = g8s[slot], n16, nl + 1
                 else:
                     G, ldg = Gres[f:], n16

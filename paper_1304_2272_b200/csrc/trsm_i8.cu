@@ -651,55 +651,64 @@ __global__ void slice_rows_kernel(int np, Src src, int* __restrict__ meta,
   }
 }
 
-// FP64 dosages -> int8 (exactness check: integers in [-127, 127]); rows n .. ldg-1 of each column
-// are written as zero when ldg is a multiple of 16.  One thread converts 16 consecutive rows of a
-// column: 8 x 16-byte loads, one 16-byte store (HBM-bound: 8 B read + 1 B written per dosage).
+// FP64 dosages -> int8 (exactness check: integers with |v| <= gmax); rows n .. min(ldg, n16)-1
+// of each column (n16 = n rounded up to 16) are written as zero.  One warp converts a 512-row
+// segment of a column: lane l takes rows 2 (32 h + l) + {0, 1}, h = 0..7, so every load
+// instruction reads 512 contiguous bytes (8 in flight per thread, streaming: the dosages are read
+// once and must not evict the TRSM's operands from L2) and every store writes 64 contiguous
+// bytes.  HBM-bound: 8 B read + 1 B written per dosage.
 __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long long ldx,
                               signed char* __restrict__ G, long long ldg, double gmax,
                               int* __restrict__ bad) {
-  const int chunks = (n + 15) / 16;                  // 16-row chunks per column
-  const long long total = (long long)chunks * cnt;
-  const bool vec = ((ldx & 1) == 0) && ((ldg & 15) == 0);
+  const long long nw_rows = (long long)((n + 15) & ~15) < ldg ? (long long)((n + 15) & ~15) : ldg;
+  const int rows = (int)nw_rows;
+  const int segs = (rows + 511) / 512;
+  const long long total = (long long)segs * cnt;
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const bool vec = ((ldx & 1) == 0) && ((ldg & 1) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(G) & 1) == 0);
   int local_bad = 0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long j = e / chunks;
-    const int c = (int)(e - j * chunks);
-    const int r0 = 16 * c;
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; e < total;
+       e += nwarps) {
+    const long long j = e / segs;
+    const int r0 = (int)(e - j * segs) * 512;
     const double* col = X + j * ldx + r0;
-    unsigned w[4] = {0u, 0u, 0u, 0u};
-    if (vec && r0 + 16 <= n) {
+    signed char* dst = G + j * ldg + r0;
+    if (vec && r0 + 512 <= n) {
+      double2 v[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        v[h] = __ldcs(reinterpret_cast<const double2*>(col) + 32 * h + lane);
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
-        const double2 v2 = *reinterpret_cast<const double2*>(col + 2 * h);
-        const double vv[2] = {v2.x, v2.y};
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const double v = vv[u];
-          const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
-          local_bad |= ok ? 0 : 1;
-          const int f = 2 * h + u;
-          w[f >> 2] |= (unsigned)((ok ? (int)v : 0) & 0xff) << (8 * (f & 3));
-        }
+        const bool ok0 = (v[h].x == trunc(v[h].x)) && fabs(v[h].x) <= gmax;
+        const bool ok1 = (v[h].y == trunc(v[h].y)) && fabs(v[h].y) <= gmax;
+        local_bad |= (ok0 && ok1) ? 0 : 1;
+        const unsigned w = ((unsigned)(ok0 ? (int)v[h].x : 0) & 0xffu) |
+                           (((unsigned)(ok1 ? (int)v[h].y : 0) & 0xffu) << 8);
+        *reinterpret_cast<unsigned short*>(dst + 2 * (32 * h + lane)) = (unsigned short)w;
       }
     } else {
 #pragma unroll 1
-      for (int f = 0; f < 16 && r0 + f < n; ++f) {
-        const double v = col[f];
-        const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
-        local_bad |= ok ? 0 : 1;
-        w[f >> 2] |= (unsigned)((ok ? (int)v : 0) & 0xff) << (8 * (f & 3));
+      for (int h = 0; h < 8; ++h) {
+        for (int u = 0; u < 2; ++u) {
+          const int r = 2 * (32 * h + lane) + u;
+          if (r0 + r >= rows) continue;
+          int g = 0;
+          if (r0 + r < n) {
+            const double v = col[r];
+            const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
+            local_bad |= ok ? 0 : 1;
+            g = ok ? (int)v : 0;
+          }
+          dst[r] = (signed char)g;
+        }
       }
     }
-    signed char* dst = G + j * ldg + r0;
-    if (vec && r0 + 16 <= ldg) {
-      *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-    } else {
-      for (int f = 0; f < 16 && r0 + f < n; ++f)
-        dst[f] = (signed char)((w[f >> 2] >> (8 * (f & 3))) & 0xff);
-    }
   }
-  if (__any_sync(0xffffffffu, local_bad != 0) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+  if (__any_sync(0xffffffffu, local_bad != 0) && lane == 0) atomicOr(bad, 1);
 }
 
 // int8 dosages: *bad |= 1 if any |g| exceeds gmax (the exact-int32 bound for this n).
@@ -867,7 +876,7 @@ int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, l
     return GG_EDIM;
   }
   if (cnt <= 0) return GG_OK;
-  long long grid = ((long long)((n + 15) / 16) * cnt + 255) / 256;
+  long long grid = ((long long)((n + 511) / 512) * cnt + 7) / 8;   // 8 warps per block
   if (grid > 148LL * 16) grid = 148LL * 16;
   narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, (double)i8_value_bound(n), bad);
   GG_LAUNCH_CHECK("narrow_kernel");
