@@ -118,9 +118,10 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
  * error-free into gg_i8_slices() (= 7) int8 slices per row plus an integer diagonal head:
  *     Linv[i,k] = 2^e_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  |a_s| <= 127
  * with e_i = max(e_off_i, e_diag_i - 20) (|Linv[i,k]| < 2^e_off_i over k < i, |Linv_ii| <
- * 2^e_diag_i), |h_i| < 2^20: the truncation residual is < 2^(e_i - 49), i.e. 49 bits below the
- * row's largest off-diagonal entry and >= 53 bits below its largest entry whenever the diagonal
- * is >= 16x the off-diagonal maximum (kinship-type covariances).  Each slice product is an exact
+ * 2^e_diag_i), |h_i| < 2^20; slices 0-5 truncate, the last rounds to nearest (clipped to
+ * +-127): the residual is zero-mean and <= 2^(e_i - 50), i.e. 50 bits below the row's largest
+ * off-diagonal entry and >= 54 bits below its largest entry whenever the diagonal is >= 16x the
+ * off-diagonal maximum (kinship-type covariances).  Each slice product is an exact
  * int32 integer; the head term h_i g_i and the seven products are combined exactly into two
  * int64 halves and rounded once to double (correctly rounded; per-column results independent of
  * the column's position).

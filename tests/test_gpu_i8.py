@@ -48,6 +48,29 @@ def test_i8_trsm_matches_dmma(K, n, cnt):
     assert np.array_equal(Xp, Xi.cpu().numpy()[perm])
 
 
+def test_i8_trsm_accuracy_vs_extended_precision(K):
+    """Accuracy of the sliced inverse on a kinship covariance (the BASELINE workload's M): the
+    int8 path's Xbar = Linv G against Linv G in extended precision for the same FP64 inverse.
+    7 slices + head with a round-to-nearest last slice: ~2e-15 of the column maximum (the FP64
+    DMMA TRSM's own rounding is ~1e-15); all-truncated slices were 5e-15, 6 slices 3e-13."""
+    import torch
+
+    from paper_1304_2272_b200 import datagen
+
+    n, cnt = 1500, 48
+    spec = datagen.BaselineSpec(n=n, m=cnt, p=4)
+    M = datagen.kinship_covariance_host(spec)
+    _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+    sl, expo = K._slice_inverse(Linv, n)
+    G = np.random.default_rng(5).integers(0, 3, (n, cnt))
+    Xi = K._trsm_i8_device(sl, expo, n, G)[:, :n].cpu().numpy().T      # (n, cnt)
+    Li = Linv[:n, :n].cpu().numpy().T                                   # row-major Linv
+    ref = (Li.astype(np.longdouble) @ G.astype(np.longdouble)).astype(np.float64)
+    err = np.max(np.abs(Xi - ref) / np.max(np.abs(ref), axis=0))
+    assert err <= 4e-15, err
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("case", ["seed42", "baseline_p4", "baseline_p8", "degenerate"])
 def test_i8_and_dmma_paths_agree_with_reference(K, case):
     from oracle import gls_ref as O
