@@ -59,3 +59,18 @@ for rep in range(8):
 for name, f, sl, meta, ts in libs:
     t = sorted(ts[1:])
     print(f"{name}: {t[0]:.3f} ms (median {t[len(t) // 2]:.3f})")
+# sustained: GG_AB_SUSTAIN seconds of back-to-back launches per library (power-capped clocks),
+# timing the second half
+sustain = float(os.environ.get("GG_AB_SUSTAIN", "0"))
+for rnd in range(2 if sustain > 0 else 0):
+    for name, f, sl, meta, ts in libs:
+        reps = max(int(sustain / 2.0e-3), 10)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for r in range(reps):
+            if r == reps // 2:
+                a.record()
+            f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar), ptr(P),
+              None, 0, None, 0, s)
+        b.record()
+        torch.cuda.synchronize()
+        print(f"sustained round {rnd} {name}: {a.elapsed_time(b) / (reps - reps // 2):.3f} ms")
