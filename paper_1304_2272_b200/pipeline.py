@@ -17,6 +17,7 @@ depend on the block size, so incore, ooc at any m_blk, and the sharded engine ag
 
 from __future__ import annotations
 
+import collections
 import os
 import time
 from dataclasses import dataclass, field, fields
@@ -159,11 +160,17 @@ class StreamEngine:
     """Two-region host->device genotype stream with asynchronous result return.
 
     ``submit(slot, host_block, first, cnt)`` enqueues H2D (copy stream) -> TRSM + epilogue
-    (compute stream) -> D2H of the results into the slot's pinned buffers; ``collect(slot)``
-    waits for that slot and returns its ResultArrays.  host_block is an n x >= cnt Fortran-
-    ordered (ideally pinned) array of float64 or int8."""
+    (compute stream) -> D2H of the results into pinned buffers and returns a ticket;
+    ``collect(ticket)`` waits for that block and returns its ResultArrays.  ``slot`` names the
+    caller's host input region (REGIONS = 2, the reference's double buffer): ``wait_h2d(slot)``
+    returns once the region's last H2D is done, so it may be refilled.  On the device the
+    blocks rotate through DEV_REGIONS input/workspace/result regions, so the H2D of block i+1
+    is ordered only after the compute of block i+1-DEV_REGIONS -- the copy engine runs back to
+    back instead of waiting for the host to collect block i-1.  host_block is an n x >= cnt
+    Fortran-ordered (ideally pinned) array of float64 or int8."""
 
     REGIONS = 2
+    DEV_REGIONS = 3
 
     def __init__(self, ctx, m_blk, int8=False, emit_s_inv=False):
         import torch
@@ -179,79 +186,130 @@ class StreamEngine:
         # int8 dosage rows pitched to 16 bytes (TMA operand of the tensor-core TRSM)
         self.ld_in = (-(-d.n // 16) * 16) if self.int8 else d.np_
         dt = torch.int8 if self.int8 else torch.float64
-        self.ws = [BlockWorkspace(d, self.m_blk, emit_s_inv, self.int8) for _ in range(self.REGIONS)]
-        self.dev_in = [alloc_cols(self.m_blk, self.ld_in, dtype=dt) for _ in range(self.REGIONS)]
+        R = self.DEV_REGIONS
+        self.ws = [BlockWorkspace(d, self.m_blk, emit_s_inv, self.int8) for _ in range(R)]
+        self.dev_in = [alloc_cols(self.m_blk, self.ld_in, dtype=dt) for _ in range(R)]
         p = d.p
         self.h_beta = [torch.empty((self.m_blk, p), dtype=torch.float64).pin_memory()
-                       for _ in range(self.REGIONS)]
+                       for _ in range(R)]
         self.h_status = [torch.empty((self.m_blk,), dtype=torch.int32).pin_memory()
-                         for _ in range(self.REGIONS)]
+                         for _ in range(R)]
         self.h_sinv = [torch.empty((self.m_blk, p * (p + 1) // 2), dtype=torch.float64)
-                       .pin_memory() if emit_s_inv else None for _ in range(self.REGIONS)]
+                       .pin_memory() if emit_s_inv else None for _ in range(R)]
         self.copy_stream = torch.cuda.Stream()
         self.compute_stream = torch.cuda.Stream()
-        self.h2d_done = [torch.cuda.Event() for _ in range(self.REGIONS)]
-        self.done = [torch.cuda.Event(enable_timing=True) for _ in range(self.REGIONS)]
-        self.start_ev = [torch.cuda.Event(enable_timing=True) for _ in range(self.REGIONS)]
-        self.meta = [None] * self.REGIONS
-        self.busy = [False] * self.REGIONS
+        self.h2d_start = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
+        self.h2d_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
+        self.done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
+        self.start_ev = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
+        self.meta = [None] * R
+        self.busy = [False] * R
+        self.host_ev = {}                  # host region -> event after its last H2D
+        self._h2d_open = [False] * R
+        self._next = 0
         self.device_ms = 0.0
+        self.h2d_ms = 0.0
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
     def wait_h2d(self, slot):
-        """Host rendezvous: the slot's host input region may be refilled after this."""
-        self.h2d_done[slot].synchronize()
+        """Host rendezvous: the host input region ``slot`` may be refilled after this."""
+        ev = self.host_ev.get(slot)
+        if ev is not None:
+            ev.synchronize()
 
-    def submit(self, slot, host_block, first, cnt, global_indices=None):
+    def begin(self, first, cnt, global_indices=None):
+        """Open the next device region for a block of ``cnt`` markers; returns its ticket."""
+        r = self._next % self.DEV_REGIONS
+        if self.busy[r]:
+            raise ConfigError(f"device region {r} still in flight (collect it first)")
+        if not 0 < cnt <= self.m_blk:
+            raise ConfigError(f"block of {cnt} markers does not fit m_blk={self.m_blk}")
+        self._next += 1
+        self.busy[r] = True
+        self.meta[r] = (first, cnt, global_indices)
+        self._h2d_open[r] = False
+        return r
+
+    def h2d(self, r, host_part, col0, cols, slot):
+        """Copy host columns (n x >= cols, Fortran-ordered, ideally pinned) into columns
+        col0 .. col0+cols of region r on the copy stream; ``slot`` names the host region the
+        columns came from (see wait_h2d)."""
         torch = self.torch
-        if self.busy[slot]:
-            raise ConfigError(f"stream slot {slot} still in flight")
         d = self.d
         item = 1 if self.int8 else 8
-        hb = host_block
-        if hb.shape[0] != d.n or hb.shape[1] < cnt or not hb.flags.f_contiguous:
+        hb = host_part
+        if hb.shape[0] != d.n or hb.shape[1] < cols or not hb.flags.f_contiguous:
             raise ConfigError("host block must be n x >= cnt and Fortran-ordered")
         if hb.dtype != (np.int8 if self.int8 else np.float64):
             raise ConfigError(f"host block dtype {hb.dtype} does not match the stream")
-        dst = self.dev_in[slot]
+        if col0 < 0 or col0 + cols > self.meta[r][1]:
+            raise ConfigError("host part outside the block")
+        dst = self.dev_in[r]
         with torch.cuda.stream(self.copy_stream):
-            # the device input region is free once the previous compute on this slot is done
-            self.copy_stream.wait_event(self.done[slot])
+            if not self._h2d_open[r]:
+                # the device input region is free once the previous compute on it is done
+                self.copy_stream.wait_event(self.done[r])
+                self.h2d_start[r].record(self.copy_stream)
+                self._h2d_open[r] = True
             rc = _capi.lib().gg_memcpy2d_async(
-                ptr(dst), self.ld_in * item, _capi.C.c_void_p(hb.ctypes.data), d.n * item,
-                d.n * item, int(cnt), 1, _capi.C.c_void_p(self.copy_stream.cuda_stream))
+                _capi.C.c_void_p(dst.data_ptr() + col0 * self.ld_in * item), self.ld_in * item,
+                _capi.C.c_void_p(hb.ctypes.data), d.n * item, d.n * item, int(cols), 1,
+                _capi.C.c_void_p(self.copy_stream.cuda_stream))
             check(rc, "gg_memcpy2d_async")
-            self.h2d_done[slot].record(self.copy_stream)
-        self.h2d_bytes += d.n * item * cnt
-        ws = self.ws[slot]
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        self.host_ev[slot] = ev
+        self.h2d_bytes += d.n * item * cols
+
+    def launch(self, r):
+        """All of region r's columns are queued: TRSM + epilogue + D2H of the results."""
+        torch = self.torch
+        d = self.d
+        first, cnt, gi = self.meta[r]
+        dst = self.dev_in[r]
+        self.h2d_done[r].record(self.copy_stream)
+        ws = self.ws[r]
         with torch.cuda.stream(self.compute_stream):
-            self.compute_stream.wait_event(self.h2d_done[slot])
-            self.start_ev[slot].record(self.compute_stream)
+            self.compute_stream.wait_event(self.h2d_done[r])
+            self.start_ev[r].record(self.compute_stream)
             s = _capi.C.c_void_p(self.compute_stream.cuda_stream)
             if self.int8:
                 ws.run(cnt, G8=dst, ldg=self.ld_in, stream=s)
             else:
                 ws.run(cnt, X64=dst, ldx=self.ld_in, stream=s)
-            self.h_beta[slot][:cnt].copy_(ws.beta[:cnt], non_blocking=True)
-            self.h_status[slot][:cnt].copy_(ws.status[:cnt], non_blocking=True)
+            self.h_beta[r][:cnt].copy_(ws.beta[:cnt], non_blocking=True)
+            self.h_status[r][:cnt].copy_(ws.status[:cnt], non_blocking=True)
             if self.emit_s_inv:
-                self.h_sinv[slot][:cnt].copy_(ws.sinv[:cnt], non_blocking=True)
-            self.done[slot].record(self.compute_stream)
+                self.h_sinv[r][:cnt].copy_(ws.sinv[:cnt], non_blocking=True)
+            self.done[r].record(self.compute_stream)
         self.d2h_bytes += cnt * (8 * d.p + 4 + (8 * d.p * (d.p + 1) // 2 if self.emit_s_inv else 0))
-        self.meta[slot] = (first, cnt, global_indices)
-        self.busy[slot] = True
 
-    def collect(self, slot):
-        self.done[slot].synchronize()
-        self.device_ms += self.start_ev[slot].elapsed_time(self.done[slot])
-        first, cnt, gi = self.meta[slot]
-        self.busy[slot] = False
+    def submit(self, slot, host_block, first, cnt, global_indices=None):
+        """begin + one H2D of the whole block from host region ``slot`` + launch."""
+        r = self.begin(first, cnt, global_indices)
+        try:
+            self.h2d(r, host_block, 0, cnt, slot)
+        except Exception:
+            self.busy[r] = False
+            raise
+        self.launch(r)
+        return r
+
+    def collect(self, ticket):
+        r = ticket
+        if not self.busy[r]:
+            raise ConfigError(f"device region {r} has nothing in flight")
+        self.done[r].synchronize()
+        self.device_ms += self.start_ev[r].elapsed_time(self.done[r])
+        self.h2d_ms += self.h2d_start[r].elapsed_time(self.h2d_done[r])
+        first, cnt, gi = self.meta[r]
+        self.busy[r] = False
         return kernel.ResultArrays(
             first_index=first,
-            beta=self.h_beta[slot][:cnt].numpy().copy(),
-            status=self.h_status[slot][:cnt].numpy().copy(),
-            sinv=self.h_sinv[slot][:cnt].numpy().copy() if self.emit_s_inv else None,
+            beta=self.h_beta[r][:cnt].numpy().copy(),
+            status=self.h_status[r][:cnt].numpy().copy(),
+            sinv=self.h_sinv[r][:cnt].numpy().copy() if self.emit_s_inv else None,
             global_indices=gi)
 
 
@@ -275,26 +333,30 @@ def stream_blocks(engine, blocks, fill, on_result):
     t_wait = 0.0
     cpu_times = []
     nb = len(blocks)
-    pending = None           # slot whose results are not yet collected
+    pending = collections.deque()     # tickets of blocks whose results are not yet collected
     for bi, (first, cnt) in enumerate(blocks):
         slot = bi % StreamEngine.REGIONS
         cpu0 = time.process_time()
         t0 = time.perf_counter()
         host_block = fill(slot, first, cnt, bi, nb)
         t_wait += time.perf_counter() - t0
-        engine.submit(slot, host_block, first, cnt)
-        if pending is not None:
-            on_result(engine.collect(pending))
-        pending = slot
+        if len(pending) == engine.DEV_REGIONS:     # its device region is needed again
+            on_result(engine.collect(pending.popleft()))
+        pending.append(engine.submit(slot, host_block, first, cnt))
         cpu_times.append(time.process_time() - cpu0)
-    if pending is not None:
-        on_result(engine.collect(pending))
+    while pending:
+        on_result(engine.collect(pending.popleft()))
     return t_wait, cpu_times
 
 
-def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False):
+def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, parts=2):
     """Double-buffered file -> GPU -> file loop over ``blocks`` (any subset of the plan, e.g.
-    one rank's shard).  Returns (engine, t_io_wait, block_cpu_times, t_loop)."""
+    one rank's shard).  Returns (engine, t_io_wait, block_cpu_times, t_loop).
+
+    The two host regions (the reference's double buffer, pipeline.py:174-238) are each read
+    and copied in ``parts`` column pieces: the read of piece j+2 reuses the host memory of piece
+    j+2-2*parts as soon as that piece's H2D is done, so file reads run back to back beside the
+    H2D copies and the compute instead of alternating with them."""
     n = reader.n
     int8 = reader.kind == "GWAI"
     engine = StreamEngine(ctx, m_blk, int8=int8, emit_s_inv=emit_s_inv)
@@ -302,27 +364,35 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False):
     regions = [pinned_empty(n, m_blk, dtype) for _ in range(StreamEngine.REGIONS)]
     in_bufs = [r[0] for r in regions]
     width = writer._rsz // 8
-    rec_bufs = [np.empty((m_blk, width)) for _ in range(StreamEngine.REGIONS)]
-    state = {"ticket": None, "store": None, "rec": 0, "io": 0.0}
+    rec_bufs = [np.empty((m_blk, width)) for _ in range(2)]
+    state = {"store": None, "rec": 0, "io": 0.0}
+    P = max(1, int(parts))
+    pieces = []                    # (block index, piece k, col0, col1, first, cnt)
+    for bi, (first, cnt) in enumerate(blocks):
+        edges = [(k * cnt) // P for k in range(P + 1)]
+        for k in range(P):
+            if edges[k + 1] > edges[k]:
+                pieces.append((bi, k, edges[k], edges[k + 1], first, cnt))
+    tickets = {}
+    AHEAD = 2
 
-    def fill(slot, first, cnt, bi, nb):
-        if state["ticket"] is None:          # first block: synchronous start
-            state["ticket"] = reader.start(first, cnt, in_bufs[slot])
-        blk = reader.wait(state["ticket"])
-        state["ticket"] = None
-        if bi + 1 < nb:
-            nslot = (slot + 1) % StreamEngine.REGIONS
-            engine.wait_h2d(nslot)           # its previous H2D must be finished
-            nfirst, ncnt = blocks[bi + 1]
-            state["ticket"] = reader.start(nfirst, ncnt, in_bufs[nslot])
-        return blk.data
+    def host_slot(piece):
+        bi, k = piece[0], piece[1]
+        return (bi % StreamEngine.REGIONS) * P + k
+
+    def start_read(j):
+        pc = pieces[j]
+        bi, k, c0, c1, first, cnt = pc
+        engine.wait_h2d(host_slot(pc))       # the piece that used this memory is copied
+        view = in_bufs[bi % StreamEngine.REGIONS][:, c0:c1]
+        tickets[j] = (reader.start(first + c0, c1 - c0, view), view)   # view kept alive
 
     def on_result(arr):
         t0 = time.perf_counter()
         if state["store"] is not None:
             writer.wait(state["store"])
         state["io"] += time.perf_counter() - t0
-        k = state["rec"] % StreamEngine.REGIONS
+        k = state["rec"] % 2                  # the store of the other record buffer is done
         state["rec"] += 1
         rec = writer.encode(kernel.ResultBlock.from_arrays(arr))
         buf = rec_bufs[k][:rec.shape[0]]
@@ -330,7 +400,33 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False):
         state["store"] = writer.start_records(arr.first_index, buf, key=id(rec_bufs[k]))
 
     t0 = time.perf_counter()
-    t_wait, cpu_times = stream_blocks(engine, blocks, fill, on_result)
+    t_wait = 0.0
+    cpu_times = []
+    pending = collections.deque()
+    cur = None
+    for j in range(min(AHEAD, len(pieces))):
+        start_read(j)
+    cpu0 = time.process_time()
+    for j, pc in enumerate(pieces):
+        bi, k, c0, c1, first, cnt = pc
+        tw = time.perf_counter()
+        blk = reader.wait(tickets.pop(j)[0])
+        t_wait += time.perf_counter() - tw
+        if cur is None:
+            if len(pending) == engine.DEV_REGIONS:     # its device region is needed again
+                on_result(engine.collect(pending.popleft()))
+            cur = engine.begin(first, cnt)
+        engine.h2d(cur, blk.data, c0, c1 - c0, host_slot(pc))
+        if j + AHEAD < len(pieces):
+            start_read(j + AHEAD)
+        if j + 1 == len(pieces) or pieces[j + 1][0] != bi:
+            engine.launch(cur)
+            pending.append(cur)
+            cur = None
+            cpu_times.append(time.process_time() - cpu0)
+            cpu0 = time.process_time()
+    while pending:
+        on_result(engine.collect(pending.popleft()))
     t1 = time.perf_counter()
     if state["store"] is not None:
         writer.wait(state["store"])
