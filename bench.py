@@ -344,6 +344,13 @@ def run_ours(args):
             "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
         }
 
+    if isinstance(clk, dict) and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        # the peak is quoted at the maximum SM clock; under the board's power cap the clock in the
+        # timed region is lower -- the same peak scaled to the median measured clock
+        scale = clk["sm_mhz"] / clk["sm_max_mhz"]
+        roofline["peak_at_measured_clock"] = round(roofline["peak"] * scale, 1)
+        roofline["frac_at_measured_clock"] = round(roofline["achieved"] / (roofline["peak"] * scale), 4)
+
     # ---- e2e through the public stream API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:

@@ -952,6 +952,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   {
     const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
     int clusters = sms() / 2;
+    if (const char* cap = std::getenv("GG_I8_MAX_PAIRS")) {   // tuning / what-if knob
+      const int c = std::atoi(cap);
+      if (c > 0 && c < clusters) clusters = c;
+    }
     if (clusters > pairs) clusters = pairs;
     GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_pair_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
