@@ -312,6 +312,8 @@ def run_ours(args):
     snps_per_step_total = m * world
     value = snps_per_step_total * args.steps / (elapsed_ms / 1e3)
     traffic_full, ncu = load_traffic("i8" if use_i8 else "dmma")
+    if ncu is not None and (ncu.get("n") != n or ncu.get("snps_per_launch") != m_blk):
+        traffic_full, ncu = None, None      # the committed capture is of another workload
     flops_per_step = float(n) * n * m
     trsm_tflops = flops_per_step / (trsm_ms / 1e3) / 1e12          # FP64-equivalent rate
     step_tflops = flops_per_step * args.steps / (elapsed_ms / 1e3) / 1e12
