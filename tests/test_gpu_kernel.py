@@ -364,3 +364,50 @@ def test_cholesky_reads_lower_triangle_and_checks_all_entries(K):
     with pytest.raises(NotPositiveDefinite) as e:
         K.cholesky_spd(A)
     assert e.value.pivot_index == 3
+
+
+def test_concurrent_calls_from_threads(K):
+    """Threading contract (run_spmd(transport="inproc") calls the kernel module from
+    several threads of one process): concurrent gls_solve_block calls on two contexts, from
+    threads on the default stream and on their own streams, give the sequential results bitwise
+    (per-call workspaces; the int8 kernel's tile counters are per launch)."""
+    import threading
+
+    import torch
+
+    rng = np.random.default_rng(21)
+    n1, n2, m = 300, 170, 600
+    ctx1 = K.gls_prepare(make_spd(n1, 3), np.hstack([np.ones((n1, 1)),
+                                                     rng.standard_normal((n1, 2))]),
+                         rng.standard_normal(n1))
+    ctx2 = K.gls_prepare(make_spd(n2, 4), np.hstack([np.ones((n2, 1)),
+                                                     rng.standard_normal((n2, 3))]),
+                         rng.standard_normal(n2))
+    X1 = np.asfortranarray(rng.integers(0, 3, (n1, m)).astype(np.int8))
+    X2 = rng.standard_normal((n2, m))                 # FP64 path
+    ref1 = betas(K.gls_solve_block(ctx1, K.SnpBlock(0, X1)))
+    ref2 = betas(K.gls_solve_block(ctx2, K.SnpBlock(0, X2)))
+    errors = []
+
+    def work(ctx, X, ref, own_stream):
+        try:
+            s = torch.cuda.Stream() if own_stream else None
+            for _ in range(6):
+                if s is not None:
+                    with torch.cuda.stream(s):
+                        got = betas(K.gls_solve_block(ctx, K.SnpBlock(0, X)))
+                else:
+                    got = betas(K.gls_solve_block(ctx, K.SnpBlock(0, X)))
+                if not np.array_equal(got, ref):
+                    errors.append("mismatch")
+        except Exception as e:        # noqa: BLE001 -- reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=a) for a in
+               [(ctx1, X1, ref1, False), (ctx1, X1, ref1, True), (ctx2, X2, ref2, False),
+                (ctx2, X2, ref2, True)]]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
