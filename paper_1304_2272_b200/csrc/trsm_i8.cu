@@ -121,9 +121,9 @@ __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& 
 
 // ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
 // A cluster of 2 CTAs on a TPC computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs issued
-// by the leader: each CTA stages its own 128 SNPs (A) and HALF of the slices (B is split along N:
-// CTA0 slices 0..3, CTA1 slices 4..7), so per-SM staging traffic drops by a third and 6 stages fit
-// in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
+// by the leader: each CTA stages its own 128 SNPs (A) and HALF of the 224 slice rows (B is split
+// along N: CTA0 slices 0-2 + rows 0-15 of slice 3, CTA1 the rest), so per-SM staging traffic drops
+// by a third and 6 stages fit in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
 // commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
 // threads release the accumulator on the leader's "accumulator empty" barrier.
 constexpr int P_STAGES = 6;
