@@ -48,6 +48,32 @@ def test_i8_trsm_matches_dmma(K, n, cnt):
     assert np.array_equal(Xp, Xi.cpu().numpy()[perm])
 
 
+def test_i8_trsm_small_and_ragged_shapes(K):
+    """Edge shapes of the int8 TRSM (n below / at / above the 32-row block and 128-row tile
+    boundaries, 1 .. 300 columns, partial SNP pairs) against the FP64 DMMA TRSM."""
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._device import upload_cols
+
+    for n in (1, 2, 5, 31, 32, 33, 127, 128, 129, 257):
+        M = make_spd(n, 3 * n + 1)
+        _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+        sl, expo = K._slice_inverse(Linv, n)
+        np_ = _capi.pad(n)
+        for cnt in (1, 3, 130, 300):
+            G = np.random.default_rng(n * 1000 + cnt).integers(0, 3, (n, cnt))
+            Xd = K._trsm_device(LinvP, n, upload_cols(G.astype(float), ld=np_), cnt)
+            Xi = K._trsm_i8_device(sl, expo, n, G)
+            torch.cuda.synchronize()
+            ref = Xd[:, :n].cpu().numpy()
+            got = Xi[:, :n].cpu().numpy()
+            scale = np.maximum(np.max(np.abs(ref), axis=1), 1e-300)
+            colrel = np.max(np.abs(got - ref), axis=1) / scale
+            assert colrel.max() <= 1e-13, (n, cnt, colrel.max())
+            assert bool((Xi[:, n:] == 0).all()), (n, cnt)
+
+
 def test_i8_trsm_accuracy_vs_extended_precision(K):
     """Accuracy of the sliced inverse on a kinship covariance (the BASELINE workload's M): the
     int8 path's Xbar = Linv G against Linv G in extended precision for the same FP64 inverse.
