@@ -37,16 +37,37 @@ for path in [_capi.LIB_PATH] + sys.argv[1:]:
     meta = torch.zeros(2 * _capi.pad(n), dtype=torch.int32, device="cuda")
     assert lib.gg_slice_packed_inverse_i8(n, ptr(d.LinvP), ptr(sl), ptr(meta), s) == 0
     libs.append((os.path.basename(path), f, sl, meta, []))
+# in-tree library under environment variants: GG_AB_ENVS="GG_I8_CLUSTER=4;GG_I8_MAX_PAIRS=66"
+envs = {}
+for spec_ in filter(None, os.environ.get("GG_AB_ENVS", "").split(";")):
+    k_, v_ = spec_.split("=", 1)
+    name, f, sl, meta, _ = libs[0]
+    libs.append((f"in-tree {spec_}", f, sl, meta, []))
+    envs[f"in-tree {spec_}"] = (k_, v_)
+
+
+class _Env:
+    def __init__(self, name):
+        self.kv = envs.get(name)
+
+    def __enter__(self):
+        if self.kv:
+            os.environ[self.kv[0]] = self.kv[1]
+
+    def __exit__(self, *exc):
+        if self.kv:
+            del os.environ[self.kv[0]]
 torch.cuda.synchronize()
 d.slices = None
 Pref = None
 for rep in range(8):
     for name, f, sl, meta, ts in libs:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        rc = f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
-               ptr(P), None, 0, None, 0, s)
-        b.record()
+        with _Env(name):
+            a.record()
+            rc = f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
+                   ptr(P), None, 0, None, 0, s)
+            b.record()
         torch.cuda.synchronize()
         assert rc == 0, rc
         ts.append(a.elapsed_time(b))
@@ -66,11 +87,12 @@ for rnd in range(2 if sustain > 0 else 0):
     for name, f, sl, meta, ts in libs:
         reps = max(int(sustain / 2.0e-3), 10)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for r in range(reps):
-            if r == reps // 2:
-                a.record()
-            f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar), ptr(P),
-              None, 0, None, 0, s)
-        b.record()
+        with _Env(name):
+            for r in range(reps):
+                if r == reps // 2:
+                    a.record()
+                f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
+                  ptr(P), None, 0, None, 0, s)
+            b.record()
         torch.cuda.synchronize()
         print(f"sustained round {rnd} {name}: {a.elapsed_time(b) / (reps - reps // 2):.3f} ms")
