@@ -68,6 +68,7 @@ struct I8Args {
   const int* gate;  // device flag: the kernel runs only if *gate == gate_value (nullptr: always)
   int gate_value;
   int* tile_counter;  // zeroed before the launch: clusters take tiles dynamically, heavy first
+  int rd_bytes;       // bytes per row-data slot (rd_bytes(q, P != nullptr))
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -123,20 +124,23 @@ __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& 
 // A cluster of 2 CTAs on a TPC computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs issued
 // by the leader: each CTA stages its own 128 SNPs (A) and HALF of the 224 slice rows (B is split
 // along N: CTA0 slices 0-2 + rows 0-15 of slice 3, CTA1 the rest), so per-SM staging traffic drops
-// by a third and 6 stages fit in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
+// by a third and 6-7 stages fit in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
 // commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
 // threads release the accumulator on the leader's "accumulator empty" barrier.
-constexpr int P_STAGES = 6;
+// pipeline depth: 7 stages when the per-tile row data is small enough (q <= 13), else 6
 constexpr int P_B_ROWS = TN / 2;                    // 112 slice rows per CTA of the pair
 constexpr int P_B_BYTES = P_B_ROWS * TK;             // 14 KB
 constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 30 KB
-// per-tile row data staged by the producer with bulk copies: e_i (32 ints) then the tile's 32
-// rows of XLbar's q columns and of ybar (q + 1 <= GG_PMAX columns)
+// per-tile row data staged by the producer with bulk copies: e_i and h_i (32 ints each), then
+// the tile's 32 rows of XLbar's q columns and of ybar (sized for the launch's q: a.rd_bytes)
 constexpr int RD_SLOTS = 4;
 constexpr int RD_COLS_OFF = 2 * TR * 4;   // e'_i, then the diagonal heads h_i
-constexpr int RD_BYTES = RD_COLS_OFF + GG_PMAX * TR * 8;    // 5248
-constexpr size_t P_SMEM_BYTES =
-    size_t(P_STAGES) * P_STAGE_BYTES + size_t(RD_SLOTS) * RD_BYTES + 1024 + 512;
+__host__ __device__ constexpr int rd_bytes(int q, bool partials) {
+  return RD_COLS_OFF + (partials ? (q + 1) * TR * 8 : 0);
+}
+__host__ __device__ constexpr size_t p_smem_bytes(int stages, int rdb) {
+  return size_t(stages) * P_STAGE_BYTES + size_t(RD_SLOTS) * rdb + 1024 + 512;
+}
 // dynamic tile queue: TQ slots; readers per slot: leader MMA + peer producer + one epilogue
 // group (4 warps) in each CTA
 constexpr int TQ = 8;
@@ -252,6 +256,7 @@ __device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[S][8]) {
       : "memory");
 }
 
+template <int P_STAGES>
 __global__ void __launch_bounds__(THREADS, 1)
     trsm_i8_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB3,
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* rdata = smem + P_STAGES * P_STAGE_BYTES;
+  const int RD_BYTES = a.rd_bytes;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(rdata + RD_SLOTS * RD_BYTES);
   int* tq = reinterpret_cast<int*>(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS + 2 * TQ);   // tiles
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(tq + TQ);
@@ -794,6 +800,13 @@ int sms() {
   return n;
 }
 
+int smem_optin() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return n;
+}
+
 }  // namespace
 
 int i8_slices() { return S; }
@@ -957,13 +970,16 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
       if (c > 0 && c < clusters) clusters = c;
     }
     if (clusters > pairs) clusters = pairs;
-    GG_CUDA_TRY(cudaFuncSetAttribute(trsm_i8_pair_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)P_SMEM_BYTES));
+    a.rd_bytes = rd_bytes(q, P != nullptr);
+    const bool seven = p_smem_bytes(7, a.rd_bytes) <= (size_t)smem_optin();
+    auto kern = seven ? trsm_i8_pair_kernel<7> : trsm_i8_pair_kernel<6>;
+    const size_t smem = p_smem_bytes(seven ? 7 : 6, a.rd_bytes);
+    GG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = P_SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -972,7 +988,7 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, trsm_i8_pair_kernel, mA, mB, mB1, a));
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mA, mB, mB1, a));
     return GG_OK;
   }
 }
