@@ -22,7 +22,7 @@ namespace {
 
 constexpr int NB = 128;
 constexpr int OUTER = 8 * NB;   // outer block width of the two-level Cholesky
-constexpr int LEAF_THREADS = 512;
+constexpr int LEAF_THREADS = 384;
 
 struct PotrfHeader {
   int info;                      // 0 = ok, else failing pivot + 1
@@ -74,7 +74,9 @@ __global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long 
 // barriers instead of two per column.
 constexpr int LB = 32;                  // sub-block edge
 constexpr int LDS = NB + 1;             // padded smem row stride (conflict-free columns)
-constexpr size_t LEAF2_SMEM = (size_t)(NB * LDS + 2 * 4 * LB * LB) * sizeof(double) + 16;
+constexpr int TLD = LB + 1;             // padded row stride of the T_J blocks (lanes read rows)
+constexpr int TB = LB * TLD;            // one T_J block
+constexpr size_t LEAF2_SMEM = (size_t)(NB * LDS + 4 * TB + 4 * LB * LB) * sizeof(double) + 16;
 
 // warp: factor the 32 x 32 diagonal sub-block at (j0, j0) of S in place; returns the failing
 // local column (0..31) or -1.  Lane i keeps row i in registers; the column being eliminated is
@@ -93,9 +95,11 @@ __device__ int warp_factor32(double* S, int j0, int lane) {
     if (lane == j) r[j] = piv;
     else if (lane > j) r[j] = r[j] * rp;         // dpotf2's DSCAL by the reciprocal pivot
 #pragma unroll
-    for (int c = j + 1; c < LB; ++c) {
-      const double lc = __shfl_sync(0xffffffffu, r[j], c);
-      if (lane >= c) r[c] -= r[j] * lc;
+    for (int c = 0; c < LB; ++c) {   // constant bounds: fully unrolled, r[] stays in registers
+      if (c > j) {
+        const double lc = __shfl_sync(0xffffffffu, r[j], c);
+        if (lane >= c) r[c] -= r[j] * lc;
+      }
     }
   }
 #pragma unroll
@@ -127,7 +131,7 @@ __device__ void warp_inverse32(const double* S, int j0, double* T, int lane) {
     }
   }
 #pragma unroll
-  for (int i = 0; i < LB; ++i) T[i * LB + c] = t[i];
+  for (int i = 0; i < LB; ++i) T[i * TLD + c] = t[i];
   __syncwarp();
 }
 
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
   extern __shared__ double lsm[];
   double* S = lsm;                          // 128 x 128 row-major (ld LDS): the block, then L
   double* T = lsm + NB * LDS;               // 4 x (32 x 32): T_J = L_JJ^-1
-  double* W = T + 4 * LB * LB;              // 4 x (32 x 32): scratch of the inverse phase
+  double* W = T + 4 * TB;                   // 4 x (32 x 32): scratch of the inverse phase
   int* fail = reinterpret_cast<int*>(W + 4 * LB * LB);
   if (info != nullptr && *info != 0) return;
   if (!FACTOR) k0 = blockIdx.x * NB;
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
   if (FACTOR) {
     for (int J = 0; J < NB / LB; ++J) {
       const int j0 = J * LB;
-      double* TJ = T + J * LB * LB;
+      double* TJ = T + J * TB;
       if (warp == 0) {
         const int f = warp_factor32(S, j0, lane);
         if (f >= 0) {
@@ -173,7 +177,10 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
       for (int e = tid; e < rows * LB; e += blockDim.x) {
         const int r = r0 + e / LB, c = e % LB;
         double acc = 0.0;
-        for (int k = 0; k <= c; ++k) acc += S[r * LDS + j0 + k] * TJ[c * LB + k];
+        // T_J is lower triangular (zeros stored above the diagonal): a uniform 32-term loop;
+        // lanes read rows c of T_J (padded stride: no bank conflicts), S[r] is a broadcast
+#pragma unroll
+        for (int k = 0; k < LB; ++k) acc += S[r * LDS + j0 + k] * TJ[c * TLD + k];
         W[e] = acc;
       }
       __syncthreads();
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
       Aw[r + (long long)c * ld] = (r >= c) ? S[r * LDS + c] : 0.0;
     }
   } else {
-    if (warp < NB / LB) warp_inverse32(S, warp * LB, T + warp * LB * LB, lane);
+    if (warp < NB / LB) warp_inverse32(S, warp * LB, T + warp * TB, lane);
     __syncthreads();
   }
   // ---- inverse: X_IJ = -T_I sum_{K=J}^{I-1} L_IK X_KJ, block rows I = 1..3 in order; X is
@@ -216,9 +223,9 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
       for (int K = J; K < I; ++K)
 #pragma unroll 8
         for (int k = 0; k < LB; k += 2) {
-          const double x0 = (K == J) ? T[J * LB * LB + k * LB + cc]
+          const double x0 = (K == J) ? T[J * TB + k * TLD + cc]
                                      : S[(K * LB + k) * LDS + J * LB + cc];
-          const double x1 = (K == J) ? T[J * LB * LB + (k + 1) * LB + cc]
+          const double x1 = (K == J) ? T[J * TB + (k + 1) * TLD + cc]
                                      : S[(K * LB + k + 1) * LDS + J * LB + cc];
           a0 += S[(I * LB + rr) * LDS + K * LB + k] * x0;
           a1 += S[(I * LB + rr) * LDS + K * LB + k + 1] * x1;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
     for (int e = tid; e < I * LB * LB; e += blockDim.x) {
       const int J = e / (LB * LB), rr = (e / LB) % LB, cc = e % LB;
       double acc = 0.0;
-      for (int k = 0; k <= rr; ++k) acc += T[I * LB * LB + rr * LB + k] * W[J * LB * LB + k * LB + cc];
+      for (int k = 0; k <= rr; ++k) acc += T[I * TB + rr * TLD + k] * W[J * LB * LB + k * LB + cc];
       S[(I * LB + rr) * LDS + J * LB + cc] = -acc;   // X_IJ (L_IJ no longer needed)
     }
     __syncthreads();
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
     const int I = r / LB, J = c / LB;
     double v;
     if (r < c) v = 0.0;
-    else if (I == J) v = T[I * LB * LB + (r % LB) * LB + (c % LB)];
+    else if (I == J) v = T[I * TB + (r % LB) * TLD + (c % LB)];
     else v = S[r * LDS + c];
     Db[r + (long long)c * ldi] = v;
   }
