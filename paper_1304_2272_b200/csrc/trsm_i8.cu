@@ -420,9 +420,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           fence_after();
           const unsigned sa = sbase + stage * P_STAGE_BYTES;
           const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
+          // the diagonal k tile holds nonzero slices only up to the row block's last row:
+          // k < 32 (rb + 1), i.e. its first (rb & 3) + 1 MMAs of K = 32
+          const int kk_end = (kt == nk - 1) ? (rb & 3) + 1 : TK / 32;
 #pragma unroll
           for (int kk = 0; kk < TK / 32; ++kk)
-            mma_i8_pair(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+            if (kk < kk_end)
+              mma_i8_pair(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
           mma_commit_pair(empty0 + 8 * stage);
           if (++stage == P_STAGES) {
             stage = 0;
