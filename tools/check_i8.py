@@ -33,7 +33,7 @@ def main():
         del Linv
         S = lib.gg_i8_slices()
         sl = torch.empty(int(lib.gg_inverse_slices_bytes(n)), dtype=torch.int8, device="cuda")
-        expo = torch.empty(np_, dtype=torch.int32, device="cuda")
+        expo = torch.empty(int(lib.gg_slice_meta_ints(n)), dtype=torch.int32, device="cuda")
         check(lib.gg_slice_inverse_i8(n, ptr(LinvT), np_, ptr(sl), ptr(expo), s), "slice")
         ldg = -(-n // 16) * 16
         G = datagen.genotypes_device(spec, 0, args.cnt, ld=ldg)           # (cnt, ldg) int8
