@@ -372,6 +372,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "dtype_detail": ("TRSM: exact int8 x int8 -> int32 tcgen05 products of a 7-slice split "
+                             "of the FP64 inverse (+ integer diagonal head), one FP64 rounding per "
+                             "element; reductions and p x p solves in FP64") if use_i8 else
+                            "FP64 DMMA TRSM, FP64 reductions and solves",
             "config": {
                 "workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}, m={m} SNPs "
                             f"per GPU, FP64, blocks of {m_blk}; step = TRSM + fused epilogue "
