@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -69,6 +70,7 @@ struct I8Args {
   int gate_value;
   int* tile_counter;  // zeroed before the launch: clusters take tiles dynamically, heavy first
   int rd_bytes;       // bytes per row-data slot (rd_bytes(q, P != nullptr))
+  int grp_pp;         // 256-SNP tile pairs per SNP group (tile_coords)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -115,9 +117,17 @@ __device__ __forceinline__ double pow2(int e) {
   return __longlong_as_double((long long)(1023 + e) << 52);
 }
 
-__device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int& rb, int& nt) {
-  rb = num_rb - 1 - t / num_nt;   // heavy row blocks first; a row block's SNP tiles together
-  nt = t % num_nt;
+// Tile t -> (row block rb, SNP tile nt).  The num_nt SNP tiles are cut into groups of grp; the
+// groups are swept one after the other, and inside a group the row blocks heavy first with a row
+// block's SNP tiles together (grp bounds the genotype working set that L2 has to hold while
+// every row block re-reads it).
+__device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int grp, int& rb,
+                                            int& nt) {
+  const int g = t / (num_rb * grp);
+  const int t1 = t - g * num_rb * grp;
+  const int w = min(grp, num_nt - g * grp);     // the last group may be narrower
+  rb = num_rb - 1 - t1 / w;
+  nt = g * grp + t1 % w;
 }
 
 // ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (t < 0) break;
         int rb, pp;
-        tile_coords(t, a.num_rb, num_pp, rb, pp);
+        tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
         const int nt = 2 * pp + (int)rank;
         const int nk = (rb + 4) / 4;
         {   // this CTA's row data for the tile (its own barrier): e_i, XLbar rows, ybar rows
@@ -409,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tile_read(r);
         if (t < 0) break;
         int rb, pp;
-        tile_coords(t, a.num_rb, num_pp, rb, pp);
+        tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
         const int nk = (rb + 4) / 4;
         const int ab = it & 1;
         mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) tile_read(r);
       if (t < 0) break;
       int rb, pp;
-      tile_coords(t, a.num_rb, num_pp, rb, pp);
+      tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
       const int nt = 2 * pp + (int)rank;
       const int col_g = nt * TM + m, row0_g = rb * TR;
       // this SNP's dosages on the tile's rows (the head term; rows >= n are zero), loaded before
@@ -974,6 +984,19 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
       if (c > 0 && c < clusters) clusters = c;
     }
     if (clusters > pairs) clusters = pairs;
+    // SNP groups (tile_coords): ~16 pairs (4,096 SNPs) at n = 10^4, scaled by sqrt(10^4 / n) --
+    // the genotype group must stay L2-resident while the row blocks re-read it, and every group
+    // re-reads the slices.  Measured DRAM bytes per 8,192-SNP launch (ncu): n = 10^4 2.5 GB
+    // (one group) -> 0.83 GB (16 pairs), n = 4*10^4 150 GB -> 43 GB (8 pairs).
+    const int num_pp = (a.num_nt + 1) / 2;
+    int grp = (int)(16.0 * std::sqrt(1e4 / (double)n) + 0.5);
+    if (const char* g = std::getenv("GG_I8_SNP_GROUP")) {   // tuning knob: pairs per group
+      const int v = std::atoi(g);
+      if (v > 0) grp = v;
+    }
+    grp = grp < 1 ? 1 : (grp > num_pp ? num_pp : grp);
+    const int ngroups = (num_pp + grp - 1) / grp;
+    a.grp_pp = (num_pp + ngroups - 1) / ngroups;                // equal-width groups
     a.rd_bytes = rd_bytes(q, P != nullptr);
     const bool seven = p_smem_bytes(7, a.rd_bytes) <= (size_t)smem_optin();
     auto kern = seven ? trsm_i8_pair_kernel<7> : trsm_i8_pair_kernel<6>;

@@ -281,3 +281,23 @@ def test_i8_path_all_covariate_counts(K, p):
     ref, ok = O.gls_solve_block(O.gls_prepare(M, XL, y), G.astype(float))
     rel, mism = O.compare(got, ref)
     assert mism == 0 and rel <= 1e-10, rel
+
+
+@pytest.mark.parametrize("grp", ["1", "3", "7", "1000"])
+def test_i8_trsm_snp_group_order_is_bitwise_invariant(K, grp, monkeypatch):
+    """The SNP-group tile order (GG_I8_SNP_GROUP pairs per group, default sqrt-scaled in n) only
+    changes which cluster computes a tile when: every column is bitwise the same, including the
+    ragged last group and the partial last pair."""
+    import torch
+
+    n, cnt = 700, 8 * 256 + 77                   # 9 pairs: groups of 1, 3 (3x3), 7 (7+2), all
+    M = make_spd(n, 2 * n)
+    _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+    sl, expo = K._slice_inverse(Linv, n)
+    G = np.random.default_rng(7).integers(0, 3, (n, cnt))
+    monkeypatch.delenv("GG_I8_SNP_GROUP", raising=False)
+    ref = K._trsm_i8_device(sl, expo, n, G).cpu().numpy()
+    monkeypatch.setenv("GG_I8_SNP_GROUP", grp)
+    got = K._trsm_i8_device(sl, expo, n, G).cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(got, ref)
