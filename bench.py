@@ -3,10 +3,12 @@
 
 Workload: n = 10,000 individuals, p = 4, m = 200,000 SNPs per GPU, FP64, blocks of 8,192 SNPs
 (24 full + one 3,392 tail), seeded synthetic BASELINE data.  One STEP is one
-full sweep of the rank's 200,000 SNPs: per block one DMMA TRSM launch (Xbar = Linv * X) and one
-fused epilogue launch (reductions + batched 4x4 Cholesky solve).  The genotypes (FP64, 16.2 GB
-per GPU) are resident in HBM when the timed region starts; they are larger than L2, so no L2
-flush is needed.  gls_prepare (Cholesky + inverse) runs once, outside the step, timed apart.
+full sweep of the rank's 200,000 SNPs: per block one FP64 -> int8 narrow of the dosages (side
+stream, one block ahead), one int8 tensor-core TRSM launch (Xbar = Linv * G with the per-SNP
+partial dots fused into its epilogue) and one reduce + batched p x p solve launch.  The genotypes
+(FP64, 16.2 GB per GPU) are resident in HBM when the timed region starts; they are larger than
+L2, so no L2 flush is needed.  gls_prepare (Cholesky + inverse + slicing) runs once, outside the
+step, timed apart.  `--trsm dmma` runs the FP64 DMMA TRSM + epilogue instead.
 
 Multi-GPU (torchrun): SNP-sharded weak scaling — rank r owns markers [r*m, (r+1)*m) of an
 N*m-marker panel; L is factored redundantly on every rank; no collective in the timed region
@@ -322,8 +324,8 @@ def run_ours(args):
         tops = slices * flops_per_step / (trsm_ms / 1e3) / 1e12     # int8 ops: S slices x n^2
         roofline = {
             "bound": "tensor",
-            "kernel": "trsm_i8_pair_kernel (persistent CTA-pair TMA + tcgen05.mma.kind::i8 TRSM, "
-                      "fused reductions; inverse split into int8 slices)",
+            "kernel": "trsm_i8_dual_kernel (persistent CTA-pair TMA + tcgen05.mma.kind::i8 TRSM, "
+                      "two row blocks per tile, fused reductions; inverse split into int8 slices)",
             "achieved": round(tops, 1), "peak": I8_PEAK_TOPS, "unit": "TOPS",
             "frac": round(tops / I8_PEAK_TOPS, 4),
             "traffic": traffic_full,

@@ -13,16 +13,17 @@
 //
 // Kernel (persistent, CTA pairs with cta_group::2, one CTA per SM, 10 warps):
 //   warp 0  producer: A = 128 SNPs x 128 k int8 per CTA (TMA, 128B swizzle, k >= n zero-filled),
-//           B = this CTA's half of the 7 x 32 slice rows of the tile (tile-packed slices), into a
-//           6-stage mbarrier ring (30 KB / stage); per-tile row data (e_i, h_i, XLbar/ybar rows)
-//           by bulk copies into 4 slots; pulls tiles heavy-first from a global atomic counter and
-//           posts them to a per-cluster tile queue;
-//   warp 1  MMA issuer (leader CTA, one lane): D[256 SNPs x 224] += A . B^T over the pair,
-//           int32 accumulators in TMEM, double-buffered (2 x 256 columns);
-//   warps 2-9  two epilogue groups (one per accumulator buffer): tcgen05.ld each SNP's 7 x 32
-//           accumulators, recombine, store the SNP's 32 Xbar rows and/or the fused per-SNP partial
-//           dots against XLbar / ybar (canonical order of gls_epilogue.cu).
-// Tiles = (32-row blocks of Linv) x (256-SNP column pairs); row block rb needs k < 32 (rb+1).
+//           B = this CTA's half of the 7 x 32 slice rows of each of the tile's two row blocks
+//           (tile-packed slices), into a 4-5-stage mbarrier ring (44 KB / stage); per-tile row
+//           data (e_i, h_i, XLbar/ybar rows) by bulk copies into 2 slots; pulls tiles heavy-first
+//           from a global atomic counter and posts them to a per-cluster tile queue;
+//   warp 1  MMA issuer (leader CTA, one lane): D_h[256 SNPs x 224] += A . B_h^T over the pair for
+//           the two row blocks h = 0, 1, int32 accumulators in TMEM (columns 0 and 256);
+//   warps 2-9  two epilogue groups (group h drains row block h of the tile): tcgen05.ld each
+//           SNP's 7 x 32 accumulators, recombine, store the SNP's 32 Xbar rows and/or the fused
+//           per-SNP partial dots against XLbar / ybar (canonical order of gls_epilogue.cu).
+// Tiles = (pairs of 32-row blocks of Linv) x (256-SNP column pairs), swept in SNP groups
+// (tile_coords); row block rb needs k < 32 (rb+1).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -130,31 +131,23 @@ __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int g
   nt = g * grp + t1 % w;
 }
 
-// ---- CTA-pair variant (cta_group::2) ----------------------------------------------------------
-// A cluster of 2 CTAs on a TPC computes a 256-SNP x (S x 32)-column tile with M = 256 MMAs issued
-// by the leader: each CTA stages its own 128 SNPs (A) and HALF of the 224 slice rows (B is split
-// along N: CTA0 slices 0-2 + rows 0-15 of slice 3, CTA1 the rest), so per-SM staging traffic drops
-// by a third and 6-7 stages fit in shared memory.  Both CTAs' TMA loads complete on the leader's "full" barrier; the leader's
-// commits are multicast to both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue
-// threads release the accumulator on the leader's "accumulator empty" barrier.
-// pipeline depth: 7 stages when the per-tile row data is small enough (q <= 13), else 6
+// ---- CTA-pair kernel (cta_group::2) ------------------------------------------------------------
+// A cluster of 2 CTAs on a TPC computes 256-SNP x (S x 32)-column products with M = 256 MMAs
+// issued by the leader: each CTA stages its own 128 SNPs (A) and HALF of the 224 slice rows of a
+// row block (B is split along N: CTA0 slices 0-2 + rows 0-15 of slice 3, CTA1 the rest).  Both
+// CTAs' TMA loads complete on the leader's "full" barrier; the leader's commits are multicast to
+// both CTAs' "empty" / "accumulator full" barriers; both CTAs' epilogue threads release an
+// accumulator on the leader's "accumulator empty" barrier.
 constexpr int P_B_ROWS = TN / 2;                    // 112 slice rows per CTA of the pair
 constexpr int P_B_BYTES = P_B_ROWS * TK;             // 14 KB
-constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES;   // 30 KB
-// per-tile row data staged by the producer with bulk copies: e_i and h_i (32 ints each), then
-// the tile's 32 rows of XLbar's q columns and of ybar (sized for the launch's q: a.rd_bytes)
-constexpr int RD_SLOTS = 4;
+// per-row-block data staged by the producer with bulk copies: e_i and h_i (32 ints each), then
+// the block's 32 rows of XLbar's q columns and of ybar (sized for the launch's q: a.rd_bytes)
 constexpr int RD_COLS_OFF = 2 * TR * 4;   // e'_i, then the diagonal heads h_i
 __host__ __device__ constexpr int rd_bytes(int q, bool partials) {
   return RD_COLS_OFF + (partials ? (q + 1) * TR * 8 : 0);
 }
-__host__ __device__ constexpr size_t p_smem_bytes(int stages, int rdb) {
-  return size_t(stages) * P_STAGE_BYTES + size_t(RD_SLOTS) * rdb + 1024 + 512;
-}
-// dynamic tile queue: TQ slots; readers per slot: leader MMA + peer producer + one epilogue
-// group (4 warps) in each CTA
+// dynamic tile queue: TQ slots, posted by the leader's producer to both CTAs
 constexpr int TQ = 8;
-constexpr int TQ_READERS = 2 + 2 * 4;
 constexpr unsigned IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(TN >> 3) << 17) |
                             ((unsigned)(2 * TM >> 4) << 24);
 constexpr unsigned PEER_MASK = 0xFEFFFFFFu;          // clear the CTA-rank bit: the leader's copy
@@ -266,29 +259,45 @@ __device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[S][8]) {
       : "memory");
 }
 
+// A tile is 256 SNPs x TWO adjacent 32-row blocks (2 rbp, 2 rbp + 1: the same
+// 128-row slice tile, so the same k range): each stage's genotype tile A feeds two N = 224 MMAs
+// (accumulators at TMEM columns 0 and 256), halving the A bytes per MAC (44 KB per stage for
+// 2 x 3.67 M MACs per SM; one row block per tile with double-buffered accumulators moved 30 KB for
+// 3.67 M and was 2.5-3% slower, burst and sustained, at n = 10^4 and 4*10^4).  The accumulators are single-buffered:
+// epilogue group g drains row block 2 rbp + g and releases its half as soon as it is in
+// registers, so the next tile's MMAs into that half wait only for the drain.
+constexpr int D_STAGE_BYTES = A_BYTES + 2 * P_B_BYTES;   // 44 KB
+constexpr int D_RD_SLOTS = 2;                            // row-data slots (x2 halves)
+__host__ __device__ constexpr size_t d_smem_bytes(int stages, int rdb) {
+  return size_t(stages) * D_STAGE_BYTES + size_t(D_RD_SLOTS) * 2 * rdb + 1024 + 512;
+}
+constexpr int D_TQ_READERS = 2 + 2 * 8;   // leader MMA + peer producer + 8 epilogue warps per CTA
+
 template <int P_STAGES>
 __global__ void __launch_bounds__(THREADS, 1)
-    trsm_i8_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+    trsm_i8_dual_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB3,
                         const __grid_constant__ CUtensorMap tmB1, I8Args a) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* rdata = smem + P_STAGES * P_STAGE_BYTES;
+  unsigned char* rdata = smem + P_STAGES * D_STAGE_BYTES;
   const int RD_BYTES = a.rd_bytes;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(rdata + RD_SLOTS * RD_BYTES);
-  int* tq = reinterpret_cast<int*>(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS + 2 * TQ);   // tiles
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(rdata + D_RD_SLOTS * 2 * RD_BYTES);
+  // barriers: full[P], empty[P], accf, acce[2], rdf[RD], rde[RD], tqf[TQ], tqe[TQ]
+  int* tq = reinterpret_cast<int*>(bars + 2 * P_STAGES + 3 + 2 * D_RD_SLOTS + 2 * TQ);
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(tq + TQ);
   const unsigned sbase = smem_u32(smem);
   const unsigned rbase = smem_u32(rdata);
   const unsigned full0 = smem_u32(bars);
   const unsigned empty0 = smem_u32(bars + P_STAGES);
-  const unsigned accf0 = smem_u32(bars + 2 * P_STAGES);
-  const unsigned acce0 = smem_u32(bars + 2 * P_STAGES + 2);
-  const unsigned rdf0 = smem_u32(bars + 2 * P_STAGES + 4);              // row data full  [4]
-  const unsigned rde0 = smem_u32(bars + 2 * P_STAGES + 4 + RD_SLOTS);   // row data empty [4]
-  const unsigned tqf0 = smem_u32(bars + 2 * P_STAGES + 4 + 2 * RD_SLOTS);   // tile posted [TQ]
-  const unsigned tqe0 = tqf0 + 8 * TQ;                                        // tile read   [TQ]
+  const unsigned accf = smem_u32(bars + 2 * P_STAGES);
+  const unsigned acce0 = smem_u32(bars + 2 * P_STAGES + 1);
+  const unsigned rdf0 = smem_u32(bars + 2 * P_STAGES + 3);
+  const unsigned rde0 = rdf0 + 8 * D_RD_SLOTS;
+  const unsigned tqf0 = rde0 + 8 * D_RD_SLOTS;
+  const unsigned tqe0 = tqf0 + 8 * TQ;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned rank = cluster_rank();
   const bool leader = rank == 0;
@@ -299,17 +308,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, 2 * 4 * 32);   // both CTAs' epilogue threads (leader's copy used)
-    }
-    for (int b = 0; b < RD_SLOTS; ++b) {
+    mbar_init(accf, 1);
+    for (int h = 0; h < 2; ++h) mbar_init(acce0 + 8 * h, 2 * 4 * 32);   // both CTAs' group h
+    for (int b = 0; b < D_RD_SLOTS; ++b) {
       mbar_init(rdf0 + 8 * b, 1);
-      mbar_init(rde0 + 8 * b, 4 * 32);
+      mbar_init(rde0 + 8 * b, 8 * 32);
     }
     for (int b = 0; b < TQ; ++b) {
       mbar_init(tqf0 + 8 * b, 1);
-      mbar_init(tqe0 + 8 * b, TQ_READERS);   // leader's copy used
+      mbar_init(tqe0 + 8 * b, D_TQ_READERS);   // leader's copy used
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -326,19 +333,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned tmem_base = *tmem_slot;
 
   const int num_pp = (a.num_nt + 1) / 2;          // 256-SNP tile pairs
-  const int total = a.num_rb * num_pp;
+  const int num_rbp = a.num_rb / 2;               // row-block pairs (num_rb is a multiple of 4)
+  const int total = num_rbp * num_pp;
   const bool partials = a.P != nullptr;
   const unsigned peer_tq = mapa_peer(smem_u32(tq));
-  // r-th tile of this cluster (-1: none left).  The leader's producer takes tiles from the global
-  // counter and posts them to both CTAs' queues; every other role reads its CTA's copy.
   auto tile_at = [&](int r) -> int {
     const int slot = r % TQ;
     mbar_wait_acq_cluster(tqf0 + 8 * slot, (r / TQ) & 1);
     return *reinterpret_cast<volatile int*>(tq + slot);
   };
-  auto tile_read = [&](int r) {   // this reader is done with queue slot r % TQ
-    mbar_arrive_cluster((tqe0 + 8 * (r % TQ)) & PEER_MASK);
-  };
+  auto tile_read = [&](int r) { mbar_arrive_cluster((tqe0 + 8 * (r % TQ)) & PEER_MASK); };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -355,52 +359,51 @@ __global__ void __launch_bounds__(THREADS, 1)
           st_cluster_s32(peer_tq + 4 * slot, t);
           mbar_arrive(tqf0 + 8 * slot);
           mbar_arrive_remote_release(mapa_peer(tqf0 + 8 * slot));
-          if (t < 0) {   // the other epilogue group reads the next slot: end it there too
-            const int s2 = (r + 1) % TQ;
-            mbar_wait(tqe0 + 8 * s2, (((r + 1) / TQ) & 1) ^ 1);
-            tq[s2] = -1;
-            st_cluster_s32(peer_tq + 4 * s2, -1);
-            mbar_arrive(tqf0 + 8 * s2);
-            mbar_arrive_remote_release(mapa_peer(tqf0 + 8 * s2));
-          }
         } else {
           t = tile_at(r);
           tile_read(r);
         }
         if (t < 0) break;
-        int rb, pp;
-        tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
+        int rbp, pp;
+        tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
         const int nt = 2 * pp + (int)rank;
-        const int nk = (rb + 4) / 4;
-        {   // this CTA's row data for the tile (its own barrier): e_i, XLbar rows, ybar rows
-          const int slot = r % RD_SLOTS;
-          mbar_wait(rde0 + 8 * slot, ((r / RD_SLOTS) & 1) ^ 1);
-          const unsigned rbar = rdf0 + 8 * slot, dst = rbase + slot * RD_BYTES;
-          const int row0 = rb * TR;
-          mbar_expect_tx(rbar, 2 * TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0));
-          bulk_g2s(dst, a.expo + row0, TR * 4, rbar);
-          bulk_g2s(dst + TR * 4, a.expo + a.num_rb * TR + row0, TR * 4, rbar);
-          if (partials) {
-            for (int c = 0; c < a.q; ++c)
-              bulk_g2s(dst + RD_COLS_OFF + c * TR * 8, a.XL + c * a.ldxl + row0, TR * 8, rbar);
-            bulk_g2s(dst + RD_COLS_OFF + a.q * TR * 8, a.y + row0, TR * 8, rbar);
+        const int rb0 = 2 * rbp;
+        const int nk = (rb0 + 4) / 4;
+        {   // row data of both row blocks (this CTA's own barrier)
+          const int slot = r % D_RD_SLOTS;
+          mbar_wait(rde0 + 8 * slot, ((r / D_RD_SLOTS) & 1) ^ 1);
+          const unsigned rbar = rdf0 + 8 * slot;
+          mbar_expect_tx(rbar, 2 * (2 * TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0)));
+          for (int h = 0; h < 2; ++h) {
+            const unsigned dst = rbase + (2 * slot + h) * RD_BYTES;
+            const int row0 = (rb0 + h) * TR;
+            bulk_g2s(dst, a.expo + row0, TR * 4, rbar);
+            bulk_g2s(dst + TR * 4, a.expo + a.num_rb * TR + row0, TR * 4, rbar);
+            if (partials) {
+              for (int c = 0; c < a.q; ++c)
+                bulk_g2s(dst + RD_COLS_OFF + c * TR * 8, a.XL + c * a.ldxl + row0, TR * 8, rbar);
+              bulk_g2s(dst + RD_COLS_OFF + a.q * TR * 8, a.y + row0, TR * 8, rbar);
+            }
           }
         }
+        const int tile0 = (rb0 >> 2) * ((rb0 >> 2) + 1) / 2;
         for (int kt = 0; kt < nk; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const unsigned fb = full0 + 8 * stage;
-          if (leader) mbar_expect_tx(fb, 2 * P_STAGE_BYTES);
-          const unsigned dA = sbase + stage * P_STAGE_BYTES;
+          if (leader) mbar_expect_tx(fb, 2 * D_STAGE_BYTES);
+          const unsigned dA = sbase + stage * D_STAGE_BYTES;
           tma_2d_pair(dA, &tmA, fb & PEER_MASK, kt * TK, nt * TM);
-          // this CTA's 112 slice rows: CTA0 = slices 0-2 + rows 0-15 of slice 3,
-          // CTA1 = rows 16-31 of slice 3 + slices 4-6 (accumulator column = 32 s + row)
-          const int tile = (rb >> 2) * ((rb >> 2) + 1) / 2 + kt, r0 = (rb & 3) * TR;
-          if (rank == 0) {
-            tma_4d_pair(dA + A_BYTES, &tmB3, fb & PEER_MASK, 0, r0, 0, tile);
-            tma_4d_pair(dA + A_BYTES + 3 * TR * TK, &tmB1, fb & PEER_MASK, 0, r0, 3, tile);
-          } else {
-            tma_4d_pair(dA + A_BYTES, &tmB1, fb & PEER_MASK, 0, r0 + TR / 2, 3, tile);
-            tma_4d_pair(dA + A_BYTES + (TR / 2) * TK, &tmB3, fb & PEER_MASK, 0, r0, 4, tile);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {   // this CTA's 112 slice rows of row block rb0 + h
+            const unsigned dB = dA + A_BYTES + h * P_B_BYTES;
+            const int r0 = ((rb0 + h) & 3) * TR;
+            if (rank == 0) {
+              tma_4d_pair(dB, &tmB3, fb & PEER_MASK, 0, r0, 0, tile0 + kt);
+              tma_4d_pair(dB + 3 * TR * TK, &tmB1, fb & PEER_MASK, 0, r0, 3, tile0 + kt);
+            } else {
+              tma_4d_pair(dB, &tmB1, fb & PEER_MASK, 0, r0 + TR / 2, 3, tile0 + kt);
+              tma_4d_pair(dB + (TR / 2) * TK, &tmB3, fb & PEER_MASK, 0, r0, 4, tile0 + kt);
+            }
           }
           if (++stage == P_STAGES) {
             stage = 0;
@@ -413,55 +416,57 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0 && leader) {
       int stage = 0;
       unsigned phase = 0;
-      int it = 0;
-      for (int r = 0;; ++r, ++it) {
+      for (int r = 0;; ++r) {
         const int t = tile_at(r);
         tile_read(r);
         if (t < 0) break;
-        int rb, pp;
-        tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
-        const int nk = (rb + 4) / 4;
-        const int ab = it & 1;
-        mbar_wait(acce0 + 8 * ab, ((it >> 1) & 1) ^ 1);
-        fence_after();
-        const unsigned d_tmem = tmem_base + ab * ACC_COLS;
+        int rbp, pp;
+        tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
+        const int rb0 = 2 * rbp;
+        const int nk = (rb0 + 4) / 4;
         for (int kt = 0; kt < nk; ++kt) {
           mbar_wait(full0 + 8 * stage, phase);
           fence_after();
-          const unsigned sa = sbase + stage * P_STAGE_BYTES;
-          const unsigned long long da = smem_desc(sa), db = smem_desc(sa + A_BYTES);
-          // the diagonal k tile holds nonzero slices only up to the row block's last row:
-          // k < 32 (rb + 1), i.e. its first (rb & 3) + 1 MMAs of K = 32
-          const int kk_end = (kt == nk - 1) ? (rb & 3) + 1 : TK / 32;
+          const unsigned sa = sbase + stage * D_STAGE_BYTES;
+          const unsigned long long da = smem_desc(sa);
 #pragma unroll
-          for (int kk = 0; kk < TK / 32; ++kk)
-            if (kk < kk_end)
-              mma_i8_pair(d_tmem, da + 2 * kk, db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+          for (int h = 0; h < 2; ++h) {
+            if (kt == 0) {   // this half's accumulator drained by the previous tile's group h
+              mbar_wait(acce0 + 8 * h, (r & 1) ^ 1);
+              fence_after();
+            }
+            const unsigned long long db = smem_desc(sa + A_BYTES + h * P_B_BYTES);
+            // the diagonal k tile: nonzero slices only for k < 32 (rb + 1)
+            const int kk_end = (kt == nk - 1) ? ((rb0 + h) & 3) + 1 : TK / 32;
+#pragma unroll
+            for (int kk = 0; kk < TK / 32; ++kk)
+              if (kk < kk_end)
+                mma_i8_pair(tmem_base + h * ACC_COLS, da + 2 * kk, db + 2 * kk,
+                            (kt > 0 || kk > 0) ? 1u : 0u);
+          }
           mma_commit_pair(empty0 + 8 * stage);
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_pair(accf0 + 8 * ab);
+        mma_commit_pair(accf);
       }
     }
   } else {
-    const int group = (warp - 2) >> 2;         // group g drains accumulator buffer g
+    const int group = (warp - 2) >> 2;         // group g drains row block 2 rbp + g
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;
-    for (int r = group;; r += 2) {
-      const int it = r;
+    for (int r = 0;; ++r) {
       const int t = tile_at(r);
       __syncwarp();
       if (lane == 0) tile_read(r);
       if (t < 0) break;
-      int rb, pp;
-      tile_coords(t, a.num_rb, num_pp, a.grp_pp, rb, pp);
+      int rbp, pp;
+      tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
+      const int rb = 2 * rbp + group;
       const int nt = 2 * pp + (int)rank;
       const int col_g = nt * TM + m, row0_g = rb * TR;
-      // this SNP's dosages on the tile's rows (the head term; rows >= n are zero), loaded before
-      // the accumulator wait so their latency hides behind it
       int gq[TR / 4];
       {
         const signed char* gp = a.G + (long long)(col_g < a.N ? col_g : 0) * a.ldg + row0_g;
@@ -483,21 +488,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      const int ab = it & 1;
-      mbar_wait(accf0 + 8 * ab, (it >> 1) & 1);
+      mbar_wait(accf, r & 1);
       fence_after();
-      const int slot = it % RD_SLOTS;
-      const unsigned char* rd = rdata + slot * RD_BYTES;
+      const int slot = r % D_RD_SLOTS;
+      const unsigned char* rd = rdata + (2 * slot + group) * RD_BYTES;
       const int* ex = reinterpret_cast<const int*>(rd);
       const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
-      // X = RN(2^(e'_i - 49) T), T = h_i g_i 2^49 + sum_s C_s 2^(7 (6 - s)): the two exact int64
-      // halves hi = h g 2^21 + C_0 2^14 + C_1 2^7 + C_2 and lo = C_3 2^21 + ... + C_6 (both
-      // < 2^53) are converted exactly and combined with ONE rounding (4 FP64 instructions per
-      // element: the FP64 pipe is throttled while the tensor core runs)
-      mbar_wait(rdf0 + 8 * slot, (it / RD_SLOTS) & 1);
+      mbar_wait(rdf0 + 8 * slot, (r / D_RD_SLOTS) & 1);
       const int* hd = reinterpret_cast<const int*>(rd + TR * 4);
       double acc[TR];
-      const unsigned taddr = tmem_base + ab * ACC_COLS + ((unsigned)(quarter * 32) << 16);
+      const unsigned taddr = tmem_base + group * ACC_COLS + ((unsigned)(quarter * 32) << 16);
 #pragma unroll
       for (int q4 = 0; q4 < TR / 8; ++q4) {
         int v[S][8];
@@ -515,12 +515,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       fence_before();
-      mbar_arrive_cluster((acce0 + 8 * ab) & PEER_MASK);
-      const int col = nt * TM + m;
-      const int row0 = rb * TR;
+      mbar_arrive_cluster((acce0 + 8 * group) & PEER_MASK);
+      const int col = col_g;
       if (col < a.N) {
         if (a.X != nullptr) {
-          double* dst = a.X + (long long)col * a.ldx + row0;
+          double* dst = a.X + (long long)col * a.ldx + row0_g;
 #pragma unroll
           for (int i = 0; i < TR; i += 2)
             *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
@@ -977,7 +976,7 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.tile_counter = tile_counter(s);
   if (a.tile_counter == nullptr) return GG_ECUDA;
   {
-    const int pairs = a.num_rb * ((a.num_nt + 1) / 2);
+    const int pairs = (a.num_rb / 2) * ((a.num_nt + 1) / 2);   // tiles
     int clusters = sms() / 2;
     if (const char* cap = std::getenv("GG_I8_MAX_PAIRS")) {   // tuning / what-if knob
       const int c = std::atoi(cap);
@@ -998,9 +997,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     const int ngroups = (num_pp + grp - 1) / grp;
     a.grp_pp = (num_pp + ngroups - 1) / ngroups;                // equal-width groups
     a.rd_bytes = rd_bytes(q, P != nullptr);
-    const bool seven = p_smem_bytes(7, a.rd_bytes) <= (size_t)smem_optin();
-    auto kern = seven ? trsm_i8_pair_kernel<7> : trsm_i8_pair_kernel<6>;
-    const size_t smem = p_smem_bytes(seven ? 7 : 6, a.rd_bytes);
+    // 5 stages of 44 KB when the row data is small (q <= 3), else 4
+    const bool five = d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
+    auto kern = five ? trsm_i8_dual_kernel<5> : trsm_i8_dual_kernel<4>;
+    const size_t smem = d_smem_bytes(five ? 5 : 4, a.rd_bytes);
     GG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     cudaLaunchConfig_t cfg = {};

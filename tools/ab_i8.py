@@ -14,7 +14,7 @@ from paper_1304_2272_b200 import _capi, datagen, kernel  # noqa: E402
 from paper_1304_2272_b200._capi import ptr  # noqa: E402
 
 n, cnt = int(os.environ.get("GG_AB_N", "10000")), 8192
-spec = datagen.BaselineSpec(n=n, m=cnt, p=4)
+spec = datagen.BaselineSpec(n=n, m=cnt, p=int(os.environ.get("GG_AB_P", "4")))
 ctx = kernel.gls_prepare(datagen.kinship_covariance_device(spec), *datagen.covariates_host(spec))
 d = ctx._dev
 n16 = -(-n // 16) * 16

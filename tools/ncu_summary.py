@@ -112,8 +112,8 @@ def main():
         if trsm:
             k = trsm[0]
             rd, wr = k.get("dram__bytes_read.sum"), k.get("dram__bytes_write.sum")
-            if args.engine == "i8":   # int8 dosages in, S=8 int8 slices of the triangle, partials out
-                algo = args.n * args.cnt + 8 * args.n * args.n / 2 + 8.0 * 5 * args.cnt * args.n / 32
+            if args.engine == "i8":   # int8 dosages in, 7 int8 slices of the triangle, partials out
+                algo = args.n * args.cnt + 7 * args.n * args.n / 2 + 8.0 * 5 * args.cnt * args.n / 32
             else:                     # FP64 block in, packed FP64 triangle, FP64 Xbar out
                 algo = 8.0 * (args.n * args.cnt * 2 + args.n * args.n / 2)
             summ = {
