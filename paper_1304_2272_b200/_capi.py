@@ -55,6 +55,9 @@ SIGNATURES = {
     "gg_gls_reduce_solve_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
+    "gg_gemm_ozaki_workspace_bytes": (_sz, [_i, _i, _i, _i]),
+    "gg_gemm_ozaki_f64": (_i, [_i, _i, _i, _vp, _ll, _ll, _vp, _ll, _ll, _vp, _ll, _d, _d, _i,
+                               _vp, _sz, _vp]),
     "gg_widen_i8_f64": (_i, [_i, _i, _vp, _ll, _vp, _i, _vp]),
     "gg_gls_dots_f64": (_i, [_i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp]),
     "gg_small_spd_solve_f64": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

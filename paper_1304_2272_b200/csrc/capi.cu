@@ -242,6 +242,24 @@ int gg_transpose_f64(int np, const double* A, int lda, double* T, int ldt, void*
   return gg::transpose_square_run(np, A, lda, T, ldt, as_stream(stream));
 }
 
+size_t gg_gemm_ozaki_workspace_bytes(int m, int ncols, int k, int b_is_a) {
+  if (m < 1 || ncols < 1 || k < 1) return 0;
+  return gg::ozaki_ws_bytes(m, ncols, k, b_is_a != 0);
+}
+
+int gg_gemm_ozaki_f64(int m, int ncols, int k, const double* A, long long a_rs, long long a_cs,
+                      const double* B, long long b_rs, long long b_cs, double* C, long long ldc,
+                      double alpha, double beta, int flags, void* work, size_t work_bytes,
+                      void* stream) {
+  if (A == nullptr || C == nullptr || m < 0 || ncols < 0 || k < 0 || ldc < m ||
+      (flags & ~7) != 0) {
+    gg::set_error("gemm_ozaki: bad arguments");
+    return GG_EARG;
+  }
+  return gg::ozaki_gemm_run(m, ncols, k, A, a_rs, a_cs, B, b_rs, b_cs, C, ldc, alpha, beta, flags,
+                            work, work_bytes, nullptr, as_stream(stream));
+}
+
 int gg_dgemm_f64(int m, int ncols, int k, double alpha, const double* A, int lda, const double* B,
                  int ldb, int trans_b, double beta, double* C, int ldc, void* stream) {
   if (A == nullptr || B == nullptr || C == nullptr) {

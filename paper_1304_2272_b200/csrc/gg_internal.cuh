@@ -48,6 +48,16 @@ struct GemmArgs {
 // Launch C = alpha*A*op(B) + beta*C.  trans_b selects op(B) = B^T (B stored N x K).
 int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s);
 
+// ---- FP64 GEMM on the int8 tensor cores, Ozaki scheme (ozaki_i8.cu) -------------------------
+// C = beta C + alpha A~ B~^T, A~(i,k) = A[i a_rs + k a_cs] (M x K), B~(j,k) = B[j b_rs + k b_cs]
+// (N x K; B == nullptr: B~ = A~).  flags: GEMM_A_LOWER (A~(i,k) = 0 for k > i), GEMM_B_LOWER
+// (B~(j,k) = 0 for k < j), GEMM_C_LOWER (tiles strictly above the diagonal skipped).
+size_t ozaki_ws_bytes(int M, int N, int K, bool b_is_a);
+int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long long a_cs,
+                   const double* B, long long b_rs, long long b_cs, double* C, long long ldc,
+                   double alpha, double beta, int flags, void* ws, size_t ws_bytes,
+                   const int* abort_flag, cudaStream_t s);
+
 // ---- dense factorisation (potrf_f64.cu) ----------------------------------------------
 int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv, int ldp,
               void* work,

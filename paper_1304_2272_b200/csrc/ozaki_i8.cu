@@ -1,0 +1,579 @@
+// FP64 GEMM on the int8 tensor cores (Ozaki scheme): C = beta C + alpha A B^T for FP64 operands,
+// used for the large updates of the Cholesky factorisation (potrf_f64.cu).
+//
+// FP64 has no tcgen05 kind on sm_100a; the DMMA path peaks at 37 TFLOP/s while the int8 tensor
+// cores do 4.4 POPS.  Each row i of A (and row j of B) is split error-free into 8 int8 slices
+// below its own power of two:
+//     A[i,k] = 2^e_i sum_{s=0..7} a_s[i,k] 2^(-7 (s+1)),   |a_s| <= 127
+// (slices 0-6 truncate with exact remainders, the last rounds to nearest), so
+//     (A B^T)[i,j] = 2^(e_i + f_j) sum_d D_d[i,j] 2^(-7 (d+2)),   D_d = sum_{s+t=d} a_s b_t^T.
+// The 36 slice products with s + t <= 7 are issued as tcgen05.mma.kind::i8 into 8 int32 TMEM
+// accumulators (one per diagonal d, 64 columns each = all 512 columns); every D_d is exact for
+// K <= 16384 ((d+1) 127^2 K < 2^31; the host splits K into launches of <= 8192).  The dropped terms (s+t >= 8)
+// and the operand residuals are below 2^-56 of 2^(e_i+f_j) per product term -- the same order as
+// FP64 rounding.  The epilogue forms the exact int64 halves hi = D_0..D_3, lo = D_4..D_7 (base
+// 2^7) and rounds once: r = fma(hi, 2^(E-35), lo 2^(E-63)); then C = beta C + alpha r.
+//
+// Kernel (persistent, one CTA per SM, 6 warps): warp 0 TMA producer (per 32-k stage: the 8
+// slices of a 128-row A tile and of a 64-row B tile, 48 KB, SWIZZLE_32B, 4-stage ring), warp 1
+// MMA issuer (one lane, M = 128 x N = 64..256 x K = 32, 12 MMAs covering the 36 slice products
+// per stage), warps 2-5 epilogue
+// (TMEM lane = tile row; releases TMEM once the tile is in registers, then updates C).
+// Results are bitwise deterministic (exact integer accumulation, fixed rounding).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <climits>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "gg_internal.cuh"
+
+namespace gg {
+namespace {
+
+constexpr int OZ_S = 8;                    // slices per operand
+constexpr int OZ_BM = 128;                 // tile rows (MMA M)
+constexpr int OZ_BN = 64;                  // tile columns (MMA N, one accumulator per diagonal)
+constexpr int OZ_KC = 32;                  // k per stage (one int8 MMA K, a 32-byte swizzle row)
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_KC;   // 32 KB
+constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_KC;   // 16 KB
+constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
+constexpr int OZ_THREADS = 6 * 32;
+constexpr size_t OZ_SMEM = size_t(OZ_STAGES) * OZ_STAGE_BYTES + 1024 + 256;
+constexpr int OZ_KMAX = 8192;              // k per launch: exact int32 diagonals need
+                                           // 8 * 127^2 * K < 2^31 (K <= 16384); 8192 bounds the
+                                           // slice workspace
+constexpr unsigned OZ_IDESC_BASE = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OZ_BM >> 4) << 24);
+
+struct OzArgs {
+  int M, N, kb, ke;        // rows of A / C, rows of B / columns of C, k range [kb, ke)
+  int koff;                // global k of this launch's k = 0 (triangular operands, k chunks)
+  const int* exA;          // row exponents of A (M) and B (N)
+  const int* exB;
+  double* C;
+  long long ldc;
+  double alpha, beta;
+  int flags;               // GEMM_A_LOWER / GEMM_B_LOWER / GEMM_C_LOWER
+  int gm;                  // row tiles per tile group (oz_tile)
+  const int* abort_flag;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "OZW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra OZW_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+// K-major, 32-byte-swizzled descriptor: rows of 32 B, 8-row groups 256 B apart (SBO), version 1,
+// layout SWIZZLE_32B (6)
+__device__ __forceinline__ unsigned long long desc32(unsigned saddr) {
+  return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (16ull << 32) |
+         (1ull << 46) | (6ull << 61);
+}
+__device__ __forceinline__ void tma_3d(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// D[128 x 64 nb] (+)= A . B^T for nb consecutive B slices stacked along N (N = 64 nb <= 256)
+__device__ __forceinline__ void mma_i8(unsigned d_tmem, unsigned long long a, unsigned long long b,
+                                       int nb, unsigned accumulate) {
+  const unsigned idesc = OZ_IDESC_BASE | ((unsigned)(OZ_BN * nb >> 3) << 17);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(unsigned bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ double pow2(int e) {   // 2^e, |e| < 1022
+  return __longlong_as_double((long long)(1023 + e) << 52);
+}
+// 8 columns x the 8 diagonals of one warp quarter: v[d][c]
+__device__ __forceinline__ void tmem_ld_diag8(unsigned taddr, int (&v)[OZ_S][8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%65];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%66];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%67];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%68];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%69];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%70];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%56,%57,%58,%59,%60,%61,%62,%63}, [%71];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]),
+        "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]), "=r"(v[1][7]),
+        "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]), "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]),
+        "=r"(v[3][0]), "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]), "=r"(v[3][6]), "=r"(v[3][7]),
+        "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]), "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
+        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]), "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]),
+        "=r"(v[6][0]), "=r"(v[6][1]), "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]), "=r"(v[6][7]),
+        "=r"(v[7][0]), "=r"(v[7][1]), "=r"(v[7][2]), "=r"(v[7][3]), "=r"(v[7][4]), "=r"(v[7][5]), "=r"(v[7][6]), "=r"(v[7][7])
+      : "r"(taddr + 0 * OZ_BN), "r"(taddr + 1 * OZ_BN), "r"(taddr + 2 * OZ_BN), "r"(taddr + 3 * OZ_BN),
+        "r"(taddr + 4 * OZ_BN), "r"(taddr + 5 * OZ_BN), "r"(taddr + 6 * OZ_BN), "r"(taddr + 7 * OZ_BN)
+      : "memory");
+}
+
+// tile t -> (mt, nt, k range); false when the tile is skipped (strictly above the diagonal of a
+// lower C).  Tiles are taken in groups of a.gm row tiles swept column by column, so the
+// concurrently running tiles share ~gm A row panels and ~148/gm B row panels (L2 reuse);
+// triangular A: heavy (last) row tiles first.
+// A group's column range: all num_nt, or for a lower C up to the diagonal of its last row tile.
+__device__ __forceinline__ int oz_group_nt(const OzArgs& a, int g, int num_mt, int num_nt) {
+  if (!(a.flags & GEMM_C_LOWER)) return num_nt;
+  const int lo = g * a.gm, hi = min(num_mt, lo + a.gm) - 1;
+  const int mt_max = (a.flags & GEMM_A_LOWER) ? num_mt - 1 - lo : hi;
+  return min(num_nt, 2 * mt_max + 2);   // n0 < m0 + 128
+}
+// number of tile indices (the grid-stride loops run over [0, oz_total))
+__device__ __forceinline__ int oz_total(const OzArgs& a, int num_mt, int num_nt) {
+  int tot = 0;
+  for (int g = 0; g * a.gm < num_mt; ++g)
+    tot += min(a.gm, num_mt - g * a.gm) * oz_group_nt(a, g, num_mt, num_nt);
+  return tot;
+}
+__device__ __forceinline__ bool oz_tile(const OzArgs& a, int t, int num_mt, int num_nt, int& mt,
+                                        int& nt, int& kb, int& ke) {
+  int g = 0, gm = 0, gn = 0;
+  for (;; ++g) {   // the group holding index t (a few dozen groups at most)
+    gm = min(a.gm, num_mt - g * a.gm);   // the last group may be shorter
+    gn = oz_group_nt(a, g, num_mt, num_nt);
+    if (t < gm * gn) break;
+    t -= gm * gn;
+  }
+  nt = t / gm;
+  const int lin = g * a.gm + t % gm;
+  mt = (a.flags & GEMM_A_LOWER) ? num_mt - 1 - lin : lin;
+  const int m0 = mt * OZ_BM, n0 = nt * OZ_BN;
+  if ((a.flags & GEMM_C_LOWER) && n0 >= m0 + OZ_BM) return false;
+  kb = a.kb;
+  ke = a.ke;
+  if (a.flags & GEMM_A_LOWER) ke = min(ke, m0 + OZ_BM - a.koff);   // A(i, k) = 0 for k > i
+  if (a.flags & GEMM_B_LOWER) kb = max(kb, n0 - a.koff);           // B(j, k) = 0 for k < j
+  return true;
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      OzArgs a) {
+  if (a.abort_flag != nullptr && *a.abort_flag != 0) return;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(smem + OZ_STAGES * OZ_STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * OZ_STAGES + 2);
+  const unsigned sbase = smem_u32(smem);
+  const unsigned full0 = smem_u32(bars), empty0 = full0 + 8 * OZ_STAGES;
+  const unsigned accf = empty0 + 8 * OZ_STAGES, acce = accf + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accf, 1);
+    mbar_init(acce, 4 * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const unsigned tmem_base = *tmem_slot;
+  const int num_mt = (a.M + OZ_BM - 1) / OZ_BM, num_nt = (a.N + OZ_BN - 1) / OZ_BN;
+  const int total = oz_total(a, num_mt, num_nt);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int mt, nt, kb, ke;
+        if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
+        for (int k = kb; k < ke; k += OZ_KC) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const unsigned fb = full0 + 8 * stage, dA = sbase + stage * OZ_STAGE_BYTES;
+          mbar_expect_tx(fb, OZ_STAGE_BYTES);
+          tma_3d(dA, &tmA, fb, k, mt * OZ_BM, 0);
+          tma_3d(dA + OZ_A_BYTES, &tmB, fb, k, nt * OZ_BN, 0);
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int mt, nt, kb, ke;
+        if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
+        if (ke <= kb) continue;
+        mbar_wait(acce, (it & 1) ^ 1);   // the epilogue has the previous tile in registers
+        fence_after();
+        for (int k = kb; k < ke; k += OZ_KC) {
+          mbar_wait(full0 + 8 * stage, phase);
+          fence_after();
+          const unsigned sA = sbase + stage * OZ_STAGE_BYTES, sB = sA + OZ_A_BYTES;
+          // A slice s times B slices u = 0 .. 7-s: the B slices sit consecutively along N, and
+          // product (s, u) belongs to diagonal s + u at TMEM column 64 (s + u), so one MMA covers
+          // up to 4 of them (N = 256): 12 MMAs per stage instead of 36, so the tensor core reads
+          // each A slice from shared memory once or twice rather than 8 - s times.  s = 0 opens
+          // every diagonal.
+#pragma unroll
+          for (int s = 0; s < OZ_S; ++s) {
+            const unsigned long long da = desc32(sA + s * (OZ_BM * OZ_KC));
+#pragma unroll
+            for (int u = 0; u < OZ_S - s; u += 4) {
+              const int nb = (OZ_S - s - u) < 4 ? (OZ_S - s - u) : 4;
+              mma_i8(tmem_base + (s + u) * OZ_BN, da, desc32(sB + u * (OZ_BN * OZ_KC)), nb,
+                     (k > kb || s > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(empty0 + 8 * stage);
+          if (++stage == OZ_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(accf);
+        ++it;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;            // TMEM lanes 32 quarter .. +31
+    const int row_l = quarter * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int mt, nt, kb, ke;
+      if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
+      const int row = mt * OZ_BM + row_l, n0 = nt * OZ_BN;
+      double r[OZ_BN];
+      if (ke > kb) {
+        mbar_wait(accf, it & 1);
+        fence_after();
+        const int ea = row < a.M ? a.exA[row] : 0;
+        const unsigned taddr = tmem_base + ((unsigned)(quarter * 32) << 16);
+#pragma unroll
+        for (int c8 = 0; c8 < OZ_BN / 8; ++c8) {
+          int v[OZ_S][8];
+          tmem_ld_diag8(taddr + c8 * 8, v);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int col = n0 + c8 * 8 + c;
+            const int e = ea + (col < a.N ? __ldg(a.exB + col) : 0);
+            const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
+                                 v[3][c];
+            const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
+                                 v[7][c];
+            r[c8 * 8 + c] = fma((double)hi, pow2(e - 35), (double)lo * pow2(e - 63));
+          }
+        }
+        fence_before();
+        mbar_arrive(acce);
+        ++it;
+      } else {
+#pragma unroll
+        for (int c = 0; c < OZ_BN; ++c) r[c] = 0.0;
+      }
+      if (row < a.M) {   // C = beta C + alpha r in chunks of 16 columns, next chunk's loads in flight
+        constexpr int CH = 16;
+        double* cbase = a.C + (long long)n0 * a.ldc + row;
+        const int ncol = min(OZ_BN, a.N - n0);
+        const bool rd = a.beta != 0.0;
+        double cv[CH], cn[CH];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) cv[c] = (rd && c < ncol) ? cbase[(long long)c * a.ldc] : 0.0;
+#pragma unroll
+        for (int ch = 0; ch < OZ_BN / CH; ++ch) {
+          if (ch + 1 < OZ_BN / CH) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              const int cc = (ch + 1) * CH + c;
+              cn[c] = (rd && cc < ncol) ? cbase[(long long)cc * a.ldc] : 0.0;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int cc = ch * CH + c;
+            if (cc < ncol)
+              cbase[(long long)cc * a.ldc] = rd ? fma(a.alpha, r[cc], a.beta * cv[c]) : a.alpha * r[cc];
+          }
+#pragma unroll
+          for (int c = 0; c < CH; ++c) cv[c] = cn[c];
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
+// ---- slicing -----------------------------------------------------------------------------------
+// X(r, k) = X[r rs + k cs], rows [0, R), k in [0, K).  Tiles of 32 rows x 128 k staged through
+// shared memory with the coalesced thread mapping for whichever stride is 1.
+constexpr int SL_R = 32, SL_K = 128, SL_THREADS = 256;
+
+__device__ __forceinline__ void load_tile(double (*T)[SL_K + 1], const double* X, long long rs,
+                                          long long cs, int R, int K, int r0, int k0) {
+  if (rs <= cs) {   // rows contiguous: lane -> row
+    for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
+      const int r = i % SL_R, k = i / SL_R;
+      T[r][k] = (r0 + r < R && k0 + k < K) ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs]
+                                           : 0.0;
+    }
+  } else {          // k contiguous: lane -> k
+    for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
+      const int k = i % SL_K, r = i / SL_K;
+      T[r][k] = (r0 + r < R && k0 + k < K) ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs]
+                                           : 0.0;
+    }
+  }
+}
+
+// ex[r] = e with max_k |X(r,k)| < 2^e (0 for an all-zero row)
+__global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, const double* X,
+                                                                long long rs, long long cs,
+                                                                int* ex, const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag != 0) return;
+  __shared__ double T[SL_R][SL_K + 1];
+  __shared__ double mx[SL_R][SL_THREADS / SL_R];
+  const int r0 = blockIdx.x * SL_R;
+  const int r = threadIdx.x % SL_R, part = threadIdx.x / SL_R;
+  double m = 0.0;
+  for (int k0 = 0; k0 < K; k0 += SL_K) {
+    __syncthreads();
+    load_tile(T, X, rs, cs, R, K, r0, k0);
+    __syncthreads();
+    for (int k = part; k < SL_K; k += SL_THREADS / SL_R) m = fmax(m, fabs(T[r][k]));
+  }
+  mx[r][part] = m;
+  __syncthreads();
+  if (threadIdx.x < SL_R && r0 + threadIdx.x < R) {
+    double v = 0.0;
+    for (int p = 0; p < SL_THREADS / SL_R; ++p) v = fmax(v, mx[threadIdx.x][p]);
+    int e = 0;
+    if (v > 0.0) frexp(v, &e);
+    ex[r0 + threadIdx.x] = e;
+  }
+}
+
+// Sl[s][r][k] (row stride kp bytes, slice stride kp * R) for k in [0, kp): exact slices below 2^ex[r]
+__global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, const double* X,
+                                                               long long rs, long long cs,
+                                                               const int* ex, signed char* Sl,
+                                                               long long kp, const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag != 0) return;
+  __shared__ double T[SL_R][SL_K + 1];
+  const int r0 = blockIdx.x * SL_R, k0 = blockIdx.y * SL_K;
+  load_tile(T, X, rs, cs, R, K, r0, k0);
+  __syncthreads();
+  const int r = threadIdx.x / 8, kq = (threadIdx.x % 8) * 16;   // 16 consecutive k per thread
+  if (r0 + r >= R || k0 + kq >= kp) return;
+  const int e = ex[r0 + r];
+  unsigned w[OZ_S][4] = {};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double v = ldexp(T[r][kq + j], -e);   // |v| < 1
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) {
+      const double t = v * 128.0;         // exact
+      const double q = (s < OZ_S - 1) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
+      w[s][j / 4] |= ((unsigned)(int)q & 0xffu) << (8 * (j % 4));
+      v = t - q;
+    }
+  }
+  const long long off = (long long)(r0 + r) * kp + k0 + kq;
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s)
+    *reinterpret_cast<uint4*>(Sl + (long long)s * kp * R + off) =
+        make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_oz() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int encode_slices(CUtensorMap* map, const signed char* Sl, int R, int K, long long kp, int box_rows) {
+  auto fn = encode_fn_oz();
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* v = getenv("GG_OZ_PROMO"))   // tuning knob: 0 none, 1 64B, 2 128B, 3 256B
+    promo = (CUtensorMapL2promotion)atoi(v);
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return GG_ECUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)R, (cuuint64_t)OZ_S};
+  cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)kp * R};
+  cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_S};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(Sl), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                  promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (ozaki slices) failed (code " + std::to_string((int)r) + ")");
+    return GG_ECUDA;
+  }
+  return GG_OK;
+}
+
+inline long long oz_kp(int K) { return ((long long)(K < OZ_KMAX ? K : OZ_KMAX) + 15) / 16 * 16; }
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+inline size_t oz_operand_bytes(int R, int K) {
+  return align256((size_t)OZ_S * R * oz_kp(K)) + align256((size_t)R * sizeof(int));
+}
+
+int sms_oz() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int slice_operand(int R, int Kc, const double* X, long long rs, long long cs, signed char* Sl,
+                  int* ex, long long kp, const int* abort_flag, cudaStream_t s) {
+  oz_rowexp_kernel<<<(R + SL_R - 1) / SL_R, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, abort_flag);
+  GG_LAUNCH_CHECK("oz_rowexp_kernel");
+  dim3 g((R + SL_R - 1) / SL_R, (unsigned)((kp + SL_K - 1) / SL_K));
+  oz_slice_kernel<<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, abort_flag);
+  GG_LAUNCH_CHECK("oz_slice_kernel");
+  return GG_OK;
+}
+
+}  // namespace
+
+size_t ozaki_ws_bytes(int M, int N, int K, bool b_is_a) {
+  return oz_operand_bytes(M, K) + (b_is_a ? 0 : oz_operand_bytes(N, K));
+}
+
+int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long long a_cs,
+                   const double* B, long long b_rs, long long b_cs, double* C, long long ldc,
+                   double alpha, double beta, int flags, void* ws, size_t ws_bytes,
+                   const int* abort_flag, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return GG_OK;
+  const bool same = (B == nullptr);
+  if (same && M != N) {
+    set_error("ozaki_gemm: B = A needs M == N");
+    return GG_EDIM;
+  }
+  if (ws == nullptr || ws_bytes < ozaki_ws_bytes(M, N, K, same)) {
+    set_error("ozaki_gemm: workspace too small");
+    return GG_EARG;
+  }
+  if (K <= 0) {   // C = beta C: the GEMM with an empty k range
+    if (beta == 1.0) return GG_OK;
+    set_error("ozaki_gemm: K == 0 with beta != 1 is not supported");
+    return GG_EARG;
+  }
+  const long long kp = oz_kp(K);
+  signed char* SlA = static_cast<signed char*>(ws);
+  int* exA = reinterpret_cast<int*>(static_cast<char*>(ws) + align256((size_t)OZ_S * M * kp));
+  signed char* SlB = SlA;
+  int* exB = exA;
+  if (!same) {
+    SlB = static_cast<signed char*>(ws) + oz_operand_bytes(M, K);
+    exB = reinterpret_cast<int*>(reinterpret_cast<char*>(SlB) + align256((size_t)OZ_S * N * kp));
+  }
+  GG_CUDA_TRY(cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)OZ_SMEM));
+  // k chunks of at most OZ_KMAX (exact int32 diagonals); beta applies to the first chunk only
+  for (int k0 = 0; k0 < K; k0 += OZ_KMAX) {
+    const int Kc = (K - k0 < OZ_KMAX) ? (K - k0) : OZ_KMAX;
+    int rc = slice_operand(M, Kc, A + (long long)k0 * a_cs, a_rs, a_cs, SlA, exA, kp, abort_flag, s);
+    if (rc != GG_OK) return rc;
+    if (!same) {
+      rc = slice_operand(N, Kc, B + (long long)k0 * b_cs, b_rs, b_cs, SlB, exB, kp, abort_flag, s);
+      if (rc != GG_OK) return rc;
+    }
+    CUtensorMap mA, mB;
+    rc = encode_slices(&mA, SlA, M, Kc, kp, OZ_BM);
+    if (rc != GG_OK) return rc;
+    rc = encode_slices(&mB, SlB, N, Kc, kp, OZ_BN);
+    if (rc != GG_OK) return rc;
+    OzArgs a{};
+    a.M = M;
+    a.N = N;
+    // triangular operands: k is relative to this chunk; the row/column offsets of the triangle
+    // move with the chunk start
+    a.kb = 0;
+    a.ke = Kc;
+    a.koff = k0;
+    a.exA = exA;
+    a.exB = exB;
+    a.C = C;
+    a.ldc = ldc;
+    a.alpha = alpha;
+    a.beta = (k0 == 0) ? beta : 1.0;
+    a.flags = flags;
+    a.gm = 8;
+    if (const char* v = getenv("GG_OZ_GM")) a.gm = atoi(v) > 0 ? atoi(v) : 8;   // tuning knob
+    a.abort_flag = abort_flag;
+    const int tiles = ((M + OZ_BM - 1) / OZ_BM) * ((N + OZ_BN - 1) / OZ_BN);
+    const int grid = tiles < sms_oz() ? tiles : sms_oz();
+    ozaki_gemm_kernel<<<grid, OZ_THREADS, OZ_SMEM, s>>>(mA, mB, a);
+    GG_LAUNCH_CHECK("ozaki_gemm_kernel");
+  }
+  return GG_OK;
+}
+
+}  // namespace gg

@@ -22,6 +22,7 @@ namespace {
 
 constexpr int NB = 128;
 constexpr int OUTER = 8 * NB;   // outer block width of the two-level Cholesky
+constexpr bool OZAKI_DEFAULT = true;
 constexpr int LEAF_THREADS = 384;
 
 struct PotrfHeader {
@@ -260,16 +261,56 @@ int grid_for(long long total) {
   return (int)g;
 }
 
+// The large factorisation GEMMs go to the int8 tensor cores (ozaki_i8.cu) unless
+// GG_FACTOR_OZAKI=0; below OZ_MIN_DIM in any dimension the DMMA kernel is used.
+constexpr int OZ_MIN_DIM = 512;
+bool use_ozaki() {
+  const char* v = getenv("GG_FACTOR_OZAKI");
+  return v == nullptr ? OZAKI_DEFAULT : v[0] != '0';
+}
+bool oz_shape(int M, int N, int K) {
+  return M >= OZ_MIN_DIM && N >= OZ_MIN_DIM && K >= OZ_MIN_DIM;
+}
+
+// Ozaki workspace of the trtri recursion on [lo, hi) (its two GEMMs per level)
+size_t trtri_oz_bytes(int lo, int hi) {
+  const int nblk = (hi - lo) / NB;
+  if (nblk < 2) return 0;
+  const int mid = lo + (nblk / 2) * NB;
+  size_t b = trtri_oz_bytes(lo, mid);
+  const size_t b2 = trtri_oz_bytes(mid, hi);
+  if (b2 > b) b = b2;
+  if (oz_shape(hi - mid, mid - lo, mid - lo)) {
+    const size_t g1 = ozaki_ws_bytes(hi - mid, mid - lo, mid - lo, false);
+    const size_t g2 = ozaki_ws_bytes(hi - mid, mid - lo, hi - mid, false);
+    if (g1 > b) b = g1;
+    if (g2 > b) b = g2;
+  }
+  return b;
+}
+
 // Off-diagonal blocks of Linv for the block range [lo, hi) (diagonal blocks already set).
 int trtri_offdiag(int lo, int hi, const double* L, double* Linv, long long ldp, double* T,
-                  long long ldt, const int* abort_flag, cudaStream_t s) {
+                  long long ldt, void* oz, size_t oz_bytes, const int* abort_flag,
+                  cudaStream_t s) {
   const int nblk = (hi - lo) / NB;
   if (nblk < 2) return GG_OK;
   const int mid = lo + (nblk / 2) * NB;
-  int rc = trtri_offdiag(lo, mid, L, Linv, ldp, T, ldt, abort_flag, s);
+  int rc = trtri_offdiag(lo, mid, L, Linv, ldp, T, ldt, oz, oz_bytes, abort_flag, s);
   if (rc != GG_OK) return rc;
-  rc = trtri_offdiag(mid, hi, L, Linv, ldp, T, ldt, abort_flag, s);
+  rc = trtri_offdiag(mid, hi, L, Linv, ldp, T, ldt, oz, oz_bytes, abort_flag, s);
   if (rc != GG_OK) return rc;
+  if (oz != nullptr && oz_shape(hi - mid, mid - lo, mid - lo)) {
+    // T = L[mid:hi, lo:mid] Linv[lo:mid, lo:mid]  (B~(j,k) = Linv[lo+k, lo+j], zero for k < j)
+    rc = ozaki_gemm_run(hi - mid, mid - lo, mid - lo, L + mid + (long long)lo * ldp, 1, ldp,
+                        Linv + lo + (long long)lo * ldp, ldp, 1, T, ldt, 1.0, 0.0, GEMM_B_LOWER,
+                        oz, oz_bytes, abort_flag, s);
+    if (rc != GG_OK) return rc;
+    // Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] T  (A~ lower triangular, B~(j,k) = T[k, j])
+    return ozaki_gemm_run(hi - mid, mid - lo, hi - mid, Linv + mid + (long long)mid * ldp, 1, ldp,
+                          T, ldt, 1, Linv + mid + (long long)lo * ldp, ldp, -1.0, 0.0,
+                          GEMM_A_LOWER, oz, oz_bytes, abort_flag, s);
+  }
   // T = L[mid:hi, lo:mid] * Linv[lo:mid, lo:mid]      (op(B) lower triangular)
   GemmArgs g1{};
   g1.M = hi - mid; g1.N = mid - lo; g1.K = mid - lo;
@@ -296,21 +337,47 @@ void trtri_T_dims(int np, long long* rows, long long* cols) {
   *rows = (long long)(nblk - nblk / 2) * NB;
 }
 
+
+// Workspace: [header][panel / trtri T][Ozaki slices]
+size_t t_region_bytes(int np) {
+  long long r, c;
+  trtri_T_dims(np, &r, &c);
+  return ((size_t)(r * c) * sizeof(double) + 255) & ~size_t(255);
+}
+size_t oz_region_bytes(int np, bool factor) {
+  size_t b = trtri_oz_bytes(0, np);
+  if (factor) {   // the trailing SYRKs: largest at the first outer block
+    const int rem = np - OUTER;
+    if (rem > 0 && oz_shape(rem, rem, OUTER)) {
+      const size_t sy = ozaki_ws_bytes(rem, rem, OUTER, true);
+      if (sy > b) b = sy;
+    }
+  }
+  return b;
+}
+
 }  // namespace
 
 size_t trtri_ws_bytes(int n) {
   const int np = pad_rows(n);
-  long long r, c;
-  trtri_T_dims(np, &r, &c);
-  return HDR_BYTES + (size_t)(r * c) * sizeof(double);
+  return HDR_BYTES + t_region_bytes(np) + oz_region_bytes(np, false);
 }
 
 size_t potrf_ws_bytes(int n) {
   const int np = pad_rows(n);
-  const size_t panel = (size_t)np * NB * sizeof(double);
-  const size_t tri = trtri_ws_bytes(n) - HDR_BYTES;
-  return HDR_BYTES + (panel > tri ? panel : tri);
+  size_t panel = ((size_t)np * NB * sizeof(double) + 255) & ~size_t(255);
+  const size_t tri = t_region_bytes(np);
+  if (tri > panel) panel = tri;
+  return HDR_BYTES + panel + oz_region_bytes(np, true);
 }
+
+namespace {
+size_t p_region_bytes(int np) {
+  size_t panel = ((size_t)np * NB * sizeof(double) + 255) & ~size_t(255);
+  const size_t tri = t_region_bytes(np);
+  return tri > panel ? tri : panel;
+}
+}  // namespace
 
 int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv, int ldp, void* work,
               int* info_host, cudaStream_t s) {
@@ -328,6 +395,8 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   info_host[1] = 0;
   PotrfHeader* hdr = static_cast<PotrfHeader*>(work);
   double* P = reinterpret_cast<double*>(static_cast<char*>(work) + HDR_BYTES);
+  const size_t oz_bytes = use_ozaki() ? oz_region_bytes(np, true) : 0;
+  void* oz = oz_bytes ? static_cast<char*>(work) + HDR_BYTES + p_region_bytes(np) : nullptr;
   GG_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(int) * 2, s));
   GG_CUDA_TRY(cudaMemsetAsync(&hdr->nonfinite, 0xff, sizeof(unsigned long long), s));
   const long long rs = m_row_major ? ldm : 1, cs = m_row_major ? 1 : ldm;
@@ -396,20 +465,27 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
     if (timing) cudaEventRecord(ev[2], s);
     // trailing SYRK of depth w: A22 -= L21 L21^T, L21 = L[K0+w:, K0:K0+w] (read in place;
     // disjoint from the updated region), lower tiles only
-    GemmArgs upd{};
-    upd.M = rem; upd.N = rem; upd.K = w;
-    upd.A = L + (K0 + w) + (long long)K0 * ldp; upd.lda = ldp;
-    upd.B = L + (K0 + w) + (long long)K0 * ldp; upd.ldb = ldp;
-    upd.C = L + (K0 + w) + (long long)(K0 + w) * ldp; upd.ldc = ldp;
-    upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
-    int rc = launch_dgemm(upd, true, s);
+    int rc;
+    if (oz != nullptr && oz_shape(rem, rem, w)) {
+      rc = ozaki_gemm_run(rem, rem, w, L + (K0 + w) + (long long)K0 * ldp, 1, ldp, nullptr, 0, 0,
+                          L + (K0 + w) + (long long)(K0 + w) * ldp, ldp, -1.0, 1.0, GEMM_C_LOWER,
+                          oz, oz_bytes, &hdr->info, s);
+    } else {
+      GemmArgs upd{};
+      upd.M = rem; upd.N = rem; upd.K = w;
+      upd.A = L + (K0 + w) + (long long)K0 * ldp; upd.lda = ldp;
+      upd.B = L + (K0 + w) + (long long)K0 * ldp; upd.ldb = ldp;
+      upd.C = L + (K0 + w) + (long long)(K0 + w) * ldp; upd.ldc = ldp;
+      upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
+      rc = launch_dgemm(upd, true, s);
+    }
     if (rc != GG_OK) return rc;
     lap(t_upd, ev[2], ev[3]);
   }
   if (timing) cudaEventRecord(ev[0], s);
   long long tr, tc;
   trtri_T_dims(np, &tr, &tc);
-  int rc = trtri_offdiag(0, np, L, Linv, ldp, P, tr > 0 ? tr : 1, &hdr->info, s);
+  int rc = trtri_offdiag(0, np, L, Linv, ldp, P, tr > 0 ? tr : 1, oz, oz_bytes, &hdr->info, s);
   if (rc != GG_OK) return rc;
   lap(t_inv, ev[0], ev[1]);
   if (timing) {
@@ -459,7 +535,9 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
   GG_LAUNCH_CHECK("trtri leaf_kernel");
   long long tr, tc;
   trtri_T_dims(np, &tr, &tc);
-  return trtri_offdiag(0, np, L, Linv, ldp, T, tr > 0 ? tr : 1, nullptr, s);
+  const size_t oz_bytes = use_ozaki() ? oz_region_bytes(np, false) : 0;
+  void* oz = oz_bytes ? static_cast<char*>(work) + HDR_BYTES + t_region_bytes(np) : nullptr;
+  return trtri_offdiag(0, np, L, Linv, ldp, T, tr > 0 ? tr : 1, oz, oz_bytes, nullptr, s);
 }
 
 }  // namespace gg
