@@ -286,6 +286,7 @@ class DeviceOps:
         self.torch = torch
         self.capi = _capi
         self.dev = _capi.device()
+        self._oz_ws = None      # Ozaki GEMM workspace, grown on demand
 
     # -- buffers (column-major (rows x cols) matrix = torch tensor (cols, rows)) --------------
     def empty(self, ncols, nrows):
@@ -324,7 +325,25 @@ class DeviceOps:
         return -1, L, Li
 
     def gemm(self, C, cr, cc, m, n, A, ar, ac, B, br, bc, k, alpha, beta, trans_b):
+        """C[cr:cr+m, cc:cc+n] = beta C + alpha A op(B).  Large updates (every dimension >= 512:
+        the trailing updates of dist_potrf_inv) run on the int8 tensor cores through the
+        Ozaki-scheme GEMM (gg_gemm_ozaki_f64, FP64-GEMM accuracy) unless GG_FACTOR_OZAKI=0;
+        the rest on the DMMA GEMM."""
         capi = self.capi
+        if min(m, n, k) >= 512 and os.environ.get("GG_FACTOR_OZAKI", "1") != "0":
+            lib = capi.lib()
+            need = int(lib.gg_gemm_ozaki_workspace_bytes(m, n, k, 0))
+            if self._oz_ws is None or self._oz_ws.numel() < need:
+                self._oz_ws = None
+                self._oz_ws = self.torch.empty(need, dtype=self.torch.uint8, device=self.dev)
+            ldb = B.shape[1]
+            b_rs, b_cs = (1, ldb) if trans_b else (ldb, 1)
+            rc = lib.gg_gemm_ozaki_f64(m, n, k, self._p(A, ar, ac), 1, A.shape[1],
+                                       self._p(B, br, bc), b_rs, b_cs, self._p(C, cr, cc),
+                                       C.shape[1], alpha, beta, 0, capi.ptr(self._oz_ws),
+                                       self._oz_ws.numel(), capi.stream_handle())
+            capi.check(rc, "gg_gemm_ozaki_f64")
+            return
         rc = capi.lib().gg_dgemm_f64(m, n, k, alpha, self._p(A, ar, ac), A.shape[1],
                                      self._p(B, br, bc), B.shape[1], 1 if trans_b else 0, beta,
                                      self._p(C, cr, cc), C.shape[1], capi.stream_handle())

@@ -9,12 +9,12 @@ from conftest import golden, make_spd, write_golden_dataset
 pytestmark = pytest.mark.gpu
 
 
-def test_device_dist_factor_inverse_pack(gpu):
+@pytest.mark.parametrize("n,nb", [(1000, 256), (2100, 512)])   # nb = 512: Ozaki updates
+def test_device_dist_factor_inverse_pack(gpu, n, nb):
     from scipy.linalg import cholesky, solve_triangular
 
     from paper_1304_2272_b200 import distgrid, kernel
 
-    n, nb = 1000, 256
     M = make_spd(n, 3)
     ops = distgrid.DeviceOps()
     lay = distgrid.BlockCyclic(n, nb, distgrid.grid_create(1), 0)
