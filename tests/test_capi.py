@@ -48,6 +48,10 @@ def test_host_only_entry_points():
     assert lib.gg_version().decode().startswith("gwasgls_b200")
     assert lib.gg_pad(1) == 128 and lib.gg_pad(128) == 128 and lib.gg_pad(129) == 256
     assert lib.gg_potrf_workspace_bytes(10000) >= 8 * 10112 * 128
+    # 8 int8 slices per operand row over the k range, plus the row exponents
+    assert lib.gg_gemm_ozaki_workspace_bytes(1000, 500, 300, 0) >= 8 * 1500 * 304 + 4 * 1500
+    assert lib.gg_gemm_ozaki_workspace_bytes(1000, 1000, 300, 1) < \
+        lib.gg_gemm_ozaki_workspace_bytes(1000, 1000, 300, 0)
     assert lib.gg_trtri_workspace_bytes(10000) > 0
     # exact-int32 bound of the int8 path: 127 up to n = 133,144, then shrinking
     assert lib.gg_i8_value_bound(10000) == 127 and lib.gg_i8_value_bound(133144) == 127 and lib.gg_i8_value_bound(133145) == 126
@@ -117,6 +121,11 @@ def test_argument_validation_without_a_gpu():
         (lib.gg_narrow_f64_i8, (0, 1, V, 1, V, 1, V, V), EARG),
         (lib.gg_small_spd_solve_f64, (1, 0, V, V, V, V, V, V), EARG),
         (lib.gg_gls_dots_f64, (10, 1, 25, V, 128, V, 128, V, V, V, V), EARG),
+        # Ozaki GEMM: null A, then a workspace smaller than gg_gemm_ozaki_workspace_bytes
+        (lib.gg_gemm_ozaki_f64, (64, 64, 64, V, 1, 64, V, 1, 64, V, 64, 1.0, 0.0, 0, V, 0, V),
+         EARG),
+        (lib.gg_gemm_ozaki_f64, (64, 64, 64, 16, 1, 64, 16, 1, 64, 16, 64, 1.0, 0.0, 0, 16, 1,
+                                 V), EARG),
     ]
     for fn, args, want in cases:
         rc = fn(*args)
