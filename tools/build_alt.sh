@@ -6,7 +6,7 @@ d=$(mktemp -d)
 cd "$(dirname "$0")/../paper_1304_2272_b200/csrc"
 for f in *.cu; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC \
-    --expt-relaxed-constexpr -c "$f" -o "$d/${f%.cu}.o" &
+    --expt-relaxed-constexpr $GG_ALT_FLAGS -c "$f" -o "$d/${f%.cu}.o" &
 done
 wait
 mkdir -p ../../tools/alt
