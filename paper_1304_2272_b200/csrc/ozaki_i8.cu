@@ -269,12 +269,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
           for (int s = 0; s < OZ_S; ++s) {
             const unsigned long long da = desc32(sA + s * (OZ_BM * OZ_KC));
-#pragma unroll
-            for (int u = 0; u < OZ_S - s; u += 4) {
-              const int nb = (OZ_S - s - u) < 4 ? (OZ_S - s - u) : 4;
-              mma_i8(tmem_base + (s + u) * OZ_BN, da, desc32(sB + u * (OZ_BN * OZ_KC)), nb,
-                     (k > kb || s > 0) ? 1u : 0u);
-            }
+            // 8 - s products in one or two MMAs, split evenly (N = 64 runs at 62% of the int8
+            // rate on this B200 -- shared-memory bound -- N = 128..256 at 94-100%, tools/i8_peak)
+            const int cnt = OZ_S - s;
+            const int first = cnt > 4 ? (cnt + 1) / 2 : cnt;
+            mma_i8(tmem_base + s * OZ_BN, da, desc32(sB), first, (k > kb || s > 0) ? 1u : 0u);
+            if (cnt > first)
+              mma_i8(tmem_base + (s + first) * OZ_BN, da, desc32(sB + first * (OZ_BN * OZ_KC)),
+                     cnt - first, (k > kb || s > 0) ? 1u : 0u);
           }
           mma_commit(empty0 + 8 * stage);
           if (++stage == OZ_STAGES) {

@@ -3,6 +3,7 @@
 // from fixed shared-memory operands into TMEM, committing to an mbarrier every 64 MMAs.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/i8_peak tools/i8_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
@@ -11,9 +12,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-constexpr unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
-
-__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int* sink) {
+// usage: tools/i8_peak [N ...]  (MMA N per instruction, default 256: tests N granularity)
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int N, int* sink) {
+  const unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (((unsigned)N >> 3) << 17) | ((128u >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ unsigned long long bar;
   __shared__ unsigned tslot;
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int* sink) {
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
   int* sink;
@@ -67,18 +68,21 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int rep = 0; rep < 3; ++rep) {
-    const int iters = rep == 0 ? 10 : 2000;
-    cudaEventRecord(e0);
-    i8_peak_kernel<<<prop.multiProcessorCount, 128, smem>>>(iters, sink);
-    cudaEventRecord(e1);
-    CK(cudaEventSynchronize(e1));
-    CK(cudaGetLastError());
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    const double ops = 2.0 * 128 * 256 * 32 * 64.0 * iters * prop.multiProcessorCount;
-    printf("int8 tcgen05 M128 N256 K32 x %d SMs: %.1f TOPS (%.3f ms)\n", prop.multiProcessorCount,
-           ops / ms / 1e9, ms);
+  for (int a = 0; a < (argc > 1 ? argc - 1 : 1); ++a) {
+    const int N = argc > 1 ? atoi(argv[a + 1]) : 256;
+    for (int rep = 0; rep < 3; ++rep) {
+      const int iters = rep == 0 ? 10 : 2000;
+      cudaEventRecord(e0);
+      i8_peak_kernel<<<prop.multiProcessorCount, 128, smem>>>(iters, N, sink);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      CK(cudaGetLastError());
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double ops = 2.0 * 128 * N * 32 * 64.0 * iters * prop.multiProcessorCount;
+      printf("int8 tcgen05 M128 N%d K32 x %d SMs: %.1f TOPS (%.3f ms)\n", N,
+             prop.multiProcessorCount, ops / ms / 1e9, ms);
+    }
   }
   return 0;
 }
