@@ -194,3 +194,32 @@ def test_config1_full_size_block(mods):
     res_p = P.solve_array(ctx, np.asfortranarray(G[:, perm].astype(float)), m_blk=8192)
     assert np.array_equal(res_p.beta, res.beta[perm])
     torch.cuda.empty_cache()
+
+
+def test_config3_full_size_sample(mods):
+    """BASELINE config 3 at full n = 40,000, p = 8 (M = 0.5 K + 0.5 I): the Ozaki-factorised,
+    int8-swept path against the CPU oracle on a sample of SNPs from an 8,192-SNP block, plus
+    bitwise equality of the int8 and FP64 host inputs on that sample."""
+    import torch
+
+    from oracle import gls_ref as O
+
+    K, P, F, D = mods
+    spec = D.CONFIGS[3]
+    Mt = D.kinship_covariance_device(spec)
+    XL, y = D.covariates_host(spec)
+    ctx = K.gls_prepare(Mt, XL, y)
+    M = Mt.cpu().numpy()
+    del Mt
+    G = D.genotypes_device(spec, 0, 8192).cpu().numpy().T          # n x 8192 int8
+    res = P.solve_array(ctx, np.asfortranarray(G), m_blk=8192)
+    assert np.all(res.ok)
+    sample = np.r_[0:6, 5000:5003, 8189:8192]
+    octx = O.gls_prepare(M, XL, y)                                  # CPU dpotrf at n = 4e4
+    ob, ok = O.gls_solve_block(octx, G[:, sample].astype(float))
+    rel, mism = O.compare(res.beta[sample], ob)
+    assert mism == 0 and rel <= 1e-9, rel
+    res_f = P.solve_array(ctx, np.asfortranarray(G[:, sample].astype(float)), m_blk=8192)
+    assert np.array_equal(res_f.beta, res.beta[sample])
+    del ctx
+    torch.cuda.empty_cache()
