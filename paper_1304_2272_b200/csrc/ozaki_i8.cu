@@ -12,7 +12,7 @@
 // K <= 16384 ((d+1) 127^2 K < 2^31; the host splits K into launches of <= 8192).  The dropped terms (s+t >= 8)
 // and the operand residuals are below 2^-56 of 2^(e_i+f_j) per product term -- the same order as
 // FP64 rounding.  The epilogue forms the exact int64 halves hi = D_0..D_3, lo = D_4..D_7 (base
-// 2^7) and rounds once: r = fma(hi, 2^(E-35), lo 2^(E-63)); then C = beta C + alpha r.
+// 2^7) and rounds once: r = 2^E fma(hi, 2^-35, lo 2^-63); then C = beta C + alpha r.
 //
 // Kernel (persistent, one CTA per SM, 6 warps): warp 0 TMA producer (per 32-k stage: the 8
 // slices of a 128-row A tile and of a 64-row B tile, 48 KB, SWIZZLE_32B, 4-stage ring), warp 1
@@ -308,18 +308,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           tmem_ld_diag8(taddr + c8 * 8, v);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const int col = n0 + c8 * 8 + c;
-            const int e = ea + (col < a.N ? __ldg(a.exB + col) : 0);
             const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
                                  v[3][c];
             const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
                                  v[7][c];
-            r[c8 * 8 + c] = fma((double)hi, pow2(e - 35), (double)lo * pow2(e - 63));
+            r[c8 * 8 + c] = fma((double)hi, 0x1p-35, (double)lo * 0x1p-63);   // the one rounding
           }
         }
         fence_before();
         mbar_arrive(acce);
         ++it;
+        // scale by 2^(e_i + f_j) after the accumulators are released: exact for normal results
+        // (the same bits as rounding at the final scale); ldexp gives the IEEE inf / subnormal
+        // at the ends of the exponent range
+#pragma unroll
+        for (int c = 0; c < OZ_BN; ++c) {
+          const int col = n0 + c;
+          const int e = ea + (col < a.N ? __ldg(a.exB + col) : 0);
+          r[c] = (e > -1000 && e < 1000) ? r[c] * pow2(e) : ldexp(r[c], e);
+        }
       } else {
 #pragma unroll
         for (int c = 0; c < OZ_BN; ++c) r[c] = 0.0;

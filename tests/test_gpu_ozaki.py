@@ -168,3 +168,28 @@ def test_gls_parity_with_ozaki_factor(gpu, monkeypatch):
     ob, ok = O.gls_solve_block(O.gls_prepare(M, XL, y), G)
     rel, mism = O.compare(beta, ob)
     assert mism == 0 and rel <= 1e-11, (rel, mism)
+
+
+def test_ozaki_gemm_extreme_exponents(gpu):
+    """Rows scaled near the ends of the FP64 range: products that overflow give inf, products
+    deep in the subnormal range round like IEEE, normal ones stay accurate."""
+    rng = np.random.default_rng(17)
+    A = rng.standard_normal((130, 96))
+    B = rng.standard_normal((70, 96))
+    A[0] *= 2.0 ** 600
+    B[0] *= 2.0 ** 600                   # (0, 0) overflows
+    A[1] *= 2.0 ** -540
+    B[1] *= 2.0 ** -540                  # (1, 1) ~2^-1080: subnormal
+    A[2] *= 2.0 ** 500
+    B[2] *= 2.0 ** -500                  # (2, 2) normal after huge and tiny scales
+    got = _ozaki(A, B, np.zeros((130, 70)), 1.0, 0.0, 0)
+    with np.errstate(over="ignore", under="ignore", invalid="ignore"):
+        ref = A.astype(np.longdouble) @ B.astype(np.longdouble).T
+    assert np.isinf(got[0, 0])
+    assert abs(got[1, 1] - float(ref[1, 1])) <= 2.0 ** -1074 * 4 + 1e-15 * abs(float(ref[1, 1]))
+    assert abs(got[2, 2] - float(ref[2, 2])) <= 1e-14 * float(np.abs(A[2]) @ np.abs(B[2]))
+    mask = np.ones_like(got, bool)
+    mask[:3, :] = False
+    mask[:, :3] = False
+    with np.errstate(over="ignore", invalid="ignore"):
+        assert float(np.max(np.abs(got - ref.astype(np.float64))[mask])) <= 1e-13
