@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (ke > kb) {
         mbar_wait(accf, it & 1);
         fence_after();
-        const int ea = row < a.M ? a.exA[row] : 0;
+        const int ea = row < a.M ? max(a.exA[row], -4000) : 0;   // EX_NONE: all-zero row
         const unsigned taddr = tmem_base + ((unsigned)(quarter * 32) << 16);
 #pragma unroll
         for (int c8 = 0; c8 < OZ_BN / 8; ++c8) {
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < OZ_BN; ++c) {
           const int col = n0 + c;
-          const int e = ea + (col < a.N ? __ldg(a.exB + col) : 0);
+          const int e = ea + (col < a.N ? max(__ldg(a.exB + col), -4000) : 0);
           r[c] = (e > -1000 && e < 1000) ? r[c] * pow2(e) : ldexp(r[c], e);
         }
       } else {
@@ -373,48 +373,59 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 // X(r, k) = X[r rs + k cs], rows [0, R), k in [0, K).  Tiles of 32 rows x 128 k staged through
 // shared memory with the coalesced thread mapping for whichever stride is 1.
 constexpr int SL_R = 32, SL_K = 128, SL_THREADS = 256;
+constexpr int SL_KP = SL_K + SL_K / 16;   // one pad double per 16: conflict-free 16-k reads
+constexpr int EX_NONE = (int)0x80808080;  // row-exponent sentinel (memset 0x80): no nonzero yet
+__device__ __forceinline__ int tix(int k) { return k + (k >> 4); }
 
-__device__ __forceinline__ void load_tile(double (*T)[SL_K + 1], const double* X, long long rs,
+__device__ __forceinline__ void load_tile(double (*T)[SL_KP], const double* X, long long rs,
                                           long long cs, int R, int K, int r0, int k0) {
   if (rs <= cs) {   // rows contiguous: lane -> row
     for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
       const int r = i % SL_R, k = i / SL_R;
-      T[r][k] = (r0 + r < R && k0 + k < K) ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs]
-                                           : 0.0;
+      T[r][tix(k)] = (r0 + r < R && k0 + k < K)
+                         ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
     }
   } else {          // k contiguous: lane -> k
     for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
       const int k = i % SL_K, r = i / SL_K;
-      T[r][k] = (r0 + r < R && k0 + k < K) ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs]
-                                           : 0.0;
+      T[r][tix(k)] = (r0 + r < R && k0 + k < K)
+                         ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
     }
   }
 }
 
-// ex[r] = e with max_k |X(r,k)| < 2^e (0 for an all-zero row)
+// ex[r] = max(ex[r], e) with max_k |X(r,k)| < 2^e over this CTA's k chunk (ex starts at EX_NONE;
+// the exponent of the row maximum is the maximum of the chunk exponents).  Rows contiguous: a
+// thread per row walks RX_K values of k (warps read 256 contiguous bytes); k contiguous: a warp per
+// row, lanes across k.
+constexpr int RX_K = 256;
 __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, const double* X,
                                                                 long long rs, long long cs,
                                                                 int* ex, const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;
-  __shared__ double T[SL_R][SL_K + 1];
-  __shared__ double mx[SL_R][SL_THREADS / SL_R];
-  const int r0 = blockIdx.x * SL_R;
-  const int r = threadIdx.x % SL_R, part = threadIdx.x / SL_R;
+  const int k0 = blockIdx.y * RX_K, k1 = min(K, k0 + RX_K);
   double m = 0.0;
-  for (int k0 = 0; k0 < K; k0 += SL_K) {
-    __syncthreads();
-    load_tile(T, X, rs, cs, R, K, r0, k0);
-    __syncthreads();
-    for (int k = part; k < SL_K; k += SL_THREADS / SL_R) m = fmax(m, fabs(T[r][k]));
+  int r;
+  if (rs <= cs) {
+    r = blockIdx.x * SL_THREADS + threadIdx.x;
+    if (r >= R) return;
+    const double* p = X + (long long)r * rs;
+#pragma unroll 8
+    for (int k = k0; k < k1; ++k) m = fmax(m, fabs(p[(long long)k * cs]));
+  } else {
+    const int lane = threadIdx.x & 31;
+    r = blockIdx.x * (SL_THREADS / 32) + (threadIdx.x >> 5);
+    if (r >= R) return;
+    const double* p = X + (long long)r * rs;
+#pragma unroll 4
+    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs(p[(long long)k * cs]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane != 0) return;
   }
-  mx[r][part] = m;
-  __syncthreads();
-  if (threadIdx.x < SL_R && r0 + threadIdx.x < R) {
-    double v = 0.0;
-    for (int p = 0; p < SL_THREADS / SL_R; ++p) v = fmax(v, mx[threadIdx.x][p]);
-    int e = 0;
-    if (v > 0.0) frexp(v, &e);
-    ex[r0 + threadIdx.x] = e;
+  if (m > 0.0) {
+    int e;
+    frexp(m, &e);
+    atomicMax(ex + r, e);
   }
 }
 
@@ -424,17 +435,18 @@ __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, cons
                                                                const int* ex, signed char* Sl,
                                                                long long kp, const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;
-  __shared__ double T[SL_R][SL_K + 1];
+  __shared__ double T[SL_R][SL_KP];
   const int r0 = blockIdx.x * SL_R, k0 = blockIdx.y * SL_K;
   load_tile(T, X, rs, cs, R, K, r0, k0);
   __syncthreads();
   const int r = threadIdx.x / 8, kq = (threadIdx.x % 8) * 16;   // 16 consecutive k per thread
   if (r0 + r >= R || k0 + kq >= kp) return;
-  const int e = ex[r0 + r];
+  const int ee = ex[r0 + r];
+  const int e = ee == EX_NONE ? 0 : ee;   // all-zero row
   unsigned w[OZ_S][4] = {};
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    double v = ldexp(T[r][kq + j], -e);   // |v| < 1
+    double v = ldexp(T[r][tix(kq + j)], -e);   // |v| < 1
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
       const double t = v * 128.0;         // exact
@@ -501,7 +513,10 @@ int sms_oz() {
 
 int slice_operand(int R, int Kc, const double* X, long long rs, long long cs, signed char* Sl,
                   int* ex, long long kp, const int* abort_flag, cudaStream_t s) {
-  oz_rowexp_kernel<<<(R + SL_R - 1) / SL_R, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, abort_flag);
+  GG_CUDA_TRY(cudaMemsetAsync(ex, 0x80, (size_t)R * sizeof(int), s));   // EX_NONE
+  const int rows_per_cta = rs <= cs ? SL_THREADS : SL_THREADS / 32;
+  dim3 gx((R + rows_per_cta - 1) / rows_per_cta, (Kc + RX_K - 1) / RX_K);
+  oz_rowexp_kernel<<<gx, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, abort_flag);
   GG_LAUNCH_CHECK("oz_rowexp_kernel");
   dim3 g((R + SL_R - 1) / SL_R, (unsigned)((kp + SL_K - 1) / SL_K));
   oz_slice_kernel<<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, abort_flag);
