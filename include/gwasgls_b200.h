@@ -59,7 +59,10 @@ int gg_pad(int n);                               /* round n up to GG_TILE       
  *            row-major order (a C-contiguous numpy array uploaded as is), 0 column-major.
  *   L      : np x np output, ld = ldp (>= np, multiple of 2); lower factor, upper zero.
  *   Linv   : np x np output, ld = ldp; lower inverse, upper zero.
- *   work   : gg_potrf_workspace_bytes(n) bytes of device scratch.
+ *   work   : gg_potrf_workspace_bytes(n) bytes of device scratch (includes the int8
+ *            slices of the Ozaki-scheme updates: ~0.6 GB at n = 1e4, ~5.8 GB at 4e4).
+ * The large trailing SYRKs and inverse updates run as FP64 GEMMs on the int8 tensor
+ * cores (gg_gemm_ozaki_f64, FP64-GEMM accuracy); GG_FACTOR_OZAKI=0 selects DMMA.
  *   info_host[0] : -1 on success, else the 0-based failing pivot (LAPACK info-1, or
  *                  for non-finite input the row of the first non-finite entry in
  *                  row-major order, kernel.py:101-103).
