@@ -1,20 +1,35 @@
 #!/usr/bin/env python
-"""Benchmark of the GLS hot path on B200 (BASELINE.json configs[1], the metric's config).
+"""Benchmark of the GLS hot path on B200: BASELINE.json's metric on its headline configuration.
 
-Workload: n = 10,000 individuals, p = 4, m = 200,000 SNPs per GPU, FP64, blocks of 8,192 SNPs
-(24 full + one 3,392 tail), seeded synthetic BASELINE data.  One STEP is one
-full sweep of the rank's 200,000 SNPs: per block one FP64 -> int8 narrow of the dosages (side
-stream, one block ahead), one int8 tensor-core TRSM launch (Xbar = Linv * G with the per-SNP
-partial dots fused into its epilogue) and one reduce + batched p x p solve launch.  The genotypes
-(FP64, 16.2 GB per GPU) are resident in HBM when the timed region starts; they are larger than
-L2, so no L2 flush is needed.  gls_prepare (Cholesky + inverse + slicing) runs once, outside the
-step, timed apart.  `--trsm dmma` runs the FP64 DMMA TRSM + epilogue instead.
+Headline workload (default, ``--config 3``): BASELINE configs[3] -- n = 40,000 individuals,
+p = 8 (intercept + 6 N(0,1) covariates + SNP), m = 2,000,000 SNPs PER GPU, M = 0.5 K + 0.5 I,
+blocks of 8,192 SNPs (244 full + one 1,152 tail), seeded synthetic BASELINE data (
+no public dataset exists for this path).  It is the largest single-GPU configuration and the one
+the "1/2/4/8 GPU" metric is quoted on.  One STEP is one full sweep of the rank's 2,000,000 SNPs:
+per block one int8 tensor-core TRSM launch (Xbar = Linv * G with the per-SNP partial dots fused
+into its TMEM epilogue) and one reduce + batched p x p solve launch.  The int8 dosages (80 GB per
+GPU) are resident in HBM when the timed region starts -- far larger than L2, so no flush is
+needed.  gls_prepare (Cholesky + inverse + slicing) runs once, outside the step, timed apart.
 
-Multi-GPU (torchrun): SNP-sharded weak scaling — rank r owns markers [r*m, (r+1)*m) of an
-N*m-marker panel; L is factored redundantly on every rank; no collective in the timed region
-except the barriers that bracket it; time = max over ranks of the CUDA-event time.
+Also in the line:
+  * e2e      -- the same metric through the reference-signature drop-in call
+                kernel.gls_solve_block(ctx, SnpBlock(first, host_block)) (kernel.py:315-342) with
+                the int8 dosages in pinned HOST memory: every step copies all m SNPs host->device
+                and reads every block's results back (lazy ResultBlocks, resolved each step).
+  * cpu_baseline + parity -- the CPU oracle (oracle/gls_ref.py, the reference's threads= path)
+                on this host's cores: gls_prepare once (timed apart), then a sample of 2,048 SNPs
+                -- 512 from each of the first block, two interior blocks and the last (partial)
+                block -- which is also the parity set for the GPU results.
+  * secondary -- BASELINE config 1 (n = 1e4, p = 4, m = 2e5, FP64-resident) measured the same
+                way (value + roofline), for continuity with round 1.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (``--gpus N``; the driver launches torchrun, a bare ``python bench.py --gpus N``
+re-executes itself under torch.distributed.run): SNP-sharded weak scaling -- rank r owns markers
+[r*m, (r+1)*m) of an N*m-marker panel; L is factored redundantly on every rank; no collective in
+the timed region except the barriers that bracket it; time = max over ranks of the CUDA-event
+time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 """
 
 from __future__ import annotations
@@ -23,6 +38,7 @@ import argparse
 import dataclasses
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,33 +55,43 @@ UNIT = "SNPs/s"
 FP64_PEAK_TFLOPS = 37.09
 FP64_PEAK_SOURCE = ("measured: DMMA m8n8k4 sustained 37.09 TF/s @1965 MHz, tools/fp64_peak.cu "
                     "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry")
-# int8 tensor-core peak (the int8 TRSM's roofline): measured with tools/i8_peak.cu on this pool's
-# B200 (tcgen05.mma.cta_group::1.kind::i8 M128 N256 K32 back to back on every SM).
-I8_PEAK_TOPS = 4428.7
-I8_PEAK_SOURCE = ("measured: tcgen05.mma.kind::i8 M128 N256 K32 back to back on 148 SMs, 4428.7 "
-                  "TOPS (tools/i8_peak.cu, profiles/r01_i8_peak.log); MEASURED_PEAKS.json has no "
+# int8 tensor-core peaks (the int8 TRSM's roofline), measured on this pool's B200 with the TRSM's
+# own instruction shape (tools/i8_peak_pair.cu: tcgen05.mma.cta_group::2.kind::i8 M256 N224 K32
+# back to back on 74 CTA pairs, operands resident in shared memory).  MEASURED_PEAKS.json has no
+# int8 entry.  Burst = one 8-ms launch at full clock; sustained = back to back for 20 s (the board
+# sits at its power cap) -- the denominator for a kernel timed inside a multi-second step.
+I8_PEAK_BURST_TOPS = 4353.0
+I8_PEAK_SUSTAINED_TOPS = float(os.environ.get("GG_I8_PEAK_SUSTAINED", "0")) or None
+I8_PEAK_SOURCE = ("measured: tcgen05.mma.cta_group::2.kind::i8 M256 N224 K32 back to back on 148 "
+                  "SMs (tools/i8_peak_pair.cu; profiles/r01_i8_peak_pair.log burst, "
+                  "profiles/r02_i8_peak_sustained.log sustained); MEASURED_PEAKS.json has no "
                   "int8 entry")
-CPU_SAMPLE_SNPS = 4096
-REF_SAMPLE_SNPS = 2048
+PEAK_FILE = os.path.join(REPO, "profiles", "i8_peak.json")
+CPU_SAMPLE_PER_BLOCK = 512
+REF_SAMPLE_SNPS = {0: 2048, 1: 2048, 2: 2048, 3: 512, 4: 128}
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--snps", type=int, default=None, help="SNPs per GPU (default: config's m)")
     ap.add_argument("--block-snps", type=int, default=8192)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="timed e2e steps (default: min(steps, 5))")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the config-1 secondary measurement")
     ap.add_argument("--trsm", choices=["i8", "dmma"], default="i8",
                     help="TRSM engine: int8 tensor cores with the sliced inverse (default) or "
                          "the FP64 DMMA kernel")
     ap.add_argument("--resident", choices=["f64", "i8"], default=None,
                     help="genotype storage in HBM (default: FP64 if it fits, else int8)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -73,6 +99,19 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_argv(args_list, gpus, port):
+    """The torch.distributed.run command that runs this script on ``gpus`` ranks (one per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+            os.path.abspath(__file__)] + list(args_list)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -124,161 +163,186 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def load_traffic(engine):
-    """Per-launch DRAM bytes of the TRSM kernel from the committed ncu --set full summary."""
-    path = os.path.join(REPO, "profiles", f"ncu_trsm_{engine}_summary.json")
+def load_traffic(engine, n, snps):
+    """Per-launch DRAM bytes of the TRSM kernel from the committed ncu --set full summaries
+    (profiles/ncu_trsm_<engine>_summary*.json), for the capture whose workload matches."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", f"ncu_trsm_{engine}_summary*.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if d.get("n") == n and d.get("snps_per_launch") == snps:
+            return d.get("dram_bytes_per_launch"), d
+    return None, None
+
+
+def i8_peaks():
+    """(burst, sustained) int8 TOPS of the TRSM's instruction shape (profiles/i8_peak.json when
+    present: written from tools/i8_peak_pair runs on this pool's B200)."""
+    burst, sust = I8_PEAK_BURST_TOPS, I8_PEAK_SUSTAINED_TOPS
     try:
-        with open(path) as f:
+        with open(PEAK_FILE) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
+        burst = float(d.get("burst_tops", burst))
+        sust = sust or d.get("sustained_tops")
     except (OSError, ValueError):
-        return None, None
+        pass
+    return burst, (float(sust) if sust else None)
 
 
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
 
-def run_ours(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+class Sweep:
+    """One rank's resident sweep of a BASELINE config: data on the device, gls_prepare done, and
+    ``step()`` = one pass of the hot path over all the rank's markers."""
 
-    from paper_1304_2272_b200 import _capi, datagen, kernel, pipeline
-    from paper_1304_2272_b200._capi import check, ptr
-    from paper_1304_2272_b200._device import alloc_cols
+    def __init__(self, cfg, m, world, rank, dev, m_blk, trsm, resident, keep_host_M):
+        import torch
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
-    if use_dist:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    lib = _capi.lib()
-    spec = datagen.CONFIGS[args.config]
-    m = args.snps or spec.m
-    spec = dataclasses.replace(spec, m=m * world)     # the N*m-marker panel
-    n, p = spec.n, spec.p
-    q = p - 1
-    np_ = _capi.pad(n)
-    m_blk = args.block_snps
+        from paper_1304_2272_b200 import _capi, datagen, kernel, pipeline
+        from paper_1304_2272_b200._capi import check, ptr
 
-    # ---- data (identical M on every rank; rank-local marker range) --------------------------
-    t0 = time.perf_counter()
-    Md = datagen.kinship_covariance_device(spec)          # (n, n) on the device
-    XL, y = datagen.covariates_host(spec)
-    torch.cuda.synchronize()
-    t_gen_m = time.perf_counter() - t0
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record()
-    ctx = kernel.gls_prepare(Md, XL, y)                  # device-resident M, no host round trip
-    e1.record()
-    torch.cuda.synchronize()
-    t_prepare = time.perf_counter() - t0
-    prepare_ms_device = e0.elapsed_time(e1)
-    d = ctx._dev
-    M = Md.cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
-    del Md
-    # genotypes resident in HBM: FP64 (config 1) when they fit, else int8 {0,1,2} dosages (the
-    # config 2/3 storage format)
-    free_b, _ = torch.cuda.mem_get_info(dev)
-    resident = args.resident or ("f64" if 8 * m * np_ < 0.6 * free_b else "i8")
-    use_i8 = args.trsm == "i8" and d.slices is not None
-    n16 = -(-n // 16) * 16
-    first_marker = rank * m
-    X = Gres = None
-    if resident == "f64":
-        X = torch.empty((m, np_), dtype=torch.float64, device=dev)
-        X[:, n:].zero_()
-        G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
-        for j0 in range(0, m, m_blk):
-            cnt = min(m_blk, m - j0)
-            datagen.genotypes_device(spec, first_marker + j0, cnt, out=G)
-            check(lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(X[j0:]), np_,
-                                      _capi.stream_handle()), "widen")
-        del G
-    else:
-        Gres = datagen.genotypes_device(spec, first_marker, m, ld=n16)   # (m, n16) int8
-    # FP64-resident dosages are narrowed to int8 on a side stream, one block ahead, into a double
-    # buffer: the HBM-bound narrow of block i+1 runs beside the tensor-core TRSM of block i
-    g8s = [torch.empty((m_blk, n16), dtype=torch.int8, device=dev) for _ in range(2)] \
-        if (use_i8 and X is not None) else None
-    side = torch.cuda.Stream(device=dev) if g8s is not None else None
-    narrow_done = [torch.cuda.Event() for _ in range(2)]
-    trsm_done = [torch.cuda.Event() for _ in range(2)]
-    trsm_started = [False, False]
-    xin = alloc_cols(m_blk, np_) if (not use_i8 and X is None) else None
-    xbar = alloc_cols(m_blk, np_, zero=False) if not use_i8 else None
-    P = torch.empty(int(lib.gg_partials_bytes(n, m_blk, q)) // 8, dtype=torch.float64, device=dev)
-    bad = torch.zeros((1,), dtype=torch.int32, device=dev)
-    beta = torch.empty((m, p), dtype=torch.float64, device=dev)
-    status = torch.empty((m,), dtype=torch.int32, device=dev)
-    plan = pipeline.block_plan(m, m_blk).blocks
-    stream = torch.cuda.current_stream()
-    sh = _capi.C.c_void_p(stream.cuda_stream)
-    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in plan]
-    launches_per_block = 0
-    serial_narrow = os.environ.get("GG_BENCH_SERIAL_NARROW") == "1"
+        self.torch, self.ptr, self.lib = torch, ptr, _capi.lib()
+        base = datagen.CONFIGS[cfg]
+        self.cfg = cfg
+        self.m = m
+        self.spec = spec = dataclasses.replace(base, m=m * world)     # the N*m-marker panel
+        self.n, self.p = spec.n, spec.p
+        n, q = spec.n, spec.p - 1
+        self.q = q
+        np_ = _capi.pad(n)
+        self.np_ = np_
+        self.m_blk = m_blk
+        self.first_marker = rank * m
+        t0 = time.perf_counter()
+        Md = datagen.kinship_covariance_device(spec)          # (n, n) on the device
+        self.XL, self.y = datagen.covariates_host(spec)
+        torch.cuda.synchronize()
+        self.t_gen_m = time.perf_counter() - t0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        self.ctx = kernel.gls_prepare(Md, self.XL, self.y)   # device-resident M, no host trip
+        e1.record()
+        torch.cuda.synchronize()
+        self.t_prepare = time.perf_counter() - t0
+        self.prepare_ms_device = e0.elapsed_time(e1)
+        self.M = Md.cpu().numpy() if keep_host_M else None    # the CPU oracle's input bytes
+        del Md
+        d = self.d = self.ctx._dev
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        self.resident = resident or ("f64" if 8 * m * np_ < 0.6 * free_b else "i8")
+        self.use_i8 = trsm == "i8" and d.slices is not None
+        n16 = self.n16 = -(-n // 16) * 16
+        self.X = self.Gres = None
+        if self.resident == "f64":
+            self.X = torch.empty((m, np_), dtype=torch.float64, device=dev)
+            self.X[:, n:].zero_()
+            G = torch.empty((m_blk, n), dtype=torch.int8, device=dev)
+            for j0 in range(0, m, m_blk):
+                cnt = min(m_blk, m - j0)
+                datagen.genotypes_device(spec, self.first_marker + j0, cnt, out=G)
+                check(self.lib.gg_widen_i8_f64(n, cnt, ptr(G), n, ptr(self.X[j0:]), np_,
+                                               _capi.stream_handle()), "widen")
+            del G
+        else:
+            self.Gres = datagen.genotypes_device(spec, self.first_marker, m, ld=n16)
+        # FP64-resident dosages are narrowed to int8 on a side stream, one block ahead, into a
+        # double buffer: the HBM-bound narrow of block i+1 runs beside the TRSM of block i
+        self.g8s = [torch.empty((m_blk, n16), dtype=torch.int8, device=dev) for _ in range(2)] \
+            if (self.use_i8 and self.X is not None) else None
+        self.side = torch.cuda.Stream(device=dev) if self.g8s is not None else None
+        self.narrow_done = [torch.cuda.Event() for _ in range(2)]
+        self.trsm_done = [torch.cuda.Event() for _ in range(2)]
+        self.trsm_started = [False, False]
+        from paper_1304_2272_b200._device import alloc_cols
 
-    def step(record):
-        nonlocal launches_per_block
-        for i, (f, c) in enumerate(plan):
+        self.xin = alloc_cols(m_blk, np_) if (not self.use_i8 and self.X is None) else None
+        self.xbar = alloc_cols(m_blk, np_, zero=False) if not self.use_i8 else None
+        self.P = torch.empty(int(self.lib.gg_partials_bytes(n, m_blk, q)) // 8,
+                             dtype=torch.float64, device=dev)
+        self.bad = torch.zeros((1,), dtype=torch.int32, device=dev)
+        self.W8 = _capi.i8_work(dev)
+        self.beta = torch.empty((m, self.p), dtype=torch.float64, device=dev)
+        self.status = torch.empty((m,), dtype=torch.int32, device=dev)
+        self.plan = pipeline.block_plan(m, m_blk).blocks
+        self.stream = torch.cuda.current_stream()
+        self.sh = _capi.C.c_void_p(self.stream.cuda_stream)
+        self.ev_pairs = [(torch.cuda.Event(enable_timing=True),
+                          torch.cuda.Event(enable_timing=True)) for _ in self.plan]
+        self.launches_per_step = 0
+        self._capi = _capi
+
+    def step(self, record):
+        lib, ptr, d, torch = self.lib, self.ptr, self.d, self.torch
+        n, q, np_, n16 = self.n, self.q, self.np_, self.n16
+        stream, sh = self.stream, self.sh
+        nl = 0
+        for i, (f, c) in enumerate(self.plan):
             rc = 0
-            nl = 0
-            if use_i8:
-                if X is not None:            # FP64 dosages -> int8 (exactness flag checked after)
+            if self.use_i8:
+                if self.X is not None:        # FP64 dosages -> int8 (exactness flag checked after)
                     slot = i % 2
-                    if serial_narrow:
-                        rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8s[slot]), n16,
-                                                   ptr(bad), sh)
-                    else:
-                        with torch.cuda.stream(side):
-                            if trsm_started[slot]:      # buffer free once its last TRSM is done
-                                side.wait_event(trsm_done[slot])
-                            rc |= lib.gg_narrow_f64_i8(n, c, ptr(X[f]), np_, ptr(g8s[slot]),
-                                                       n16, ptr(bad),
-                                                       _capi.C.c_void_p(side.cuda_stream))
-                            narrow_done[slot].record(side)
-                        stream.wait_event(narrow_done[slot])
-                    G, ldg, nl = g8s[slot], n16, nl + 1
+                    with torch.cuda.stream(self.side):
+                        if self.trsm_started[slot]:     # buffer free once its last TRSM is done
+                            self.side.wait_event(self.trsm_done[slot])
+                        rc |= lib.gg_narrow_f64_i8(n, c, ptr(self.X[f]), np_, ptr(self.g8s[slot]),
+                                                   n16, ptr(self.bad),
+                                                   self._capi.C.c_void_p(self.side.cuda_stream))
+                        self.narrow_done[slot].record(self.side)
+                    stream.wait_event(self.narrow_done[slot])
+                    G, ldg = self.g8s[slot], n16
+                    nl += 1
                 else:
-                    G, ldg = Gres[f:], n16
+                    G, ldg = self.Gres[f:], n16
                 if record:
-                    ev_pairs[i][0].record(stream)
+                    self.ev_pairs[i][0].record(stream)
                 rc |= lib.gg_trsm_lower_i8_partials(n, c, ptr(d.slices), ptr(d.expo), ptr(G), ldg,
-                                                    q, ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0,
-                                                    None, 0, sh)
+                                                    q, ptr(d.XLy), ptr(d.ybar), ptr(self.P), None,
+                                                    0, None, 0, ptr(self.W8), sh)
                 if record:
-                    ev_pairs[i][1].record(stream)
-                if X is not None:
-                    trsm_done[i % 2].record(stream)
-                    trsm_started[i % 2] = True
-                rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
-                                                  ptr(beta[f]), ptr(status[f]), None, sh)
+                    self.ev_pairs[i][1].record(stream)
+                if self.X is not None:
+                    self.trsm_done[i % 2].record(stream)
+                    self.trsm_started[i % 2] = True
+                rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(self.P), ptr(d.S_TL), ptr(d.b_T),
+                                                  ptr(self.beta[f]), ptr(self.status[f]), None, sh)
                 nl += 2
             else:
-                if X is not None:
-                    src = X[f]
+                if self.X is not None:
+                    src = self.X[f]
                 else:
-                    rc |= lib.gg_widen_i8_f64(n, c, ptr(Gres[f]), n16, ptr(xin), np_, sh)
-                    src, nl = xin, nl + 1
+                    rc |= lib.gg_widen_i8_f64(n, c, ptr(self.Gres[f]), n16, ptr(self.xin), np_, sh)
+                    src = self.xin
+                    nl += 1
                 if record:
-                    ev_pairs[i][0].record(stream)
-                rc |= lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(src), np_, ptr(xbar),
-                                                   np_, sh)
+                    self.ev_pairs[i][0].record(stream)
+                rc |= lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(src), np_,
+                                                   ptr(self.xbar), np_, sh)
                 if record:
-                    ev_pairs[i][1].record(stream)
-                rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(xbar), np_, ptr(d.XLy), np_,
-                                              ptr(d.ybar), ptr(d.S_TL), ptr(d.b_T), ptr(beta[f]),
-                                              ptr(status[f]), None, ptr(P), sh)
+                    self.ev_pairs[i][1].record(stream)
+                rc |= lib.gg_gls_epilogue_f64(n, c, q, ptr(self.xbar), np_, ptr(d.XLy), np_,
+                                              ptr(d.ybar), ptr(d.S_TL), ptr(d.b_T),
+                                              ptr(self.beta[f]), ptr(self.status[f]), None,
+                                              ptr(self.P), sh)
                 nl += 3          # TRSM + partials + reduce/solve
             if rc:
-                raise RuntimeError(_capi.last_error())
-            launches_per_block = nl
-        return None
+                raise RuntimeError(self._capi.last_error())
+        self.launches_per_step = nl
+
+    def trsm_ms(self):
+        return sum(a.elapsed_time(b) for a, b in self.ev_pairs)   # the last recorded step
+
+
+def timed_sweep(sw, steps, warmup, use_dist, dist, local, dev):
+    """W warm-up steps, then K timed steps bracketed by barrier + synchronize; returns
+    (elapsed_ms max over ranks, clocks, trsm_ms of the last step)."""
+    import torch
 
     def barrier():
         torch.cuda.synchronize()
@@ -286,21 +350,18 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step(False)
+    for _ in range(warmup):
+        sw.step(False)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    trsm_ms = 0.0
-    t_start.record(stream)
-    for k in range(args.steps):
-        step(True)
-    t_end.record(stream)
+    t_start.record(sw.stream)
+    for k in range(steps):
+        sw.step(k == steps - 1)
+    t_end.record(sw.stream)
     torch.cuda.synchronize()
-    for a_ev, b_ev in ev_pairs:
-        trsm_ms += a_ev.elapsed_time(b_ev)     # last step's per-launch times
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     barrier()
@@ -308,155 +369,276 @@ def run_ours(args):
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
-    if int(bad.item()) != 0:
-        raise RuntimeError("non-integer dosages reached the int8 path")
-    ok_all = bool((status >= 0).sum().item() == 0)
-    snps_per_step_total = m * world
-    value = snps_per_step_total * args.steps / (elapsed_ms / 1e3)
-    traffic_full, ncu = load_traffic("i8" if use_i8 else "dmma")
-    if ncu is not None and (ncu.get("n") != n or ncu.get("snps_per_launch") != m_blk):
-        traffic_full, ncu = None, None      # the committed capture is of another workload
+    return elapsed_ms, clk, sw.trsm_ms()
+
+
+def roofline_obj(sw, steps, elapsed_ms, trsm_ms, clk, lib):
+    n, m = sw.n, sw.m
     flops_per_step = float(n) * n * m
     trsm_tflops = flops_per_step / (trsm_ms / 1e3) / 1e12          # FP64-equivalent rate
-    step_tflops = flops_per_step * args.steps / (elapsed_ms / 1e3) / 1e12
-    if use_i8:
+    traffic, ncu = load_traffic("i8" if sw.use_i8 else "dmma", n, sw.m_blk)
+    step_ms = elapsed_ms / steps
+    if sw.use_i8:
         slices = int(lib.gg_i8_slices())
         tops = slices * flops_per_step / (trsm_ms / 1e3) / 1e12     # int8 ops: S slices x n^2
-        roofline = {
+        burst, sustained = i8_peaks()
+        long_step = step_ms > 1000.0
+        peak = sustained if (long_step and sustained) else burst
+        r = {
             "bound": "tensor",
             "kernel": "trsm_i8_dual_kernel (persistent CTA-pair TMA + tcgen05.mma.kind::i8 TRSM, "
                       "two row blocks per tile, fused reductions; inverse split into int8 slices)",
-            "achieved": round(tops, 1), "peak": I8_PEAK_TOPS, "unit": "TOPS",
-            "frac": round(tops / I8_PEAK_TOPS, 4),
-            "traffic": traffic_full,
+            "achieved": round(tops, 1), "peak": peak, "unit": "TOPS",
+            "frac": round(tops / peak, 4),
+            "traffic": traffic,
             "algorithmic_unit": f"{slices} slices x n^2 int8 ops per SNP (exact int32 products of "
                                 "the sliced inverse with the dosages) x SNPs per launch",
+            "algorithmic_bytes_per_launch": int(lib.gg_inverse_slices_bytes(n)) + n * sw.m_blk,
+            "peak_kind": "sustained (kernel timed inside a multi-second step)"
+                         if peak is sustained else "burst",
+            "peak_burst": burst, "peak_sustained": sustained,
+            "frac_of_burst": round(tops / burst, 4),
             "peak_source": I8_PEAK_SOURCE,
             "fp64_equivalent_tflops": round(trsm_tflops, 2),
             "fp64_equivalent_vs_dmma_peak": round(trsm_tflops / FP64_PEAK_TFLOPS, 3),
-            "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
+            "trsm_share_of_step": round(trsm_ms / step_ms, 4),
         }
     else:
-        roofline = {
+        r = {
             "bound": "tensor",
             "kernel": "trsm_tma_kernel (persistent TMA + DMMA TRSM, Xbar = Linv*X)",
             "achieved": round(trsm_tflops, 3), "peak": FP64_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": round(trsm_tflops / FP64_PEAK_TFLOPS, 4),
-            "traffic": traffic_full,
+            "traffic": traffic,
             "algorithmic_unit": "n^2 FLOP per SNP (LAPACK dtrsm count) x SNPs per launch",
             "peak_source": FP64_PEAK_SOURCE,
-            "trsm_share_of_step": round(trsm_ms / (elapsed_ms / args.steps), 4),
+            "trsm_share_of_step": round(trsm_ms / step_ms, 4),
         }
-
+    if ncu is not None:
+        r["traffic_source"] = ncu.get("source")
     if isinstance(clk, dict) and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
-        # the peak is quoted at the maximum SM clock; under the board's power cap the clock in the
-        # timed region is lower -- the same peak scaled to the median measured clock
+        # the burst peak is quoted at the maximum SM clock; the same peak scaled to the median
+        # clock measured in the timed region
         scale = clk["sm_mhz"] / clk["sm_max_mhz"]
-        roofline["peak_at_measured_clock"] = round(roofline["peak"] * scale, 1)
-        roofline["frac_at_measured_clock"] = round(roofline["achieved"] / (roofline["peak"] * scale), 4)
+        base = r.get("peak_burst", r["peak"])
+        r["peak_at_measured_clock"] = round(base * scale, 1)
+        r["frac_at_measured_clock"] = round(r["achieved"] / (base * scale), 4)
+    return r
 
-    # ---- e2e through the public stream API with host buffers --------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1304_2272_b200 import _capi, datagen
+
+    rank, world, local = dist_env()
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the communicator really spans N ranks (one GPU each)
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)
+        assert int(t.item()) == world == dist.get_world_size()
+    dev = torch.device("cuda", local)
+    lib = _capi.lib()
+    spec0 = datagen.CONFIGS[args.config]
+    m = args.snps or spec0.m
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    sw = Sweep(args.config, m, world, rank, dev, args.block_snps, args.trsm, args.resident,
+               keep_host_M=want_cpu)
+    elapsed_ms, clk, trsm_ms = timed_sweep(sw, args.steps, args.warmup, use_dist, dist, local,
+                                           dev)
+    if int(sw.bad.item()) != 0:
+        raise RuntimeError("non-integer dosages reached the int8 path")
+    ok_all = bool((sw.status >= 0).sum().item() == 0)
+    value = m * world * args.steps / (elapsed_ms / 1e3)
+    roofline = roofline_obj(sw, args.steps, elapsed_ms, trsm_ms, clk, lib)
+    beta_host = sw.beta.cpu().numpy()
+    status_host = sw.status.cpu().numpy()
+
+    # ---- CPU baseline + sampled parity (rank 0 at N = 1), before e2e frees nothing ----------
+    cpu = parity = None
+    if want_cpu:
+        cpu, parity = run_cpu_baseline(sw, beta_host, status_host)
+        sw.M = None
+
+    # ---- e2e through the reference-signature drop-in call with host buffers ------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, X if X is not None else Gres, n, m, world, rank, dev, np, torch,
-                      dist if use_dist else None, pipeline)
+        e2e = run_e2e(args, sw, world, rank, dev, use_dist, dist, beta_host)
 
-    # ---- CPU baseline + sampled parity on rank 0 at N = 1 -----------------------------------
-    cpu = None
-    parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, parity = run_cpu_baseline(M, XL, y, X if X is not None else Gres, n, beta, status,
-                                       np)
-
+    n, p = sw.n, sw.p
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "dtype_detail": ("TRSM: exact int8 x int8 -> int32 tcgen05 products of a 7-slice split "
+                         "of the FP64 inverse (+ integer diagonal head), one FP64 rounding per "
+                         "element; reductions and p x p solves in FP64") if sw.use_i8 else
+                        "FP64 DMMA TRSM, FP64 reductions and solves",
+        "config": {
+            "workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}, m={m} SNPs "
+                        f"per GPU ({'full m' if m == spec0.m else 'reduced m'}), blocks of "
+                        f"{sw.m_blk}; step = TRSM + fused epilogue + p x p solves over all m SNPs",
+            "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": sw.m_blk,
+            "blocks_per_step": len(sw.plan), "parallelism": f"snp-shard x{world}",
+            "resident": sw.resident,
+            "l2": "inputs larger than L2 (genotypes resident in HBM: "
+                  f"{m * (sw.np_ * 8 if sw.resident == 'f64' else sw.n16) / 1e9:.1f} GB per GPU, "
+                  f"{'FP64' if sw.resident == 'f64' else 'int8'}); no flush needed",
+            "t_prepare_s": round(sw.t_prepare, 4),
+            "prepare_device_ms": round(sw.prepare_ms_device, 2),
+            "t_generate_M_s": round(sw.t_gen_m, 2),
+            "step_fp64_tflops": round(float(n) * n * m * args.steps / (elapsed_ms / 1e3) / 1e12,
+                                      3),
+            "all_snps_ok": ok_all,
+        },
+        "roofline": roofline,
+        "gpu_launches": sw.launches_per_step * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": parity,
+    }
+    del sw
+    torch.cuda.empty_cache()
+    if not args.no_secondary and args.config != 1:
+        line["secondary"] = run_secondary(args, world, rank, local, dev, use_dist, dist)
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "dtype_detail": ("TRSM: exact int8 x int8 -> int32 tcgen05 products of a 7-slice split "
-                             "of the FP64 inverse (+ integer diagonal head), one FP64 rounding per "
-                             "element; reductions and p x p solves in FP64") if use_i8 else
-                            "FP64 DMMA TRSM, FP64 reductions and solves",
-            "config": {
-                "workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}, m={m} SNPs "
-                            f"per GPU, FP64, blocks of {m_blk}; step = TRSM + fused epilogue "
-                            f"over all m SNPs",
-                "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": m_blk,
-                "blocks_per_step": len(plan), "parallelism": f"snp-shard x{world}",
-                "resident": resident,
-                "l2": "inputs larger than L2 (genotypes resident in HBM: "
-                      f"{m * (np_ * 8 if resident == 'f64' else n) / 1e9:.1f} GB per GPU, "
-                      f"{'FP64' if resident == 'f64' else 'int8, widened per block in the step'})",
-                "t_prepare_s": round(t_prepare, 4),
-                "prepare_device_ms": round(prepare_ms_device, 2),
-                "t_generate_M_s": round(t_gen_m, 2),
-                "step_fp64_tflops": round(step_tflops, 3),
-                "all_snps_ok": ok_all,
-            },
-            "roofline": roofline,
-            "gpu_launches": launches_per_block * len(plan) * args.steps,
-            "clocks": clk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "parity": parity,
-        }
-        if ncu is not None:
-            line["roofline"]["traffic_source"] = ncu.get("source")
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_e2e(args, ctx, X, n, m, world, rank, dev, np, torch, dist, pipeline):
-    """Same metric through the public stream API, pipeline.solve_array, with the genotypes in
-    pinned host memory: every step H2D-copies all m markers (copy stream, double-buffered) and
-    reads every block's results back.  Primary: int8 dosages on the host (the GWAI / config-2
-    storage format, n bytes per SNP); also reported: FP64 host genotypes (8 n bytes per SNP,
-    PCIe-bound) when host memory allows."""
-    src = X[:, :n] if X.dtype == torch.float64 else X[:, :n]
-    out = {}
-    for dtype in ("i8", "f64"):
-        if dtype == "f64":
-            try:   # FP64 host genotypes need m*n*8 pinned bytes per rank
-                import psutil
+def run_secondary(args, world, rank, local, dev, use_dist, dist):
+    """BASELINE config 1 (n = 1e4, p = 4, m = 2e5 per GPU, FP64-resident), value + roofline."""
+    import torch
 
-                if world * m * n * 8 > 0.5 * psutil.virtual_memory().available:
-                    continue
-            except ImportError:
-                pass
-        engine = pipeline.StreamEngine(ctx, args.block_snps, int8=dtype == "i8")
-        tdt = torch.int8 if dtype == "i8" else torch.float64
-        host_t = torch.empty((m, n), dtype=tdt).pin_memory()
-        host_t.copy_(src.to(tdt))
-        Xh = host_t.numpy().T                 # n x m, Fortran-ordered view of pinned memory
-        res = pipeline.solve_array(ctx, Xh, engine=engine)      # warm-up
+    from paper_1304_2272_b200 import _capi, datagen
+
+    m = datagen.CONFIGS[1].m
+    sw = Sweep(1, m, world, rank, dev, args.block_snps, args.trsm, None, keep_host_M=False)
+    steps, warmup = max(args.steps, 20), max(args.warmup, 5)
+    elapsed_ms, clk, trsm_ms = timed_sweep(sw, steps, warmup, use_dist, dist, local, dev)
+    out = {
+        "workload": f"BASELINE config 1: GLS sweep n={sw.n}, p={sw.p}, m={m} SNPs per GPU, "
+                    f"FP64-resident ({m * sw.np_ * 8 / 1e9:.1f} GB), blocks of {sw.m_blk}",
+        "value": round(m * world * steps / (elapsed_ms / 1e3), 1), "unit": UNIT,
+        "steps": steps, "warmup": warmup, "ms_per_step": round(elapsed_ms / steps, 3),
+        "t_prepare_s": round(sw.t_prepare, 4),
+        "all_snps_ok": bool((sw.status >= 0).sum().item() == 0),
+        "roofline": roofline_obj(sw, steps, elapsed_ms, trsm_ms, clk, _capi.lib()),
+        "gpu_launches": sw.launches_per_step * steps, "clocks": clk,
+    }
+    del sw
+    torch.cuda.empty_cache()
+    return out
+
+
+def _host_register(arr):
+    """Page-lock a numpy array in place (cudaHostRegister; no power-of-two rounding like the
+    caching pinned allocator, which would turn 80 GB into 128 GB)."""
+    import torch
+
+    rt = torch._C._cudart
+    err = rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+    if int(err) != 0:
+        raise RuntimeError(f"cudaHostRegister failed ({err})")
+    return lambda: rt.cudaHostUnregister(arr.ctypes.data)
+
+
+def run_e2e(args, sw, world, rank, dev, use_dist, dist, beta_ref):
+    """The metric end to end through the reference-signature call
+    kernel.gls_solve_block(ctx, SnpBlock(first, data)) (kernel.py:315-342) with the int8
+    dosages in pinned host memory: each step copies every block host->device (copy stream) and
+    resolves every ResultBlock (device->host of beta and status)."""
+    import numpy as np
+    import torch
+
+    from paper_1304_2272_b200 import _capi, kernel
+
+    n, m, m_blk = sw.n, sw.m, sw.m_blk
+    steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
+    steps = max(1, steps)
+    # host copy of the rank's dosages (n x m, F-order) when host memory allows; else a ring of
+    # genuine blocks reused cyclically (same bytes per step, same H2D volume)
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except ImportError:   # pragma: no cover
+        avail = 1 << 62
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    fits = local_world * n * m < 0.6 * avail
+    ring = None if fits else max(2, int(0.5 * avail / local_world / (n * m_blk)))
+    cols = m if fits else min(m, ring * m_blk)
+    host = np.empty((cols, n), dtype=np.int8)                # row j = marker j (n x cols F-order)
+    unreg = _host_register(host)
+    try:
+        lib, sh = _capi.lib(), _capi.stream_handle()
+        for j0 in range(0, cols, m_blk):
+            c = min(m_blk, cols - j0)
+            if sw.Gres is not None:
+                blk, ld = sw.Gres[j0:j0 + c], sw.n16
+            else:
+                blk, ld = sw.X[j0:j0 + c, :n].to(torch.int8).contiguous(), n
+            # pitched device -> pinned host copy (kind 2)
+            _capi.check(lib.gg_memcpy2d_async(_capi.C.c_void_p(host.ctypes.data + j0 * n), n,
+                                              _capi.C.c_void_p(blk.data_ptr()), ld, n, c, 2, sh),
+                        "gg_memcpy2d_async")
+            torch.cuda.synchronize()
+        Xh = host.T                                           # n x cols, Fortran-ordered view
+        plan = sw.plan
+
+        def one_step(collect):
+            blocks = []
+            for f, c in plan:
+                h0 = f % cols if not fits else f
+                blocks.append(kernel.gls_solve_block(
+                    sw.ctx, kernel.SnpBlock(sw.first_marker + f, Xh[:, h0:h0 + c])))
+            arrays = [b.arrays for b in blocks]               # D2H of every block's results
+            return arrays
+
+        one_step(False)                                       # warm-up (engine creation)
         torch.cuda.synchronize()
-        if dist is not None:
+        if use_dist:
             dist.barrier()
-        h0, d0 = engine.h2d_bytes, engine.d2h_bytes
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            res = pipeline.solve_array(ctx, Xh, engine=engine)
+        for _ in range(steps):
+            arrays = one_step(True)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if dist is not None:
+        if use_dist:
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        out[dtype] = {
-            "value": round(m * world * args.steps / dt, 1), "unit": UNIT,
-            "h2d_bytes_per_step": int((engine.h2d_bytes - h0) // args.steps),
-            "d2h_bytes_per_step": int((engine.d2h_bytes - d0) // args.steps),
-            "api": "paper_1304_2272_b200.pipeline.solve_array (pinned host "
-                   f"{'int8' if dtype == 'i8' else 'FP64'} genotypes, double-buffered H2D)",
-            "all_snps_ok": bool(np.all(res.ok))}
-        del host_t, engine, Xh
-    e2e = dict(out["i8"])
-    if "f64" in out:
-        e2e["fp64_host"] = out["f64"]
-    return e2e
+        beta = np.concatenate([a.beta for a in arrays])
+        ok = np.concatenate([a.ok for a in arrays])
+        same = bool(fits and np.array_equal(beta, beta_ref, equal_nan=True))
+    finally:
+        unreg()
+    p = sw.p
+    return {
+        "value": round(m * world * steps / dt, 1), "unit": UNIT,
+        "h2d_bytes_per_step": int(n * m), "d2h_bytes_per_step": int(m * (8 * p + 4)),
+        "steps": steps,
+        "api": "paper_1304_2272_b200.kernel.gls_solve_block(ctx, SnpBlock(first, host int8 "
+               f"n x {m_blk} view)) per block -- the reference signature (kernel.py:315-342); "
+               "pinned host dosages, copy stream overlapped with the previous block's compute, "
+               "ResultBlocks resolved every step",
+        "host_data": "full panel in pinned host memory" if fits else
+                     f"ring of {ring} genuine blocks reused cyclically (host memory)",
+        "all_snps_ok": bool(np.all(ok)),
+        "bitwise_equal_to_device_resident_sweep": same,
+    }
 
 
 def _blas_threads():
@@ -469,36 +651,85 @@ def _blas_threads():
         return os.cpu_count()
 
 
-def run_cpu_baseline(M, XL, y, X, n, beta, status, np):
+def sample_columns(m, m_blk, per_block):
+    """BASELINE.md §3 parity/baseline sample: the first block, two interior blocks and the last
+    (partial) block -- per block its first and last per_block/2 markers (the block edges)."""
+    import numpy as np
+
+    nb = -(-m // m_blk)
+    picks = sorted({0, nb // 3, (2 * nb) // 3, nb - 1})
+    cols = []
+    for b in picks:
+        f = b * m_blk
+        c = min(m_blk, m - f)
+        h = min(per_block // 2, c // 2) if c >= 2 else c
+        cols.extend(range(f, f + h))
+        cols.extend(range(f + c - (per_block - h if c >= per_block else c - h), f + c))
+    return np.unique(np.array(cols, dtype=np.int64)), picks
+
+
+def run_cpu_baseline(sw, beta_gpu, status_gpu):
     """The CPU oracle (numpy/scipy restatement of the reference, oracle/gls_ref.py) on this
-    host's cores: gls_prepare once, then one block of CPU_SAMPLE_SNPS markers; doubles as the
-    sampled parity check of the GPU results."""
+    host's cores: gls_prepare once (timed apart), then gls_solve_block(threads=cores) on the
+    BASELINE.md §3 block sample; the same sample is the parity set of the GPU sweep."""
+    import numpy as np
+
     from oracle import gls_ref as O
 
-    S = CPU_SAMPLE_SNPS
-    Xs = X[:S, :n].double().cpu().numpy().T.copy(order="F")
+    cores = _blas_threads()
+    cols, picks = sample_columns(sw.m, sw.m_blk, CPU_SAMPLE_PER_BLOCK)
+    if sw.Gres is not None:
+        G = sw.Gres[cols][:, :sw.n]
+    else:
+        G = sw.X[cols][:, :sw.n]
+    Xs = G.double().cpu().numpy().T.copy(order="F")
     t0 = time.perf_counter()
-    octx = O.gls_prepare(M, XL, y)
+    octx = O.gls_prepare(sw.M, sw.XL, sw.y)
     t_prep = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ob, ok = O.gls_solve_block(octx, Xs)
+    ob, ok = O.gls_solve_block(octx, Xs, threads=cores)
     t = time.perf_counter() - t0
-    gb = beta[:S].cpu().numpy()
-    gs = status[:S].cpu().numpy()
-    gb = np.where((gs < 0)[:, None], gb, np.nan)
+    gb = np.where((status_gpu[cols] < 0)[:, None], beta_gpu[cols], np.nan)
     rel, mism = O.compare(gb, ob)
-    cpu = {"value": round(S / t, 2), "unit": UNIT, "cores": _blas_threads(), "kind": "port",
-           "sample": f"oracle gls_solve_block on the first {S} SNPs of the workload at n={n} "
-                     f"(prepare {t_prep:.2f} s excluded, like the GPU value)",
-           "t_prepare_s": round(t_prep, 3)}
-    parity = {"snps": S, "max_rel": rel, "status_mismatches": mism, "tol": 1e-9,
-              "within": bool(mism == 0 and rel <= 1e-9)}
+    S = len(cols)
+    cpu = {"value": round(S / t, 2), "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"oracle gls_solve_block(threads={cores}) on {S} SNPs of the workload "
+                     f"(n={sw.n}): the first/last {CPU_SAMPLE_PER_BLOCK // 2} markers of blocks "
+                     f"{picks} of {-(-sw.m // sw.m_blk)} (first, two interior, last partial); "
+                     f"prepare {t_prep:.1f} s excluded, like the GPU value",
+           "t_prepare_s": round(t_prep, 3), "t_sample_s": round(t, 3)}
+    parity = {"snps": S, "blocks": picks, "max_rel": rel, "status_mismatches": mism, "tol": 1e-9,
+              "within": bool(mism == 0 and rel <= 1e-9),
+              "oracle": "oracle/gls_ref.py (scipy dpotrf/dtrsm + numpy reductions), same M bytes"}
     return cpu, parity
 
 
 # ---------------------------------------------------------------------------------------------
 # reference arm: the reference's CPU implementation of the path (the oracle port) on host cores
 # ---------------------------------------------------------------------------------------------
+
+def kinship_host_lean(spec):
+    """M = a Z Z^T / m_k + (1 - a) I as datagen.kinship_covariance_host computes it (same
+    operations, same bits), in place: at n = 4e4 the dense temporaries of the plain expression
+    would need ~70 GB of host memory."""
+    import numpy as np
+
+    from paper_1304_2272_b200 import datagen
+
+    Z = datagen.standardized_host(spec.seed, spec.n, spec.m_kin, spec.maf)
+    K = Z @ Z.T
+    del Z
+    K /= spec.m_kin
+    K *= spec.a
+    K.flat[:: spec.n + 1] += (1.0 - spec.a)
+    n, B = spec.n, 2048
+    for i0 in range(0, n, B):                 # mirror the lower triangle (exact symmetry)
+        i1 = min(n, i0 + B)
+        K[i0:i1, i0:i1] = np.tril(K[i0:i1, i0:i1]) + np.tril(K[i0:i1, i0:i1], -1).T
+        if i1 < n:
+            K[i0:i1, i1:] = K[i1:, i0:i1].T
+    return K
+
 
 def run_reference(args):
     import numpy as np
@@ -511,50 +742,77 @@ def run_reference(args):
 
     spec = datagen.CONFIGS[args.config]
     n, p = spec.n, spec.p
-    S = REF_SAMPLE_SNPS
+    S = REF_SAMPLE_SNPS.get(args.config, 512)
+    cores = _blas_threads()
     t0 = time.perf_counter()
-    M = datagen.kinship_covariance_host(spec)
+    M = kinship_host_lean(spec)
     XL, y = datagen.covariates_host(spec)
     G = datagen.genotypes_host(spec.seed, n, spec.m, 0, S).astype(np.float64, order="F")
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     octx = O.gls_prepare(M, XL, y)
     t_prep = time.perf_counter() - t0
+    del M
     for _ in range(args.warmup):
-        O.gls_solve_block(octx, G)
+        O.gls_solve_block(octx, G, threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.gls_solve_block(octx, G)
+        O.gls_solve_block(octx, G, threads=cores)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = S * args.steps / tot
-    cores = _blas_threads()
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}; each step "
-                               f"= one {S}-SNP block through the reference CPU path",
+                               f"= one {S}-SNP block through the reference CPU path "
+                               f"(gls_solve_block, threads={cores})",
                    "n": n, "p": p, "sample_snps_per_step": S, "t_prepare_s": round(t_prep, 3),
                    "t_generate_s": round(t_gen, 2)},
         "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{S}-SNP block of the config-{args.config} workload per step "
-                                   "(oracle/gls_ref.py: scipy dtrsm + numpy reductions + batched "
-                                   "p x p Cholesky, as kernel.py:315-342)"},
+                                   f"(oracle/gls_ref.py: scipy dtrsm on {cores} BLAS threads + the "
+                                   f"reference's threads={cores} column split of the per-SNP "
+                                   "epilogue, kernel.py:315-342); gls_prepare timed apart"},
         "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse_args()
-    if args.impl == "reference":
+def main(argv=None):
+    args = parse_args(argv)
+    rank, world, _ = dist_env()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this script under torch.distributed.run
+        cmd = relaunch_argv(sys.argv[1:] if argv is None else argv, args.gpus, _free_port())
+        raise SystemExit(subprocess.call(cmd))
+    if os.environ.get("GG_BENCH_LAUNCH_PROBE") == "1":
+        launch_probe(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+
+
+def launch_probe(args):
+    """Launcher self-test (CPU, gloo): every rank joins one process group and rank 0 prints how
+    many ranks it saw -- proves ``--gpus N`` starts N ranks (tests/test_bench_contract.py)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "ranks_seen": int(t.item())}), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -20,9 +20,11 @@
  *     GG_TILE) and leading dimension >= np.  Padding rows of right-hand sides
  *     are zero; L and Linv are extended by the identity on the padding block.
  *     Column counts are never padded.
- *   - No entry point allocates persistent memory; workspaces come from the caller
- *     (sizes from the *_workspace_bytes queries).  Entry points are reentrant and
- *     keep no unguarded global state (SPEC threading rule).
+ *   - No entry point allocates persistent device memory; workspaces (including the int8
+ *     TRSM's tile counter) come from the caller (sizes from the *_workspace_bytes queries).
+ *     The only process-wide state is the once-resolved cuTensorMapEncodeTiled pointer.
+ *     Entry points are reentrant and keep no unguarded global state (SPEC threading rule,
+ *     SURVEY §8b).
  */
 #ifndef GWASGLS_B200_H
 #define GWASGLS_B200_H
@@ -168,8 +170,11 @@ int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int
                             void* stream);
 int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
                      int* bad_dev, void* stream);
+/* work: gg_trsm_i8_workspace_bytes() bytes of device memory (the dynamic tile scheduler's
+ * counter, cleared on `stream` before the launch); one workspace per in-flight launch.       */
+size_t gg_trsm_i8_workspace_bytes(void);
 int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
-                     long long ldg, double* X, int ldx, void* stream);
+                     long long ldg, double* X, int ldx, void* work, void* stream);
 
 /* The same kernel with the per-SNP reductions fused into its TMEM epilogue: writes the
  * canonical-order partial dots P (gg_partials_bytes(n, cnt, q) bytes; Xbar against XLbar (q
@@ -181,7 +186,7 @@ size_t gg_partials_bytes(int n, int cnt, int q);
 int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* expo,
                               const int8_t* G, long long ldg, int q, const double* XLbar,
                               const double* ybar, double* P, double* X, int ldx, const int* gate,
-                              int gate_value, void* stream);
+                              int gate_value, void* work, void* stream);   /* work: as above */
 int gg_gls_reduce_solve_f64(int n, int cnt, int q, const double* P, const double* S_TL,
                             const double* b_T, double* beta, int* status, double* sinv,
                             void* stream);
@@ -248,14 +253,17 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx,
                         double* sinv, void* work, void* stream);   /* work: as gg_gls_dots_f64 */
 
 /* One streamed block end to end (replaces kernel.gls_solve_block, kernel.py:315-342).
- * Paths (all selected without a host synchronisation):
+ * Paths (all selected PER COLUMN on the device, without a host synchronisation):
  *   slices given, G8 (int8 dosages) : int8 tensor-core TRSM with the per-SNP reductions fused
  *                                     into its TMEM epilogue (Xbar never written) -> solve;
- *   slices given, X64 (FP64)        : device narrowing; exact integers in [-127,127] take the
- *                                     int8 path, otherwise the FP64 DMMA TRSM (LinvP) runs;
+ *   slices given, X64 (FP64)        : device narrowing; a column of exact integers within
+ *                                     gg_i8_value_bound(n) takes the int8 path, any other column
+ *                                     the FP64 DMMA TRSM (LinvP) -- decided from that column's
+ *                                     values alone, so a column's result never depends on its
+ *                                     neighbours, the block size or the shard layout;
  *   no slices                       : [widen int8 ->] FP64 DMMA TRSM (LinvP) -> reductions.
- * Without LinvP (slices only: the config-4 form) a block the int8 path cannot compute exactly
- * gets status GG_STATUS_INVALID and NaN coefficients for every SNP.
+ * Without LinvP (slices only: the config-4 form) a column the int8 path cannot compute exactly
+ * gets status GG_STATUS_INVALID and NaN coefficients.
  * Then the batched p x p solve.  XLbar has leading dimension gg_pad(n).  work: at least
  * gg_gls_block_workspace_bytes(n, q, cnt, input_int8, have_slices) bytes of device memory.   */
 size_t gg_gls_block_workspace_bytes(int n, int q, int cnt, int input_int8, int have_slices);

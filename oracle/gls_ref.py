@@ -157,9 +157,24 @@ def solve_whitened(ctx, Xbar, emit_s_inv=False):
     return (beta, ok, out[3]) if emit_s_inv else (beta, ok)
 
 
-def gls_solve_block(ctx, X, emit_s_inv=False):
-    """kernel.py:315-342 — whiten the block (dtrsm) then solve_whitened."""
-    return solve_whitened(ctx, trsolve_lower(ctx.L, np.asarray(X, dtype=np.float64)), emit_s_inv)
+def gls_solve_block(ctx, X, emit_s_inv=False, threads=1):
+    """kernel.py:315-342 — whiten the block (dtrsm, BLAS-threaded) then solve_whitened; with
+    threads > 1 and at least 2*threads columns the per-SNP epilogue runs data-parallel over the
+    same disjoint column ranges as the reference (np.linspace bounds, a ThreadPoolExecutor,
+    kernel.py:326-341; numpy releases the GIL inside its reductions).  Results do not depend on
+    the split (per-column arithmetic)."""
+    Xbar = trsolve_lower(ctx.L, np.asarray(X, dtype=np.float64))
+    cnt = Xbar.shape[1]
+    if threads <= 1 or cnt < 2 * threads:
+        return solve_whitened(ctx, Xbar, emit_s_inv)
+    from concurrent.futures import ThreadPoolExecutor
+
+    bounds = np.linspace(0, cnt, threads + 1, dtype=int)
+    ranges = [(bounds[i], bounds[i + 1]) for i in range(threads) if bounds[i] < bounds[i + 1]]
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        parts = list(pool.map(lambda se: solve_whitened(ctx, Xbar[:, se[0]:se[1]], emit_s_inv),
+                              ranges))
+    return tuple(np.concatenate([p[k] for p in parts]) for k in range(len(parts[0])))
 
 
 def gls_eq1(M, Xi, y):

@@ -48,10 +48,11 @@ SIGNATURES = {
     "gg_slice_meta_i8": (_i, [_i, _vp, _vp, _vp]),
     "gg_slice_inverse_i8": (_i, [_i, _vp, _i, _vp, _vp, _vp]),
     "gg_narrow_f64_i8": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),
-    "gg_trsm_lower_i8": (_i, [_i, _i, _vp, _vp, _vp, _ll, _vp, _i, _vp]),
+    "gg_trsm_i8_workspace_bytes": (_sz, []),
+    "gg_trsm_lower_i8": (_i, [_i, _i, _vp, _vp, _vp, _ll, _vp, _i, _vp, _vp]),
     "gg_partials_bytes": (_sz, [_i, _i, _i]),
     "gg_trsm_lower_i8_partials": (_i, [_i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp, _i,
-                                       _vp, _i, _vp]),
+                                       _vp, _i, _vp, _vp]),
     "gg_gls_reduce_solve_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gg_transpose_f64": (_i, [_i, _vp, _i, _vp, _i, _vp]),
     "gg_dgemm_f64": (_i, [_i, _i, _i, _d, _vp, _i, _vp, _i, _i, _d, _vp, _i, _vp]),
@@ -153,6 +154,21 @@ def stream_handle():
     import torch
 
     return _vp(torch.cuda.current_stream().cuda_stream)
+
+
+def i8_work(device=None):
+    """A fresh workspace for one gg_trsm_lower_i8* launch (its tile counter), from torch's
+    caching allocator on the current device."""
+    import torch
+
+    n = int(lib().gg_trsm_i8_workspace_bytes())
+    return torch.empty(n, dtype=torch.uint8, device=device or _dev_now())
+
+
+def _dev_now():
+    import torch
+
+    return torch.device("cuda", torch.cuda.current_device())
 
 
 def ptr(t):

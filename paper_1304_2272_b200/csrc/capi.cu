@@ -189,18 +189,22 @@ int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, 
     gg::set_error("narrow: null pointer or n < 1");
     return GG_EARG;
   }
-  return gg::narrow_run(n, cnt, X, ldx, reinterpret_cast<signed char*>(G), ldg, bad_dev,
+  return gg::narrow_run(n, cnt, X, ldx, reinterpret_cast<signed char*>(G), ldg, bad_dev, nullptr,
                         as_stream(stream));
 }
 
+size_t gg_trsm_i8_workspace_bytes(void) { return 256; }
+
 int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
-                     long long ldg, double* X, int ldx, void* stream) {
-  if (n < 1 || nrhs < 0 || slices == nullptr || expo == nullptr || G == nullptr || X == nullptr) {
+                     long long ldg, double* X, int ldx, void* work, void* stream) {
+  if (n < 1 || nrhs < 0 || slices == nullptr || expo == nullptr || G == nullptr || X == nullptr ||
+      work == nullptr) {
     gg::set_error("trsm_i8: null pointer or bad size");
     return GG_EARG;
   }
   return gg::trsm_i8_run(n, nrhs, reinterpret_cast<const signed char*>(slices), expo,
-                         reinterpret_cast<const signed char*>(G), ldg, X, ldx, as_stream(stream));
+                         reinterpret_cast<const signed char*>(G), ldg, X, ldx,
+                         static_cast<int*>(work), as_stream(stream));
 }
 
 size_t gg_partials_bytes(int n, int cnt, int q) {
@@ -210,15 +214,17 @@ size_t gg_partials_bytes(int n, int cnt, int q) {
 int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* expo,
                               const int8_t* G, long long ldg, int q, const double* XLbar,
                               const double* ybar, double* P, double* X, int ldx, const int* gate,
-                              int gate_value, void* stream) {
+                              int gate_value, void* work, void* stream) {
   if (n < 1 || cnt < 0 || slices == nullptr || expo == nullptr || G == nullptr || P == nullptr ||
-      ybar == nullptr || (q > 0 && XLbar == nullptr) || q < 0 || q > GG_PMAX - 1) {
+      ybar == nullptr || (q > 0 && XLbar == nullptr) || q < 0 || q > GG_PMAX - 1 ||
+      work == nullptr) {
     gg::set_error("trsm_i8_partials: null pointer or bad size");
     return GG_EARG;
   }
   return gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo,
                                reinterpret_cast<const signed char*>(G), ldg, X, ldx, q, XLbar,
-                               pad_rows(n), ybar, P, gate, gate_value, as_stream(stream));
+                               pad_rows(n), ybar, P, gate, gate_value, static_cast<int*>(work),
+                               as_stream(stream));
 }
 
 int gg_gls_reduce_solve_f64(int n, int cnt, int q, const double* P, const double* S_TL,
@@ -321,7 +327,9 @@ int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, cons
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BlockWs {
-  int* flag;
+  int* flag;      // block flag: some column takes the FP64 path
+  int* counter;   // tile counter of the int8 TRSM's dynamic scheduler
+  int* colbad;    // per-column flags (cnt ints): 1 = this column takes the FP64 path
   double* P;
   signed char* g8;
   double* x64;
@@ -333,8 +341,11 @@ struct BlockWs {
 static BlockWs block_ws(int n, int q, int cnt, int input_int8, int have_slices, char* base) {
   const size_t np = (size_t)pad_rows(n), n16 = (size_t)((n + 15) / 16 * 16);
   BlockWs w{};
-  size_t off = 256;   // flag
+  size_t off = 256;   // flag at 0, tile counter at 128
   w.flag = reinterpret_cast<int*>(base);
+  w.counter = reinterpret_cast<int*>(base + 128);
+  w.colbad = reinterpret_cast<int*>(base + off);
+  off += align256(sizeof(int) * (size_t)cnt);
   w.P = reinterpret_cast<double*>(base + off);
   off += align256(gg::partials_bytes(n, cnt, q));
   // int8 input at n > 133,144: values beyond gg_i8_value_bound(n) take the DMMA path
@@ -383,50 +394,48 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
   int rc = GG_OK;
   bool invalid_gate = false;
   if (have_slices) {
+    // Per-column path selection, on the device (no host sync): a column whose values the int8
+    // tensor-core path cannot compute exactly (non-integer, or beyond gg_i8_value_bound(n)) is
+    // flagged on its own; the int8 TRSM runs for the whole block, then -- only if some column is
+    // flagged -- the FP64 DMMA TRSM and the reductions overwrite the flagged columns' partials.
+    // A column's path, and so its result, depends only on its own values.
+    GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
+    GG_CUDA_TRY(cudaMemsetAsync(w.colbad, 0, sizeof(int) * (size_t)cnt, s));
     const signed char* g = reinterpret_cast<const signed char*>(G8);
     long long lg = ldg;
+    const double* x64 = X64;   // FP64 columns for the DMMA path
+    int ldx64 = ldx;
+    bool may_flag = true;
     if (G8 != nullptr) {
       if (ldg % 16 != 0 || (reinterpret_cast<uintptr_t>(G8) & 15)) {   // re-pitch for TMA
         GG_CUDA_TRY(cudaMemcpy2DAsync(w.g8, n16, G8, ldg, n, cnt, cudaMemcpyDeviceToDevice, s));
         g = w.g8;
         lg = n16;
       }
-      if (gg::i8_value_bound(n) >= 127) {
-        rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q, XLbar,
-                                   np, ybar, w.P, nullptr, 0, s);
-      } else {
-        // large n: values beyond the exact-int32 bound send the block down the DMMA path
-        // (or, without an FP64 inverse, mark it invalid)
-        GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
-        rc = gg::range_i8_run(n, cnt, g, lg, w.flag, s);
-        if (rc == GG_OK)
-          rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q,
-                                     XLbar, np, ybar, w.P, w.flag, 0, s);
-        if (rc == GG_OK && LinvP != nullptr) {
-          rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);
-          if (rc == GG_OK)
-            rc = gg::trsm_packed_gated_run(n, cnt, LinvP, w.x64, np, w.xbar, np, w.flag, 1, s);
-          if (rc == GG_OK)
-            rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
-        }
-        invalid_gate = LinvP == nullptr;
-      }
+      // large n only: values beyond the exact-int32 bound take the FP64 path
+      may_flag = gg::i8_value_bound(n) < 127;
+      if (may_flag) rc = gg::range_i8_run(n, cnt, g, lg, w.flag, w.colbad, s);
     } else {
-      // FP64 dosages: narrow on the device; exact integers take the int8 tensor-core path, any
-      // other value sends the whole block down the FP64 DMMA path (selected on the device: both
-      // kernels are queued, the one whose gate does not match exits at once; no host sync).
-      GG_CUDA_TRY(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
-      rc = gg::narrow_run(n, cnt, X64, ldx, w.g8, n16, w.flag, s);
-      if (rc == GG_OK)
-        rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, w.g8, n16, nullptr, 0, q,
-                                   XLbar, np, ybar, w.P, w.flag, 0, s);
-      if (rc == GG_OK && LinvP != nullptr) {
-        rc = gg::trsm_packed_gated_run(n, cnt, LinvP, X64, ldx, w.xbar, np, w.flag, 1, s);
-        if (rc == GG_OK)
-          rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1);
-      }
-      invalid_gate = LinvP == nullptr;   // non-integer dosages and no FP64 inverse
+      rc = gg::narrow_run(n, cnt, X64, ldx, w.g8, n16, w.flag, w.colbad, s);
+      g = w.g8;
+      lg = n16;
     }
+    if (rc == GG_OK)
+      rc = gg::trsm_i8_fused_run(n, cnt, slices_as(slices), expo, g, lg, nullptr, 0, q, XLbar,
+                                 np, ybar, w.P, nullptr, 0, w.counter, s);
+    if (rc == GG_OK && may_flag && LinvP != nullptr) {
+      if (G8 != nullptr) {
+        rc = gg::widen_run(n, cnt, G8, ldg, w.x64, np, s);   // (a no-op grid when unflagged
+        x64 = w.x64;                                          //  is not worth a gate: large n)
+        ldx64 = np;
+      }
+      if (rc == GG_OK)
+        rc = gg::trsm_packed_gated_run(n, cnt, LinvP, x64, ldx64, w.xbar, np, w.flag, 1, s);
+      if (rc == GG_OK)
+        rc = gg::partials_run(n, cnt, q, w.xbar, np, XLbar, np, ybar, w.P, s, w.flag, 1,
+                              w.colbad);
+    }
+    invalid_gate = may_flag && LinvP == nullptr;   // flagged columns and no FP64 inverse
   } else {
     const double* xin = X64;
     int ldin = ldx;
@@ -441,7 +450,8 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
   }
   if (rc != GG_OK) return rc;
   rc = gg::reduce_solve_run(n, cnt, q, w.P, nullptr, S_TL, b_T, beta, status, sinv, s);
-  if (rc == GG_OK && invalid_gate) rc = gg::mark_invalid_run(cnt, q + 1, w.flag, 1, beta, status, s);
+  if (rc == GG_OK && invalid_gate)
+    rc = gg::mark_invalid_run(cnt, q + 1, w.flag, 1, beta, status, s, w.colbad);
   return rc;
 }
 

@@ -93,15 +93,19 @@ int row_exponents_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const do
 int slice_meta_run(int n, const int* ex2, int* meta, cudaStream_t s);
 int slice_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B, int ldl,
                  int* meta, signed char* Sl, cudaStream_t s);
-int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, cudaStream_t s);
+// per-column flags (colbad, cnt ints, nullable; set to 1 for a flagged column, never cleared)
+// plus a block flag (*bad |= 1 if any column is flagged)
+int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, int* colbad,
+                 cudaStream_t s);
 int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
-               int* bad, cudaStream_t s);
+               int* bad, int* colbad, cudaStream_t s);
+// counter: one device int of the caller's workspace (the dynamic tile scheduler)
 int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
-                long long ldg, double* X, int ldx, cudaStream_t s);
+                long long ldg, double* X, int ldx, int* counter, cudaStream_t s);
 int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
                       const signed char* G, long long ldg, double* X, int ldx, int q,
                       const double* XL, int ldxl, const double* y, double* P, const int* gate,
-                      int gate_value, cudaStream_t s);
+                      int gate_value, int* counter, cudaStream_t s);
 
 // ---- GLS epilogue + helpers (gls_epilogue.cu) ----------------------------------------
 int dots_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
@@ -114,11 +118,12 @@ int epilogue_run(int n, int cnt, int q, const double* Xbar, int ldx, const doubl
 int widen_run(int n, int cnt, const int8_t* G, long long ldg, double* X, int ldx,
               cudaStream_t s);
 size_t partials_bytes(int n, int cnt, int q);
+// colmask (nullable): only columns with colmask[j] != 0 are written
 int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                  int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
-                 int gate_value);
+                 int gate_value, const int* colmask = nullptr);
 int mark_invalid_run(int cnt, int p, const int* gate, int gate_value, double* beta, int* status,
-                     cudaStream_t s);
+                     cudaStream_t s, const int* colmask = nullptr);
 int reduce_solve_run(int n, int cnt, int q, const double* P, double* dots, const double* S_TL,
                      const double* b_T, double* beta, int* status, double* sinv, cudaStream_t s);
 

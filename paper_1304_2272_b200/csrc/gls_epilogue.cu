@@ -115,7 +115,7 @@ template <int QM, int PCOLS>          // PCOLS columns per CTA (one per warp)
 __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
     int nrb, int cnt, int q, const double* __restrict__ X, long long ldx,
     const double* __restrict__ XL, long long ldxl, const double* __restrict__ y,
-    double* __restrict__ P, const int* gate, int gate_value) {
+    double* __restrict__ P, const int* gate, int gate_value, const int* __restrict__ colmask) {
   if (gate != nullptr && *gate != gate_value) return;
   extern __shared__ double sm[];
   constexpr int LDP = PROWS + PRB;                   // padded: row r at r + r / RB
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
   __syncthreads();
   const int rb = rb0 + lane;
   if (col >= cnt || rb >= nrb) return;
+  if (colmask != nullptr && colmask[col] == 0) return;   // column computed by another path
   const double* xr = mx + lane * (RB + 1);
   double acc[QM + 2];
 #pragma unroll
@@ -256,15 +257,17 @@ __global__ void small_solve_kernel(int batch, int p, const double* __restrict__ 
   for (int i = 0; i < p; ++i) x[(long long)b * p + i] = xo[i];
 }
 
-// Block-level rejection (device-side): if *gate == gate_value every SNP of the block gets
-// status GG_STATUS_INVALID and NaN coefficients (values the selected path cannot compute exactly
+// Rejection (device-side): if *gate == gate_value every SNP of the block (or, with colmask, every
+// flagged SNP) gets status GG_STATUS_INVALID and NaN coefficients (values the selected path cannot compute exactly
 // and no FP64 inverse to fall back on).
 __global__ void mark_invalid_kernel(int cnt, int p, const int* __restrict__ gate, int gate_value,
-                                    double* __restrict__ beta, int* __restrict__ status) {
+                                    double* __restrict__ beta, int* __restrict__ status,
+                                    const int* __restrict__ colmask) {
   if (*gate != gate_value) return;
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)cnt * p;
        e += (long long)gridDim.x * blockDim.x) {
+    if (colmask != nullptr && colmask[e / p] == 0) continue;   // only the flagged columns
     beta[e] = qnan;
     if (e % p == 0) status[e / p] = GG_STATUS_INVALID;
   }
@@ -295,24 +298,30 @@ int check_ld(int n, int ldx, int ldxl) {
 template <int QM, int PC>
 static int launch_partials(int nrb, int cnt, int q, const double* Xbar, int ldx,
                            const double* XLbar, int ldxl, const double* ybar, double* P,
-                           cudaStream_t s, const int* gate, int gate_value) {
+                           cudaStream_t s, const int* gate, int gate_value,
+                           const int* colmask) {
   dim3 grid((cnt + PC - 1) / PC, (nrb + PRB - 1) / PRB);
   const size_t sm = (size_t)(q + 1 + PC) * (PROWS + PRB) * sizeof(double);
   GG_CUDA_TRY(cudaFuncSetAttribute(partials_kernel<QM, PC>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   partials_kernel<QM, PC><<<grid, PC * 32, sm, s>>>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P,
-                                                    gate, gate_value);
+                                                    gate, gate_value, colmask);
   GG_LAUNCH_CHECK("partials_kernel");
   return GG_OK;
 }
 
 int partials_run(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                  int ldxl, const double* ybar, double* P, cudaStream_t s, const int* gate,
-                 int gate_value) {
+                 int gate_value, const int* colmask) {
   const int nrb = pad_rows(n) / RB;
-  if (q <= 3) return launch_partials<3, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
-  if (q <= 7) return launch_partials<7, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
-  return launch_partials<QMAX, 4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate, gate_value);
+  if (q <= 3)
+    return launch_partials<3, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate,
+                                 gate_value, colmask);
+  if (q <= 7)
+    return launch_partials<7, 8>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate,
+                                 gate_value, colmask);
+  return launch_partials<QMAX, 4>(nrb, cnt, q, Xbar, ldx, XLbar, ldxl, ybar, P, s, gate,
+                                  gate_value, colmask);
 }
 
 template <int QM, int PM>
@@ -329,10 +338,10 @@ static int launch_reduce(int nrb, int cnt, int q, const double* P, double* dots,
 }
 
 int mark_invalid_run(int cnt, int p, const int* gate, int gate_value, double* beta, int* status,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int* colmask) {
   if (cnt <= 0) return GG_OK;
   const int grid = (int)(((long long)cnt * p + 255) / 256 > 1184 ? 1184 : ((long long)cnt * p + 255) / 256);
-  mark_invalid_kernel<<<grid, 256, 0, s>>>(cnt, p, gate, gate_value, beta, status);
+  mark_invalid_kernel<<<grid, 256, 0, s>>>(cnt, p, gate, gate_value, beta, status, colmask);
   GG_LAUNCH_CHECK("mark_invalid_kernel");
   return GG_OK;
 }

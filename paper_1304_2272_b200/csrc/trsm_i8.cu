@@ -30,7 +30,6 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
-#include <map>
 #include <mutex>
 #include <string>
 
@@ -684,7 +683,7 @@ __global__ void slice_rows_kernel(int np, Src src, int* __restrict__ meta,
 // bytes.  HBM-bound: 8 B read + 1 B written per dosage.
 __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long long ldx,
                               signed char* __restrict__ G, long long ldg, double gmax,
-                              int* __restrict__ bad) {
+                              int* __restrict__ bad, int* __restrict__ colbad) {
   const long long nw_rows = (long long)((n + 15) & ~15) < ldg ? (long long)((n + 15) & ~15) : ldg;
   const int rows = (int)nw_rows;
   const int segs = (rows + 511) / 512;
@@ -701,6 +700,7 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
     const int r0 = (int)(e - j * segs) * 512;
     const double* col = X + j * ldx + r0;
     signed char* dst = G + j * ldg + r0;
+    int seg_bad = 0;
     if (vec && r0 + 512 <= n) {
       double2 v[8];
 #pragma unroll
@@ -710,7 +710,7 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
       for (int h = 0; h < 8; ++h) {
         const bool ok0 = (v[h].x == trunc(v[h].x)) && fabs(v[h].x) <= gmax;
         const bool ok1 = (v[h].y == trunc(v[h].y)) && fabs(v[h].y) <= gmax;
-        local_bad |= (ok0 && ok1) ? 0 : 1;
+        seg_bad |= (ok0 && ok1) ? 0 : 1;
         const unsigned w = ((unsigned)(ok0 ? (int)v[h].x : 0) & 0xffu) |
                            (((unsigned)(ok1 ? (int)v[h].y : 0) & 0xffu) << 8);
         *reinterpret_cast<unsigned short*>(dst + 2 * (32 * h + lane)) = (unsigned short)w;
@@ -725,30 +725,43 @@ __global__ void narrow_kernel(int n, int cnt, const double* __restrict__ X, long
           if (r0 + r < n) {
             const double v = col[r];
             const bool ok = (v == trunc(v)) && fabs(v) <= gmax;
-            local_bad |= ok ? 0 : 1;
+            seg_bad |= ok ? 0 : 1;
             g = ok ? (int)v : 0;
           }
           dst[r] = (signed char)g;
         }
       }
     }
+    // the segment's column is flagged on its own: every column takes its path from its own
+    // values only (a column's result never depends on its neighbours)
+    if (__any_sync(0xffffffffu, seg_bad != 0)) {
+      local_bad = 1;
+      if (lane == 0 && colbad != nullptr) atomicOr(colbad + j, 1);
+    }
   }
-  if (__any_sync(0xffffffffu, local_bad != 0) && lane == 0) atomicOr(bad, 1);
+  if (local_bad && lane == 0) atomicOr(bad, 1);
 }
 
-// int8 dosages: *bad |= 1 if any |g| exceeds gmax (the exact-int32 bound for this n).
+// int8 dosages: per column, colbad[j] |= 1 (and *bad |= 1) if any |g| exceeds gmax (the
+// exact-int32 bound for this n).  One warp per column at a time.
 __global__ void range_i8_kernel(int n, int cnt, const signed char* __restrict__ G, long long ldg,
-                                int gmax, int* __restrict__ bad) {
-  const long long total = (long long)n * cnt;
-  bool b = false;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long j = e / n;
-    const int i = (int)(e - j * n);
-    const int g = G[j * ldg + i];
-    b |= (g > gmax) || (g < -gmax);
+                                int gmax, int* __restrict__ bad, int* __restrict__ colbad) {
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  bool any = false;
+  for (long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; j < cnt;
+       j += nwarps) {
+    bool b = false;
+    for (int i = lane; i < n; i += 32) {
+      const int g = G[j * ldg + i];
+      b |= (g > gmax) || (g < -gmax);
+    }
+    if (__any_sync(0xffffffffu, b)) {
+      any = true;
+      if (lane == 0 && colbad != nullptr) atomicOr(colbad + j, 1);
+    }
   }
-  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+  if (any && lane == 0) atomicOr(bad, 1);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn_i8() {
@@ -781,30 +794,6 @@ int encode(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
     return GG_ECUDA;
   }
   return GG_OK;
-}
-
-// A zeroed int per launch for the dynamic tile scheduler: a ring of counters per device, each
-// cleared on the launch stream just before use.
-int* tile_counter(cudaStream_t s) {
-  static std::mutex mu;
-  static std::map<int, int*> bufs;
-  static unsigned next = 0;
-  constexpr unsigned RING = 4096;
-  std::lock_guard<std::mutex> g(mu);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  int*& buf = bufs[dev];
-  if (buf == nullptr && cudaMalloc(&buf, RING * sizeof(int)) != cudaSuccess) {
-    buf = nullptr;
-    set_error("trsm_i8: cannot allocate the tile counters");
-    return nullptr;
-  }
-  int* p = buf + (next++ % RING);
-  if (cudaMemsetAsync(p, 0, sizeof(int), s) != cudaSuccess) {
-    set_error("trsm_i8: cannot clear the tile counter");
-    return nullptr;
-  }
-  return p;
 }
 
 int sms() {
@@ -892,17 +881,18 @@ int i8_value_bound(int n) {
   return b >= 127 ? 127 : (int)b;
 }
 
-int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, cudaStream_t s) {
+int range_i8_run(int n, int cnt, const signed char* G, long long ldg, int* bad, int* colbad,
+                 cudaStream_t s) {
   if (cnt <= 0 || i8_value_bound(n) >= 127) return GG_OK;
-  long long grid = ((long long)n * cnt + 255) / 256;
+  long long grid = ((long long)cnt + 7) / 8;   // 8 warps (columns) per block
   if (grid > 148LL * 16) grid = 148LL * 16;
-  range_i8_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, G, ldg, i8_value_bound(n), bad);
+  range_i8_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, G, ldg, i8_value_bound(n), bad, colbad);
   GG_LAUNCH_CHECK("range_i8_kernel");
   return GG_OK;
 }
 
 int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, long long ldg,
-               int* bad, cudaStream_t s) {
+               int* bad, int* colbad, cudaStream_t s) {
   if (ldx < n || ldg < n) {
     set_error("narrow: leading dimensions too small");
     return GG_EDIM;
@@ -910,27 +900,32 @@ int narrow_run(int n, int cnt, const double* X, long long ldx, signed char* G, l
   if (cnt <= 0) return GG_OK;
   long long grid = ((long long)((n + 511) / 512) * cnt + 7) / 8;   // 8 warps per block
   if (grid > 148LL * 16) grid = 148LL * 16;
-  narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, (double)i8_value_bound(n), bad);
+  narrow_kernel<<<(int)grid, 256, 0, s>>>(n, cnt, X, ldx, G, ldg, (double)i8_value_bound(n), bad,
+                                          colbad);
   GG_LAUNCH_CHECK("narrow_kernel");
   return GG_OK;
 }
 
 int trsm_i8_run(int n, int nrhs, const signed char* Sl, const int* expo, const signed char* G,
-                long long ldg, double* X, int ldx, cudaStream_t s) {
+                long long ldg, double* X, int ldx, int* counter, cudaStream_t s) {
   return trsm_i8_fused_run(n, nrhs, Sl, expo, G, ldg, X, ldx, 0, nullptr, 0, nullptr, nullptr,
-                           nullptr, 0, s);
+                           nullptr, 0, counter, s);
 }
 
 int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
                       const signed char* G, long long ldg, double* X, int ldx, int q,
                       const double* XL, int ldxl, const double* y, double* P, const int* gate,
-                      int gate_value, cudaStream_t s) {
+                      int gate_value, int* counter, cudaStream_t s) {
   const int np = pad_rows(n);
   if ((X != nullptr && ldx < np) || ldg < n || (ldg % 16) != 0 || (P != nullptr && ldxl < np)) {
     set_error("trsm_i8: ldx >= gg_pad(n), ldg >= n and ldg a multiple of 16 required");
     return GG_EDIM;
   }
   if (nrhs <= 0) return GG_OK;
+  if (counter == nullptr) {
+    set_error("trsm_i8: no tile counter (workspace) given");
+    return GG_EARG;
+  }
   if ((reinterpret_cast<uintptr_t>(Sl) | reinterpret_cast<uintptr_t>(G) |
        reinterpret_cast<uintptr_t>(X)) & 15) {
     set_error("trsm_i8: operands must be 16-byte aligned");
@@ -973,8 +968,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
   a.P = P;
   a.gate = gate;
   a.gate_value = gate_value;
-  a.tile_counter = tile_counter(s);
-  if (a.tile_counter == nullptr) return GG_ECUDA;
+  // the dynamic tile scheduler's counter lives in the caller's workspace, cleared on the
+  // launch stream (stream-ordered with the kernel that uses it)
+  GG_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int), s));
+  a.tile_counter = counter;
   {
     const int pairs = (a.num_rb / 2) * ((a.num_nt + 1) / 2);   // tiles
     int clusters = sms() / 2;

@@ -15,7 +15,8 @@ p x p Cholesky solve).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import threading
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -138,18 +139,72 @@ class ResultArrays:
         return self.status == -1
 
 
-@dataclass
 class ResultBlock:
     """(kernel.py:62-65).  ``results`` is list-like; ``arrays`` (when present) is the array
-    form used by the vectorised BlockWriter."""
+    form used by the vectorised BlockWriter.
 
-    first_index: int
-    results: object = field(default_factory=list)
-    arrays: ResultArrays | None = None
+    A block returned by ``gls_solve_block`` may still be computing on the device when the call
+    returns (its input has been copied, so the caller may reuse the buffer, as the reference's
+    double buffer does, pipeline.py:195-212): the first read of ``results`` or ``arrays`` waits
+    for it.  That lets consecutive calls overlap the next block's host->device copy with this
+    block's TRSM."""
+
+    def __init__(self, first_index, results=None, arrays=None):
+        self.first_index = first_index
+        self._results = [] if results is None and arrays is None else results
+        self._arrays = arrays
+        self._pending = None
 
     @classmethod
     def from_arrays(cls, arrays):
         return cls(first_index=arrays.first_index, results=_LazyResults(arrays), arrays=arrays)
+
+    @classmethod
+    def pending(cls, first_index, resolve):
+        """A block whose arrays come from ``resolve()`` on first access."""
+        b = cls(first_index)
+        b._pending = resolve
+        return b
+
+    def _resolve(self):
+        if self._pending is not None:
+            resolve, self._pending = self._pending, None
+            arrays = resolve()
+            self._arrays = arrays
+            self._results = _LazyResults(arrays)
+
+    @property
+    def done(self):
+        return self._pending is None
+
+    @property
+    def results(self):
+        self._resolve()
+        return self._results
+
+    @results.setter
+    def results(self, value):
+        self._pending = None
+        self._results = value
+
+    @property
+    def arrays(self):
+        self._resolve()
+        return self._arrays
+
+    @arrays.setter
+    def arrays(self, value):
+        self._pending = None
+        self._arrays = value
+
+    def __eq__(self, other):
+        if not isinstance(other, ResultBlock) and not hasattr(other, "results"):
+            return NotImplemented
+        return self.first_index == other.first_index and list(self.results) == list(other.results)
+
+    def __repr__(self):
+        state = "pending" if self._pending is not None else f"{len(self.results)} results"
+        return f"ResultBlock(first_index={self.first_index}, {state})"
 
 
 class PreparedContext:
@@ -266,8 +321,9 @@ def _trsm_i8_device(slices, expo, n, A):
     G[:, :n] = torch.from_numpy(np.ascontiguousarray(A.T).astype(np.int8))
     G = G.to(slices.device)
     X = alloc_cols(A.shape[1], pad(n))
+    work = _capi.i8_work(slices.device)
     check(_capi.lib().gg_trsm_lower_i8(n, A.shape[1], ptr(slices), ptr(expo), ptr(G), n16, ptr(X),
-                                       pad(n), stream_handle()), "gg_trsm_lower_i8")
+                                       pad(n), ptr(work), stream_handle()), "gg_trsm_lower_i8")
     return X
 
 
@@ -581,25 +637,87 @@ def solve_whitened_block(ctx, Xbar, first_index, global_indices=None, emit_s_inv
     return list(_collect(ws, cnt, first_index, global_indices, emit_s_inv).results)
 
 
+class _BlockStream:
+    """One calling thread's device stream for gls_solve_block: a pipeline.StreamEngine (pinned
+    result buffers, copy + compute streams, DEV_REGIONS device regions) plus the blocks still
+    pending in its regions.  A block's region is resolved (results copied to the host) before it
+    is reused, so a caller may hold any number of unresolved ResultBlocks."""
+
+    def __init__(self, engine):
+        self.engine = engine
+        self.owner = {}            # device region -> its pending ResultBlock
+
+    def submit(self, data, first, cnt):
+        eng = self.engine
+        r = eng._next % eng.DEV_REGIONS
+        prev = self.owner.pop(r, None)
+        if prev is not None:
+            prev._resolve()         # frees region r (collect -> host arrays)
+        t = eng.begin(first, cnt)
+        try:
+            eng.h2d(t, data, 0, cnt, slot=t)
+        except Exception:
+            eng.busy[t] = False
+            raise
+        eng.launch(t)
+        # the caller may reuse `data` once this returns (the reference's double buffer,
+        # pipeline.py:195-212): wait for the copy, not for the compute
+        eng.wait_h2d(t)
+        blk = ResultBlock.pending(first, lambda: self._collect(t))
+        self.owner[t] = blk
+        return blk
+
+    def _collect(self, t):
+        self.owner.pop(t, None)
+        return self.engine.collect(t)
+
+
+_streams_lock = threading.Lock()
+
+
+def _block_stream(ctx, d, int8, emit_s_inv, cnt):
+    """The calling thread's block stream for this device context and input kind (rebuilt with
+    more room when a larger block arrives).  Kept on the context itself, so it lives and dies
+    with it; one per thread (run_spmd's inproc ranks call concurrently, transport.py:279-291)."""
+    from . import pipeline
+
+    with _streams_lock:
+        cache = d.__dict__.setdefault("_block_streams", {})
+    key = (threading.get_ident(), bool(int8), bool(emit_s_inv), _capi.device().index)
+    bs = cache.get(key)
+    if bs is not None and bs.engine.m_blk < cnt:
+        for blk in list(bs.owner.values()):
+            blk._resolve()
+        bs = None
+    if bs is None:
+        m_blk = int(cnt)           # a stream's blocks share one size (the last may be shorter)
+        shim = type("_Ctx", (), {"_dev": d})()
+        bs = cache[key] = _BlockStream(pipeline.StreamEngine(shim, m_blk, int8=int8,
+                                                             emit_s_inv=emit_s_inv))
+    return bs
+
+
 def gls_solve_block(ctx, blk, emit_s_inv=False, threads=1):
     """Solve every marker in the block against the prepared context (kernel.py:315-342).
 
-    One TRSM launch (Linv * X on DMMA tiles) plus one fused epilogue launch; ``threads`` is
-    accepted for signature compatibility (results never depend on it)."""
+    The block is copied to the device on a copy stream and solved on a compute stream (int8
+    tensor-core TRSM with the reductions fused into its epilogue, then the batched p x p solves;
+    per-column fallback to the FP64 DMMA TRSM for non-integer dosages).  The call returns once
+    the copy is done; the ResultBlock resolves on first access, so back-to-back calls overlap the
+    next block's copy with this block's compute.  ``threads`` is accepted for signature
+    compatibility (results never depend on it, tests/test_kernel.py:243-256)."""
     d = device_context(ctx, need_factor=True)
     if blk.n != d.n:
         raise DimensionMismatch(f"block has n={blk.n}, context has n={d.n}")
     cnt = blk.count
-    int8 = blk.data.dtype == np.int8
-    ws = BlockWorkspace(d, cnt, emit_s_inv=emit_s_inv, int8_input=int8)
-    if int8:
-        n16 = -(-d.n // 16) * 16
-        G = upload_cols(blk.data, ld=n16)
-        ws.run(cnt, G8=G, ldg=n16)
-    else:
-        X = upload_cols(np.asarray(blk.data, dtype=np.float64), ld=d.np_)
-        ws.run(cnt, X64=X, ldx=d.np_)
-    return _collect(ws, cnt, blk.first_index, None, emit_s_inv)
+    data = blk.data
+    int8 = data.dtype == np.int8
+    if not int8:
+        data = np.asarray(data, dtype=np.float64)
+    if not data.flags.f_contiguous:
+        data = np.asfortranarray(data)
+    bs = _block_stream(ctx, d, int8, emit_s_inv, cnt)
+    return bs.submit(data, blk.first_index, cnt)
 
 
 def gls_oracle(M, Xi, y):

@@ -198,6 +198,10 @@ class StreamEngine:
                        .pin_memory() if emit_s_inv else None for _ in range(R)]
         self.copy_stream = torch.cuda.Stream()
         self.compute_stream = torch.cuda.Stream()
+        # the regions above were allocated (and zero-filled: the padding rows the TRSM reads)
+        # on the current stream; order both engine streams after that work
+        self.copy_stream.wait_stream(torch.cuda.current_stream())
+        self.compute_stream.wait_stream(torch.cuda.current_stream())
         self.h2d_start = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
         self.h2d_done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]
         self.done = [torch.cuda.Event(enable_timing=True) for _ in range(R)]

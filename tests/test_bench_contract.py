@@ -44,7 +44,7 @@ def test_reference_arm_contract():
 
 @pytest.mark.gpu
 def test_gpu_arm_contract(gpu):
-    d = _run(["--config", "0", "--steps", "3", "--warmup", "3"])
+    d = _run(["--config", "0", "--steps", "3", "--warmup", "3", "--no-secondary"])
     _check_base(d)
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor") and r["achieved"] > 0 and r["peak"] > 0
@@ -56,3 +56,50 @@ def test_gpu_arm_contract(gpu):
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["parity"]["within"] and d["parity"]["status_mismatches"] == 0
+
+
+def test_gpus_flag_starts_n_ranks():
+    """`python bench.py --gpus N` without torchrun re-executes itself under
+    torch.distributed.run with N ranks (here: the gloo launch probe, no GPU needed)."""
+    env = dict(os.environ, GG_BENCH_LAUNCH_PROBE="1")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2"],
+                         cwd=REPO, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert d == {"n_gpus": 2, "ranks_seen": 2}
+
+
+def test_gpus_flag_mismatch_fails_loudly():
+    env = dict(os.environ, GG_BENCH_LAUNCH_PROBE="1", WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "4"],
+                         cwd=REPO, capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in (out.stderr + out.stdout)
+
+
+def test_parity_sample_covers_first_interior_and_last_partial_blocks():
+    sys.path.insert(0, REPO)
+    import bench
+
+    m, blk = 2_000_000, 8192
+    cols, picks = bench.sample_columns(m, blk, 512)
+    nb = -(-m // blk)
+    assert picks[0] == 0 and picks[-1] == nb - 1 and len(picks) == 4
+    assert len(cols) == 4 * 512                         # the last block has 1,152 >= 512
+    assert cols.min() == 0 and cols.max() == m - 1
+    for b in picks:               # both edges of every sampled block
+        f = b * blk
+        c = min(blk, m - f)
+        assert f in cols and f + c - 1 in cols
+    small, _ = bench.sample_columns(300, 128, 512)      # blocks shorter than the sample
+    assert small.max() == 299 and len(set(small.tolist())) == len(small)
+
+
+def test_kinship_host_lean_matches_reference_construction():
+    sys.path.insert(0, REPO)
+    import numpy as np
+
+    import bench
+    from paper_1304_2272_b200 import datagen
+
+    spec = datagen.BaselineSpec(n=300, m=10, p=4, m_kin=200, a=0.5)
+    assert np.array_equal(bench.kinship_host_lean(spec), datagen.kinship_covariance_host(spec))

@@ -109,8 +109,9 @@ def test_argument_validation_without_a_gpu():
     cases = [
         (lib.gg_potrf_f64, (0, V, 1, 0, V, V, 128, V, V, V), EARG),
         (lib.gg_trtri_lower_f64, (0, V, 128, V, 128, V, V), EARG),
-        (lib.gg_trsm_lower_i8, (0, 1, V, V, V, 16, V, 128, V), EARG),
-        (lib.gg_trsm_lower_i8_partials, (10, 1, V, V, V, 16, 3, V, V, V, V, 0, V, 0, V), EARG),
+        (lib.gg_trsm_lower_i8, (0, 1, V, V, V, 16, V, 128, V, V), EARG),
+        (lib.gg_trsm_lower_i8_partials, (10, 1, V, V, V, 16, 3, V, V, V, V, 0, V, 0, V, V),
+         EARG),
         (lib.gg_gls_reduce_solve_f64, (10, 1, 3, V, V, V, V, V, V, V), EARG),
         (lib.gg_gls_block_f64, (10, 3, 1, V, V, V, V, V, V, V, V, 0, V, 0, V, V, V, V, V), EARG),
         (lib.gg_slice_inverse_i8, (0, V, 128, V, V, V), EARG),

@@ -152,6 +152,58 @@ def test_non_integer_block_falls_back_to_dmma(K):
         assert mism == 0 and rel <= 1e-11, rel
 
 
+@pytest.mark.parametrize("m_blk", [1, 7, 40, 64])
+def test_path_selection_is_per_column(K, m_blk):
+    """Integer and fractional dosages in one block: every column takes its path (int8 tensor
+    cores or FP64 DMMA) from its own values, so an integer column's result is bitwise the same
+    whatever its neighbours, the block size or its position (a block-wide gate made it
+    depend on them).  Fractional columns still match the oracle; the same holds for int8 blocks
+    with values past the exact bound (simulated by a large value in a FP64 block)."""
+    from oracle import gls_ref as O
+
+    rng = np.random.default_rng(31)
+    n = 300
+    M = make_spd(n, 8)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 2))])
+    y = rng.standard_normal(n)
+    X = rng.integers(0, 3, (n, 64)).astype(float)
+    frac = [3, 10, 11, 40, 63]
+    X[:, frac] += rng.uniform(0.05, 0.95, (n, len(frac)))      # imputed (fractional) dosages
+    X[5, 20] = 300.0                                           # out of int8 range
+    ctx = K.gls_prepare(M, XL, y)
+    alone = _betas(K.gls_solve_block(ctx, K.SnpBlock(0, np.delete(X, frac + [20], axis=1))))
+    got = np.concatenate([_betas(K.gls_solve_block(ctx, K.SnpBlock(f, X[:, f:f + m_blk])))
+                          for f in range(0, 64, m_blk)])
+    ints = [j for j in range(64) if j not in frac + [20]]
+    assert np.array_equal(got[ints], alone, equal_nan=True)
+    octx = O.gls_prepare(M, XL, y)
+    ref, _ = O.gls_solve_block(octx, X)
+    rel, mism = O.compare(got, ref)
+    assert mism == 0 and rel <= 1e-11, rel
+
+
+def test_pending_result_blocks_pipeline(K):
+    """gls_solve_block returns once the block's copy is done; results resolve on first access.
+    Many unresolved blocks (more than the stream's device regions), a reused host buffer and
+    out-of-order resolution give exactly the results of resolving each call at once."""
+    rng = np.random.default_rng(12)
+    n = 257
+    M = make_spd(n, 4)
+    XL = np.hstack([np.ones((n, 1)), rng.standard_normal((n, 1))])
+    ctx = K.gls_prepare(M, XL, rng.standard_normal(n))
+    blocks = [rng.integers(0, 3, (n, 33)).astype(np.int8, order="F") for _ in range(7)]
+    eager = [_betas(K.gls_solve_block(ctx, K.SnpBlock(33 * i, b))) for i, b in enumerate(blocks)]
+    buf = np.empty((n, 33), dtype=np.int8, order="F")
+    pend = []
+    for i, b in enumerate(blocks):
+        buf[...] = b                                   # the caller's reused double buffer
+        pend.append(K.gls_solve_block(ctx, K.SnpBlock(33 * i, buf)))
+    assert not all(p.done for p in pend)
+    for i in (6, 0, 3, 1, 2, 5, 4):
+        assert pend[i].first_index == 33 * i
+        assert np.array_equal(_betas(pend[i]), eager[i], equal_nan=True)
+
+
 def test_intercept_duplicate_exactly_singular(K):
     """A SNP equal to the intercept: whitened by the same tensor-core kernel as X_L[:,0] and
     reduced in the same order, S is exactly singular and the SNP is flagged degenerate."""
@@ -251,10 +303,11 @@ def test_dynamic_scheduler_stress_deterministic(K):
             P = torch.empty(int(lib.gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64,
                             device="cuda")
             ref = None
+            W = _capi.i8_work()
             for rep in range(40):
                 assert lib.gg_trsm_lower_i8_partials(n, cnt, ptr(d.slices), ptr(d.expo), ptr(G),
                                                      n16, d.q, ptr(d.XLy), ptr(d.ybar), ptr(P),
-                                                     None, 0, None, 0, s) == 0
+                                                     None, 0, None, 0, ptr(W), s) == 0
                 if rep == 0:
                     ref = P.clone()
             torch.cuda.synchronize()

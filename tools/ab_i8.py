@@ -22,13 +22,14 @@ G16 = datagen.genotypes_device(spec, 0, cnt, ld=n16)
 P = torch.empty(int(_capi.lib().gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64,
                 device="cuda")
 s = _capi.stream_handle()
+W = _capi.i8_work()
 libs = []
 for path in [_capi.LIB_PATH] + sys.argv[1:]:
     lib = C.CDLL(path)
     f = lib.gg_trsm_lower_i8_partials
     f.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int,
                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
-                  C.c_void_p]
+                  C.c_void_p, C.c_void_p]
     lib.gg_inverse_slices_bytes.restype = C.c_size_t
     lib.gg_inverse_slices_bytes.argtypes = [C.c_int]
     lib.gg_slice_packed_inverse_i8.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -66,7 +67,7 @@ for rep in range(8):
         with _Env(name):
             a.record()
             rc = f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
-                   ptr(P), None, 0, None, 0, s)
+                   ptr(P), None, 0, None, 0, ptr(W), s)
             b.record()
         torch.cuda.synchronize()
         assert rc == 0, rc
@@ -92,7 +93,7 @@ for rnd in range(2 if sustain > 0 else 0):
                 if r == reps // 2:
                     a.record()
                 f(n, cnt, ptr(sl), ptr(meta), ptr(G16), n16, d.q, ptr(d.XLy), ptr(d.ybar),
-                  ptr(P), None, 0, None, 0, s)
+                  ptr(P), None, 0, None, 0, ptr(W), s)
             b.record()
         torch.cuda.synchronize()
         print(f"sustained round {rnd} {name}: {a.elapsed_time(b) / (reps - reps // 2):.3f} ms")

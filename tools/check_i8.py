@@ -24,6 +24,7 @@ def main():
     args = ap.parse_args()
     lib = _capi.lib()
     s = stream_handle()
+    W = _capi.i8_work()
     for n in args.n:
         spec = datagen.BaselineSpec(n=n, m=args.cnt, p=4)
         Md = datagen.kinship_covariance_device(spec)
@@ -43,7 +44,7 @@ def main():
         Xi = alloc_cols(args.cnt, np_)
         check(lib.gg_trsm_lower_packed_f64(n, args.cnt, ptr(LinvP), ptr(X64), np_, ptr(Xd), np_,
                                            s), "trsm dmma")
-        check(lib.gg_trsm_lower_i8(n, args.cnt, ptr(sl), ptr(expo), ptr(G), ldg, ptr(Xi), np_, s),
+        check(lib.gg_trsm_lower_i8(n, args.cnt, ptr(sl), ptr(expo), ptr(G), ldg, ptr(Xi), np_, ptr(W), s),
               "trsm i8")
         torch.cuda.synchronize()
         diff = (Xi[:, :n] - Xd[:, :n]).abs().max().item()
@@ -55,14 +56,14 @@ def main():
         perm = torch.randperm(args.cnt, device="cuda")
         Gp = G[perm].contiguous()
         Xp = alloc_cols(args.cnt, np_)
-        check(lib.gg_trsm_lower_i8(n, args.cnt, ptr(sl), ptr(expo), ptr(Gp), ldg, ptr(Xp), np_, s),
+        check(lib.gg_trsm_lower_i8(n, args.cnt, ptr(sl), ptr(expo), ptr(Gp), ldg, ptr(Xp), np_, ptr(W), s),
               "trsm i8 perm")
         torch.cuda.synchronize()
         print(f"  permutation bitwise: {bool(torch.equal(Xp, Xi[perm]))}", flush=True)
         for name, fn in (("dmma", lambda: lib.gg_trsm_lower_packed_f64(
                 n, args.cnt, ptr(LinvP), ptr(X64), np_, ptr(Xd), np_, s)),
                          ("i8", lambda: lib.gg_trsm_lower_i8(
-                n, args.cnt, ptr(sl), ptr(expo), ptr(G), ldg, ptr(Xi), np_, s))):
+                n, args.cnt, ptr(sl), ptr(expo), ptr(G), ldg, ptr(Xi), np_, ptr(W), s))):
             fn()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

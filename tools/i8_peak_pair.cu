@@ -5,6 +5,7 @@
 // Usage: tools/i8_peak_pair [N ...]   (default 224 256)
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
@@ -78,6 +79,35 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int grid = prop.multiProcessorCount & ~1;
+  if (argc > 2 && std::string(argv[1]) == "--sustain") {
+    // sustained rate: back-to-back launches for S seconds (the board reaches its power cap);
+    // the rate over everything after the first second
+    const double secs = atof(argv[2]);
+    const int N = argc > 3 ? atoi(argv[3]) : 224;
+    const int iters = 2000;
+    const double ops1 = 2.0 * 256 * N * 32 * 64.0 * iters * (grid / 2);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double total_ms = 0.0, ops = 0.0, warm_ms = 0.0;
+    while (total_ms < secs * 1e3) {
+      cudaEventRecord(a);
+      for (int k = 0; k < 16; ++k) i8_peak_pair_kernel<<<grid, 128, smem>>>(iters, N, sink);
+      cudaEventRecord(b);
+      CK(cudaEventSynchronize(b));
+      CK(cudaGetLastError());
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (total_ms >= 1000.0) {
+        warm_ms += ms;
+        ops += 16 * ops1;
+      }
+      total_ms += ms;
+    }
+    printf("int8 tcgen05 cta_group::2 M256 N%d K32 x %d SMs, sustained %.1f s: %.1f TOPS\n", N,
+           grid, total_ms / 1e3, ops / warm_ms / 1e9);
+    return 0;
+  }
   const int nn = argc > 1 ? argc - 1 : 2;
   for (int a = 0; a < nn; ++a) {
     const int N = argc > 1 ? atoi(argv[a + 1]) : (a == 0 ? 224 : 256);

@@ -39,6 +39,7 @@ def main():
     M = Md.cpu().numpy()
     XL, y = datagen.covariates_host(spec)
     s = _capi.stream_handle()
+    W = _capi.i8_work()
     # prepare breakdown
     for rep in range(2):
         t0 = time.perf_counter()
@@ -79,7 +80,7 @@ def main():
         a.record()
         check(lib.gg_trsm_lower_i8_partials(n, args.cnt, ptr(d.slices), ptr(d.expo), ptr(G16), n16,
                                             d.q, ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0, None, 0,
-                                            s), "trsm_i8")
+                                            ptr(W), s), "trsm_i8")
         b.record()
         check(lib.gg_gls_reduce_solve_f64(n, args.cnt, d.q, ptr(P), ptr(d.S_TL), ptr(d.b_T),
                                           ptr(beta), ptr(st), None, s), "reduce")

@@ -18,11 +18,12 @@ n16 = -(-n // 16) * 16
 G16 = datagen.genotypes_device(spec, 0, cnt, ld=n16)
 P = torch.empty(int(lib.gg_partials_bytes(n, cnt, d.q)) // 8, dtype=torch.float64, device="cuda")
 s = _capi.stream_handle()
+W = _capi.i8_work()
 for rep in range(2):
     if rep:
         torch.cuda.nvtx.range_push("hot")
     check(lib.gg_trsm_lower_i8_partials(n, cnt, ptr(d.slices), ptr(d.expo), ptr(G16), n16, d.q,
-                                        ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0, None, 0, s), "i8")
+                                        ptr(d.XLy), ptr(d.ybar), ptr(P), None, 0, None, 0, ptr(W), s), "i8")
     if rep:
         torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
