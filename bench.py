@@ -279,6 +279,13 @@ class Sweep:
         self._capi = _capi
 
     def step(self, record):
+        self.torch.cuda.nvtx.range_push("step")
+        try:
+            self._step(record)
+        finally:
+            self.torch.cuda.nvtx.range_pop()
+
+    def _step(self, record):
         lib, ptr, d, torch = self.lib, self.ptr, self.d, self.torch
         n, q, np_, n16 = self.n, self.q, self.np_, self.n16
         stream, sh = self.stream, self.sh

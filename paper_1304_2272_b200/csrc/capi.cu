@@ -1,12 +1,17 @@
 // extern "C" entry points of libgwasgls_b200.so (declared in include/gwasgls_b200.h).
 // Each validates its arguments, runs on the caller's stream and current device, and reports
 // failures through a status code plus a thread-local message.
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdio>
 #include <string>
 
 #include "gg_internal.cuh"
 
 namespace gg {
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 namespace {
 thread_local std::string g_last_error;
@@ -40,6 +45,7 @@ size_t gg_potrf_workspace_bytes(int n) { return n < 1 ? 0 : gg::potrf_ws_bytes(n
 
 int gg_potrf_f64(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv,
                  int ldp, void* work, int* info_host, void* stream) {
+  GG_NVTX("gg_potrf_f64");
   return gg::potrf_run(n, M, ldm, m_row_major, L, Linv, ldp, work, info_host, as_stream(stream));
 }
 
@@ -47,6 +53,7 @@ size_t gg_trtri_workspace_bytes(int n) { return n < 1 ? 0 : gg::trtri_ws_bytes(n
 
 int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp, void* work,
                        void* stream) {
+  GG_NVTX("gg_trtri_lower_f64");
   return gg::trtri_run(n, L, ldl, Linv, ldp, work, as_stream(stream));
 }
 
@@ -115,6 +122,7 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
 
 int gg_trsm_lower_packed_f64(int n, int nrhs, const double* LinvP, const double* B, int ldb,
                              double* X, int ldx, void* stream) {
+  GG_NVTX("gg_trsm_lower_packed_f64");
   if (n < 1 || nrhs < 0 || LinvP == nullptr || B == nullptr || X == nullptr) {
     gg::set_error("trsm: null pointer or bad size");
     return GG_EARG;
@@ -134,6 +142,7 @@ size_t gg_inverse_slices_bytes(int n) { return n < 1 ? 0 : gg::inverse_slices_by
 
 int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int* expo,
                         void* stream) {
+  GG_NVTX("gg_slice_inverse_i8");
   if (n < 1 || LinvT == nullptr || slices == nullptr || expo == nullptr) {
     gg::set_error("slice_inverse: null pointer or n < 1");
     return GG_EARG;
@@ -144,6 +153,7 @@ int gg_slice_inverse_i8(int n, const double* LinvT, int ldp, int8_t* slices, int
 
 int gg_slice_packed_inverse_i8(int n, const double* LinvP, int8_t* slices, int* expo,
                                void* stream) {
+  GG_NVTX("gg_slice_packed_inverse_i8");
   if (n < 1 || LinvP == nullptr || slices == nullptr || expo == nullptr) {
     gg::set_error("slice_packed_inverse: null pointer or n < 1");
     return GG_EARG;
@@ -185,6 +195,7 @@ int gg_slice_blockcyclic_i8(int n, int nb, int grid_r, int grid_c, int prow, int
 
 int gg_narrow_f64_i8(int n, int cnt, const double* X, long long ldx, int8_t* G, long long ldg,
                      int* bad_dev, void* stream) {
+  GG_NVTX("gg_narrow_f64_i8");
   if (n < 1 || X == nullptr || G == nullptr || bad_dev == nullptr) {
     gg::set_error("narrow: null pointer or n < 1");
     return GG_EARG;
@@ -197,6 +208,7 @@ size_t gg_trsm_i8_workspace_bytes(void) { return 256; }
 
 int gg_trsm_lower_i8(int n, int nrhs, const int8_t* slices, const int* expo, const int8_t* G,
                      long long ldg, double* X, int ldx, void* work, void* stream) {
+  GG_NVTX("gg_trsm_lower_i8");
   if (n < 1 || nrhs < 0 || slices == nullptr || expo == nullptr || G == nullptr || X == nullptr ||
       work == nullptr) {
     gg::set_error("trsm_i8: null pointer or bad size");
@@ -215,6 +227,7 @@ int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* e
                               const int8_t* G, long long ldg, int q, const double* XLbar,
                               const double* ybar, double* P, double* X, int ldx, const int* gate,
                               int gate_value, void* work, void* stream) {
+  GG_NVTX("gg_trsm_lower_i8_partials");
   if (n < 1 || cnt < 0 || slices == nullptr || expo == nullptr || G == nullptr || P == nullptr ||
       ybar == nullptr || (q > 0 && XLbar == nullptr) || q < 0 || q > GG_PMAX - 1 ||
       work == nullptr) {
@@ -230,6 +243,7 @@ int gg_trsm_lower_i8_partials(int n, int cnt, const int8_t* slices, const int* e
 int gg_gls_reduce_solve_f64(int n, int cnt, int q, const double* P, const double* S_TL,
                             const double* b_T, double* beta, int* status, double* sinv,
                             void* stream) {
+  GG_NVTX("gg_gls_reduce_solve_f64");
   if (n < 1 || P == nullptr || beta == nullptr || status == nullptr || q < 0 || q > GG_PMAX - 1 ||
       (q > 0 && (S_TL == nullptr || b_T == nullptr))) {
     gg::set_error("reduce_solve: null pointer or bad size");
@@ -257,6 +271,7 @@ int gg_gemm_ozaki_f64(int m, int ncols, int k, const double* A, long long a_rs, 
                       const double* B, long long b_rs, long long b_cs, double* C, long long ldc,
                       double alpha, double beta, int flags, void* work, size_t work_bytes,
                       void* stream) {
+  GG_NVTX("gg_gemm_ozaki_f64");
   if (A == nullptr || C == nullptr || m < 0 || ncols < 0 || k < 0 || ldc < m ||
       (flags & ~7) != 0) {
     gg::set_error("gemm_ozaki: bad arguments");
@@ -294,6 +309,7 @@ int gg_widen_i8_f64(int n, int cnt, const int8_t* G, long long ldg, double* X, i
 
 int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                     int ldxl, const double* ybar, double* dots, void* work, void* stream) {
+  GG_NVTX("gg_gls_dots_f64");
   if (Xbar == nullptr || ybar == nullptr || dots == nullptr || work == nullptr ||
       (q > 0 && XLbar == nullptr)) {
     gg::set_error("dots: null pointer");
@@ -305,6 +321,7 @@ int gg_gls_dots_f64(int n, int cnt, int q, const double* Xbar, int ldx, const do
 
 int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs, double* x,
                            int* status, double* sinv_packed, void* stream) {
+  GG_NVTX("gg_small_spd_solve_f64");
   if (S == nullptr || rhs == nullptr || x == nullptr || status == nullptr) {
     gg::set_error("small_spd_solve: null pointer");
     return GG_EARG;
@@ -315,6 +332,7 @@ int gg_small_spd_solve_f64(int batch, int p, const double* S, const double* rhs,
 int gg_gls_epilogue_f64(int n, int cnt, int q, const double* Xbar, int ldx, const double* XLbar,
                         int ldxl, const double* ybar, const double* S_TL, const double* b_T,
                         double* beta, int* status, double* sinv, void* work, void* stream) {
+  GG_NVTX("gg_gls_epilogue_f64");
   if (Xbar == nullptr || ybar == nullptr || beta == nullptr || status == nullptr ||
       work == nullptr || (q > 0 && (XLbar == nullptr || S_TL == nullptr || b_T == nullptr))) {
     gg::set_error("epilogue: null pointer");
@@ -373,6 +391,7 @@ int gg_gls_block_f64(int n, int q, int cnt, const double* LinvP, const int8_t* s
                      const double* b_T, const double* X64, int ldx, const int8_t* G8,
                      long long ldg, void* work, double* beta, int* status, double* sinv,
                      void* stream) {
+  GG_NVTX("gg_gls_block_f64");
   cudaStream_t s = as_stream(stream);
   if ((X64 == nullptr) == (G8 == nullptr)) {
     gg::set_error("gls_block: exactly one of X64 / G8 must be given");
@@ -474,6 +493,7 @@ int gg_memcpy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, 
 int gg_gen_genotypes_i8(unsigned long long seed, int stream_maf, int stream_geno, int n,
                         long long m, long long first, int cnt, double maf_lo, double maf_hi,
                         int8_t* G, long long ldg, double* Z, int ldz, void* stream) {
+  GG_NVTX("gg_gen_genotypes_i8");
   return gg::gen_genotypes_run(seed, stream_maf, stream_geno, n, m, first, cnt, maf_lo, maf_hi, G,
                                ldg, Z, ldz, as_stream(stream));
 }

@@ -27,6 +27,14 @@ int cuda_fail(cudaError_t e, const char* what);
 
 inline int pad_rows(int n) { return ((n + GG_TILE - 1) / GG_TILE) * GG_TILE; }
 
+// NVTX range around a C-ABI entry point (header-only NVTX 3: a few ns when no tool listens);
+// nsys / ncu --nvtx see gg_* ranges around every library call.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
+#define GG_NVTX(name) ::gg::NvtxRange _gg_nvtx_range(name)
+
 // ---- FP64 DMMA GEMM (gemm_f64.cu) ----------------------------------------------------
 enum GemmFlags : int {
   GEMM_A_LOWER = 1,   // A lower triangular: row tile mt only needs k < (mt+1)*BM

@@ -64,8 +64,8 @@ def test_run_dist_end_to_end(gpu, tmp_path, case, fp64_inverse):
 
 
 def test_slices_only_context_rejects_non_integer_blocks(gpu):
-    """Without an FP64 inverse a non-integer block cannot be computed: every SNP of the block is
-    marked invalid on the device and the host raises (no silent wrong numbers)."""
+    """Without an FP64 inverse a non-integer column cannot be computed: it is marked invalid on
+    the device and the host raises (no silent wrong numbers)."""
     from paper_1304_2272_b200 import kernel
     from paper_1304_2272_b200.errors import DeviceError
 
@@ -79,5 +79,5 @@ def test_slices_only_context_rejects_non_integer_blocks(gpu):
     ok = kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X))
     assert all(r.status in ("ok", "degenerate") for r in ok.results)
     X[5, 3] = 0.25
-    with pytest.raises(DeviceError):
-        kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X))
+    with pytest.raises(DeviceError):       # raised when the (asynchronous) block resolves
+        kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X)).results

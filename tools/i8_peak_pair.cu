@@ -3,6 +3,7 @@
 // (128B swizzle, K-major) into TMEM, one commit (multicast to both CTAs) every 64 MMAs.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/i8_peak_pair tools/i8_peak_pair.cu
 // Usage: tools/i8_peak_pair [N ...]   (default 224 256)
+//        tools/i8_peak_pair --sustain SECONDS [N [rand]]   (back to back; rand: TRSM-like data)
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -15,7 +16,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-    i8_peak_pair_kernel(int iters, int N, int* sink) {
+    i8_peak_pair_kernel(int iters, int N, int* sink, int rnd) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ unsigned long long bar;
   __shared__ unsigned tslot;
@@ -24,7 +25,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   const int warp = threadIdx.x >> 5;
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
-  for (int i = threadIdx.x; i < 48 * 1024; i += blockDim.x) smem[i] = (unsigned char)(i & 3);
+  // operands: a fixed pattern (i & 3), or -- rnd -- the TRSM's data statistics: A (genotype tile,
+  // first 16 KB) dosages {0,1,2}, B (slices) uniformly random int8 (toggle activity sets power)
+  for (int i = threadIdx.x; i < 48 * 1024; i += blockDim.x) {
+    unsigned h = (unsigned)i * 2654435761u + 0x9E3779B9u * (blockIdx.x + 1);
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+    smem[i] = !rnd ? (unsigned char)(i & 3) : (i < 16 * 1024 ? (unsigned char)(h % 3) : (unsigned char)h);
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;\n");
@@ -84,6 +91,7 @@ int main(int argc, char** argv) {
     // the rate over everything after the first second
     const double secs = atof(argv[2]);
     const int N = argc > 3 ? atoi(argv[3]) : 224;
+    const int rnd = argc > 4 && std::string(argv[4]) == "rand";
     const int iters = 2000;
     const double ops1 = 2.0 * 256 * N * 32 * 64.0 * iters * (grid / 2);
     cudaEvent_t a, b;
@@ -92,7 +100,7 @@ int main(int argc, char** argv) {
     double total_ms = 0.0, ops = 0.0, warm_ms = 0.0;
     while (total_ms < secs * 1e3) {
       cudaEventRecord(a);
-      for (int k = 0; k < 16; ++k) i8_peak_pair_kernel<<<grid, 128, smem>>>(iters, N, sink);
+      for (int k = 0; k < 16; ++k) i8_peak_pair_kernel<<<grid, 128, smem>>>(iters, N, sink, rnd);
       cudaEventRecord(b);
       CK(cudaEventSynchronize(b));
       CK(cudaGetLastError());
@@ -104,8 +112,9 @@ int main(int argc, char** argv) {
       }
       total_ms += ms;
     }
-    printf("int8 tcgen05 cta_group::2 M256 N%d K32 x %d SMs, sustained %.1f s: %.1f TOPS\n", N,
-           grid, total_ms / 1e3, ops / warm_ms / 1e9);
+    printf("int8 tcgen05 cta_group::2 M256 N%d K32 x %d SMs, %s operands, sustained %.1f s: "
+           "%.1f TOPS\n", N, grid, rnd ? "TRSM-like random" : "i&3 pattern", total_ms / 1e3,
+           ops / warm_ms / 1e9);
     return 0;
   }
   const int nn = argc > 1 ? argc - 1 : 2;
@@ -114,7 +123,7 @@ int main(int argc, char** argv) {
     for (int rep = 0; rep < 3; ++rep) {
       const int iters = rep == 0 ? 10 : 2000;
       cudaEventRecord(e0);
-      i8_peak_pair_kernel<<<grid, 128, smem>>>(iters, N, sink);
+      i8_peak_pair_kernel<<<grid, 128, smem>>>(iters, N, sink, 0);
       cudaEventRecord(e1);
       CK(cudaEventSynchronize(e1));
       CK(cudaGetLastError());

@@ -1,4 +1,5 @@
-"""One int8 TRSM (+ fused partials) launch at config-1 sizes inside NVTX range "hot/", for ncu."""
+"""One int8 TRSM (+ fused partials) launch at config-1 (or CFG=3) sizes inside NVTX range "hot/", for
+ncu."""
 import os
 import sys
 
@@ -10,8 +11,15 @@ from paper_1304_2272_b200 import _capi, datagen, kernel  # noqa: E402
 from paper_1304_2272_b200._capi import check, ptr  # noqa: E402
 
 lib = _capi.lib()
-n, cnt = int(os.environ.get("N", "10000")), 8192
-spec = datagen.BaselineSpec(n=n, m=cnt, p=4)
+import dataclasses  # noqa: E402
+
+# CFG=3: BASELINE config 3 (n = 4e4, p = 8, a = 0.5); default config 1 (N overrides n)
+cfg = int(os.environ.get("CFG", "1"))
+cnt = 8192
+spec = dataclasses.replace(datagen.CONFIGS[cfg], m=cnt)
+if "N" in os.environ:
+    spec = dataclasses.replace(spec, n=int(os.environ["N"]))
+n = spec.n
 ctx = kernel.gls_prepare(datagen.kinship_covariance_device(spec), *datagen.covariates_host(spec))
 d = ctx._dev
 n16 = -(-n // 16) * 16
