@@ -100,6 +100,7 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--cnt", type=int, default=8192)
+    ap.add_argument("--q", type=int, default=3, help="covariates (p - 1) of the workload")
     ap.add_argument("--engine", choices=["dmma", "i8"], default="i8")
     args = ap.parse_args()
     os.makedirs(PROFILES, exist_ok=True)
@@ -113,7 +114,8 @@ def main():
             k = trsm[0]
             rd, wr = k.get("dram__bytes_read.sum"), k.get("dram__bytes_write.sum")
             if args.engine == "i8":   # int8 dosages in, 7 int8 slices of the triangle, partials out
-                algo = args.n * args.cnt + 7 * args.n * args.n / 2 + 8.0 * 5 * args.cnt * args.n / 32
+                algo = (args.n * args.cnt + 7 * args.n * args.n / 2
+                        + 8.0 * (args.q + 2) * args.cnt * args.n / 32)
             else:                     # FP64 block in, packed FP64 triangle, FP64 Xbar out
                 algo = 8.0 * (args.n * args.cnt * 2 + args.n * args.n / 2)
             summ = {
@@ -127,7 +129,9 @@ def main():
                 "dmma_pipe_active_pct": k.get(
                     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
             }
-            with open(os.path.join(PROFILES, f"ncu_trsm_{args.engine}_summary.json"), "w") as f:
+            suffix = "" if args.n == 10000 else f"_n{args.n}"
+            with open(os.path.join(PROFILES, f"ncu_trsm_{args.engine}_summary{suffix}.json"),
+                      "w") as f:
                 json.dump(summ, f, indent=1)
             print(json.dumps(summ, indent=1))
     if args.launches:
