@@ -6,24 +6,36 @@ SNP block) with a B200 design:
 
 * M and L live 2D BLOCK-cyclic (block nb = 512 by default; nb = 1 would be the reference's
   element-cyclic map) on the r x c grid of ``grid_create`` (same rule as distgrid.py:43-52);
-  every rank reads or generates only its own blocks — there is no root scatter.
+  every rank reads (``local_from_gwam``: block-column panels of the file) or generates
+  (``local_from_spec``: its own M_IJ = a/m_k Z_I Z_J^T + (1-a) delta_IJ from the counter-based
+  kinship markers, on its GPU) only its own blocks -- no root scatter, no host-dense step.
 * ``dist_potrf_inv``: right-looking blocked Cholesky FUSED with the triangular inverse (a
   right-looking TRSM of the identity, X = L^-1), one pass over the block columns K:
     1. the owner of (K, K) factors and inverts the diagonal block on its GPU (gg_potrf_f64);
-       the inverse is broadcast to all ranks;
-    2. process column K%c forms the panel L_IK = A_IK L_KK^-T, process row K%r forms the
-       inverse's block row X_KJ = L_KK^-1 B_KJ (DMMA GEMMs);
-    3. panel and block row are made global with one NCCL all-reduce each over disjoint
-       supports (exact: every element has exactly one non-zero contributor);
-    4. every rank updates its own blocks: A_IJ -= L_IK L_JK^T and B_IJ -= L_IK X_KJ.
-  NCCL carries ~2 n nb doubles per step (n = 150,000, nb = 512: 1.2 GB, < 2 ms on NVLink 5)
-  against (n - K nb)^2 nb / (r c) FMAs of local GEMM.
-* ``assemble_packed_inverse``: each rank writes its blocks of L^-1 into the packed tile-major
-  layout of the TRSM (zeros elsewhere, gg_pack_lower_blockcyclic_f64) and one all-reduce makes
-  the packed inverse replicated: 90 GB at n = 150,000, which fits one B200's 180 GB although M
-  (180 GB) does not.  From there the SNP sweep is the single-GPU stream, sharded over ranks with
-  no per-block communication (the reference redistributes every block twice,
-  distgrid.py:422-428).
+       the status and the nb x nb inverse are broadcast;
+    2. process column K%c forms the panel L_IK = A_IK L_KK^-T and BROADCASTS it along each process
+       row (row sub-communicator); the rows of the panel a rank needs for its trailing COLUMNS
+       are assembled by one all-reduce over disjoint supports in its process column;
+    3. process row K%r forms the inverse's block row X_KJ = L_KK^-1 B_KJ and broadcasts it along
+       each process column;
+    4. every rank updates its own blocks: A_IJ -= L_IK L_JK^T and B_IJ -= L_IK X_KJ (the large
+       ones on the int8 tensor cores through the Ozaki-scheme GEMM).
+  Per step a rank moves (m_loc + 2 n_loc) nb doubles on NVLink instead of world all-reduces of
+  2 n nb (n = 150,000, nb = 512, 2 x 4 grid: ~0.6 GB vs 1.2 GB, all-reduce traffic halved again).
+* ``assemble_slices``: replicated int8 slices of L^-1 (79 GB at n = 1.5e5) from the block-cyclic
+  shares (MAX all-reduce of row exponents, SUM all-reduce of disjoint slices) -- no replicated
+  FP64 inverse; from there the SNP sweep is the single-GPU tensor-core stream sharded over ranks
+  with no per-block communication (the reference redistributes every block twice,
+  distgrid.py:422-428).  ``assemble_packed_inverse`` replicates the packed FP64 inverse instead
+  when it fits (90 GB at config 4).
+* ``dist_trsolve_bc``: the distributed TRSM for a replicated right-hand side -- blocked forward
+  substitution over the block rows (partial products reduced along the process row, the
+  diagonal block's inverse applied by its owner, the solved block broadcast).
+
+The reference's own signatures are kept on top (``dist_cholesky(M, t, nb)``,
+``dist_trsolve(L, B, t, nb)``, ``run_dist(t, paths, cfg)``, distgrid.py:248-469): they accept the
+reference's element-cyclic ``DistMatrix2D`` and any Transport (``comm.TransportComm``) or our
+``transport.NcclTransport``, and redistribute element-cyclic <-> block-cyclic with one all-to-all.
 
 Local matrices are column-major torch tensors of shape (local_cols, local_rows).  The numerical
 work goes through an ``ops`` object: ``DeviceOps`` (the sm_100a library) in production; the CPU
@@ -40,9 +52,11 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import fileio
+from .comm import GridComm, as_comm
 from .errors import ConfigError, DimensionMismatch, NotPositiveDefinite
 
 DEFAULT_NB = 512
+SMALL_NB = 128          # block size the reference-signature adapters use below 8 * DEFAULT_NB
 
 
 @dataclass(frozen=True)
@@ -113,58 +127,84 @@ class BlockCyclic:
         return self.global_rows([J for J in self.col_blocks if J <= K])
 
 
+# ---------------------------------------------------------------------------------------------
+# this rank's blocks
+# ---------------------------------------------------------------------------------------------
+
 def local_from_global(M, layout, ops):
-    """This rank's blocks of the (host) n x n matrix M, identity on the padding; A_loc and the
-    identity's share B_loc (column-major local tensors)."""
-    n, nb = layout.n, layout.nb
+    """This rank's blocks of a (host, small-n) n x n matrix M -- identity on the padding -- and
+    the identity's share B (column-major local tensors; B built on the device)."""
+    n = layout.n
     rows = layout.global_rows(layout.row_blocks)
     cols = layout.global_rows(layout.col_blocks)
-    Mp = np.zeros((len(rows), len(cols)))
     rv, cv = rows < n, cols < n
+    Mp = np.zeros((len(rows), len(cols)))
     if rv.any() and cv.any():
         Mp[np.ix_(rv, cv)] = np.asarray(M)[np.ix_(rows[rv], cols[cv])]
-    eye = (rows[:, None] == cols[None, :])
-    pad = eye & (rows[:, None] >= n)
-    Mp[pad] = 1.0
     A = ops.from_host(Mp)
-    B = ops.from_host(eye.astype(np.float64))
-    return A, B
+    _pad_identity(A, layout, ops)
+    return A, ops.identity_share(layout)
+
+
+def _pad_identity(A, layout, ops):
+    """Ones on the diagonal of the padding rows (i >= n) of this rank's diagonal blocks."""
+    n, nb = layout.n, layout.nb
+    for I in layout.row_blocks:
+        if I in layout.col_blocks and (I + 1) * nb > n:
+            lo = max(n - I * nb, 0)
+            ops.set_diag(A, layout.lrow(I), layout.lcol(I), lo, nb, 1.0, add=False)
 
 
 def local_from_gwam(path, layout, ops):
-    """Read only this rank's blocks of a GWAM file (memory-mapped), identity on the padding."""
+    """Read only this rank's blocks of a GWAM file: one block-column panel (n x nb, contiguous
+    in the column-major file) at a time, local rows selected and uploaded -- host memory is one
+    panel (614 MB at n = 1.5e5), never the dense share."""
     n = fileio.read_dims(path, "GWAM")[0]
     if n != layout.n:
         raise DimensionMismatch("covariance file does not match the layout")
+    nb = layout.nb
     mm = np.memmap(path, dtype="<f8", mode="r", offset=fileio.header_size("GWAM"),
                    shape=(n, n), order="F")
-    return local_from_global(mm, layout, ops)
+    rows = layout.global_rows(layout.row_blocks)
+    rv = rows[rows < n]
+    A = ops.zeros(layout.n_loc, layout.m_loc)
+    for jl, J in enumerate(layout.col_blocks):
+        c0, c1 = J * nb, min((J + 1) * nb, n)
+        if c0 >= n or not len(rv):
+            continue
+        panel = np.zeros((layout.m_loc, nb))
+        panel[:len(rv), :c1 - c0] = np.asarray(mm[:, c0:c1])[rv]
+        ops.copy_block(A, 0, jl * nb, ops.from_host(panel))
+    del mm
+    _pad_identity(A, layout, ops)
+    return A, ops.identity_share(layout)
 
 
-def _allreduce(t, dist):
-    if dist is not None:
-        dist.all_reduce(t)
-    return t
+def local_from_spec(spec, layout, ops):
+    """This rank's blocks of the BASELINE kinship covariance M = a Z Z^T / m_k + (1 - a) I
+    (datagen.kinship_covariance_device), generated on its own GPU: the standardised kinship
+    markers Z (n x m_k) come from the counter-based streams (every rank draws the same Z, no
+    communication), then one GEMM of the rank's row blocks of Z against its column blocks.
+    Nothing n x n exists anywhere; host memory stays small.  Returns (A, B) like
+    ``local_from_global``."""
+    A = ops.kinship_blocks(spec, layout)
+    _pad_identity(A, layout, ops)
+    return A, ops.identity_share(layout)
 
 
-def _allreduce_max(t, dist):
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return t
+# ---------------------------------------------------------------------------------------------
+# the fused distributed Cholesky + inverse
+# ---------------------------------------------------------------------------------------------
 
-
-def _broadcast(t, src, dist):
-    if dist is not None:
-        dist.broadcast(t, src)
-    return t
-
-
-def dist_potrf_inv(A, B, layout, ops, dist=None):
+def dist_potrf_inv(A, B, layout, ops, comm=None):
     """Fused distributed Cholesky + inverse (see module doc).  A (this rank's blocks of M) is
     overwritten with L, B (this rank's blocks of I) with L^-1.  Raises NotPositiveDefinite with
-    the global pivot on every rank."""
+    the global pivot on every rank.  ``comm``: a communicator, the torch.distributed module or a
+    reference transport (None: one rank)."""
+    comm = as_comm(comm)
     nb, g = layout.nb, layout.grid
     rank = layout.rank
+    gcm = GridComm(comm, g) if comm is not None and comm.size > 1 else None
     for K in range(layout.nblk):
         owner = layout.owner(K, K)
         Dinv = ops.empty(nb, nb)
@@ -175,72 +215,93 @@ def dist_potrf_inv(A, B, layout, ops, dist=None):
             if st < 0:
                 ops.copy_block(A, layout.lrow(K), layout.lcol(K), Lkk)
                 Dinv.copy_(Linvkk)
-        _broadcast(status, owner, dist)
+        if gcm is not None:
+            gcm.world.broadcast(status, owner)
         st = int(status.item())
         if st >= 0:
             raise NotPositiveDefinite(K * nb + st)
-        _broadcast(Dinv, owner, dist)
+        if gcm is not None:
+            gcm.world.broadcast(Dinv, owner)
         r0 = layout.rows_through(K)
         m_below = layout.m_loc - r0
-        grows = layout.rows_after_global(K)
-        # panel L_IK = A_IK Dinv^T on process column K % c; made global by an exact all-reduce
-        Pfull = ops.zeros(nb, layout.n_pad)                      # (n_pad x nb) column-major
-        if layout.pc == K % g.c and m_below > 0:
-            tmp = ops.empty(nb, m_below)
-            ops.gemm(tmp, 0, 0, m_below, nb, A, r0, layout.lcol(K), Dinv, 0, 0, nb,
-                     1.0, 0.0, trans_b=True)
-            ops.copy_block(A, r0, layout.lcol(K), tmp)
-            ops.scatter_cols_rows(Pfull, grows, tmp)
-        _allreduce(Pfull, dist)
-        # block row K of the inverse, X_KJ = Dinv B_KJ on process row K % r
-        cl = layout.cols_through(K)
-        gcols = layout.cols_through_global(K)
-        Xfull = ops.zeros(layout.n_pad, nb)                      # (nb x n_pad) column-major
-        if layout.pr == K % g.r and cl > 0:
-            tmpx = ops.empty(cl, nb)
-            ops.gemm(tmpx, 0, 0, nb, cl, Dinv, 0, 0, B, layout.lrow(K), 0, nb, 1.0, 0.0,
-                     trans_b=False)
-            ops.copy_block(B, layout.lrow(K), 0, tmpx)
-            ops.scatter_cols(Xfull, gcols, tmpx)
-        _allreduce(Xfull, dist)
-        if m_below == 0:
-            continue
-        P_rows = ops.gather_rows(Pfull, grows)                   # (m_below x nb)
         c0 = layout.cols_through(K)
         n_right = layout.n_loc - c0
+        # panel L_IK for this rank's row blocks I > K: formed on process column K % c, broadcast
+        # along the process row (m_below is uniform over a process row)
+        P_rows = None
+        if m_below > 0:
+            P_rows = ops.empty(nb, m_below)                       # (m_below x nb)
+            if layout.pc == K % g.c:
+                ops.gemm(P_rows, 0, 0, m_below, nb, A, r0, layout.lcol(K), Dinv, 0, 0, nb,
+                         1.0, 0.0, trans_b=True)
+                ops.copy_block(A, r0, layout.lcol(K), P_rows)
+            if gcm is not None:
+                gcm.row.broadcast(P_rows, K % g.c)
+        # panel rows J > K for this rank's column blocks: the rank of process row J % r in this
+        # process column holds them (J is one of its row blocks); one all-reduce over disjoint
+        # supports along the process column
+        P_cols = None
         if n_right > 0:
-            P_cols = ops.gather_rows(Pfull, layout.cols_after_global(K))   # (n_right x nb)
+            P_cols = ops.zeros(nb, n_right)
+            if P_rows is not None:
+                below = [I for I in layout.row_blocks if I > K]
+                right = [J for J in layout.col_blocks if J > K]
+                pos = {I: i for i, I in enumerate(below)}
+                for jj, J in enumerate(right):
+                    if J in pos:
+                        ii = pos[J]
+                        ops.copy_block(P_cols, jj * nb, 0, P_rows[:, ii * nb:(ii + 1) * nb])
+            if gcm is not None:
+                gcm.col.all_reduce(P_cols)
+        # block row K of the inverse, X_KJ = Dinv B_KJ (J <= K) on process row K % r, broadcast
+        # along the process column (c0 is uniform over a process column)
+        X_cols = None
+        if c0 > 0:
+            X_cols = ops.empty(c0, nb)                            # (nb x c0)
+            if layout.pr == K % g.r:
+                ops.gemm(X_cols, 0, 0, nb, c0, Dinv, 0, 0, B, layout.lrow(K), 0, nb, 1.0, 0.0,
+                         trans_b=False)
+                ops.copy_block(B, layout.lrow(K), 0, X_cols)
+            if gcm is not None:
+                gcm.col.broadcast(X_cols, K % g.r)
+        if m_below == 0:
+            continue
+        if n_right > 0:
             ops.gemm(A, r0, c0, m_below, n_right, P_rows, 0, 0, P_cols, 0, 0, nb, -1.0, 1.0,
                      trans_b=True)
-        if cl > 0:
-            X_cols = ops.gather_cols(Xfull, gcols)               # (nb x cl)
-            ops.gemm(B, r0, 0, m_below, cl, P_rows, 0, 0, X_cols, 0, 0, nb, -1.0, 1.0,
+        if c0 > 0:
+            ops.gemm(B, r0, 0, m_below, c0, P_rows, 0, 0, X_cols, 0, 0, nb, -1.0, 1.0,
                      trans_b=False)
     ops.zero_upper_blocks(A, layout)
     return A, B
 
 
-def assemble_packed_inverse(B, layout, ops, dist=None):
+def assemble_packed_inverse(B, layout, ops, comm=None):
     """Replicate the packed tile-major inverse on every rank from the block-cyclic shares."""
     P = ops.pack_blockcyclic(B, layout)
-    return _allreduce(P, dist)
+    comm = as_comm(comm)
+    return comm.all_reduce(P) if comm is not None else P
 
 
-def assemble_slices(B, layout, ops, dist=None):
+def assemble_slices(B, layout, ops, comm=None):
     """Replicated int8 slices + slice metadata of the inverse from the block-cyclic shares: each
     rank takes its rows' off-diagonal / diagonal exponents over its blocks (MAX all-reduce), turns
     them into the row exponents, then cuts the slices of the elements it owns (zeros elsewhere)
     and the heads of the diagonals it owns; SUM all-reduces of both over disjoint supports are
     exact.  Needs 3.5 np^2 bytes per rank (79 GB at n = 1.5e5) and no replicated FP64 inverse."""
+    comm = as_comm(comm)
     ex2 = ops.row_exponents(B, layout)
-    _allreduce_max(ex2, dist)
+    if comm is not None:
+        comm.all_reduce(ex2, op="max")
     meta = ops.slice_meta(ex2, layout)
     S = ops.slice_blockcyclic(B, layout, meta)
-    _allreduce(meta[meta.numel() // 2:], dist)
-    return _allreduce(S, dist), meta
+    if comm is not None:
+        comm.all_reduce(meta[meta.numel() // 2:])
+        comm.all_reduce(S)
+    return S, meta
 
 
-def whiten_blockcyclic(B, layout, ops, RHS, dist=None):
+def whiten_blockcyclic(B, layout, ops, RHS, comm=None):
     """[X_L | y] bar = L^-1 [X_L | y] from the block-cyclic inverse: one local GEMM of this
     rank's blocks against the rows of RHS it needs, scattered to global rows and summed over
     ranks (FP64 all-reduce).  RHS: host (n x k).  Returns a replicated (k, n_pad) tensor."""
@@ -256,10 +317,52 @@ def whiten_blockcyclic(B, layout, ops, RHS, dist=None):
         ops.gemm(Yloc, 0, 0, layout.m_loc, k, B, 0, 0, Xloc, 0, 0, layout.n_loc, 1.0, 0.0,
                  trans_b=False)
         ops.scatter_cols_rows(Y, rows, Yloc)
-    return _allreduce(Y, dist)
+    comm = as_comm(comm)
+    return comm.all_reduce(Y) if comm is not None else Y
 
 
-def gather_matrix(D, layout, ops, dist=None):
+def dist_trsolve_bc(L, layout, ops, RHS, comm=None):
+    """Distributed TRSM X = L^-1 RHS for a block-cyclic lower-triangular L and a replicated host
+    right-hand side (n x k): blocked forward substitution over the block rows K --
+        X_K = L_KK^-1 (RHS_K - sum_{J<K} L_KJ X_J)
+    -- each rank of process row K%r forms the partial product of its column blocks J < K, one
+    all-reduce along that process row sums them, the owner of (K, K) applies the inverse of the
+    diagonal block (gg_trtri_lower_f64) and broadcasts X_K.  Backward-stable blocked substitution
+    (diagonal-block inverses only); returns the replicated X as a host (n x k) array."""
+    comm = as_comm(comm)
+    nb, g = layout.nb, layout.grid
+    n, k = RHS.shape
+    gcm = GridComm(comm, g) if comm is not None and comm.size > 1 else None
+    full = np.zeros((layout.n_pad, k))
+    full[:n] = RHS
+    X = ops.from_host(full)                                  # (k, n_pad), replicated
+    for K in range(layout.nblk):
+        owner = layout.owner(K, K)
+        rk = slice(K * nb, (K + 1) * nb)
+        if layout.pr == K % g.r:
+            part = ops.zeros(k, nb)
+            jl = [jj for jj, J in enumerate(layout.col_blocks) if J < K]
+            if jl:
+                c_before = len(jl) * nb                    # local col blocks J < K come first
+                Xj = ops.gather_rows(X, layout.global_rows(layout.col_blocks[:len(jl)]))
+                ops.gemm(part, 0, 0, nb, k, L, layout.lrow(K), 0, Xj, 0, 0, c_before,
+                         1.0, 0.0, trans_b=False)
+            if gcm is not None:
+                gcm.row.all_reduce(part)
+            if layout.rank == owner:
+                rhs = (X[:, rk] - part).contiguous()
+                Dinv = ops.trtri(L, layout.lrow(K), layout.lcol(K), nb)
+                xk = ops.empty(k, nb)
+                ops.gemm(xk, 0, 0, nb, k, Dinv, 0, 0, rhs, 0, 0, nb, 1.0, 0.0, trans_b=False)
+                X[:, rk] = xk
+        if gcm is not None:
+            xk = X[:, rk].contiguous()
+            gcm.world.broadcast(xk, owner)
+            X[:, rk] = xk
+    return ops.to_host(X)[:n]
+
+
+def gather_matrix_bc(D, layout, ops, comm=None):
     """Full n x n host copy of a block-cyclic matrix on every rank (tests / small n only)."""
     full = np.zeros((layout.n_pad, layout.n_pad))
     rows = layout.global_rows(layout.row_blocks)
@@ -267,8 +370,166 @@ def gather_matrix(D, layout, ops, dist=None):
     if len(rows) and len(cols):
         full[np.ix_(rows, cols)] = ops.to_host(D)
     t = ops.from_host(full)
-    _allreduce(t, dist)
+    comm = as_comm(comm)
+    if comm is not None:
+        comm.all_reduce(t)
     return ops.to_host(t)[:layout.n, :layout.n]
+
+
+def gather_matrix(D, layout, ops, comm=None):
+    """Alias of ``gather_matrix_bc`` for block-cyclic matrices."""
+    return gather_matrix_bc(D, layout, ops, comm)
+
+
+# ---------------------------------------------------------------------------------------------
+# element-cyclic (the reference's DistMatrix2D) <-> block-cyclic
+# ---------------------------------------------------------------------------------------------
+
+def _ec_rows(gr, grid, prow):
+    return np.arange(prow, gr, grid.r)
+
+
+def _ec_cols(gc, grid, pcol):
+    return np.arange(pcol, gc, grid.c)
+
+
+def ec_to_bc(local, gr, gc, grid, rank, layout, comm, ops, pad_identity=True):
+    """Element-cyclic local part (A[prow::r, pcol::c], distgrid.py:76-89) -> this rank's
+    block-cyclic blocks (column-major device tensor), one all-to-all of host bytes.  Rows /
+    columns beyond (gr, gc) are zero (identity on the diagonal when ``pad_identity``)."""
+    prow, pcol = grid.coord(rank)
+    rows = _ec_rows(gr, grid, prow)
+    cols = _ec_cols(gc, grid, pcol)
+    nb = layout.nb
+    drow = (rows // nb) % grid.r
+    dcol = (cols // nb) % grid.c
+    local = np.asarray(local, dtype=np.float64)
+    slices = []
+    for dst in range(grid.np_):
+        a, b = grid.coord(dst)
+        piece = local[np.ix_(drow == a, dcol == b)]
+        slices.append(np.ascontiguousarray(piece).tobytes())
+    recv = comm.alltoall_bytes(slices) if comm is not None else slices
+    out = np.zeros((layout.m_loc, layout.n_loc))
+
+    def lpos(g, blocks_stride, p):
+        I = g // nb
+        return (I // blocks_stride) * nb + g % nb
+
+    for src in range(grid.np_):
+        a, b = grid.coord(src)
+        srows = _ec_rows(gr, grid, a)
+        scols = _ec_cols(gc, grid, b)
+        mine_r = srows[(srows // nb) % grid.r == layout.pr]
+        mine_c = scols[(scols // nb) % grid.c == layout.pc]
+        if not len(mine_r) or not len(mine_c):
+            continue
+        piece = np.frombuffer(recv[src], dtype=np.float64).reshape(len(mine_r), len(mine_c))
+        out[np.ix_(lpos(mine_r, grid.r, layout.pr), lpos(mine_c, grid.c, layout.pc))] = piece
+    A = ops.from_host(out)
+    if pad_identity:
+        _pad_identity(A, layout, ops)
+    return A
+
+
+def bc_to_ec(A, gr, gc, grid, rank, layout, comm, ops):
+    """Inverse of ``ec_to_bc``: this rank's element-cyclic local part of a block-cyclic matrix."""
+    nb = layout.nb
+    loc = ops.to_host(A) if A.numel() else np.zeros((layout.m_loc, layout.n_loc))
+    grow = layout.global_rows(layout.row_blocks)
+    gcol = layout.global_rows(layout.col_blocks)
+    keep_r, keep_c = grow < gr, gcol < gc
+    slices = []
+    for dst in range(grid.np_):
+        a, b = grid.coord(dst)
+        rsel = keep_r & (grow % grid.r == a)
+        csel = keep_c & (gcol % grid.c == b)
+        slices.append(np.ascontiguousarray(loc[np.ix_(rsel, csel)]).tobytes())
+    recv = comm.alltoall_bytes(slices) if comm is not None else slices
+    prow, pcol = grid.coord(rank)
+    rows = _ec_rows(gr, grid, prow)
+    cols = _ec_cols(gc, grid, pcol)
+    out = np.zeros((len(rows), len(cols)))
+    for src in range(grid.np_):
+        a, b = grid.coord(src)
+        lay = BlockCyclic(max(gr, gc), nb, grid, src)
+        sr = lay.global_rows(lay.row_blocks)
+        sc = lay.global_rows(lay.col_blocks)
+        sr = sr[(sr < gr) & (sr % grid.r == prow)]
+        sc = sc[(sc < gc) & (sc % grid.c == pcol)]
+        if not len(sr) or not len(sc):
+            continue
+        piece = np.frombuffer(recv[src], dtype=np.float64).reshape(len(sr), len(sc))
+        out[np.ix_(sr // grid.r, sc // grid.c)] = piece
+    return out
+
+
+def _adapter_nb(n):
+    return DEFAULT_NB if n >= 8 * DEFAULT_NB else SMALL_NB
+
+
+def _like(M, gr, gc, local, rank):
+    """A DistMatrix2D of the caller's own class (the reference's, or a duck-typed stand-in)."""
+    return type(M)(gr=gr, gc=gc, grid=M.grid, rank=rank, local=local)
+
+
+def _ops_or_device(ops):
+    return ops if ops is not None else DeviceOps()
+
+
+def dist_cholesky(M, t, nb=64, ops=None):
+    """The reference's ``dist_cholesky(M, t, nb)`` (distgrid.py:248-288) on the B200 engine:
+    M is the reference's element-cyclic DistMatrix2D, t its transport (or our NcclTransport).
+    One rank: kernel.cholesky_spd of the local matrix (bitwise equal to the replicated factor,
+    tests/test_distgrid.py:167-174).  Several: element-cyclic -> block-cyclic (one all-to-all),
+    the fused device Cholesky + inverse (``dist_potrf_inv``), L back to element-cyclic.  ``nb``
+    (the reference's panel width) is accepted; the engine's block is its own (128 / 512).
+    Raises NotPositiveDefinite with the global pivot on every rank."""
+    from . import kernel
+
+    n = M.gr
+    if M.gr != M.gc:
+        raise DimensionMismatch("dist_cholesky needs a square matrix")
+    if M.grid.np_ == 1:
+        return _like(M, n, n, kernel.cholesky_spd(M.local), t.rank)
+    comm = as_comm(t)
+    ops = _ops_or_device(ops)
+    lay = BlockCyclic(n, _adapter_nb(n), M.grid, t.rank)
+    A = ec_to_bc(M.local, n, n, M.grid, t.rank, lay, comm, ops)
+    B = ops.identity_share(lay)
+    dist_potrf_inv(A, B, lay, ops, comm)
+    return _like(M, n, n, bc_to_ec(A, n, n, M.grid, t.rank, lay, comm, ops), t.rank)
+
+
+def dist_trsolve(L, B, t, nb=64, ops=None):
+    """The reference's ``dist_trsolve(L, B, t, nb)`` (distgrid.py:291-314): solve L X = B for an
+    element-cyclic lower-triangular L and right-hand side B; returns X element-cyclic like B.
+    One rank: kernel.trsolve_lower of the local matrices (bitwise, tests/test_distgrid.py:225-238).
+    Several: L to block-cyclic (one all-to-all), B replicated (one gather), the blocked
+    distributed substitution ``dist_trsolve_bc``, X cut back to B's element-cyclic share."""
+    from . import kernel
+
+    n = L.gr
+    if B.gr != n:
+        raise DimensionMismatch("dist_trsolve: RHS rows do not match L")
+    if L.grid.np_ == 1:
+        return _like(B, B.gr, B.gc, kernel.trsolve_lower(L.local, B.local), t.rank)
+    comm = as_comm(t)
+    ops = _ops_or_device(ops)
+    grid = L.grid
+    lay = BlockCyclic(n, _adapter_nb(n), grid, t.rank)
+    Lb = ec_to_bc(L.local, n, n, grid, t.rank, lay, comm, ops)
+    # the right-hand side, replicated (gathered element-cyclic shares)
+    parts = comm.allgather_obj(np.asarray(B.local, dtype=np.float64))
+    Bfull = np.zeros((B.gr, B.gc))
+    for src, part in enumerate(parts):
+        a, b = grid.coord(src)
+        Bfull[np.ix_(_ec_rows(B.gr, grid, a), _ec_cols(B.gc, grid, b))] = part
+    X = dist_trsolve_bc(Lb, lay, ops, Bfull, comm)
+    prow, pcol = grid.coord(t.rank)
+    return _like(B, B.gr, B.gc,
+                 X[np.ix_(_ec_rows(B.gr, grid, prow), _ec_cols(B.gc, grid, pcol))].copy(),
+                 t.rank)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -305,6 +566,25 @@ class DeviceOps:
     def to_host(self, T):
         return T.cpu().numpy().T
 
+    def identity_share(self, layout):
+        """This rank's blocks of the n_pad x n_pad identity, built on the device."""
+        B = self.zeros(layout.n_loc, layout.m_loc)
+        nb = layout.nb
+        for I in layout.row_blocks:
+            if I in layout.col_blocks:
+                self.set_diag(B, layout.lrow(I), layout.lcol(I), 0, nb, 1.0, add=False)
+        return B
+
+    def set_diag(self, A, r0, c0, lo, hi, value, add):
+        """A[r0 + i, c0 + i] (+)= value for i in [lo, hi)."""
+        if hi <= lo:
+            return
+        idx = self.torch.arange(lo, hi, device=self.dev)
+        if add:
+            A[c0 + idx, r0 + idx] += value
+        else:
+            A[c0 + idx, r0 + idx] = value
+
     def _p(self, T, r0, c0):
         return self.capi.C.c_void_p(T.data_ptr() + (c0 * T.shape[1] + r0) * 8)
 
@@ -324,12 +604,30 @@ class DeviceOps:
         capi.check(rc, "gg_potrf_f64")
         return -1, L, Li
 
+    def trtri(self, A, r0, c0, nb):
+        """Inverse of the lower-triangular nb x nb block at (r0, c0) (gg_trtri_lower_f64)."""
+        torch, capi = self.torch, self.capi
+        Lb = A[c0:c0 + nb, r0:r0 + nb].contiguous()
+        Li = self.empty(nb, nb)
+        ws = torch.empty(int(capi.lib().gg_trtri_workspace_bytes(nb)), dtype=torch.uint8,
+                         device=self.dev)
+        capi.check(capi.lib().gg_trtri_lower_f64(nb, capi.ptr(Lb), nb, capi.ptr(Li), nb,
+                                                 capi.ptr(ws), capi.stream_handle()),
+                   "gg_trtri_lower_f64")
+        return Li
+
     def gemm(self, C, cr, cc, m, n, A, ar, ac, B, br, bc, k, alpha, beta, trans_b):
         """C[cr:cr+m, cc:cc+n] = beta C + alpha A op(B).  Large updates (every dimension >= 512:
         the trailing updates of dist_potrf_inv) run on the int8 tensor cores through the
         Ozaki-scheme GEMM (gg_gemm_ozaki_f64, FP64-GEMM accuracy) unless GG_FACTOR_OZAKI=0;
-        the rest on the DMMA GEMM."""
+        the rest on the DMMA GEMM (operands padded to its tile when needed)."""
         capi = self.capi
+        if m == 0 or n == 0:
+            return
+        if k == 0:
+            if beta != 1.0:
+                C[cc:cc + n, cr:cr + m].mul_(beta)
+            return
         if min(m, n, k) >= 512 and os.environ.get("GG_FACTOR_OZAKI", "1") != "0":
             lib = capi.lib()
             need = int(lib.gg_gemm_ozaki_workspace_bytes(m, n, k, 0))
@@ -344,10 +642,35 @@ class DeviceOps:
                                        self._oz_ws.numel(), capi.stream_handle())
             capi.check(rc, "gg_gemm_ozaki_f64")
             return
+        if m % 128 or k % 16 or (trans_b and n % 128):
+            self._gemm_padded(C, cr, cc, m, n, A, ar, ac, B, br, bc, k, alpha, beta, trans_b)
+            return
         rc = capi.lib().gg_dgemm_f64(m, n, k, alpha, self._p(A, ar, ac), A.shape[1],
                                      self._p(B, br, bc), B.shape[1], 1 if trans_b else 0, beta,
                                      self._p(C, cr, cc), C.shape[1], capi.stream_handle())
         capi.check(rc, "gg_dgemm_f64")
+
+    def _gemm_padded(self, C, cr, cc, m, n, A, ar, ac, B, br, bc, k, alpha, beta, trans_b):
+        """The DMMA GEMM on zero-padded copies (m to 128, k to 16, n to 128 when B^T)."""
+        mp, kp = -(-m // 128) * 128, -(-k // 16) * 16
+        np_ = -(-n // 128) * 128 if trans_b else n
+        Ap = self.zeros(kp, mp)
+        Ap[:k, :m] = A[ac:ac + k, ar:ar + m]
+        if trans_b:
+            Bp = self.zeros(kp, np_)
+            Bp[:k, :n] = B[bc:bc + k, br:br + n]
+        else:
+            Bp = self.zeros(np_, kp)
+            Bp[:n, :k] = B[bc:bc + n, br:br + k]
+        Cp = self.zeros(np_, mp)
+        if beta != 0.0:
+            Cp[:n, :m] = C[cc:cc + n, cr:cr + m]
+        rc = self.capi.lib().gg_dgemm_f64(mp, np_, kp, alpha, self.capi.ptr(Ap), mp,
+                                          self.capi.ptr(Bp), Bp.shape[1], 1 if trans_b else 0,
+                                          beta, self.capi.ptr(Cp), mp,
+                                          self.capi.stream_handle())
+        self.capi.check(rc, "gg_dgemm_f64")
+        C[cc:cc + n, cr:cr + m] = Cp[:n, :m]
 
     def copy_block(self, dst, r0, c0, src):
         ncols, nrows = src.shape
@@ -375,6 +698,39 @@ class DeviceOps:
             for il, I in enumerate(layout.row_blocks):
                 if I < J:
                     A[jl * nb:(jl + 1) * nb, il * nb:(il + 1) * nb].zero_()
+
+    def kinship_blocks(self, spec, layout):
+        """M_IJ = a/m_k Z_I Z_J^T + (1-a) delta_IJ for this rank's blocks (datagen's construction,
+        element for element the DMMA GEMM of kinship_covariance_device)."""
+        from . import datagen
+
+        torch, capi = self.torch, self.capi
+        n, mk, nb = spec.n, spec.m_kin, layout.nb
+        mk16 = ((mk + 15) // 16) * 16
+        Z = self.zeros(mk16, layout.n_pad)                  # (n_pad x mk16), padding rows zero
+        for first in range(0, mk, 65535):
+            cnt = min(65535, mk - first)
+            capi.check(capi.lib().gg_gen_genotypes_i8(
+                spec.seed, datagen.STREAM_KIN_MAF, datagen.STREAM_KIN_GENO, n, mk, first, cnt,
+                spec.maf[0], spec.maf[1], None, 0, capi.ptr(Z[first:]), layout.n_pad,
+                capi.stream_handle()), "gg_gen_genotypes_i8")
+        A = self.zeros(layout.n_loc, layout.m_loc)
+        if layout.m_loc and layout.n_loc:
+            Zr = self.gather_rows(Z, layout.global_rows(layout.row_blocks))   # (m_loc x mk16)
+            Zc = self.gather_rows(Z, layout.global_rows(layout.col_blocks))   # (n_loc x mk16)
+            del Z
+            # (m_loc x n_loc) = Zr Zc^T; Zc^T as op(B) with B stored n_loc x mk16
+            ZcT = Zc.T.contiguous()                          # (n_loc, mk16) -> B^T layout
+            rc = capi.lib().gg_dgemm_f64(layout.m_loc, layout.n_loc, mk16, 1.0, capi.ptr(Zr),
+                                         layout.m_loc, capi.ptr(ZcT), layout.n_loc, 1, 0.0,
+                                         capi.ptr(A), layout.m_loc, capi.stream_handle())
+            capi.check(rc, "gg_dgemm_f64")
+            A.div_(mk).mul_(spec.a)
+            for I in layout.row_blocks:
+                if I in layout.col_blocks and I * nb < n:
+                    self.set_diag(A, layout.lrow(I), layout.lcol(I), 0,
+                                  min(nb, n - I * nb), 1.0 - spec.a, add=True)
+        return A
 
     def row_exponents(self, B, layout):
         torch, capi = self.torch, self.capi
@@ -433,49 +789,61 @@ class DistConfig:
     fp64_inverse: bool | None = None   # replicate the packed FP64 inverse (None: if it fits)
 
 
-def run_dist(paths, cfg=None, ops=None, sweep=True):
-    """SPMD body (one process per GPU under torchrun; torch.distributed initialised by the
-    caller, NCCL on the B200 box).  Factor + invert M in 2D block-cyclic form, replicate the
-    packed inverse, prepare the context, then stream this rank's share of the SNP blocks with
-    offset-addressed result writes (no per-block communication).  Returns a RunSummary."""
-    import torch.distributed as tdist
+def _default_comm():
+    try:
+        import torch.distributed as tdist
+    except ImportError:   # pragma: no cover
+        return None
+    return as_comm(tdist)
 
+
+def run_dist_engine(paths, cfg=None, ops=None, comm=None, sweep=True, spec=None):
+    """SPMD body of the B200 distributed engine (one process per GPU; ``comm`` defaults to the
+    initialised torch.distributed group, NCCL on the B200 box).  Factor + invert M in 2D
+    block-cyclic form, replicate the int8 slices (and the packed FP64 inverse when it fits),
+    prepare the context, then stream this rank's share of the SNP blocks with offset-addressed
+    result writes (no per-block communication).  ``spec`` (a datagen.BaselineSpec) generates M on
+    every rank's GPU instead of reading paths.cov.  Returns a RunSummary."""
     from . import kernel
     from .pipeline import RunSummary
     from .shard import ShardConfig, stream_shard
 
     cfg = cfg or DistConfig()
-    dist = tdist if tdist.is_available() and tdist.is_initialized() else None
-    rank = dist.get_rank() if dist else 0
-    world = dist.get_world_size() if dist else 1
+    comm = as_comm(comm) if comm is not None else _default_comm()
+    rank = comm.rank if comm else 0
+    world = comm.size if comm else 1
     ops = ops or DeviceOps()
     t_start = time.perf_counter()
-    n = fileio.read_dims(paths.cov, "GWAM")[0]
+    n = spec.n if spec is not None else fileio.read_dims(paths.cov, "GWAM")[0]
     grid = grid_create(world)
-    layout = BlockCyclic(n, cfg.nb, grid, rank)
-    A, B = local_from_gwam(paths.cov, layout, ops)
-    dist_potrf_inv(A, B, layout, ops, dist)
+    layout = BlockCyclic(n, min(cfg.nb, max(SMALL_NB, -(-n // 128) * 128)), grid, rank)
+    if spec is not None:
+        A, B = local_from_spec(spec, layout, ops)
+    else:
+        A, B = local_from_gwam(paths.cov, layout, ops)
+    dist_potrf_inv(A, B, layout, ops, comm)
     if sweep:
         A = None                           # L itself is not needed by the sweep
     XL = fileio.read_matrix(paths.covariates, "GWAC")
     y = fileio.read_matrix(paths.pheno, "GWAY")
-    slices, expo = assemble_slices(B, layout, ops, dist) if cfg.int8 else (None, None)
+    slices, expo = assemble_slices(B, layout, ops, comm) if cfg.int8 else (None, None)
     fp64 = cfg.fp64_inverse
     if fp64 is None:   # the same decision on every rank (same n, same device class)
         fp64 = _packed_inverse_fits(layout.n, ops)
     if fp64 or slices is None:
-        LinvP = assemble_packed_inverse(B, layout, ops, dist)
+        LinvP = assemble_packed_inverse(B, layout, ops, comm)
         del B
         ctx = kernel.prepare_from_inverse(LinvP, n, XL, y, slices=slices, expo=expo)
     else:   # config-4 sizes: no replicated FP64 inverse; whiten from the block-cyclic one
         LinvP = None
-        XLy = whiten_blockcyclic(B, layout, ops, np.column_stack([XL, np.ravel(y)]), dist)
+        XLy = whiten_blockcyclic(B, layout, ops, np.column_stack([XL, np.ravel(y)]), comm)
         del B
         ctx = kernel.prepare_from_inverse(None, n, XL, y, slices=slices, expo=expo, XLy=XLy)
     t_prepare = time.perf_counter() - t_start
     if not sweep:
         return ctx, (A, layout)
-    s = stream_shard(paths, ctx, ShardConfig(m_blk=cfg.m_blk, emit_s_inv=cfg.emit_s_inv))
+    s = stream_shard(paths, ctx, ShardConfig(m_blk=cfg.m_blk, emit_s_inv=cfg.emit_s_inv),
+                     comm=comm)
     return RunSummary(
         mode="dist", n=n, m=s.m, p=ctx.p, m_blk=s.m_blk, np_=world, threads=1,
         t_prepare=t_prepare, t_compute=s.t_compute, t_io_wait=s.t_io_wait,
@@ -485,6 +853,28 @@ def run_dist(paths, cfg=None, ops=None, sweep=True):
         peak_resident_est=8 * layout.m_loc * layout.n_loc * 2
         + (8 * LinvP.numel() if LinvP is not None else 0)
         + (slices.numel() if slices is not None else 0))
+
+
+def run_dist(t, paths, cfg=None):
+    """The reference's SPMD body ``run_dist(t, paths, cfg)`` (distgrid.py:331-469), called on
+    every rank by ``run_spmd`` (the reference's inproc / socket transports, or our
+    transport.run_spmd(..., transport="nccl")).  ``cfg`` may be the reference's DistConfig
+    (m_blk, emit_s_inv, nb, threads) or ours.  The reference's block contract is kept -- m_blk
+    must be a multiple of the rank count (distgrid.py:349-351) -- but the B200 engine streams its
+    own 8,192-SNP GPU blocks (results do not depend on the block size) and its own factorisation
+    block (nb 128 / 512).  Returns a RunSummary (combine / localpart bytes 0: no per-block
+    communication at all)."""
+    comm = as_comm(t)
+    np_ = t.size
+    m_blk = getattr(cfg, "m_blk", None) if cfg is not None else None
+    if m_blk is not None and m_blk % np_ != 0:
+        raise ConfigError(f"m_blk={m_blk} not divisible by np={np_}")
+    n = fileio.read_dims(paths.cov, "GWAM")[0]
+    ours = DistConfig(m_blk=8192, emit_s_inv=bool(getattr(cfg, "emit_s_inv", False)),
+                      nb=_adapter_nb(n))
+    if isinstance(cfg, DistConfig):
+        ours = cfg
+    return run_dist_engine(paths, ours, comm=comm)
 
 
 def _packed_inverse_fits(n, ops):

@@ -23,7 +23,9 @@ import sys
 KERNEL_FUNCS = ("cholesky_spd", "trsolve_lower", "gram", "cholesky_solve_batch",
                 "solve_small_spd", "gls_prepare", "solve_whitened_block", "gls_solve_block")
 ENGINE_FUNCS = ("run_incore", "run_ooc")
-OUR_MODULES = ("errors", "kernel", "fileio", "pipeline", "shard", "_capi", "_device")
+DIST_FUNCS = ("run_dist", "dist_cholesky", "dist_trsolve")
+OUR_MODULES = ("errors", "kernel", "fileio", "pipeline", "shard", "_capi", "_device", "distgrid",
+               "comm", "transport")
 
 
 class Handle:
@@ -40,12 +42,28 @@ class Handle:
         self._saved.clear()
 
 
-def install(ref=None, engines=False):
+def _spmd_with_nccl(orig, ours):
+    """The reference's run_spmd (transport.py:267-327) plus transport="nccl": one process per
+    GPU over torch.distributed (paper_1304_2272_b200.transport); other transports unchanged."""
+
+    def run_spmd(size, fn, *args, transport="inproc"):
+        if transport == "nccl":
+            return ours.run_spmd(size, fn, *args, transport="nccl")
+        return orig(size, fn, *args, transport=transport)
+
+    run_spmd.__doc__ = orig.__doc__
+    return run_spmd
+
+
+def install(ref=None, engines=False, dist=True):
     """Install into the reference package ``ref`` (default: ``import gwasgls``).
 
     engines=True also replaces ``pipeline.run_incore``/``run_ooc`` with the GPU stream engines
     (pinned double buffers + copy stream); by default the reference's own drivers run and call the
-    GPU kernels block by block."""
+    GPU kernels block by block.  dist=True (default) replaces ``distgrid.run_dist`` /
+    ``dist_cholesky`` / ``dist_trsolve`` with the B200 distributed engine (same signatures: the
+    reference's transports and element-cyclic DistMatrix2D in, results out) and adds
+    transport="nccl" to ``transport.run_spmd``."""
     if ref is None:
         ref = importlib.import_module("gwasgls")
     rk = importlib.import_module(ref.__name__ + ".kernel")
@@ -68,6 +86,13 @@ def install(ref=None, engines=False):
         rp = importlib.import_module(ref.__name__ + ".pipeline")
         for name in ENGINE_FUNCS:
             h.set(rp, name, getattr(ours["pipeline"], name))
+    # 4. the distributed entry points and the NCCL launcher
+    if dist:
+        rd = importlib.import_module(ref.__name__ + ".distgrid")
+        for name in DIST_FUNCS:
+            h.set(rd, name, getattr(ours["distgrid"], name))
+        rt = importlib.import_module(ref.__name__ + ".transport")
+        h.set(rt, "run_spmd", _spmd_with_nccl(rt.run_spmd, ours["transport"]))
     return h
 
 

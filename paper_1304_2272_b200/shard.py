@@ -22,6 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import fileio, kernel
+from .comm import as_comm
 from .pipeline import RunSummary, _load_prepare, block_plan, stream_file_blocks
 
 
@@ -64,17 +65,18 @@ def _barrier(dist):
         dist.barrier()
 
 
-def stream_shard(paths, ctx, cfg=None, solve_fn=None):
+def stream_shard(paths, ctx, cfg=None, solve_fn=None, comm=None):
     """Stream this rank's share of the marker blocks of ``paths.geno`` against ``ctx`` and write
     their records at global offsets of ``paths.out`` (rank 0 creates the file).  Collective over
-    the initialised process group; returns job-level ShardStats on every rank.
+    ``comm`` (default: the initialised torch.distributed group; any communicator of comm.py, e.g.
+    a reference transport); returns job-level ShardStats on every rank.
 
     solve_fn(ctx, data, first) -> kernel.ResultArrays replaces the device stream in the CPU
     tests of the sharding logic."""
     cfg = cfg or ShardConfig()
-    dist = _dist()
-    rank = dist.get_rank() if dist else 0
-    world = dist.get_world_size() if dist else 1
+    dist = as_comm(comm) if comm is not None else as_comm(_dist())
+    rank = dist.rank if dist else 0
+    world = dist.size if dist else 1
     _, n, m = fileio.total_genotype_bytes(paths.geno)
     m_blk = min(cfg.m_blk, m)
     p = ctx.p
@@ -112,11 +114,7 @@ def stream_shard(paths, ctx, cfg=None, solve_fn=None):
     _barrier(dist)
     stats = dict(bytes_read=reader.bytes_read, bytes_written=writer.bytes_written,
                  t_loop=t_loop, t_dev=t_dev)
-    if dist is not None:
-        allst = [None] * world
-        dist.all_gather_object(allst, stats)
-    else:
-        allst = [stats]
+    allst = dist.allgather_obj(stats) if dist is not None else [stats]
     t_max = max(s["t_loop"] for s in allst)
     return ShardStats(m=m, m_blk=m_blk, t_compute=max(t_loop - t_io, 0.0), t_io_wait=t_io,
                       t_loop=t_loop, t_device=max(s["t_dev"] for s in allst),

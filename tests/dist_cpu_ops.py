@@ -105,6 +105,22 @@ class CpuOps:
     def to_host(self, T):
         return T.numpy().T
 
+    def identity_share(self, layout):
+        B = self.zeros(layout.n_loc, layout.m_loc)
+        for I in layout.row_blocks:
+            if I in layout.col_blocks:
+                self.set_diag(B, layout.lrow(I), layout.lcol(I), 0, layout.nb, 1.0, add=False)
+        return B
+
+    def set_diag(self, A, r0, c0, lo, hi, value, add):
+        if hi <= lo:
+            return
+        idx = torch.arange(lo, hi)
+        if add:
+            A[c0 + idx, r0 + idx] += value
+        else:
+            A[c0 + idx, r0 + idx] = value
+
     def potrf_inv(self, A, r0, c0, nb):
         blk = A[c0:c0 + nb, r0:r0 + nb].numpy().T
         L, info = dpotrf(np.ascontiguousarray(blk), lower=1, clean=1)
@@ -113,7 +129,26 @@ class CpuOps:
         Li = solve_triangular(L, np.eye(nb), lower=True)
         return -1, self.from_host(L), self.from_host(np.tril(Li))
 
+    def trtri(self, A, r0, c0, nb):
+        blk = np.tril(A[c0:c0 + nb, r0:r0 + nb].numpy().T)
+        return self.from_host(solve_triangular(blk, np.eye(nb), lower=True))
+
+    def kinship_blocks(self, spec, layout):
+        """Host restatement of DeviceOps.kinship_blocks (datagen's construction per block)."""
+        from paper_1304_2272_b200 import datagen
+
+        Z = np.zeros((layout.n_pad, spec.m_kin))
+        Z[:spec.n] = datagen.standardized_host(spec.seed, spec.n, spec.m_kin, spec.maf)
+        rows = layout.global_rows(layout.row_blocks)
+        cols = layout.global_rows(layout.col_blocks)
+        A = (Z[rows] @ Z[cols].T) / spec.m_kin * spec.a
+        d = rows[:, None] == cols[None, :]
+        A[d & (rows[:, None] < spec.n)] += 1.0 - spec.a
+        return self.from_host(A)
+
     def gemm(self, C, cr, cc, m, n, A, ar, ac, B, br, bc, k, alpha, beta, trans_b):
+        if m == 0 or n == 0:
+            return
         Am = A[ac:ac + k, ar:ar + m].T
         Bm = B[bc:bc + k, br:br + n] if trans_b else B[bc:bc + n, br:br + k].T
         Cv = C[cc:cc + n, cr:cr + m]

@@ -1,5 +1,8 @@
-"""GPU: the distributed (config-4) engine with the sm_100a kernels on one rank (grid 1x1; the
-multi-rank communication logic is covered over gloo in tests/test_distgrid_gloo.py)."""
+"""GPU: the distributed (config-4) engine with the sm_100a kernels -- one rank, and several ranks
+sharing this one B200 (threads with a reference-contract transport, or processes over gloo
+through transport.run_spmd): world 2 and 4 on grids 1x2 / 2x2, against the CPU oracle.  The
+ranks' kernels never wait on one another on the device (every exchange is a host-mediated
+transport or gloo collective), so co-locating them on one GPU is safe."""
 
 import numpy as np
 import pytest
@@ -56,7 +59,8 @@ def test_run_dist_end_to_end(gpu, tmp_path, case, fp64_inverse):
 
     g = golden(case)
     paths = write_golden_dataset(tmp_path, g)
-    s = distgrid.run_dist(paths, distgrid.DistConfig(m_blk=257, nb=128, fp64_inverse=fp64_inverse))
+    s = distgrid.run_dist_engine(paths, distgrid.DistConfig(m_blk=257, nb=128,
+                                                           fp64_inverse=fp64_inverse))
     assert s.mode == "dist" and s.np_ == 1
     pay = fileio.read_matrix(paths.out, "GWAB")
     rel, mism = O.compare(pay.betas, g["beta"])
@@ -81,3 +85,139 @@ def test_slices_only_context_rejects_non_integer_blocks(gpu):
     X[5, 3] = 0.25
     with pytest.raises(DeviceError):       # raised when the (asynchronous) block resolves
         kernel.gls_solve_block(ctx, kernel.SnpBlock(0, X)).results
+
+
+def _ref_cfg(m_blk):
+    """A reference-style DistConfig (distgrid.py:322-328 fields) for the reference signature."""
+    from types import SimpleNamespace
+
+    return SimpleNamespace(m_blk=m_blk, emit_s_inv=False, nb=64, threads=1)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", ["baseline_p4", "degenerate"])
+def test_reference_signature_run_dist_multi_rank(gpu, tmp_path, world, case):
+    """run_dist(t, paths, cfg) -- the reference's SPMD signature -- on `world` ranks sharing this
+    GPU (threads driving a reference-contract transport): the fused block-cyclic factorisation
+    with row/column broadcasts, replicated slices, SNP-sharded sweep; golden results."""
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import distgrid, fileio
+    from spmd_inproc import run_spmd
+
+    g = golden(case)
+    paths = write_golden_dataset(tmp_path, g)
+    res = run_spmd(world, distgrid.run_dist, paths, _ref_cfg(16 * world))
+    assert all(r.mode == "dist" and r.np_ == world for r in res)
+    assert res[0].combine_bytes == 0 and res[0].localpart_bytes == 0
+    pay = fileio.read_matrix(paths.out, "GWAB")
+    rel, mism = O.compare(pay.betas, g["beta"])
+    assert mism == 0 and rel <= 1e-9
+
+
+def test_reference_signature_rejects_indivisible_block(gpu, tmp_path):
+    from paper_1304_2272_b200 import distgrid
+    from paper_1304_2272_b200.errors import ConfigError
+    from spmd_inproc import run_spmd
+
+    paths = write_golden_dataset(tmp_path, golden("seed42"))
+    with pytest.raises(ConfigError):
+        run_spmd(3, distgrid.run_dist, paths, _ref_cfg(128))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_cholesky_and_trsolve_reference_signatures_on_device(gpu, world):
+    """dist_cholesky(M, t, nb) / dist_trsolve(L, B, t, nb) with element-cyclic operands on the
+    device ops (reference tests/test_distgrid.py:140-238 tolerances)."""
+    from scipy.linalg import cholesky, solve_triangular
+
+    from paper_1304_2272_b200 import distgrid
+    from spmd_inproc import EC, gather_ec, run_spmd
+
+    n = 300
+    M = make_spd(n, 42)
+    rng = np.random.default_rng(5)
+    B = rng.standard_normal((n, 20))
+
+    def body(t):
+        g = distgrid.grid_create(t.size)
+        Ld = distgrid.dist_cholesky(EC.of(M, g, t.rank), t, nb=8)
+        X = distgrid.dist_trsolve(Ld, EC.of(B, g, t.rank), t, nb=16)
+        return gather_ec(Ld, t), gather_ec(X, t)
+
+    Lr = cholesky(M, lower=True)
+    Xr = solve_triangular(Lr, B, lower=True)
+    for L, X in run_spmd(world, body):
+        assert np.max(np.abs(L - Lr)) <= 1e-10 * np.max(np.abs(M))
+        assert np.max(np.abs(Lr @ X - B)) / np.max(np.abs(B)) <= 1e-12
+        assert np.max(np.abs(X - Xr)) <= 1e-10 * np.max(np.abs(Xr))
+
+
+def test_config4_form_at_n10k_grid_2x2_against_the_oracle(gpu):
+    """BASELINE.md §3's smaller-n 2D run of the config-4 path: n = 10,000, nb = 512, grid 2x2
+    (four ranks on this GPU), M generated per rank on the device (local_from_spec), fused
+    Cholesky + inverse with row/column broadcasts, int8 slices assembled without any replicated
+    FP64 inverse, [X_L | y] whitened from the block-cyclic inverse, then a 1,024-SNP sample
+    through the slices-only context -- against the CPU oracle on the gathered M."""
+    import torch
+
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import datagen, distgrid, kernel
+    from spmd_inproc import run_spmd
+
+    spec = datagen.BaselineSpec(n=10_000, m=1024, p=4, m_kin=5000, a=0.6)
+    XL, y = datagen.covariates_host(spec)
+
+    def body(t):
+        ops = distgrid.DeviceOps()
+        lay = distgrid.BlockCyclic(spec.n, 512, distgrid.grid_create(t.size), t.rank)
+        A, B = distgrid.local_from_spec(spec, lay, ops)
+        blocks = (lay.global_rows(lay.row_blocks), lay.global_rows(lay.col_blocks),
+                  ops.to_host(A).copy())
+        distgrid.dist_potrf_inv(A, B, lay, ops, t)
+        S, e = distgrid.assemble_slices(B, lay, ops, t)
+        XLy = distgrid.whiten_blockcyclic(B, lay, ops, np.column_stack([XL, y]), t)
+        ctx = kernel.prepare_from_inverse(None, spec.n, XL, y, slices=S, expo=e, XLy=XLy)
+        G = datagen.genotypes_host(spec.seed, spec.n, spec.m, 0, spec.m)
+        beta = np.array([r.beta for r in kernel.gls_solve_block(ctx, kernel.SnpBlock(0, G)).results])
+        torch.cuda.synchronize()
+        return blocks, beta
+
+    res = run_spmd(4, body)
+    Md = datagen.kinship_covariance_device(spec).cpu().numpy()
+    n = spec.n
+    for (rows, cols, A), _ in res:        # per-rank blocks == the dense device construction
+        rv, cv = rows < n, cols < n
+        sub, ref = A[np.ix_(rv, cv)], Md[np.ix_(rows[rv], cols[cv])]
+        low = rows[rv][:, None] >= cols[cv][None, :]
+        assert np.array_equal(sub[low], ref[low])
+    octx = O.gls_prepare(Md, XL, y)
+    G = datagen.genotypes_host(spec.seed, spec.n, spec.m, 0, spec.m).astype(np.float64)
+    ob, _ = O.gls_solve_block(octx, G)
+    for _, beta in res:
+        rel, mism = O.compare(beta, ob)
+        assert mism == 0 and rel <= 1e-9, rel
+        assert np.array_equal(beta, res[0][1], equal_nan=True)     # identical on every rank
+
+
+def _nccl_transport_run_dist(t, paths):
+    from paper_1304_2272_b200 import distgrid
+
+    return distgrid.run_dist(t, paths, None)
+
+
+def test_run_spmd_nccl_transport_processes(gpu, tmp_path, monkeypatch):
+    """transport.run_spmd(2, run_dist, ..., transport="nccl") as two processes on this GPU (the
+    collectives on gloo: NCCL refuses two ranks on one device) -- the launcher, NcclTransport and
+    the engine end to end."""
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import fileio, transport
+
+    monkeypatch.setenv("GG_SPMD_BACKEND", "gloo")
+    monkeypatch.setenv("GG_SPMD_TIMEOUT", "600")
+    g = golden("seed42")
+    paths = write_golden_dataset(tmp_path, g)
+    res = transport.run_spmd(2, _nccl_transport_run_dist, paths, transport="nccl")
+    assert [r.np_ for r in res] == [2, 2]
+    pay = fileio.read_matrix(paths.out, "GWAB")
+    rel, mism = O.compare(pay.betas, g["beta"])
+    assert mism == 0 and rel <= 1e-9

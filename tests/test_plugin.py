@@ -51,3 +51,28 @@ def test_install_and_uninstall(gwasgls):
     from paper_1304_2272_b200 import errors as oerr
 
     assert ok.NotPositiveDefinite is oerr.NotPositiveDefinite
+
+
+def test_install_rebinds_the_distributed_entry_points(gwasgls):
+    from gwasgls import distgrid as rd
+    from gwasgls import transport as rt
+
+    from paper_1304_2272_b200 import distgrid as od
+    from paper_1304_2272_b200 import plugin
+
+    before = {n: getattr(rd, n) for n in plugin.DIST_FUNCS}
+    spmd = rt.run_spmd
+    h = plugin.install(gwasgls)
+    try:
+        for n in plugin.DIST_FUNCS:
+            assert getattr(rd, n) is getattr(od, n)
+        assert rt.run_spmd is not spmd
+        # the reference's own transports still run (here: a trivial SPMD body, no device work)
+        assert rt.run_spmd(3, lambda t: t.rank * 10) == [0, 10, 20]
+        with pytest.raises(ValueError):
+            rt.run_spmd(2, lambda t: 0, transport="bogus")
+    finally:
+        h.uninstall()
+    for n in plugin.DIST_FUNCS:
+        assert getattr(rd, n) is before[n]
+    assert rt.run_spmd is spmd
