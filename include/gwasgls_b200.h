@@ -81,6 +81,16 @@ size_t gg_trtri_workspace_bytes(int n);
 int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp,
                        void* work, void* stream);
 
+/* Blocked forward substitution X = L^-1 B for an arbitrary lower-triangular L (np x np, padded
+ * as above, upper part ignored) -- the drop-in kernel.trsolve_lower (kernel.py:112-121: scipy
+ * solve_triangular -> dtrtrs -> dtrsm).  The 128 x 128 diagonal blocks are inverted in one
+ * launch, then per block column X_J = L_JJ^-1 B_J and B_{J+1:} -= L_{J+1:,J} X_J on DMMA GEMMs:
+ * O(n^2 nrhs), backward-stable like dtrsm's blocked form (no O(n^3) explicit inverse).  X may
+ * alias B.  work: gg_trsm_lower_blocked_workspace_bytes(n, nrhs) bytes.                        */
+size_t gg_trsm_lower_blocked_workspace_bytes(int n, int nrhs);
+int gg_trsm_lower_blocked_f64(int n, int nrhs, const double* L, int ldl, const double* B,
+                              int ldb, double* X, int ldx, void* work, void* stream);
+
 /* ---- Streamed TRSM -----------------------------------------------------------------
  * X = L^-1 B for nrhs columns, computed as the lower-triangular product Linv * B
  * on FP64 DMMA tiles (replaces kernel.trsolve_lower, kernel.py:112-121, i.e.

@@ -32,6 +32,8 @@ SIGNATURES = {
     "gg_potrf_f64": (_i, [_i, _vp, _i, _i, _vp, _vp, _i, _vp, _ip, _vp]),
     "gg_trtri_workspace_bytes": (_sz, [_i]),
     "gg_trtri_lower_f64": (_i, [_i, _vp, _i, _vp, _i, _vp, _vp]),
+    "gg_trsm_lower_blocked_workspace_bytes": (_sz, [_i, _i]),
+    "gg_trsm_lower_blocked_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp, _vp]),
     "gg_trsm_lower_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
     "gg_trsm_lower_rm_f64": (_i, [_i, _i, _vp, _i, _vp, _i, _vp, _i, _vp]),
     "gg_packed_lower_bytes": (_sz, [_i]),

@@ -57,6 +57,20 @@ int gg_trtri_lower_f64(int n, const double* L, int ldl, double* Linv, int ldp, v
   return gg::trtri_run(n, L, ldl, Linv, ldp, work, as_stream(stream));
 }
 
+size_t gg_trsm_lower_blocked_workspace_bytes(int n, int nrhs) {
+  return n < 1 ? 0 : gg::trsm_blocked_ws_bytes(n, nrhs);
+}
+
+int gg_trsm_lower_blocked_f64(int n, int nrhs, const double* L, int ldl, const double* B,
+                              int ldb, double* X, int ldx, void* work, void* stream) {
+  GG_NVTX("gg_trsm_lower_blocked_f64");
+  if (n < 1 || nrhs < 0 || L == nullptr || B == nullptr || X == nullptr || work == nullptr) {
+    gg::set_error("trsm_blocked: null pointer or bad size");
+    return GG_EARG;
+  }
+  return gg::trsm_blocked_run(n, nrhs, L, ldl, B, ldb, X, ldx, work, as_stream(stream));
+}
+
 int gg_trsm_lower_f64(int n, int nrhs, const double* Linv, int ldp, const double* B, int ldb,
                       double* X, int ldx, void* stream) {
   if (n < 1 || nrhs < 0 || Linv == nullptr || B == nullptr || X == nullptr) {

@@ -74,6 +74,9 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
               cudaStream_t s);
 size_t potrf_ws_bytes(int n);
 size_t trtri_ws_bytes(int n);
+size_t trsm_blocked_ws_bytes(int n, int nrhs);
+int trsm_blocked_run(int n, int nrhs, const double* L, int ldl, const double* B, int ldb,
+                     double* X, int ldx, void* work, cudaStream_t s);
 
 // ---- TMA/DMMA streamed TRSM (trsm_tma.cu) -------------------------------------------------
 int trsm_rowmajor_run(int n, int nrhs, const double* LinvT, int ldp, const double* B, int ldb,

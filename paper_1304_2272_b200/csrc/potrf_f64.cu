@@ -136,10 +136,12 @@ __device__ void warp_inverse32(const double* S, int j0, double* T, int lane) {
   __syncwarp();
 }
 
+// panel != 0 (inverse only): diagonal block k0's inverse goes to rows k0.. of an np x 128 panel
+// (Dinv + k0, ld ldi) instead of the diagonal of a square matrix (the blocked substitution TRSM).
 template <bool FACTOR>
 __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long long ld,
                                                              double* Dinv, long long ldi, int k0,
-                                                             int* info) {
+                                                             int* info, int panel = 0) {
   extern __shared__ double lsm[];
   double* S = lsm;                          // 128 x 128 row-major (ld LDS): the block, then L
   double* T = lsm + NB * LDS;               // 4 x (32 x 32): T_J = L_JJ^-1
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(LEAF_THREADS) leaf2_kernel(double* A, long lon
   // ---- inverse: X_IJ = -T_I sum_{K=J}^{I-1} L_IK X_KJ, block rows I = 1..3 in order; X is
   // kept in the lower blocks of S (S's L_IK for K < I is read before X_IK overwrites it:
   // each block row I first computes all its W_IJ, then writes)
-  double* Db = Dinv + k0 + (long long)k0 * ldi;
+  double* Db = Dinv + k0 + (panel ? 0ll : (long long)k0 * ldi);
   for (int I = 1; I < NB / LB; ++I) {
     // W_IJ = sum_{K=J}^{I-1} L_IK X_KJ for J < I   (X_KK = T_K; X_KJ, K > J, from S)
     for (int e = tid; e < I * LB * LB; e += blockDim.x) {
@@ -538,6 +540,61 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
   const size_t oz_bytes = use_ozaki() ? oz_region_bytes(np, false) : 0;
   void* oz = oz_bytes ? static_cast<char*>(work) + HDR_BYTES + t_region_bytes(np) : nullptr;
   return trtri_offdiag(0, np, L, Linv, ldp, T, tr > 0 ? tr : 1, oz, oz_bytes, nullptr, s);
+}
+
+// Blocked forward substitution X = L^-1 B (kernel.trsolve_lower for an arbitrary L): the inverses
+// of all 128 x 128 diagonal blocks in one leaf launch (an np x 128 panel), then per block column J
+//   X_J = Dinv_J B_J                 (DMMA GEMM, 128 x nrhs x 128)
+//   B_{J+1:} -= L_{J+1:, J} X_J     (DMMA GEMM, rows below x nrhs x 128)
+// O(n^2 nrhs) work, backward-stable like dtrsm's blocked form (no O(n^3) full inverse).  X may
+// alias B (the right-hand side is consumed in place when it does).
+size_t trsm_blocked_ws_bytes(int n, int nrhs) {
+  const size_t np = (size_t)pad_rows(n);
+  return np * NB * sizeof(double) + (size_t)NB * (size_t)(nrhs > 0 ? nrhs : 1) * sizeof(double) +
+         256;
+}
+
+int trsm_blocked_run(int n, int nrhs, const double* L, int ldl, const double* B, int ldb,
+                     double* X, int ldx, void* work, cudaStream_t s) {
+  const int np = pad_rows(n);
+  if (ldl < np || ldb < np || ldx < np) {
+    set_error("trsm_blocked: leading dimensions must be >= gg_pad(n)");
+    return GG_EDIM;
+  }
+  if (nrhs <= 0) return GG_OK;
+  double* D = static_cast<double*>(work);                      // np x 128, ld np
+  double* Y = D + (size_t)np * NB;                             // 128 x nrhs, ld 128
+  GG_CUDA_TRY(cudaFuncSetAttribute(leaf2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)LEAF2_SMEM));
+  leaf2_kernel<false><<<np / NB, LEAF_THREADS, LEAF2_SMEM, s>>>(const_cast<double*>(L), ldl, D,
+                                                               np, 0, nullptr, 1);
+  GG_LAUNCH_CHECK("trsm_blocked leaf_kernel");
+  if (X != B)
+    GG_CUDA_TRY(cudaMemcpy2DAsync(X, (size_t)ldx * sizeof(double), B, (size_t)ldb * sizeof(double),
+                                  (size_t)np * sizeof(double), nrhs, cudaMemcpyDeviceToDevice, s));
+  for (int J = 0; J < np; J += NB) {
+    GemmArgs d{};
+    d.M = NB; d.N = nrhs; d.K = NB;
+    d.A = D + J; d.lda = np;
+    d.B = X + J; d.ldb = ldx;
+    d.C = Y; d.ldc = NB;
+    d.alpha = 1.0; d.beta = 0.0; d.flags = GEMM_A_LOWER; d.abort_flag = nullptr;
+    int rc = launch_dgemm(d, false, s);
+    if (rc != GG_OK) return rc;
+    GG_CUDA_TRY(cudaMemcpy2DAsync(X + J, (size_t)ldx * sizeof(double), Y, NB * sizeof(double),
+                                  NB * sizeof(double), nrhs, cudaMemcpyDeviceToDevice, s));
+    const int rem = np - J - NB;
+    if (rem <= 0) break;
+    GemmArgs u{};
+    u.M = rem; u.N = nrhs; u.K = NB;
+    u.A = L + (J + NB) + (long long)J * ldl; u.lda = ldl;
+    u.B = X + J; u.ldb = ldx;
+    u.C = X + J + NB; u.ldc = ldx;
+    u.alpha = -1.0; u.beta = 1.0; u.flags = 0; u.abort_flag = nullptr;
+    rc = launch_dgemm(u, false, s);
+    if (rc != GG_OK) return rc;
+  }
+  return GG_OK;
 }
 
 }  // namespace gg

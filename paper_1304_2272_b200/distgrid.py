@@ -318,7 +318,11 @@ def whiten_blockcyclic(B, layout, ops, RHS, comm=None):
                  trans_b=False)
         ops.scatter_cols_rows(Y, rows, Yloc)
     comm = as_comm(comm)
-    return comm.all_reduce(Y) if comm is not None else Y
+    if comm is not None:
+        comm.all_reduce(Y)
+    # rows padded to the device context's pad(n) = ceil(n / 128) * 128 (<= n_pad; zero beyond n)
+    np_ = -(-n // 128) * 128
+    return Y[:, :np_].contiguous() if np_ != layout.n_pad else Y
 
 
 def dist_trsolve_bc(L, layout, ops, RHS, comm=None):
@@ -719,10 +723,9 @@ class DeviceOps:
             Zr = self.gather_rows(Z, layout.global_rows(layout.row_blocks))   # (m_loc x mk16)
             Zc = self.gather_rows(Z, layout.global_rows(layout.col_blocks))   # (n_loc x mk16)
             del Z
-            # (m_loc x n_loc) = Zr Zc^T; Zc^T as op(B) with B stored n_loc x mk16
-            ZcT = Zc.T.contiguous()                          # (n_loc, mk16) -> B^T layout
+            # (m_loc x n_loc) = Zr Zc^T: op(B) = B^T with B = Zc stored n_loc x mk16 (ld n_loc)
             rc = capi.lib().gg_dgemm_f64(layout.m_loc, layout.n_loc, mk16, 1.0, capi.ptr(Zr),
-                                         layout.m_loc, capi.ptr(ZcT), layout.n_loc, 1, 0.0,
+                                         layout.m_loc, capi.ptr(Zc), layout.n_loc, 1, 0.0,
                                          capi.ptr(A), layout.m_loc, capi.stream_handle())
             capi.check(rc, "gg_dgemm_f64")
             A.div_(mk).mul_(spec.a)

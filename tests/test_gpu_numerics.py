@@ -1,0 +1,126 @@
+"""GPU: numerics beyond the benign BASELINE matrices (VERDICT r1 "harden the numerics").
+
+* trsolve_lower on rough-diagonal and ill-conditioned triangular factors: the blocked device
+  substitution keeps the reference's residual bar (tests/test_kernel.py:71-76) and stays as
+  accurate as scipy's dtrsm against an extended-precision solve;
+* GLS on ill-conditioned covariances (cond 1e6 .. 1e10) and on covariances whose inverse rows
+  are NOT diagonal-dominant (AR(1) correlation, rho = 0.99 / 0.999 -- the int8 slicing then
+  sets each row's exponent by its off-diagonal entries): the GPU results are at least as close
+  to an extended-precision (80-bit long double) evaluation of Eq. 1 as the CPU oracle's, and
+  within the north-star 1e-9 of the oracle wherever the problem's condition allows it.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LD = np.longdouble
+
+
+def _chol_ld(M):
+    A = np.array(M, dtype=LD)
+    n = A.shape[0]
+    L = np.zeros_like(A)
+    for j in range(n):
+        d = A[j, j] - np.dot(L[j, :j], L[j, :j])
+        L[j, j] = np.sqrt(d)
+        L[j + 1:, j] = (A[j + 1:, j] - L[j + 1:, :j] @ L[j, :j]) / L[j, j]
+    return L
+
+
+def _fwd_ld(L, B):
+    X = np.array(B, dtype=LD)
+    for i in range(L.shape[0]):
+        X[i] = (X[i] - L[i, :i] @ X[:i]) / L[i, i]
+    return X
+
+
+def _small_solve_ld(S, r):
+    p = S.shape[0]
+    L = np.zeros_like(S)
+    for j in range(p):
+        L[j, j] = np.sqrt(S[j, j] - np.dot(L[j, :j], L[j, :j]))
+        for i in range(j + 1, p):
+            L[i, j] = (S[i, j] - np.dot(L[i, :j], L[j, :j])) / L[j, j]
+    z = _fwd_ld(L, r)
+    x = np.zeros_like(z)
+    for i in range(p - 1, -1, -1):
+        x[i] = (z[i] - L[i + 1:, i] @ x[i + 1:]) / L[i, i]
+    return x
+
+
+def _gls_ld(M, XL, y, G):
+    """Eq. 1 through an extended-precision Cholesky (the truth for the comparisons)."""
+    L = _chol_ld(M)
+    XLb = _fwd_ld(L, XL)
+    yb = _fwd_ld(L, y)
+    Xb = _fwd_ld(L, G)
+    out = []
+    for j in range(G.shape[1]):
+        A = np.column_stack([XLb, Xb[:, j]])
+        out.append(_small_solve_ld(A.T @ A, A.T @ yb))
+    return np.array(out, dtype=np.float64)
+
+
+def _rel(a, b):
+    return float(np.max(np.max(np.abs(a - b), axis=1) / np.max(np.abs(b), axis=1)))
+
+
+def test_trsolve_rough_diagonal_and_ill_conditioned(gpu):
+    from scipy.linalg import solve_triangular
+
+    from paper_1304_2272_b200 import kernel
+
+    rng = np.random.default_rng(21)
+    for n, diag in ((300, 8.0), (300, 2.0), (513, 1.0)):
+        L = np.tril(rng.standard_normal((n, n)))
+        L[np.diag_indices(n)] = np.abs(L[np.diag_indices(n)]) + diag
+        B = rng.standard_normal((n, 17))
+        X = kernel.trsolve_lower(L, B)
+        Xs = solve_triangular(L, B, lower=True)
+        Xt = np.array(_fwd_ld(L, B), dtype=np.float64)
+        res = np.max(np.abs(L @ X - B)) / np.max(np.abs(B))
+        res_s = np.max(np.abs(L @ Xs - B)) / np.max(np.abs(B))
+        assert res <= max(1e-12, 8 * res_s), (n, diag, res, res_s)
+        err = np.max(np.abs(X - Xt)) / np.max(np.abs(Xt))
+        err_s = np.max(np.abs(Xs - Xt)) / np.max(np.abs(Xt))
+        assert err <= max(4e-15, 8 * err_s), (n, diag, err, err_s)
+
+
+def _spd_with_cond(n, cond, rng):
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    M = (Q * np.logspace(0, -np.log10(cond), n)) @ Q.T
+    return np.tril(M) + np.tril(M, -1).T
+
+
+def _ar1(n, rho):
+    i = np.arange(n)
+    return rho ** np.abs(i[:, None] - i[None, :])
+
+
+@pytest.mark.parametrize("kind,param", [("cond", 1e6), ("cond", 1e8), ("cond", 1e10),
+                                        ("ar1", 0.99), ("ar1", 0.999)])
+def test_gls_hard_covariances_vs_extended_precision(gpu, kind, param):
+    from oracle import gls_ref as O
+    from paper_1304_2272_b200 import kernel
+
+    rng = np.random.default_rng(7)
+    n = 400
+    M = _spd_with_cond(n, param, rng) if kind == "cond" else _ar1(n, param)
+    XL = np.column_stack([np.ones(n), rng.standard_normal((n, 2))])
+    y = rng.standard_normal(n)
+    G = rng.integers(0, 3, (n, 24)).astype(np.float64)
+    truth = _gls_ld(M, XL, y, G)
+    ctx = kernel.gls_prepare(M, XL, y)
+    rb8 = kernel.gls_solve_block(ctx, kernel.SnpBlock(0, np.asfortranarray(G.astype(np.int8))))
+    got = np.array([r.beta for r in rb8.results])                 # int8 tensor-core path
+    octx = O.gls_prepare(M, XL, y)
+    ob, _ = O.gls_solve_block(octx, G)
+    e_gpu, e_cpu = _rel(got, truth), _rel(ob, truth)
+    # at least as accurate as the reference's own LAPACK path (up to a small factor), and the
+    # north-star bar against the oracle where the conditioning leaves digits to compare
+    assert e_gpu <= max(1e-13, 10 * e_cpu), (kind, param, e_gpu, e_cpu)
+    if e_cpu < 1e-11:
+        rel, mism = O.compare(got, ob)
+        assert mism == 0 and rel <= 1e-9, (kind, param, rel)
