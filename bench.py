@@ -447,7 +447,9 @@ def run_ours(args):
     use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1304_2272_b200.comm import init_process_group
+
+        init_process_group("nccl", device=torch.device("cuda", local))
         # the communicator really spans N ranks (one GPU each)
         t = torch.ones(1, device="cuda")
         dist.all_reduce(t)
@@ -636,6 +638,7 @@ def run_e2e(args, sw, world, rank, dev, use_dist, dist, beta_ref):
     return {
         "value": round(m * world * steps / dt, 1), "unit": UNIT,
         "h2d_bytes_per_step": int(n * m), "d2h_bytes_per_step": int(m * (8 * p + 4)),
+        "host_link_gbs": round(n * m * steps / dt / 1e9, 2),
         "steps": steps,
         "api": "paper_1304_2272_b200.kernel.gls_solve_block(ctx, SnpBlock(first, host int8 "
                f"n x {m_blk} view)) per block -- the reference signature (kernel.py:315-342); "

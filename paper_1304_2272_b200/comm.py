@@ -22,6 +22,8 @@ transport.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -49,21 +51,32 @@ class TorchComm:
     def _src(self, root):
         return self.members[root] if self.members is not None else root
 
+    def _run(self, what, fn, *a, **kw):
+        """A collective; a communicator failure (NCCL error or watchdog timeout surfaced by
+        torch.distributed) becomes TransportFailure(rank, ...) -- the reference's class for a
+        failed exchange (errors.py) and the C-ABI's GG_ENCCL meaning."""
+        try:
+            return fn(*a, **kw)
+        except RuntimeError as e:
+            from .errors import TransportFailure
+
+            raise TransportFailure(self.rank, f"{what} on {self.backend} failed: {e}") from e
+
     def all_reduce(self, t, op="sum"):
         if self.size > 1:
             d = self.dist
-            self.dist.all_reduce(t, op=d.ReduceOp.MAX if op == "max" else d.ReduceOp.SUM,
-                                 group=self.group)
+            self._run("all_reduce", d.all_reduce, t,
+                      op=d.ReduceOp.MAX if op == "max" else d.ReduceOp.SUM, group=self.group)
         return t
 
     def broadcast(self, t, root):
         if self.size > 1:
-            self.dist.broadcast(t, src=self._src(root), group=self.group)
+            self._run("broadcast", self.dist.broadcast, t, src=self._src(root), group=self.group)
         return t
 
     def barrier(self):
         if self.size > 1:
-            self.dist.barrier(group=self.group)
+            self._run("barrier", self.dist.barrier, group=self.group)
 
     def allgather_obj(self, obj):
         out = [None] * self.size
@@ -237,6 +250,26 @@ def _unpack(data):
         parts.append(bytes(data[off:off + ln]))
         off += ln
     return parts
+
+
+def init_process_group(backend, rank=None, world_size=None, device=None):
+    """torch.distributed.init_process_group with the engine's failure policy: NCCL's async error
+    handling on (a failed or hung collective aborts the communicator and surfaces as an
+    exception instead of blocking every rank forever) and a bounded timeout
+    (GG_COLLECTIVE_TIMEOUT_S, default 1800 s)."""
+    import datetime
+
+    import torch.distributed as dist
+
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    kw = {"timeout": datetime.timedelta(
+        seconds=float(os.environ.get("GG_COLLECTIVE_TIMEOUT_S", "1800")))}
+    if rank is not None:
+        kw.update(rank=rank, world_size=world_size)
+    if device is not None and backend == "nccl":
+        kw["device_id"] = device
+    dist.init_process_group(backend, **kw)
+    return dist
 
 
 def as_comm(x):

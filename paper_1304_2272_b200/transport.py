@@ -24,7 +24,7 @@ import traceback
 
 import numpy as np
 
-from .comm import TorchComm
+from .comm import TorchComm, init_process_group
 from .errors import TransportFailure
 
 
@@ -124,13 +124,12 @@ def _worker(rank, size, port, backend, fn, args, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(size), LOCAL_RANK=str(rank))
     try:
-        kw = {}
+        device = None
         if torch.cuda.is_available():
             dev = rank % torch.cuda.device_count()
             torch.cuda.set_device(dev)
-            if backend == "nccl":
-                kw["device_id"] = torch.device("cuda", dev)
-        dist.init_process_group(backend, rank=rank, world_size=size, **kw)
+            device = torch.device("cuda", dev)
+        init_process_group(backend, rank=rank, world_size=size, device=device)
         t = NcclTransport(rank, size)
         try:
             res = fn(t, *args)
