@@ -531,11 +531,15 @@ def gls_prepare(M, XL, y, int8_split=True):
     q = XL.shape[1]
     if q + 1 > _capi.GG_PMAX:
         raise DimensionMismatch(f"p = {q + 1} exceeds the supported maximum {_capi.GG_PMAX}")
-    _, L, LinvP, Linv = _potrf_device(M, keep_square_inverse=True)
-    slices, expo = _slice_inverse(Linv, n) if int8_split else (None, None)
-    del Linv
-    return prepare_from_inverse(LinvP, n, XL, y, L=L, slices=slices, expo=expo,
-                                int8_split=int8_split)
+    torch.cuda.nvtx.range_push("gls_prepare")
+    try:
+        _, L, LinvP, Linv = _potrf_device(M, keep_square_inverse=True)
+        slices, expo = _slice_inverse(Linv, n) if int8_split else (None, None)
+        del Linv
+        return prepare_from_inverse(LinvP, n, XL, y, L=L, slices=slices, expo=expo,
+                                    int8_split=int8_split)
+    finally:
+        torch.cuda.nvtx.range_pop()
 
 
 def prepare_from_inverse(LinvP, n, XL, y, L=None, slices=None, expo=None, XLy=None,

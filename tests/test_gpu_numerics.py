@@ -121,8 +121,12 @@ def test_gls_hard_covariances_vs_extended_precision(gpu, kind, param):
     rel, mism = O.compare(got, ob)
     print(f"{kind}={param:g}: GPU vs extended {e_gpu:.2e}, oracle vs extended {e_cpu:.2e}, "
           f"GPU vs oracle {rel:.2e}")
-    # the north-star bar against the oracle, on every case
-    assert mism == 0 and rel <= 1e-9, (kind, param, rel)
+    # the north-star bar against the oracle wherever the problem leaves ~10 digits to compare
+    # (measured r02: at cond(M) = 1e8 / 1e10 LAPACK's own result is 3.5e-9 / 6.2e-7 from the
+    # truth, and ours 4.9e-9 / 4.2e-7 -- two correct FP64 evaluations cannot agree to 1e-9 there)
+    assert mism == 0
+    if e_cpu < 1e-10:
+        assert rel <= 1e-9, (kind, param, rel)
     # accuracy against the truth: the explicit inverse's forward error grows with cond(L) where
     # substitution's does not -- measured (r02): ill-conditioned random spectra within a few x of
     # LAPACK; AR(1) (whitening = a differencing filter, ~1/(1-rho) cancellation in L^-1 x) loses
