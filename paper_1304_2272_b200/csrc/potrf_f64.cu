@@ -32,19 +32,42 @@ struct PotrfHeader {
 };
 constexpr size_t HDR_BYTES = 256;
 
-__global__ void init_factor_kernel(int n, int np, const double* __restrict__ M, long long rs, long long cs,
-                                   double* __restrict__ L, double* __restrict__ Linv,
-                                   long long ldp) {
-  const long long total = (long long)np * np;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx % np), j = (int)(idx / np);
-    double v;
-    if (i < n && j < n) v = (i >= j) ? M[i * rs + j * cs] : 0.0;
-    else v = (i == j) ? 1.0 : 0.0;   // identity extension on the padding block
-    L[i + j * ldp] = v;
-    if (Linv != nullptr) Linv[i + j * ldp] = 0.0;
+// The factor's input pass: L = lower(M) extended by the identity on the padding block, Linv
+// zeroed, and the first non-finite entry of M in row-major order (kernel.py:101-103 reports its
+// row) -- one pass over M through 32 x 32 shared-memory tiles: M is read along its contiguous
+// dimension (row-major input: a C-contiguous array) and L written column-major, both coalesced
+// (element-wise forms re-read a row-major M ~9x from DRAM: 119 GB at n = 4e4).
+__global__ void __launch_bounds__(256) init_factor_tiled_kernel(
+    int n, int np, const double* __restrict__ M, long long rs, long long cs,
+    double* __restrict__ L, double* __restrict__ Linv, long long ldp,
+    unsigned long long* first) {
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const bool rowmaj = cs == 1;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  unsigned long long bad = ~0ull;
+  for (int k = ty; k < 32; k += 8) {
+    const int i = rowmaj ? i0 + k : i0 + tx, j = rowmaj ? j0 + tx : j0 + k;
+    double v = 0.0;
+    if (i < n && j < n) {
+      v = M[i * rs + j * cs];
+      if (!isfinite(v)) bad = min(bad, (unsigned long long)i * n + j);
+    }
+    if (rowmaj)
+      t[k][tx] = v;
+    else
+      t[tx][k] = v;
   }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int i = i0 + tx, j = j0 + k;
+    double v;
+    if (i < n && j < n) v = (i >= j) ? t[tx][k] : 0.0;
+    else v = (i == j) ? 1.0 : 0.0;   // identity extension on the padding block
+    L[i + (long long)j * ldp] = v;
+    if (Linv != nullptr) Linv[i + (long long)j * ldp] = 0.0;
+  }
+  if (bad != ~0ull) atomicMin(first, bad);
 }
 
 __global__ void zero_square_kernel(int np, double* __restrict__ A, long long ld) {
@@ -53,17 +76,6 @@ __global__ void zero_square_kernel(int np, double* __restrict__ A, long long ld)
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % np), j = (int)(idx / np);
     A[i + j * ld] = 0.0;
-  }
-}
-
-// First non-finite entry in row-major order (kernel.py:101-103 reports its row).
-__global__ void nonfinite_kernel(int n, const double* __restrict__ M, long long rs, long long cs,
-                                 unsigned long long* first) {
-  const long long total = (long long)n * n;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx % n), j = (int)(idx / n);
-    if (!isfinite(M[i * rs + j * cs])) atomicMin(first, (unsigned long long)i * n + j);
   }
 }
 
@@ -402,10 +414,9 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   GG_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(int) * 2, s));
   GG_CUDA_TRY(cudaMemsetAsync(&hdr->nonfinite, 0xff, sizeof(unsigned long long), s));
   const long long rs = m_row_major ? ldm : 1, cs = m_row_major ? 1 : ldm;
-  nonfinite_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(n, M, rs, cs, &hdr->nonfinite);
-  GG_LAUNCH_CHECK("nonfinite_kernel");
-  init_factor_kernel<<<grid_for((long long)np * np), 256, 0, s>>>(n, np, M, rs, cs, L, Linv, ldp);
-  GG_LAUNCH_CHECK("init_factor_kernel");
+  init_factor_tiled_kernel<<<dim3(np / 32, np / 32), 256, 0, s>>>(n, np, M, rs, cs, L, Linv, ldp,
+                                                                  &hdr->nonfinite);
+  GG_LAUNCH_CHECK("init_factor_tiled_kernel");
   GG_CUDA_TRY(cudaFuncSetAttribute(leaf2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)LEAF2_SMEM));
   // optional phase timing (GG_POTRF_TIMING=1): leaf / panel / trailing / inverse, to stderr
