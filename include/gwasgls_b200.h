@@ -40,7 +40,9 @@ extern "C" {
 #define GG_ENOTPD 1      /* Cholesky pivot <= 0 / NaN, or non-finite input      */
 #define GG_EDIM 2        /* inconsistent sizes / leading dimensions              */
 #define GG_ECUDA 3       /* CUDA runtime error                                   */
-#define GG_ENCCL 4       /* reserved for the NCCL (distributed) entry points     */
+#define GG_ENCCL 4       /* a failed collective: the distributed engine drives NCCL from its
+                            host layer (comm.py), which raises TransportFailure with this meaning;
+                            no C-ABI entry point itself calls NCCL                      */
 #define GG_EARG 5        /* invalid argument (NULL pointer, unsupported p, ...)  */
 
 #define GG_TILE 128      /* row padding unit = GEMM tile edge                    */
