@@ -443,15 +443,19 @@ def run_ours(args):
     rank, world, local = dist_env()
     if args.gpus != world:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank; GG_BENCH_BACKEND=gloo (a self-test of the multi-rank code path with several
+    # ranks sharing a GPU) maps rank -> device modulo the device count
+    backend = os.environ.get("GG_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         from paper_1304_2272_b200.comm import init_process_group
 
-        init_process_group("nccl", device=torch.device("cuda", local))
-        # the communicator really spans N ranks (one GPU each)
-        t = torch.ones(1, device="cuda")
+        init_process_group(backend, device=torch.device("cuda", local))
+        # the communicator really spans N ranks
+        t = torch.ones(1, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t)
         assert int(t.item()) == world == dist.get_world_size()
     dev = torch.device("cuda", local)
