@@ -71,7 +71,8 @@ struct I8Args {
   int* tile_counter;  // zeroed before the launch: clusters take tiles dynamically, heavy first
   int rd_bytes;       // bytes per row-data slot (rd_bytes(q, P != nullptr))
   int grp_pp;         // 256-SNP tile pairs per SNP group (tile_coords)
-  int l2hint;         // L2 cache policies on the TMA loads (genotypes evict_last, slices first)
+  int whatif;         // measurement only (GG_I8_WHATIF bits; results invalid): 1 no genotype
+                      // (A) loads, 2 no slice (B) loads, 4 no epilogue work
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -176,28 +177,6 @@ __device__ __forceinline__ void tma_4d_pair(unsigned dst, const CUtensorMap* map
       "[%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(dst),
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2),
       "r"(c3)
-      : "memory");
-}
-// the same loads with an L2 cache policy (createpolicy): the SNP group's genotypes are re-read by
-// every row block of the group (keep them: evict_last), each slice tile only by the group's few
-// SNP tiles that run concurrently (evict_first) -- the L2 then holds a larger genotype group
-__device__ __forceinline__ void tma_2d_pair_hint(unsigned dst, const CUtensorMap* map,
-                                                 unsigned bar, int c0, int c1,
-                                                 unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_4d_pair_hint(unsigned dst, const CUtensorMap* map,
-                                                 unsigned bar, int c0, int c1, int c2, int c3,
-                                                 unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7;\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2),
-      "r"(c3), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void mma_i8_pair(unsigned d_tmem, unsigned long long a,
@@ -370,11 +349,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       unsigned phase = 0;
-      unsigned long long pol_keep = 0, pol_stream = 0;
-      if (a.l2hint) {
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_stream));
-      }
       for (int r = 0;; ++r) {
         int t;
         if (leader) {   // take the next tile (heavy first) and post it to both CTAs
@@ -417,19 +391,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kt = 0; kt < nk; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const unsigned fb = full0 + 8 * stage;
-          if (leader) mbar_expect_tx(fb, 2 * D_STAGE_BYTES);
+          if (leader)
+            mbar_expect_tx(fb, 2 * (D_STAGE_BYTES - ((a.whatif & 1) ? A_BYTES : 0) -
+                                    ((a.whatif & 2) ? 2 * P_B_BYTES : 0)));
           const unsigned dA = sbase + stage * D_STAGE_BYTES;
           const unsigned fbl = fb & PEER_MASK;
           auto loadB = [&](unsigned dst, const CUtensorMap* m, int c1, int c2) {
-            if (a.l2hint)
-              tma_4d_pair_hint(dst, m, fbl, 0, c1, c2, tile0 + kt, pol_stream);
-            else
-              tma_4d_pair(dst, m, fbl, 0, c1, c2, tile0 + kt);
+            if (a.whatif & 2) return;
+            tma_4d_pair(dst, m, fbl, 0, c1, c2, tile0 + kt);
           };
-          if (a.l2hint)
-            tma_2d_pair_hint(dA, &tmA, fbl, kt * TK, nt * TM, pol_keep);
-          else
+          if (a.whatif & 1) {
+            // what-if (timing only, results invalid): no genotype loads -- the A bytes' share of
+            // the L2 -> SMEM stream and of DRAM (the leader expects only the B bytes)
+          } else {
             tma_2d_pair(dA, &tmA, fbl, kt * TK, nt * TM);
+          }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {   // this CTA's 112 slice rows of row block rb0 + h
             const unsigned dB = dA + A_BYTES + h * P_B_BYTES;
@@ -532,6 +508,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int* ex = reinterpret_cast<const int*>(rd);
       const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
       mbar_wait(rdf0 + 8 * slot, (r / D_RD_SLOTS) & 1);
+      if (a.whatif & 4) {   // what-if: release at once, no loads / math / stores
+        fence_before();
+        mbar_arrive_cluster((acce0 + 8 * group) & PEER_MASK);
+        mbar_arrive(rde0 + 8 * slot);
+        continue;
+      }
       const int* hd = reinterpret_cast<const int*>(rd + TR * 4);
       double acc[TR];
       const unsigned taddr = tmem_base + group * ACC_COLS + ((unsigned)(quarter * 32) << 16);
@@ -1031,8 +1013,8 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     grp = grp < 1 ? 1 : (grp > num_pp ? num_pp : grp);
     const int ngroups = (num_pp + grp - 1) / grp;
     a.grp_pp = (num_pp + ngroups - 1) / ngroups;                // equal-width groups
-    a.l2hint = 0;
-    if (const char* h = std::getenv("GG_I8_L2HINT")) a.l2hint = std::atoi(h) != 0;   // what-if
+    a.whatif = 0;
+    if (const char* w = std::getenv("GG_I8_WHATIF")) a.whatif = std::atoi(w);
     a.rd_bytes = rd_bytes(q, P != nullptr);
     // 5 stages of 44 KB when the row data is small (q <= 3), else 4
     const bool five = d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
