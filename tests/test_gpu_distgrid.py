@@ -221,3 +221,22 @@ def test_run_spmd_nccl_transport_processes(gpu, tmp_path, monkeypatch):
     pay = fileio.read_matrix(paths.out, "GWAB")
     rel, mism = O.compare(pay.betas, g["beta"])
     assert mism == 0 and rel <= 1e-9
+
+
+def test_config4_form_at_n40k_world2_on_one_gpu(gpu):
+    """VERDICT r1 item 4's bar: the distributed config-4 form at n = 40,000 on two ranks sharing
+    this GPU (tools/dist_n40k.py): per-rank generation, fused Cholesky + inverse with row/column
+    broadcasts, slices without a replicated FP64 inverse -- equal to the single-GPU prepare."""
+    import re
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    out = subprocess.run([sys.executable, f"{REPO}/tools/dist_n40k.py"], capture_output=True,
+                         text=True, timeout=1500)
+    assert out.returncode == 0, out.stderr[-3000:]
+    rels = [float(x) for x in re.findall(r"max rel ([0-9.e+-]+)", out.stdout)]
+    assert len(rels) == 2 and max(rels) <= 1e-9, out.stdout
+    assert "status mismatches 0" in out.stdout and "identical results on every rank: True" in \
+        out.stdout, out.stdout
