@@ -133,10 +133,10 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
 /* ---- The int8 tensor-core TRSM for dosage blocks ------------------------------------------
  * Dosages are exact int8, so X = L^-1 G runs on tcgen05.mma.kind::i8 with the inverse split
  * error-free into gg_i8_slices() (= 7) int8 slices per row plus an integer diagonal head:
- *     Linv[i,k] = 2^e_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  |a_s| <= 127
+ *     Linv[i,k] = 2^e_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  a_s in [-128, 127]
  * with e_i = max(e_off_i, e_diag_i - 20) (|Linv[i,k]| < 2^e_off_i over k < i, |Linv_ii| <
- * 2^e_diag_i), |h_i| < 2^20; slices 0-5 truncate, the last rounds to nearest (clipped to
- * +-127): the residual is zero-mean and <= 2^(e_i - 50), i.e. 50 bits below the row's largest
+ * 2^e_diag_i), |h_i| < 2^20; slices 0-5 floor (exact remainders: only slice 0 carries the sign,
+ * the others are non-negative), the last rounds to nearest (clipped to 127): the residual is zero-mean and <= 2^(e_i - 50), i.e. 50 bits below the row's largest
  * off-diagonal entry and >= 54 bits below its largest entry whenever the diagonal is >= 16x the
  * off-diagonal maximum (kinship-type covariances).  Each slice product is an exact
  * int32 integer; the head term h_i g_i and the seven products are combined exactly into two
@@ -164,7 +164,7 @@ int gg_pack_lower_blockcyclic_f64(int n, int nb, int grid_r, int grid_c, int pro
  *                         of 16, 16-byte aligned).                                            */
 int gg_i8_slices(void);
 /* Largest |value| of an int8 operand for which the int32 slice products stay exact at this n:
- * min(127, floor((2^31 - 1) / (127 n))) -- 127 up to n = 133,144; genotype dosages (<= 2) are
+ * min(127, floor((2^31 - 1) / (128 n))) -- 127 up to n = 132,104; genotype dosages (<= 2) are
  * exact for n < 8.4e6.  gg_narrow_f64_i8 and gg_gls_block_f64 enforce it (larger values take the
  * FP64 path); callers of gg_trsm_lower_i8* must respect it.                                  */
 int gg_i8_value_bound(int n);

@@ -380,7 +380,7 @@ static BlockWs block_ws(int n, int q, int cnt, int input_int8, int have_slices, 
   off += align256(sizeof(int) * (size_t)cnt);
   w.P = reinterpret_cast<double*>(base + off);
   off += align256(gg::partials_bytes(n, cnt, q));
-  // int8 input at n > 133,144: values beyond gg_i8_value_bound(n) take the DMMA path
+  // int8 input at n > 132,104: values beyond gg_i8_value_bound(n) take the DMMA path
   const bool i8_guard = have_slices && input_int8 && gg::i8_value_bound(n) < 127;
   const bool need_g8 = have_slices;                              // narrowed / re-pitched dosages
   const bool need_x64 = (!have_slices && input_int8) || i8_guard;   // widened dosages (DMMA)

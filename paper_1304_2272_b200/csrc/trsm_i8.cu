@@ -7,7 +7,7 @@
 // zero-mean, see "inverse slicing" below), so
 //     Xbar[i,j] = 2^(e_i - 49) ( h_i G[i,j] 2^49 + sum_s 2^(7 (6 - s)) C_s[i,j] ),
 //     C_s = sum_k a_s[i,k] G[k,j]
-// where every C_s is an EXACT int32 product (|C_s| <= 127 * 127 n < 2^31 up to n = 133,144;
+// where every C_s is an EXACT int32 product (|C_s| <= 128 * 127 n < 2^31 up to n = 132,104;
 // dosages <= 2 up to 8.4e6) computed by tcgen05.mma.kind::i8; the bracket is assembled as two
 // exact int64 halves and rounded once, so a column's result never depends on its position.
 //
@@ -581,7 +581,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 //     Linv[i,k] = 2^e'_i ( [k == i] h_i + sum_{s=0..6} a_s[i,k] 2^(-7 (s+1)) ),  a_s in [-127, 127]
 // with e'_i = max(e_off_i, e_diag_i - HEAD_BITS) (|Linv[i,k]| < 2^e_off_i for k < i): the large
 // diagonal element gets an integer head h_i (|h_i| < 2^20, applied in the epilogue as h_i g_i),
-// everything else 7 slices: slices 0-5 truncate (exact remainders), the last rounds to nearest,
+// everything else 7 slices: slices 0-5 floor (exact remainders in [0, 1): slices 1-5 and the
+// last are non-negative, only slice 0 carries the sign), the last rounds to nearest,
 // so the residual is zero-mean and <= 2^(e'_i - 50) (2^(e'_i - 49) in the rare clipped case):
 // 50 bits below the row's largest off-diagonal entry, >= 54 below the row maximum when the
 // diagonal dominates it 16x (kinship covariances: ~36x).  Measured on a kinship inverse at
@@ -686,9 +687,12 @@ __global__ void slice_rows_kernel(int np, Src src, int* __restrict__ meta,
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double t = v * 128.0;                     // exact
-      // truncate (exact remainder, |v| < 1); the last slice rounds to nearest instead (|q| <= 127
+      // floor (exact remainder in [0, 1)): only slice 0 carries the sign, slices 1-6 are
+      // non-negative -- the int8 datapath's power follows the operand bits, and two's-complement
+      // sign extension of random-sign digits costs ~5% of clock under the power cap (r02,
+      // profiles/r02_whatif_operands2.log); the last slice rounds to nearest instead (<= 127
       // kept): a zero-mean residual of at most half a unit, which does not build up along k
-      const double q = (s < S - 1) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
+      const double q = (s < S - 1) ? floor(t) : fmin(fmax(rint(t), -127.0), 127.0);
       Sl[slice_offset(i, k, s)] = (signed char)(int)q;
       v = t - q;
     }
@@ -897,7 +901,7 @@ int slice_bc_run(int n, int nb, int gr, int gc, int pr, int pc, const double* B,
 // Largest |dosage| for which every slice product 127 |g| n stays below 2^31 (exact int32).
 int i8_value_bound(int n) {
   if (n < 1) return 127;
-  const long long b = 2147483647LL / (127LL * (long long)n);
+  const long long b = 2147483647LL / (128LL * (long long)n);   // slice digits in [-128, 127]
   return b >= 127 ? 127 : (int)b;
 }
 

@@ -306,7 +306,7 @@ STATUS_INVALID = -2   # GG_STATUS_INVALID (include/gwasgls_b200.h)
 
 def _int8_exact(col):
     """Integer values the int8 tensor-core path computes exactly at this n (the int32 bound of
-    gg_i8_value_bound: 127 up to n = 133,144)."""
+    gg_i8_value_bound: 127 up to n = 132,104)."""
     bound = _capi.lib().gg_i8_value_bound(len(col))
     return bool(np.all(np.isfinite(col)) and np.all(col == np.trunc(col))
                 and np.all(np.abs(col) <= bound))

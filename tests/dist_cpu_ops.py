@@ -64,7 +64,7 @@ def slices_dense(Linv_rows, meta, np_):
         q = np.empty((kend, S))
         for s in range(S):
             t = v * 128.0
-            q[:, s] = np.trunc(t) if s < S - 1 else np.clip(np.rint(t), -127.0, 127.0)
+            q[:, s] = np.floor(t) if s < S - 1 else np.clip(np.rint(t), -127.0, 127.0)
             v = t - q[:, s]
         out[slice_offsets(i, k, np_)] = q.astype(np.int8)
     return out

@@ -53,9 +53,9 @@ def test_host_only_entry_points():
     assert lib.gg_gemm_ozaki_workspace_bytes(1000, 1000, 300, 1) < \
         lib.gg_gemm_ozaki_workspace_bytes(1000, 1000, 300, 0)
     assert lib.gg_trtri_workspace_bytes(10000) > 0
-    # exact-int32 bound of the int8 path: 127 up to n = 133,144, then shrinking
-    assert lib.gg_i8_value_bound(10000) == 127 and lib.gg_i8_value_bound(133144) == 127 and lib.gg_i8_value_bound(133145) == 126
-    assert lib.gg_i8_value_bound(150000) == 2147483647 // (127 * 150000) == 112
+    # exact-int32 bound of the int8 path: 127 up to n = 132,104, then shrinking
+    assert lib.gg_i8_value_bound(10000) == 127 and lib.gg_i8_value_bound(132104) == 127 and lib.gg_i8_value_bound(132105) == 126
+    assert lib.gg_i8_value_bound(150000) == 2147483647 // (128 * 150000) == 111
     # 7 tile-packed slices (112 KB per 128 x 128 tile of the triangle) + 2 np metadata ints
     assert lib.gg_i8_slices() == 7
     assert lib.gg_inverse_slices_bytes(1000) == 36 * 7 * 128 * 128

@@ -30,16 +30,23 @@ def main():
     real = sw.d.slices.clone()
     g = torch.Generator(device=dev)
     g.manual_seed(1)
-    variants = [("real slices", None), ("zero slices", 0), ("random 2-bit slices", 2),
-                ("random 4-bit slices", 4), ("random 8-bit slices", 8), ("real slices", None)]
-    for name, bits in variants:
-        if bits is None:
+    # (name, low, high): uniform random digits in [low, high); None = the real slices, 0 = zeros
+    variants = [("real slices", None), ("zero slices", 0), ("random [-2, 2)", (-2, 2)),
+                ("random [-8, 8)", (-8, 8)), ("random [-128, 128)", (-128, 128)),
+                ("random [0, 128)", (0, 128)), ("random [0, 64)", (0, 64)),
+                ("random [-64, 64)", (-64, 64)), ("real |slices|", "abs"), ("real slices", None)]
+    if os.environ.get("WHATIF_SET") == "first":
+        variants = variants[:5] + variants[-1:]
+    for name, rng in variants:
+        if rng is None:
             sw.d.slices.copy_(real)
-        elif bits == 0:
+        elif rng == 0:
             sw.d.slices.zero_()
+        elif rng == "abs":
+            sw.d.slices.copy_(real.abs())
         else:
-            r = torch.randint(-(1 << (bits - 1)), 1 << (bits - 1), real.shape, device=dev,
-                              dtype=torch.int16, generator=g)
+            r = torch.randint(rng[0], rng[1], real.shape, device=dev, dtype=torch.int16,
+                              generator=g)
             sw.d.slices.copy_(r.to(torch.int8))
         ms, clk, trsm_ms = bench.timed_sweep(sw, args.steps, 2, False, None, 0, dev)
         tops = int(_capi.lib().gg_i8_slices()) * float(sw.n) ** 2 * sw.m / (trsm_ms / 1e3) / 1e12
