@@ -5,8 +5,7 @@
 // cores do 4.4 POPS.  Each row i of A (and row j of B) is split error-free into 8 int8 slices
 // below its own power of two:
 //     A[i,k] = 2^e_i sum_{s=0..7} a_s[i,k] 2^(-7 (s+1)),   |a_s| <= 127
-// (slices 0-6 floor with exact remainders in [0, 1) -- only slice 0 carries the sign -- the last
-// rounds to nearest; digits in [-128, 127]), so
+// (slices 0-6 truncate with exact remainders, the last rounds to nearest), so
 //     (A B^T)[i,j] = 2^(e_i + f_j) sum_d D_d[i,j] 2^(-7 (d+2)),   D_d = sum_{s+t=d} a_s b_t^T.
 // The 36 slice products with s + t <= 7 are issued as tcgen05.mma.kind::i8 into 8 int32 TMEM
 // accumulators (one per diagonal d, 64 columns each = all 512 columns); every D_d is exact for
@@ -451,8 +450,10 @@ __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, cons
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
       const double t = v * 128.0;         // exact
-      // floor: slices 1.. non-negative (fewer toggling sign bits in the int8 datapath)
-      const double q = (s < OZ_S - 1) ? floor(t) : fmin(fmax(rint(t), -127.0), 127.0);
+      // truncate: the digits keep the sign of the element, so the dropped products (s + t >= 8)
+      // and the residuals have random signs and cancel along k (floor digits -- all non-negative
+      // below slice 0 -- make them add up coherently: measured 30-90x larger GEMM errors)
+      const double q = (s < OZ_S - 1) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
       w[s][j / 4] |= ((unsigned)(int)q & 0xffu) << (8 * (j % 4));
       v = t - q;
     }

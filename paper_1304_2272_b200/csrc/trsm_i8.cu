@@ -684,18 +684,27 @@ __global__ void slice_rows_kernel(int np, Src src, int* __restrict__ meta,
       if (v != 0.0) meta[np + i] = (int)h;
       v -= h;
     }
+    // truncated digits (exact remainders, |v| < 1); the last rounds to nearest instead (|q| <= 127
+    // kept): a zero-mean residual of at most half a unit, which does not build up along k.  The
+    // value they represent, V = sum_s c_s 128^(6-s) (|V| < 2^49, exact in int64), is then
+    // re-encoded with FLOOR digits -- d_0 = floor(V / 2^42) in [-128, 127], d_1..6 the base-128
+    // digits of V - d_0 2^42 in [0, 127] -- the same value, but only slice 0 carries the sign: the
+    // int8 datapath's power follows the operand bits, and the sign extension of random-sign
+    // digits costs ~5% of clock under the power cap (r02, profiles/r02_whatif_operands2.log).
+    // (Floor digits taken directly from v are not exact: a tiny negative v leaves a remainder
+    // that rounds to 1.0.)
+    long long V = 0;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const double t = v * 128.0;                     // exact
-      // floor (exact remainder in [0, 1)): only slice 0 carries the sign, slices 1-6 are
-      // non-negative -- the int8 datapath's power follows the operand bits, and two's-complement
-      // sign extension of random-sign digits costs ~5% of clock under the power cap (r02,
-      // profiles/r02_whatif_operands2.log); the last slice rounds to nearest instead (<= 127
-      // kept): a zero-mean residual of at most half a unit, which does not build up along k
-      const double q = (s < S - 1) ? floor(t) : fmin(fmax(rint(t), -127.0), 127.0);
-      Sl[slice_offset(i, k, s)] = (signed char)(int)q;
+      const double q = (s < S - 1) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
+      V = V * 128 + (long long)q;
       v = t - q;
     }
+    Sl[slice_offset(i, k, 0)] = (signed char)(V >> (7 * (S - 1)));   // arithmetic: floor
+#pragma unroll
+    for (int s = 1; s < S; ++s)
+      Sl[slice_offset(i, k, s)] = (signed char)((V >> (7 * (S - 1 - s))) & 127);
   }
 }
 

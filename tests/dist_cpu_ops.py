@@ -61,11 +61,16 @@ def slices_dense(Linv_rows, meta, np_):
             h = np.trunc(v[i])
             meta[np_ + i] = int(h)
             v[i] -= h
-        q = np.empty((kend, S))
+        V = np.zeros(kend, dtype=np.int64)      # the truncated digits' exact value
         for s in range(S):
             t = v * 128.0
-            q[:, s] = np.floor(t) if s < S - 1 else np.clip(np.rint(t), -127.0, 127.0)
-            v = t - q[:, s]
+            qs = np.trunc(t) if s < S - 1 else np.clip(np.rint(t), -127.0, 127.0)
+            V = V * 128 + qs.astype(np.int64)
+            v = t - qs
+        q = np.empty((kend, S), dtype=np.int64)  # re-encoded with floor digits
+        q[:, 0] = V >> (7 * (S - 1))
+        for s in range(1, S):
+            q[:, s] = (V >> (7 * (S - 1 - s))) & 127
         out[slice_offsets(i, k, np_)] = q.astype(np.int8)
     return out
 
