@@ -268,21 +268,31 @@ __device__ __forceinline__ void tmem_ld_rows8(unsigned taddr, int (&v)[S][8]) {
 // epilogue group g drains row block 2 rbp + g and releases its half as soon as it is in
 // registers, so the next tile's MMAs into that half wait only for the drain.
 constexpr int D_STAGE_BYTES = A_BYTES + 2 * P_B_BYTES;   // 44 KB
+// QUAD tiles (r02): ONE 32-row block x TWO 256-SNP column pairs -- each stage's slice tile B
+// feeds two N = 224 MMAs with different genotype tiles A (accumulators at TMEM columns 0 and
+// 256).  Same MACs and nearly the same bytes per stage (46 KB), but half the slice bytes per MAC:
+// the slices are random low-order mantissa digits, whose movement and multiplication is where the
+// power goes under the board's cap, while the genotypes are {0,1,2}.
+constexpr int Q_STAGE_BYTES = 2 * A_BYTES + P_B_BYTES;   // 46 KB
 constexpr int D_RD_SLOTS = 2;                            // row-data slots (x2 halves)
-__host__ __device__ constexpr size_t d_smem_bytes(int stages, int rdb) {
-  return size_t(stages) * D_STAGE_BYTES + size_t(D_RD_SLOTS) * 2 * rdb + 1024 + 512;
+__host__ __device__ constexpr size_t d_smem_bytes(int stages, int rdb, bool quad = false) {
+  return size_t(stages) * (quad ? Q_STAGE_BYTES : D_STAGE_BYTES) + size_t(D_RD_SLOTS) * 2 * rdb +
+         1024 + 512;
 }
 constexpr int D_TQ_READERS = 2 + 2 * 8;   // leader MMA + peer producer + 8 epilogue warps per CTA
 
-template <int P_STAGES>
+template <int P_STAGES, bool QUAD>
 __global__ void __launch_bounds__(THREADS, 1)
     trsm_i8_dual_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB3,
                         const __grid_constant__ CUtensorMap tmB1, I8Args a) {
+  constexpr int STAGE = QUAD ? Q_STAGE_BYTES : D_STAGE_BYTES;
+  constexpr int A_ST = QUAD ? 2 * A_BYTES : A_BYTES;          // genotype bytes per CTA stage
+  constexpr int B_ST = QUAD ? P_B_BYTES : 2 * P_B_BYTES;      // slice bytes per CTA stage
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* rdata = smem + P_STAGES * D_STAGE_BYTES;
+  unsigned char* rdata = smem + P_STAGES * STAGE;
   const int RD_BYTES = a.rd_bytes;
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(rdata + D_RD_SLOTS * 2 * RD_BYTES);
@@ -333,9 +343,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   fence_after();
   const unsigned tmem_base = *tmem_slot;
 
-  const int num_pp = (a.num_nt + 1) / 2;          // 256-SNP tile pairs
-  const int num_rbp = a.num_rb / 2;               // row-block pairs (num_rb is a multiple of 4)
-  const int total = num_rbp * num_pp;
+  // tile = (row unit ru, column unit cu): dual -- row-block pair x 256-SNP pair; QUAD -- one row
+  // block x two 256-SNP pairs.  Half h of the tile: row block rb_h, SNP tile nt_h (this CTA's)
+  const int num_cu = QUAD ? (a.num_nt + 3) / 4 : (a.num_nt + 1) / 2;
+  const int num_ru = QUAD ? a.num_rb : a.num_rb / 2;   // num_rb is a multiple of 4
+  const int total = num_ru * num_cu;
   const bool partials = a.P != nullptr;
   const unsigned peer_tq = mapa_peer(smem_u32(tq));
   auto tile_at = [&](int r) -> int {
@@ -365,17 +377,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           tile_read(r);
         }
         if (t < 0) break;
-        int rbp, pp;
-        tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
-        const int nt = 2 * pp + (int)rank;
-        const int rb0 = 2 * rbp;
-        const int nk = (rb0 + 4) / 4;
-        {   // row data of both row blocks (this CTA's own barrier)
+        int ru, cu;
+        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+        const int rb0 = QUAD ? ru : 2 * ru;        // the tile's (first) row block
+        const int nk = (QUAD ? ru : 2 * ru + 1) / 4 + 1;
+        constexpr int NRD = QUAD ? 1 : 2;          // row blocks (row data) per tile
+        {   // row data of the tile's row block(s) (this CTA's own barrier)
           const int slot = r % D_RD_SLOTS;
           mbar_wait(rde0 + 8 * slot, ((r / D_RD_SLOTS) & 1) ^ 1);
           const unsigned rbar = rdf0 + 8 * slot;
-          mbar_expect_tx(rbar, 2 * (2 * TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0)));
-          for (int h = 0; h < 2; ++h) {
+          mbar_expect_tx(rbar, NRD * (2 * TR * 4 + (partials ? (a.q + 1) * TR * 8 : 0)));
+          for (int h = 0; h < NRD; ++h) {
             const unsigned dst = rbase + (2 * slot + h) * RD_BYTES;
             const int row0 = (rb0 + h) * TR;
             bulk_g2s(dst, a.expo + row0, TR * 4, rbar);
@@ -392,9 +404,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const unsigned fb = full0 + 8 * stage;
           if (leader)
-            mbar_expect_tx(fb, 2 * (D_STAGE_BYTES - ((a.whatif & 1) ? A_BYTES : 0) -
-                                    ((a.whatif & 2) ? 2 * P_B_BYTES : 0)));
-          const unsigned dA = sbase + stage * D_STAGE_BYTES;
+            mbar_expect_tx(fb, 2 * (((a.whatif & 1) ? 0 : A_ST) + ((a.whatif & 2) ? 0 : B_ST)));
+          const unsigned dA = sbase + stage * STAGE;
           const unsigned fbl = fb & PEER_MASK;
           auto loadB = [&](unsigned dst, const CUtensorMap* m, int c1, int c2) {
             if (a.whatif & 2) return;
@@ -403,12 +414,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (a.whatif & 1) {
             // what-if (timing only, results invalid): no genotype loads -- the A bytes' share of
             // the L2 -> SMEM stream and of DRAM (the leader expects only the B bytes)
+          } else if (QUAD) {   // the CTA's two SNP tiles: 4 cu + rank and 4 cu + 2 + rank
+            tma_2d_pair(dA, &tmA, fbl, kt * TK, (4 * cu + (int)rank) * TM);
+            tma_2d_pair(dA + A_BYTES, &tmA, fbl, kt * TK, (4 * cu + 2 + (int)rank) * TM);
           } else {
-            tma_2d_pair(dA, &tmA, fbl, kt * TK, nt * TM);
+            tma_2d_pair(dA, &tmA, fbl, kt * TK, (2 * cu + (int)rank) * TM);
           }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {   // this CTA's 112 slice rows of row block rb0 + h
-            const unsigned dB = dA + A_BYTES + h * P_B_BYTES;
+          for (int h = 0; h < (QUAD ? 1 : 2); ++h) {   // this CTA's 112 slice rows of rb0 + h
+            const unsigned dB = dA + A_ST + h * P_B_BYTES;
             const int r0 = ((rb0 + h) & 3) * TR;
             if (rank == 0) {
               loadB(dB, &tmB3, r0, 0);
@@ -433,24 +447,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int t = tile_at(r);
         tile_read(r);
         if (t < 0) break;
-        int rbp, pp;
-        tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
-        const int rb0 = 2 * rbp;
-        const int nk = (rb0 + 4) / 4;
+        int ru, cu;
+        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+        const int rb0 = QUAD ? ru : 2 * ru;
+        const int nk = (QUAD ? ru : 2 * ru + 1) / 4 + 1;
         for (int kt = 0; kt < nk; ++kt) {
           mbar_wait(full0 + 8 * stage, phase);
           fence_after();
-          const unsigned sa = sbase + stage * D_STAGE_BYTES;
-          const unsigned long long da = smem_desc(sa);
+          const unsigned sa = sbase + stage * STAGE;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (kt == 0) {   // this half's accumulator drained by the previous tile's group h
               mbar_wait(acce0 + 8 * h, (r & 1) ^ 1);
               fence_after();
             }
-            const unsigned long long db = smem_desc(sa + A_BYTES + h * P_B_BYTES);
+            // dual: one genotype tile, the slices of row block rb0 + h; QUAD: genotype tile h,
+            // the one row block's slices
+            const unsigned long long da = smem_desc(sa + (QUAD ? h * A_BYTES : 0));
+            const unsigned long long db = smem_desc(sa + A_ST + (QUAD ? 0 : h * P_B_BYTES));
             // the diagonal k tile: nonzero slices only for k < 32 (rb + 1)
-            const int kk_end = (kt == nk - 1) ? ((rb0 + h) & 3) + 1 : TK / 32;
+            const int kk_end = (kt == nk - 1) ? ((rb0 + (QUAD ? 0 : h)) & 3) + 1 : TK / 32;
 #pragma unroll
             for (int kk = 0; kk < TK / 32; ++kk)
               if (kk < kk_end)
@@ -475,10 +491,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tile_read(r);
       if (t < 0) break;
-      int rbp, pp;
-      tile_coords(t, num_rbp, num_pp, a.grp_pp, rbp, pp);
-      const int rb = 2 * rbp + group;
-      const int nt = 2 * pp + (int)rank;
+      int ru, cu;
+      tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+      const int rb = QUAD ? ru : 2 * ru + group;
+      const int nt = QUAD ? 4 * cu + 2 * group + (int)rank : 2 * cu + (int)rank;
       const int col_g = nt * TM + m, row0_g = rb * TR;
       int gq[TR / 4];
       {
@@ -504,7 +520,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(accf, r & 1);
       fence_after();
       const int slot = r % D_RD_SLOTS;
-      const unsigned char* rd = rdata + (2 * slot + group) * RD_BYTES;
+      const unsigned char* rd = rdata + (2 * slot + (QUAD ? 0 : group)) * RD_BYTES;
       const int* ex = reinterpret_cast<const int*>(rd);
       const double* cols = reinterpret_cast<const double*>(rd + RD_COLS_OFF);
       mbar_wait(rdf0 + 8 * slot, (r / D_RD_SLOTS) & 1);
@@ -1017,22 +1033,32 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     // the genotype group must stay L2-resident while the row blocks re-read it, and every group
     // re-reads the slices.  Measured DRAM bytes per 8,192-SNP launch (ncu): n = 10^4 2.5 GB
     // (one group) -> 0.83 GB (16 pairs), n = 4*10^4 150 GB -> 43 GB (8 pairs).
-    const int num_pp = (a.num_nt + 1) / 2;
+    // QUAD tiles (one row block x two SNP pairs) unless GG_I8_QUAD=0 (tuning / what-if knob)
+    bool quad = true;
+    if (const char* qd = std::getenv("GG_I8_QUAD")) quad = std::atoi(qd) != 0;
+    // column units: 256-SNP pairs (dual) or 512-SNP quads (QUAD); the group size is set in pairs
+    const int num_cu = quad ? (a.num_nt + 3) / 4 : (a.num_nt + 1) / 2;
     int grp = (int)(16.0 * std::sqrt(1e4 / (double)n) + 0.5);
     if (const char* g = std::getenv("GG_I8_SNP_GROUP")) {   // tuning knob: pairs per group
       const int v = std::atoi(g);
       if (v > 0) grp = v;
     }
-    grp = grp < 1 ? 1 : (grp > num_pp ? num_pp : grp);
-    const int ngroups = (num_pp + grp - 1) / grp;
-    a.grp_pp = (num_pp + ngroups - 1) / ngroups;                // equal-width groups
+    if (quad) grp = (grp + 1) / 2;
+    grp = grp < 1 ? 1 : (grp > num_cu ? num_cu : grp);
+    const int ngroups = (num_cu + grp - 1) / grp;
+    a.grp_pp = (num_cu + ngroups - 1) / ngroups;                // equal-width groups
     a.whatif = 0;
     if (const char* w = std::getenv("GG_I8_WHATIF")) a.whatif = std::atoi(w);
     a.rd_bytes = rd_bytes(q, P != nullptr);
-    // 5 stages of 44 KB when the row data is small (q <= 3), else 4
-    const bool five = d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
-    auto kern = five ? trsm_i8_dual_kernel<5> : trsm_i8_dual_kernel<4>;
-    const size_t smem = d_smem_bytes(five ? 5 : 4, a.rd_bytes);
+    // dual: 5 stages of 44 KB when the row data is small (q <= 3), else 4; QUAD: 4 of 46 KB
+    const bool five = !quad && d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
+    auto kern = quad ? trsm_i8_dual_kernel<4, true>
+                     : (five ? trsm_i8_dual_kernel<5, false> : trsm_i8_dual_kernel<4, false>);
+    const size_t smem = d_smem_bytes(five ? 5 : 4, a.rd_bytes, quad);
+    if (smem > (size_t)smem_optin()) {
+      set_error("trsm_i8: shared memory for the pipeline exceeds the device limit");
+      return GG_ECUDA;
+    }
     GG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     cudaLaunchConfig_t cfg = {};
