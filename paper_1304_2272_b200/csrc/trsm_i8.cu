@@ -1033,8 +1033,10 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     // the genotype group must stay L2-resident while the row blocks re-read it, and every group
     // re-reads the slices.  Measured DRAM bytes per 8,192-SNP launch (ncu): n = 10^4 2.5 GB
     // (one group) -> 0.83 GB (16 pairs), n = 4*10^4 150 GB -> 43 GB (8 pairs).
-    // QUAD tiles (one row block x two SNP pairs) unless GG_I8_QUAD=0 (tuning / what-if knob)
-    bool quad = true;
+    // QUAD tiles (one row block x two SNP pairs) with GG_I8_QUAD=1 (measured r02: config 3
+    // +0.6%, within noise; config 1 -1.6% -- the slice bytes are not where the power goes, the
+    // multipliers' B-operand bit activity is: profiles/r02_peak_swap.log)
+    bool quad = false;
     if (const char* qd = std::getenv("GG_I8_QUAD")) quad = std::atoi(qd) != 0;
     // column units: 256-SNP pairs (dual) or 512-SNP quads (QUAD); the group size is set in pairs
     const int num_cu = quad ? (a.num_nt + 3) / 4 : (a.num_nt + 1) / 2;

@@ -30,7 +30,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   for (int i = threadIdx.x; i < 48 * 1024; i += blockDim.x) {
     unsigned h = (unsigned)i * 2654435761u + 0x9E3779B9u * (blockIdx.x + 1);
     h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
-    smem[i] = !rnd ? (unsigned char)(i & 3) : (i < 16 * 1024 ? (unsigned char)(h % 3) : (unsigned char)h);
+    const bool a_reg = i < 16 * 1024;   // rnd 1: A {0,1,2}, B random; rnd 2: swapped;
+    //                                     rnd 3: A {0,1,2}, B random non-negative [0, 127]
+    unsigned char v = (unsigned char)(i & 3);
+    if (rnd == 1) v = a_reg ? (unsigned char)(h % 3) : (unsigned char)h;
+    if (rnd == 2) v = a_reg ? (unsigned char)h : (unsigned char)(h % 3);
+    if (rnd == 3) v = a_reg ? (unsigned char)(h % 3) : (unsigned char)(h & 127);
+    smem[i] = v;
   }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(1));
@@ -91,7 +97,8 @@ int main(int argc, char** argv) {
     // the rate over everything after the first second
     const double secs = atof(argv[2]);
     const int N = argc > 3 ? atoi(argv[3]) : 224;
-    const int rnd = argc > 4 && std::string(argv[4]) == "rand";
+    const int rnd = argc <= 4 ? 0 : std::string(argv[4]) == "rand" ? 1
+                  : std::string(argv[4]) == "swap" ? 2 : std::string(argv[4]) == "pos" ? 3 : 0;
     const int iters = 2000;
     const double ops1 = 2.0 * 256 * N * 32 * 64.0 * iters * (grid / 2);
     cudaEvent_t a, b;
@@ -113,7 +120,7 @@ int main(int argc, char** argv) {
       total_ms += ms;
     }
     printf("int8 tcgen05 cta_group::2 M256 N%d K32 x %d SMs, %s operands, sustained %.1f s: "
-           "%.1f TOPS\n", N, grid, rnd ? "TRSM-like random" : "i&3 pattern", total_ms / 1e3,
+           "%.1f TOPS\n", N, grid, rnd == 1 ? "TRSM-like random" : rnd == 2 ? "A random, B {0,1,2}" : rnd == 3 ? "B random [0,127]" : "i&3 pattern", total_ms / 1e3,
            ops / warm_ms / 1e9);
     return 0;
   }
