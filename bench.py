@@ -593,8 +593,18 @@ def run_e2e(args, sw, world, rank, dev, use_dist, dist, beta_ref):
     fits = local_world * n * m < 0.6 * avail
     ring = None if fits else max(2, int(0.5 * avail / local_world / (n * m_blk)))
     cols = m if fits else min(m, ring * m_blk)
-    host = np.empty((cols, n), dtype=np.int8)                # row j = marker j (n x cols F-order)
-    unreg = _host_register(host)
+    while True:   # page-lock the host panel; on refusal (memlock limit, fragmentation) halve it
+        host = np.empty((cols, n), dtype=np.int8)            # row j = marker j (n x cols F-order)
+        try:
+            unreg = _host_register(host)
+            break
+        except RuntimeError:
+            if cols <= 2 * m_blk:
+                raise
+            fits = False
+            cols = max(2 * m_blk, (cols // 2) // m_blk * m_blk)
+            ring = cols // m_blk
+            del host
     try:
         lib, sh = _capi.lib(), _capi.stream_handle()
         for j0 in range(0, cols, m_blk):
