@@ -63,9 +63,10 @@ FP64_PEAK_SOURCE = ("measured: DMMA m8n8k4 sustained 37.09 TF/s @1965 MHz, tools
 I8_PEAK_BURST_TOPS = 4353.0
 I8_PEAK_SUSTAINED_TOPS = float(os.environ.get("GG_I8_PEAK_SUSTAINED", "0")) or None
 I8_PEAK_SOURCE = ("measured: tcgen05.mma.cta_group::2.kind::i8 M256 N224 K32 back to back on 148 "
-                  "SMs (tools/i8_peak_pair.cu; profiles/r01_i8_peak_pair.log burst, "
-                  "profiles/r02_i8_peak_sustained.log sustained); MEASURED_PEAKS.json has no "
-                  "int8 entry")
+                  "SMs (tools/i8_peak_pair.cu; burst: profiles/r01_i8_peak_pair.log; sustained "
+                  "on the TRSM's operand statistics -- A {0,1,2}, B digits [0,127] -- under the "
+                  "power cap: profiles/r02_peak_swap.log, profiles/i8_peak.json); "
+                  "MEASURED_PEAKS.json has no int8 entry")
 PEAK_FILE = os.path.join(REPO, "profiles", "i8_peak.json")
 CPU_SAMPLE_PER_BLOCK = 512
 REF_SAMPLE_SNPS = {0: 2048, 1: 2048, 2: 2048, 3: 512, 4: 128}
