@@ -104,7 +104,7 @@ __device__ int small_spd_solve(int p, const double* S, const double* rhs, double
 }
 
 // ---- reductions ----------------------------------------------------------------------------
-// partials[(rb * cnt + col) * (q+2) + k]: k < q -> x.XL[:,k], q -> x.x, q+1 -> x.y over the
+// partials[(rb * (q+2) + k) * cnt + col]: k < q -> x.XL[:,k], q -> x.x, q+1 -> x.y over the
 // 32-row block rb (layout shared with the fused epilogue of trsm_i8.cu).
 // CTA = 8 warps = 8 columns x 32 row blocks (1024 rows): XL/y rows staged once per CTA, each
 // warp stages its column's 1024 values (coalesced, padded against bank conflicts) and lane l
@@ -152,12 +152,12 @@ __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
     acc[QM] = fma(xv, xv, acc[QM]);
     acc[QM + 1] = fma(xv, sv[q * LDP + r], acc[QM + 1]);
   }
-  double* out = P + ((long long)rb * cnt + col) * (q + 2);
+  double* out = P + (long long)rb * (q + 2) * cnt + col;   // value-major: coalesced over col
 #pragma unroll
   for (int k = 0; k < QM; ++k)
-    if (k < q) out[k] = acc[k];
-  out[q] = acc[QM];
-  out[q + 1] = acc[QM + 1];
+    if (k < q) out[(long long)k * cnt] = acc[k];
+  out[(long long)q * cnt] = acc[QM];
+  out[(long long)(q + 1) * cnt] = acc[QM + 1];
 }
 
 // Cross-block part of the canonical order: "lane" l sums the partials of row blocks l, l+32,
@@ -184,12 +184,12 @@ __global__ void __launch_bounds__(256) reduce_solve_kernel(
     for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
     if (col < cnt) {
       for (int rb = l; rb < nrb; rb += 32) {
-        const double* pp = P + rb * stride + (long long)col * (q + 2);
+        const double* pp = P + rb * stride + col;           // value-major, coalesced over col
 #pragma unroll
         for (int k = 0; k < QM; ++k)
-          if (k < q) acc[k] = acc[k] + pp[k];
-        acc[QM] = acc[QM] + pp[q];
-        acc[QM + 1] = acc[QM + 1] + pp[q + 1];
+          if (k < q) acc[k] = acc[k] + pp[(long long)k * cnt];
+        acc[QM] = acc[QM] + pp[(long long)q * cnt];
+        acc[QM + 1] = acc[QM + 1] + pp[(long long)(q + 1) * cnt];
       }
     }
     double* dst = sh + (l * 32 + lane) * (QM + 2);

@@ -60,7 +60,7 @@ struct I8Args {
   long long ldg;
   int n;
   // fused epilogue reductions (canonical order of gls_epilogue.cu): partial dots of each SNP's
-  // 32-row block against XLbar (q columns, ld ldxl) and ybar -> P[(rb*N + col)*(q+2) + k]
+  // 32-row block against XLbar (q columns, ld ldxl) and ybar -> P[(rb*(q+2) + k)*N + col]
   int q;
   const double* XL;
   long long ldxl;
@@ -560,13 +560,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             *reinterpret_cast<double2*>(dst + i) = make_double2(acc[i], acc[i + 1]);
         }
         if (partials) {   // canonical order: one FMA chain over the 32 rows per dot
-          double* ppo = a.P + ((long long)rb * a.N + col) * (a.q + 2);
+          // value-major partials: a warp's 32 consecutive SNPs store 256 contiguous bytes per dot
+          const long long N = a.N;
+          double* ppo = a.P + (long long)rb * (a.q + 2) * N + col;
           for (int k = 0; k < a.q; ++k) {
             const double* xl = cols + k * TR;
             double sum = 0.0;
 #pragma unroll
             for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
-            ppo[k] = sum;
+            ppo[k * N] = sum;
           }
           const double* yv = cols + a.q * TR;
           double sxx = 0.0, sxy = 0.0;
@@ -575,8 +577,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             sxx = fma(acc[i], acc[i], sxx);
             sxy = fma(acc[i], yv[i], sxy);
           }
-          ppo[a.q] = sxx;
-          ppo[a.q + 1] = sxy;
+          ppo[a.q * N] = sxx;
+          ppo[(a.q + 1) * N] = sxy;
         }
       }
       mbar_arrive(rde0 + 8 * slot);   // row data slot free
