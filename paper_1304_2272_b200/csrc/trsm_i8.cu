@@ -563,7 +563,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           // value-major partials: a warp's 32 consecutive SNPs store 256 contiguous bytes per dot
           const long long N = a.N;
           double* ppo = a.P + (long long)rb * (a.q + 2) * N + col;
-          for (int k = 0; k < a.q; ++k) {
+          // what-if 8 (timing only): only the intercept's dot and x.x, x.y stay in FP64
+          const int qd = (a.whatif & 8) ? (a.q < 1 ? a.q : 1) : a.q;
+          for (int k = 0; k < qd; ++k) {
             const double* xl = cols + k * TR;
             double sum = 0.0;
 #pragma unroll
