@@ -247,10 +247,12 @@ def dist_potrf_inv(A, B, layout, ops, comm=None):
                 below = [I for I in layout.row_blocks if I > K]
                 right = [J for J in layout.col_blocks if J > K]
                 pos = {I: i for i, I in enumerate(below)}
-                for jj, J in enumerate(right):
-                    if J in pos:
-                        ii = pos[J]
-                        ops.copy_block(P_cols, jj * nb, 0, P_rows[:, ii * nb:(ii + 1) * nb])
+                pairs = [(jj, pos[J]) for jj, J in enumerate(right) if J in pos]
+                if pairs:      # one gather of every shared block (no per-block launches)
+                    off = np.arange(nb)
+                    dst = np.concatenate([jj * nb + off for jj, _ in pairs])
+                    src = np.concatenate([ii * nb + off for _, ii in pairs])
+                    ops.copy_rows(P_cols, dst, P_rows, src)
             if gcm is not None:
                 gcm.col.all_reduce(P_cols)
         # block row K of the inverse, X_KJ = Dinv B_KJ (J <= K) on process row K % r, broadcast
@@ -680,6 +682,12 @@ class DeviceOps:
         ncols, nrows = src.shape
         dst[c0:c0 + ncols, r0:r0 + nrows].copy_(src)
 
+    def copy_rows(self, dst, dst_rows, src, src_rows):
+        """dst[dst_rows, :] = src[src_rows, :] for column-major (cols, rows) tensors."""
+        di = self.torch.as_tensor(dst_rows, device=self.dev)
+        si = self.torch.as_tensor(src_rows, device=self.dev)
+        dst[:, di] = src[:, si]
+
     def scatter_cols_rows(self, full, grows, tmp):
         idx = self.torch.as_tensor(grows, device=self.dev)
         full[:, idx] = tmp
@@ -698,10 +706,11 @@ class DeviceOps:
 
     def zero_upper_blocks(self, A, layout):
         nb = layout.nb
+        rows = np.asarray(layout.row_blocks)
         for jl, J in enumerate(layout.col_blocks):
-            for il, I in enumerate(layout.row_blocks):
-                if I < J:
-                    A[jl * nb:(jl + 1) * nb, il * nb:(il + 1) * nb].zero_()
+            cnt = int(np.searchsorted(rows, J))     # row blocks I < J form a prefix (sorted)
+            if cnt:
+                A[jl * nb:(jl + 1) * nb, :cnt * nb].zero_()
 
     def kinship_blocks(self, spec, layout):
         """M_IJ = a/m_k Z_I Z_J^T + (1-a) delta_IJ for this rank's blocks (datagen's construction,

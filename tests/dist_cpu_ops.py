@@ -166,6 +166,9 @@ class CpuOps:
         ncols, nrows = src.shape
         dst[c0:c0 + ncols, r0:r0 + nrows].copy_(src)
 
+    def copy_rows(self, dst, dst_rows, src, src_rows):
+        dst[:, torch.as_tensor(dst_rows)] = src[:, torch.as_tensor(src_rows)]
+
     def scatter_cols_rows(self, full, grows, tmp):
         full[:, torch.as_tensor(grows)] = tmp
 
