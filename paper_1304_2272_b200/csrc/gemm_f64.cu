@@ -54,6 +54,11 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 template <bool BT>
 __global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
   if (a.abort_flag != nullptr && *a.abort_flag != 0) return;
+  if (blockIdx.y) {   // strided batch
+    a.A += blockIdx.y * a.sA;
+    a.B += blockIdx.y * a.sB;
+    a.C += blockIdx.y * a.sC;
+  }
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
@@ -194,20 +199,21 @@ int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s) {
     return GG_EDIM;
   }
   const long long tiles = (long long)(a.M / BM) * ((a.N + BN - 1) / BN);
-  if (tiles > 0x7fffffffLL) {
+  if (tiles > 0x7fffffffLL || a.batch > 65535) {
     set_error("dgemm: too many tiles");
     return GG_EDIM;
   }
+  const dim3 grid((unsigned)tiles, a.batch > 1 ? (unsigned)a.batch : 1u);
   if (trans_b) {
     GG_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_bytes<true>()));
-    dgemm_dmma_kernel<true><<<(unsigned)tiles, NTHREADS, smem_bytes<true>(), s>>>(a);
+    dgemm_dmma_kernel<true><<<grid, NTHREADS, smem_bytes<true>(), s>>>(a);
   } else {
     GG_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem_bytes<false>()));
-    dgemm_dmma_kernel<false><<<(unsigned)tiles, NTHREADS, smem_bytes<false>(), s>>>(a);
+    dgemm_dmma_kernel<false><<<grid, NTHREADS, smem_bytes<false>(), s>>>(a);
   }
   GG_LAUNCH_CHECK("dgemm_dmma_kernel launch");
   return GG_OK;

@@ -25,6 +25,12 @@ int cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::gg::cuda_fail(_e, what);                \
   } while (0)
 
+#define GG_TRY(expr)                                                        \
+  do {                                                                      \
+    const int _rc = (expr);                                                 \
+    if (_rc != GG_OK) return _rc;                                           \
+  } while (0)
+
 inline int pad_rows(int n) { return ((n + GG_TILE - 1) / GG_TILE) * GG_TILE; }
 
 // NVTX range around a C-ABI entry point (header-only NVTX 3: a few ns when no tool listens);
@@ -51,6 +57,8 @@ struct GemmArgs {
   double alpha, beta;
   int flags;
   const int* abort_flag;   // optional device flag: kernel is a no-op when *abort_flag != 0
+  int batch;                // strided batch (0 or 1: one problem): problem z uses
+  long long sA, sB, sC;     // A + z sA, B + z sB, C + z sC (same shape and flags)
 };
 
 // Launch C = alpha*A*op(B) + beta*C.  trans_b selects op(B) = B^T (B stored N x K).

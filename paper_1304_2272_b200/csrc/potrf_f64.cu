@@ -330,80 +330,113 @@ bool oz_shape(int M, int N, int K) {
   return M >= OZ_MIN_DIM && N >= OZ_MIN_DIM && K >= OZ_MIN_DIM;
 }
 
-// Ozaki workspace of the trtri recursion on [lo, hi) (its two GEMMs per level)
-size_t trtri_oz_bytes(int lo, int hi) {
-  const int nblk = (hi - lo) / NB;
-  if (nblk < 2) return 0;
-  const int mid = lo + (nblk / 2) * NB;
-  size_t b = trtri_oz_bytes(lo, mid);
-  const size_t b2 = trtri_oz_bytes(mid, hi);
-  if (b2 > b) b = b2;
-  if (oz_shape(hi - mid, mid - lo, mid - lo)) {
-    const size_t g1 = ozaki_ws_bytes(hi - mid, mid - lo, mid - lo, false);
-    const size_t g2 = ozaki_ws_bytes(hi - mid, mid - lo, hi - mid, false);
-    if (g1 > b) b = g1;
-    if (g2 > b) b = g2;
+// ---- off-diagonal blocks of Linv, bottom-up ----------------------------------------------------
+// Level b = 128 2^j combines pairs of already inverted diagonal ranges [lo, mid = lo + b) and
+// [mid, hi = min(lo + 2b, np)) (lo = 2b i):
+//     T = L[mid:hi, lo:mid] Linv[lo:mid, lo:mid],   Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] T.
+// The groups of a level are independent: the full ones are ONE strided-batched DMMA launch per
+// product (r02: a depth-first recursion issued ~150 launches of 1-6 CTAs at n = 1e4, 13 ms); the
+// partial last group is its own launch; levels with b >= OZ_TRTRI_MIN go to the Ozaki GEMM per
+// group (large products, where the int8 tensor cores' 2x beats DMMA).  T of group i sits at
+// T + i b^2 with ld = its row count.
+constexpr int OZ_TRTRI_MIN = 4096;
+
+struct TrtriLevel {
+  int b, nfull, mlast;   // half width, full groups, rows of the partial last group (0: none)
+};
+inline TrtriLevel trtri_level(int np, int b) {
+  TrtriLevel l{b, 0, 0};
+  for (int lo = 0; lo + b < np; lo += 2 * b) {
+    const int m = (lo + 2 * b <= np) ? b : np - lo - b;
+    if (m == b) ++l.nfull;
+    else l.mlast = m;
   }
-  return b;
+  return l;
+}
+size_t trtri_T_doubles(int np) {
+  size_t mx = 0;
+  for (int b = NB; b < np; b *= 2) {
+    const TrtriLevel l = trtri_level(np, b);
+    const size_t d = (size_t)l.nfull * b * b + (size_t)l.mlast * b;
+    if (d > mx) mx = d;
+  }
+  return mx;
+}
+size_t trtri_oz_bytes(int np) {
+  size_t mx = 0;
+  for (int b = OZ_TRTRI_MIN; b < np; b *= 2) {
+    const TrtriLevel l = trtri_level(np, b);
+    for (int m : {l.nfull ? b : 0, l.mlast}) {
+      if (m == 0 || !oz_shape(m, b, b)) continue;
+      const size_t g1 = ozaki_ws_bytes(m, b, b, false), g2 = ozaki_ws_bytes(m, b, m, false);
+      if (g1 > mx) mx = g1;
+      if (g2 > mx) mx = g2;
+    }
+  }
+  return mx;
 }
 
-// Off-diagonal blocks of Linv for the block range [lo, hi) (diagonal blocks already set).
-int trtri_offdiag(int lo, int hi, const double* L, double* Linv, long long ldp, double* T,
-                  long long ldt, void* oz, size_t oz_bytes, const int* abort_flag,
-                  cudaStream_t s) {
-  const int nblk = (hi - lo) / NB;
-  if (nblk < 2) return GG_OK;
-  const int mid = lo + (nblk / 2) * NB;
-  int rc = trtri_offdiag(lo, mid, L, Linv, ldp, T, ldt, oz, oz_bytes, abort_flag, s);
-  if (rc != GG_OK) return rc;
-  rc = trtri_offdiag(mid, hi, L, Linv, ldp, T, ldt, oz, oz_bytes, abort_flag, s);
-  if (rc != GG_OK) return rc;
-  if (oz != nullptr && oz_shape(hi - mid, mid - lo, mid - lo)) {
-    // T = L[mid:hi, lo:mid] Linv[lo:mid, lo:mid]  (B~(j,k) = Linv[lo+k, lo+j], zero for k < j)
-    rc = ozaki_gemm_run(hi - mid, mid - lo, mid - lo, L + mid + (long long)lo * ldp, 1, ldp,
-                        Linv + lo + (long long)lo * ldp, ldp, 1, T, ldt, 1.0, 0.0, GEMM_B_LOWER,
-                        oz, oz_bytes, abort_flag, s);
-    if (rc != GG_OK) return rc;
-    // Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] T  (A~ lower triangular, B~(j,k) = T[k, j])
-    return ozaki_gemm_run(hi - mid, mid - lo, hi - mid, Linv + mid + (long long)mid * ldp, 1, ldp,
-                          T, ldt, 1, Linv + mid + (long long)lo * ldp, ldp, -1.0, 0.0,
-                          GEMM_A_LOWER, oz, oz_bytes, abort_flag, s);
+// the two products of `count` consecutive groups of level b starting at group g0, M rows each
+int trtri_groups(int b, int g0, int count, int M, const double* L, double* Linv, long long ldp,
+                 double* T, void* oz, size_t oz_bytes, const int* abort_flag, cudaStream_t s) {
+  const long long step = 2ll * b * (1 + ldp);              // next group along the diagonal
+  const long long lo = 2ll * b * g0, mid = lo + b;
+  double* Tg = T + (size_t)g0 * b * b;
+  if (oz != nullptr && b >= OZ_TRTRI_MIN && oz_shape(M, b, b)) {
+    for (int i = 0; i < count; ++i) {
+      const long long o = i * step;
+      double* Ti = Tg + (size_t)i * b * b;
+      int rc = ozaki_gemm_run(M, b, b, L + mid + lo * ldp + o, 1, ldp, Linv + lo + lo * ldp + o,
+                              ldp, 1, Ti, M, 1.0, 0.0, GEMM_B_LOWER, oz, oz_bytes, abort_flag, s);
+      if (rc != GG_OK) return rc;
+      rc = ozaki_gemm_run(M, b, M, Linv + mid + mid * ldp + o, 1, ldp, Ti, M, 1,
+                          Linv + mid + lo * ldp + o, ldp, -1.0, 0.0, GEMM_A_LOWER, oz, oz_bytes,
+                          abort_flag, s);
+      if (rc != GG_OK) return rc;
+    }
+    return GG_OK;
   }
-  // T = L[mid:hi, lo:mid] * Linv[lo:mid, lo:mid]      (op(B) lower triangular)
-  GemmArgs g1{};
-  g1.M = hi - mid; g1.N = mid - lo; g1.K = mid - lo;
-  g1.A = L + mid + (long long)lo * ldp; g1.lda = ldp;
-  g1.B = Linv + lo + (long long)lo * ldp; g1.ldb = ldp;
-  g1.C = T; g1.ldc = ldt;
+  GemmArgs g1{};   // T = L[mid:hi, lo:mid] Linv[lo:mid, lo:mid]   (op(B) lower triangular)
+  g1.M = M; g1.N = b; g1.K = b;
+  g1.A = L + mid + lo * ldp; g1.lda = ldp;
+  g1.B = Linv + lo + lo * ldp; g1.ldb = ldp;
+  g1.C = Tg; g1.ldc = M;
   g1.alpha = 1.0; g1.beta = 0.0; g1.flags = GEMM_B_LOWER; g1.abort_flag = abort_flag;
-  rc = launch_dgemm(g1, false, s);
+  g1.batch = count; g1.sA = step; g1.sB = step; g1.sC = (long long)b * b;
+  int rc = launch_dgemm(g1, false, s);
   if (rc != GG_OK) return rc;
-  // Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] * T   (A lower triangular)
-  GemmArgs g2{};
-  g2.M = hi - mid; g2.N = mid - lo; g2.K = hi - mid;
-  g2.A = Linv + mid + (long long)mid * ldp; g2.lda = ldp;
-  g2.B = T; g2.ldb = ldt;
-  g2.C = Linv + mid + (long long)lo * ldp; g2.ldc = ldp;
+  GemmArgs g2{};   // Linv[mid:hi, lo:mid] = -Linv[mid:hi, mid:hi] T   (A lower triangular)
+  g2.M = M; g2.N = b; g2.K = M;
+  g2.A = Linv + mid + mid * ldp; g2.lda = ldp;
+  g2.B = Tg; g2.ldb = M;
+  g2.C = Linv + mid + lo * ldp; g2.ldc = ldp;
   g2.alpha = -1.0; g2.beta = 0.0; g2.flags = GEMM_A_LOWER; g2.abort_flag = abort_flag;
+  g2.batch = count; g2.sA = step; g2.sB = (long long)b * b; g2.sC = step;
   return launch_dgemm(g2, false, s);
 }
 
-void trtri_T_dims(int np, long long* rows, long long* cols) {
-  const int nblk = np / NB;
-  if (nblk < 2) { *rows = 0; *cols = 0; return; }
-  *cols = (long long)(nblk / 2) * NB;
-  *rows = (long long)(nblk - nblk / 2) * NB;
+// Off-diagonal blocks of Linv (its 128 x 128 diagonal blocks already set).
+int trtri_offdiag(int np, const double* L, double* Linv, long long ldp, double* T, void* oz,
+                  size_t oz_bytes, const int* abort_flag, cudaStream_t s) {
+  for (int b = NB; b < np; b *= 2) {
+    const TrtriLevel l = trtri_level(np, b);
+    int rc = GG_OK;
+    if (l.nfull > 0)
+      rc = trtri_groups(b, 0, l.nfull, b, L, Linv, ldp, T, oz, oz_bytes, abort_flag, s);
+    if (rc == GG_OK && l.mlast > 0)
+      rc = trtri_groups(b, l.nfull, 1, l.mlast, L, Linv, ldp, T, oz, oz_bytes, abort_flag, s);
+    if (rc != GG_OK) return rc;
+  }
+  return GG_OK;
 }
 
-
-// Workspace: [header][panel / trtri T][Ozaki slices]
+// Workspace: [header][panels (2 x np x 128, double-buffered for the look-ahead) / trtri T]
+//            [Ozaki slices]
 size_t t_region_bytes(int np) {
-  long long r, c;
-  trtri_T_dims(np, &r, &c);
-  return ((size_t)(r * c) * sizeof(double) + 255) & ~size_t(255);
+  return (trtri_T_doubles(np) * sizeof(double) + 255) & ~size_t(255);
 }
 size_t oz_region_bytes(int np, bool factor) {
-  size_t b = trtri_oz_bytes(0, np);
+  size_t b = trtri_oz_bytes(np);
   if (factor) {   // the trailing SYRKs: largest at the first outer block
     const int rem = np - OUTER;
     if (rem > 0 && oz_shape(rem, rem, OUTER)) {
@@ -423,7 +456,7 @@ size_t trtri_ws_bytes(int n) {
 
 size_t potrf_ws_bytes(int n) {
   const int np = pad_rows(n);
-  size_t panel = ((size_t)np * NB * sizeof(double) + 255) & ~size_t(255);
+  size_t panel = ((size_t)2 * np * NB * sizeof(double) + 255) & ~size_t(255);
   const size_t tri = t_region_bytes(np);
   if (tri > panel) panel = tri;
   return HDR_BYTES + panel + oz_region_bytes(np, true);
@@ -431,10 +464,50 @@ size_t potrf_ws_bytes(int n) {
 
 namespace {
 size_t p_region_bytes(int np) {
-  size_t panel = ((size_t)np * NB * sizeof(double) + 255) & ~size_t(255);
+  size_t panel = ((size_t)2 * np * NB * sizeof(double) + 255) & ~size_t(255);
   const size_t tri = t_region_bytes(np);
   return tri > panel ? tri : panel;
 }
+
+// The factorisation's own streams for one call: `crit` (highest priority: leaf -> panel -> next
+// block column, the dependent chain) and `side` (lowest priority: the rest of each panel's update
+// inside the outer block, overlapped with the next leaf and panel).  Joined back into the
+// caller's stream at the end; destroyed on every exit path (the driver frees them after the
+// queued work completes).
+struct PotrfStreams {
+  cudaStream_t caller = nullptr, crit = nullptr, side = nullptr;
+  cudaEvent_t ea = nullptr, eb = nullptr, join = nullptr;
+  bool own = false;
+  int open(cudaStream_t s, bool lookahead) {
+    caller = crit = s;
+    if (!lookahead) return GG_OK;
+    int least = 0, greatest = 0;
+    GG_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    GG_CUDA_TRY(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, greatest));
+    own = true;
+    GG_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
+    for (cudaEvent_t* e : {&ea, &eb, &join})
+      GG_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    GG_CUDA_TRY(cudaEventRecord(join, caller));
+    GG_CUDA_TRY(cudaStreamWaitEvent(crit, join, 0));
+    return GG_OK;
+  }
+  int close() {   // caller waits for crit (which has waited for side)
+    if (!own) return GG_OK;
+    GG_CUDA_TRY(cudaEventRecord(eb, side));
+    GG_CUDA_TRY(cudaStreamWaitEvent(crit, eb, 0));
+    GG_CUDA_TRY(cudaEventRecord(join, crit));
+    GG_CUDA_TRY(cudaStreamWaitEvent(caller, join, 0));
+    return GG_OK;
+  }
+  ~PotrfStreams() {
+    if (!own) return;
+    if (crit != caller && crit != nullptr) cudaStreamDestroy(crit);
+    if (side != nullptr) cudaStreamDestroy(side);
+    for (cudaEvent_t e : {ea, eb, join})
+      if (e != nullptr) cudaEventDestroy(e);
+  }
+};
 }  // namespace
 
 int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, double* Linv, int ldp, void* work,
@@ -463,70 +536,86 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   GG_LAUNCH_CHECK("init_factor_tiled_kernel");
   GG_CUDA_TRY(cudaFuncSetAttribute(leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)LEAF_SMEM));
-  // optional phase timing (GG_POTRF_TIMING=1): leaf / panel / trailing / inverse, to stderr
+  const char* la = getenv("GG_POTRF_LOOKAHEAD");   // tuning knob: 0 = one stream, no look-ahead
+  PotrfStreams st;
+  GG_TRY(st.open(s, la == nullptr || la[0] != '0'));
+  cudaStream_t cs_ = st.crit;
+  // optional phase timing (GG_POTRF_TIMING=1): factor / inverse, to stderr (events on the
+  // critical stream, no synchronisation inside the phases)
   const bool timing = getenv("GG_POTRF_TIMING") != nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  float t_leaf = 0.f, t_pan = 0.f, t_upd = 0.f, t_inv = 0.f;
-  if (timing)
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (timing) {
     for (auto& e : ev) cudaEventCreate(&e);
-  auto lap = [&](float& acc, cudaEvent_t a, cudaEvent_t b) {
-    if (!timing) return;
-    cudaEventRecord(b, s);
-    cudaEventSynchronize(b);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, a, b);
-    acc += ms;
-  };
+    cudaEventRecord(ev[0], cs_);
+  }
   // Two-level right-looking blocking: outer block columns of OUTER (= 8 leaves); inside one,
   // leaf + panel + an update restricted to the outer block's columns; after it, one trailing
   // SYRK of depth OUTER (8x the arithmetic intensity of a depth-128 update; 1024 measured best
   // between 256 and 4096 at n = 1e4 and 4e4).
+  // Look-ahead inside the outer block: panel k's update is split into (a) the next block column
+  // k+1 on the critical stream, then leaf k+1 and panel k+1 follow at once, while (b) the columns
+  // beyond k+1 are updated on the side stream; the critical stream waits for (b) before its next
+  // (a) (both write block column k+2).  Panels alternate between two buffers (b reads panel k
+  // while panel k+1 is formed).
   for (int K0 = 0; K0 < np; K0 += OUTER) {
     const int w = (np - K0 < OUTER) ? (np - K0) : OUTER;
+    bool pend = false;   // side-stream update not yet waited for
     for (int k = K0; k < K0 + w; k += NB) {
-      if (timing) cudaEventRecord(ev[0], s);
-      leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, s>>>(L, ldp, Linv, ldp, k, &hdr->info);
+      leaf_kernel<true><<<1, LEAF_THREADS, LEAF_SMEM, cs_>>>(L, ldp, Linv, ldp, k, &hdr->info);
       GG_LAUNCH_CHECK("potrf leaf_kernel");
-      lap(t_leaf, ev[0], ev[1]);
       const int rem = np - k - NB;          // rows below this leaf
       if (rem <= 0) break;
       const int rem_in = K0 + w - k - NB;   // columns of the outer block right of this leaf
+      double* Pk = P + (size_t)((k / NB) & 1) * np * NB;
       // P = A21 Dinv^T (all rows below), written back into L's column block
       GemmArgs pan{};
       pan.M = rem; pan.N = NB; pan.K = NB;
       pan.A = L + (k + NB) + (long long)k * ldp; pan.lda = ldp;
       pan.B = Linv + k + (long long)k * ldp; pan.ldb = ldp;
-      pan.C = P; pan.ldc = np;
+      pan.C = Pk; pan.ldc = np;
       pan.alpha = 1.0; pan.beta = 0.0; pan.flags = 0; pan.abort_flag = &hdr->info;
-      int rc = launch_dgemm(pan, true, s);
-      if (rc != GG_OK) return rc;
+      GG_TRY(launch_dgemm(pan, true, cs_));
       GG_CUDA_TRY(cudaMemcpy2DAsync(L + (k + NB) + (long long)k * ldp,
-                                    (size_t)ldp * sizeof(double), P, (size_t)np * sizeof(double),
-                                    (size_t)rem * sizeof(double), NB, cudaMemcpyDeviceToDevice, s));
-      lap(t_pan, ev[1], ev[2]);
-      if (rem_in > 0) {
-        // update only the outer block's remaining columns: A[k+NB:, k+NB:K0+w] -= P P[:rem_in]^T
-        GemmArgs upd{};
-        upd.M = rem; upd.N = rem_in; upd.K = NB;
-        upd.A = P; upd.lda = np;
-        upd.B = P; upd.ldb = np;
-        upd.C = L + (k + NB) + (long long)(k + NB) * ldp; upd.ldc = ldp;
-        upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
-        rc = launch_dgemm(upd, true, s);
-        if (rc != GG_OK) return rc;
+                                    (size_t)ldp * sizeof(double), Pk, (size_t)np * sizeof(double),
+                                    (size_t)rem * sizeof(double), NB, cudaMemcpyDeviceToDevice, cs_));
+      if (rem_in <= 0) continue;
+      if (pend) {
+        GG_CUDA_TRY(cudaStreamWaitEvent(cs_, st.eb, 0));
+        pend = false;
       }
-      lap(t_upd, ev[2], ev[3]);
+      // (a) A[k+NB:, k+NB:k+2NB] -= P P[:NB]^T   (with no side stream: all rem_in columns)
+      const int na = st.side ? (rem_in < NB ? rem_in : NB) : rem_in;
+      GemmArgs upd{};
+      upd.M = rem; upd.N = na; upd.K = NB;
+      upd.A = Pk; upd.lda = np;
+      upd.B = Pk; upd.ldb = np;
+      upd.C = L + (k + NB) + (long long)(k + NB) * ldp; upd.ldc = ldp;
+      upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
+      GG_TRY(launch_dgemm(upd, true, cs_));
+      if (rem_in > na) {
+        // (b) A[k+2NB:, k+2NB:K0+w] -= P[NB:] P[NB:rem_in]^T on the side stream
+        GG_CUDA_TRY(cudaEventRecord(st.ea, cs_));
+        GG_CUDA_TRY(cudaStreamWaitEvent(st.side, st.ea, 0));
+        GemmArgs ub{};
+        ub.M = rem - NB; ub.N = rem_in - NB; ub.K = NB;
+        ub.A = Pk + NB; ub.lda = np;
+        ub.B = Pk + NB; ub.ldb = np;
+        ub.C = L + (k + 2 * NB) + (long long)(k + 2 * NB) * ldp; ub.ldc = ldp;
+        ub.alpha = -1.0; ub.beta = 1.0; ub.flags = GEMM_C_LOWER; ub.abort_flag = &hdr->info;
+        GG_TRY(launch_dgemm(ub, true, st.side));
+        GG_CUDA_TRY(cudaEventRecord(st.eb, st.side));
+        pend = true;
+      }
     }
+    if (pend) GG_CUDA_TRY(cudaStreamWaitEvent(cs_, st.eb, 0));
     const int rem = np - K0 - w;
     if (rem <= 0) break;
-    if (timing) cudaEventRecord(ev[2], s);
     // trailing SYRK of depth w: A22 -= L21 L21^T, L21 = L[K0+w:, K0:K0+w] (read in place;
     // disjoint from the updated region), lower tiles only
-    int rc;
     if (oz != nullptr && oz_shape(rem, rem, w)) {
-      rc = ozaki_gemm_run(rem, rem, w, L + (K0 + w) + (long long)K0 * ldp, 1, ldp, nullptr, 0, 0,
-                          L + (K0 + w) + (long long)(K0 + w) * ldp, ldp, -1.0, 1.0, GEMM_C_LOWER,
-                          oz, oz_bytes, &hdr->info, s);
+      GG_TRY(ozaki_gemm_run(rem, rem, w, L + (K0 + w) + (long long)K0 * ldp, 1, ldp, nullptr, 0, 0,
+                            L + (K0 + w) + (long long)(K0 + w) * ldp, ldp, -1.0, 1.0, GEMM_C_LOWER,
+                            oz, oz_bytes, &hdr->info, cs_));
     } else {
       GemmArgs upd{};
       upd.M = rem; upd.N = rem; upd.K = w;
@@ -534,20 +623,19 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
       upd.B = L + (K0 + w) + (long long)K0 * ldp; upd.ldb = ldp;
       upd.C = L + (K0 + w) + (long long)(K0 + w) * ldp; upd.ldc = ldp;
       upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
-      rc = launch_dgemm(upd, true, s);
+      GG_TRY(launch_dgemm(upd, true, cs_));
     }
-    if (rc != GG_OK) return rc;
-    lap(t_upd, ev[2], ev[3]);
   }
-  if (timing) cudaEventRecord(ev[0], s);
-  long long tr, tc;
-  trtri_T_dims(np, &tr, &tc);
-  int rc = trtri_offdiag(0, np, L, Linv, ldp, P, tr > 0 ? tr : 1, oz, oz_bytes, &hdr->info, s);
-  if (rc != GG_OK) return rc;
-  lap(t_inv, ev[0], ev[1]);
+  if (timing) cudaEventRecord(ev[1], cs_);
+  GG_TRY(trtri_offdiag(np, L, Linv, ldp, P, oz, oz_bytes, &hdr->info, cs_));
+  GG_TRY(st.close());
   if (timing) {
-    fprintf(stderr, "[gg potrf n=%d] leaf %.2f ms, panel %.2f ms, trailing %.2f ms, inverse %.2f ms\n",
-            n, t_leaf, t_pan, t_upd, t_inv);
+    cudaEventRecord(ev[2], cs_);
+    cudaEventSynchronize(ev[2]);
+    float f = 0.f, iv = 0.f;
+    cudaEventElapsedTime(&f, ev[0], ev[1]);
+    cudaEventElapsedTime(&iv, ev[1], ev[2]);
+    fprintf(stderr, "[gg potrf n=%d] factor %.2f ms, inverse %.2f ms\n", n, f, iv);
     for (auto& e : ev) cudaEventDestroy(e);
   }
   PotrfHeader h{};
@@ -590,11 +678,9 @@ int trtri_run(int n, const double* L, int ldl, double* Linv, int ldp, void* work
   leaf_kernel<false><<<np / NB, LEAF_THREADS, LEAF_SMEM, s>>>(const_cast<double*>(L), ldl, Linv,
                                                                ldp, 0, nullptr);
   GG_LAUNCH_CHECK("trtri leaf_kernel");
-  long long tr, tc;
-  trtri_T_dims(np, &tr, &tc);
   const size_t oz_bytes = use_ozaki() ? oz_region_bytes(np, false) : 0;
   void* oz = oz_bytes ? static_cast<char*>(work) + HDR_BYTES + t_region_bytes(np) : nullptr;
-  return trtri_offdiag(0, np, L, Linv, ldp, T, tr > 0 ? tr : 1, oz, oz_bytes, nullptr, s);
+  return trtri_offdiag(np, L, Linv, ldp, T, oz, oz_bytes, nullptr, s);
 }
 
 // Blocked forward substitution X = L^-1 B (kernel.trsolve_lower for an arbitrary L): the inverses
