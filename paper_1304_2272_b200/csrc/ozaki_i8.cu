@@ -14,16 +14,19 @@
 // FP64 rounding.  The epilogue forms the exact int64 halves hi = D_0..D_3, lo = D_4..D_7 (base
 // 2^7) and rounds once: r = 2^E fma(hi, 2^-35, lo 2^-63); then C = beta C + alpha r.
 //
-// Kernel (persistent, one CTA per SM, 6 warps): warp 0 TMA producer (per 32-k stage: the 8
-// slices of a 128-row A tile and of a 64-row B tile, 48 KB, SWIZZLE_32B, 4-stage ring), warp 1
-// MMA issuer (one lane, M = 128 x N = 64..256 x K = 32, 12 MMAs covering the 36 slice products
-// per stage), warps 2-5 epilogue
-// (TMEM lane = tile row; releases TMEM once the tile is in registers, then updates C).
+// Kernel (persistent, one CTA per SM in clusters of 2, 10 warps): warp 0 TMA producer (per 32-k
+// stage: the 8 slices of a 128-row A tile -- half of them loaded here and multicast to the
+// cluster peer, which computes the neighbouring 64 columns -- and of a 64-row B tile, 48 KB,
+// SWIZZLE_32B, 4-stage ring), warp 1 MMA issuer (one lane, M = 128 x N = 64..256 x K = 32, 12 MMAs
+// covering the 36 slice products per stage), warps 2-9 epilogue (TMEM lane = tile row, two warps
+// per lane quarter, 32 columns each; release TMEM once the tile is in registers, then update C).
+// Operand entries outside a triangular operand's triangle are sliced as zeros.
 // Results are bitwise deterministic (exact integer accumulation, fixed rounding).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -41,7 +44,8 @@ constexpr int OZ_STAGES = 4;
 constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_KC;   // 32 KB
 constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_KC;   // 16 KB
 constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
-constexpr int OZ_THREADS = 6 * 32;
+constexpr int OZ_EPI_WARPS = 8;
+constexpr int OZ_THREADS = (2 + OZ_EPI_WARPS) * 32;
 constexpr size_t OZ_SMEM = size_t(OZ_STAGES) * OZ_STAGE_BYTES + 1024 + 256;
 constexpr int OZ_KMAX = 8192;              // k per launch: exact int32 diagonals need
                                            // 8 * 127^2 * K < 2^31 (K <= 16384); 8192 bounds the
@@ -59,6 +63,8 @@ struct OzArgs {
   int flags;               // GEMM_A_LOWER / GEMM_B_LOWER / GEMM_C_LOWER
   int gm;                  // row tiles per tile group (oz_tile)
   const int* abort_flag;
+  int whatif;              // measurement only (GG_OZ_WHATIF, results invalid): 1 no TMA loads,
+                           // 2 no epilogue work
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -151,49 +157,103 @@ __device__ __forceinline__ void tmem_ld_diag8(unsigned taddr, int (&v)[OZ_S][8])
       : "memory");
 }
 
-// tile t -> (mt, nt, k range); false when the tile is skipped (strictly above the diagonal of a
-// lower C).  Tiles are taken in groups of a.gm row tiles swept column by column, so the
-// concurrently running tiles share ~gm A row panels and ~148/gm B row panels (L2 reuse);
-// triangular A: heavy (last) row tiles first.
-// A group's column range: all num_nt, or for a lower C up to the diagonal of its last row tile.
-__device__ __forceinline__ int oz_group_nt(const OzArgs& a, int g, int num_mt, int num_nt) {
-  if (!(a.flags & GEMM_C_LOWER)) return num_nt;
-  const int lo = g * a.gm, hi = min(num_mt, lo + a.gm) - 1;
-  const int mt_max = (a.flags & GEMM_A_LOWER) ? num_mt - 1 - lo : hi;
-  return min(num_nt, 2 * mt_max + 2);   // n0 < m0 + 128
+// ---- clusters with multicast operand loads ---------------------------------------------------
+// The OZ_CLM x OZ_CLN CTAs of a cluster compute the tiles (mt = OZ_CLM bm + cm, nt = OZ_CLN bn + cn)
+// of one block of C in lockstep over the same k range: each A tile is needed by the OZ_CLN CTAs of
+// its row (cm) and each B tile by the OZ_CLM CTAs of its column (cn), so every CTA loads its share
+// of the slices (4 per load) and multicasts them to the CTAs that need them.  A stage is freed
+// for the producer of CTA X only when X and every CTA it multicasts into have consumed it: each
+// CTA's MMA commit arrives on the "empty" barriers of the CTAs sharing its A or B tile.
+// Measured (r02, tools/prof_ozaki.py, same box, round-robin): 1 x 2 (the A tile shared by two
+// column-neighbour CTAs: a third less L2->SM traffic, 74 resident clusters) 5-14% faster than
+// independent CTAs; 2 x 2 fits only 33 resident clusters of 4 (GPC packing: 132 SMs) and 2 x 1
+// shares the smaller B tile -- both slower.  What-if (GG_OZ_WHATIF=1, no operand loads): +34-46%
+// on the long-k GEMMs, so the loads remain the limiter.
+#ifndef OZ_CLM
+#define OZ_CLM 1
+#endif
+#ifndef OZ_CLN
+#define OZ_CLN 2
+#endif
+constexpr int OZ_CL = OZ_CLM * OZ_CLN;                        // CTAs per cluster
+constexpr int OZ_CBM = OZ_CLM * OZ_BM, OZ_CBN = OZ_CLN * OZ_BN;   // cluster block of C
+
+// blocks in groups of a.gm block rows swept block column by block column (the concurrently running
+// blocks share ~gm A row panels: L2 reuse); triangular A: heavy (last) block rows first.  A
+// group's column range: all num_bn, or for a lower C up to the diagonal of its last block row.
+__device__ __forceinline__ int oz_group_nb(const OzArgs& a, int g, int num_bm, int num_bn) {
+  if (!(a.flags & GEMM_C_LOWER)) return num_bn;
+  const int lo = g * a.gm, hi = min(num_bm, lo + a.gm) - 1;
+  const int bm_max = (a.flags & GEMM_A_LOWER) ? num_bm - 1 - lo : hi;
+  return min(num_bn, (OZ_CBM * bm_max + OZ_CBM + OZ_CBN - 1) / OZ_CBN);   // n0 < m0 + CBM
 }
-// number of tile indices (the grid-stride loops run over [0, oz_total))
-__device__ __forceinline__ int oz_total(const OzArgs& a, int num_mt, int num_nt) {
+__device__ __forceinline__ int oz_total(const OzArgs& a, int num_bm, int num_bn) {
   int tot = 0;
-  for (int g = 0; g * a.gm < num_mt; ++g)
-    tot += min(a.gm, num_mt - g * a.gm) * oz_group_nt(a, g, num_mt, num_nt);
+  for (int g = 0; g * a.gm < num_bm; ++g)
+    tot += min(a.gm, num_bm - g * a.gm) * oz_group_nb(a, g, num_bm, num_bn);
   return tot;
 }
-__device__ __forceinline__ bool oz_tile(const OzArgs& a, int t, int num_mt, int num_nt, int& mt,
-                                        int& nt, int& kb, int& ke) {
+// block t -> (bm, bn) and the block's k range (the union of its tiles' ranges: operand entries
+// outside a tile's own triangle are zero slices); false when the block lies above the diagonal
+__device__ __forceinline__ bool oz_block(const OzArgs& a, int t, int num_bm, int num_bn, int& bm,
+                                         int& bn, int& kb, int& ke) {
   int g = 0, gm = 0, gn = 0;
-  for (;; ++g) {   // the group holding index t (a few dozen groups at most)
-    gm = min(a.gm, num_mt - g * a.gm);   // the last group may be shorter
-    gn = oz_group_nt(a, g, num_mt, num_nt);
+  for (;; ++g) {
+    gm = min(a.gm, num_bm - g * a.gm);
+    gn = oz_group_nb(a, g, num_bm, num_bn);
     if (t < gm * gn) break;
     t -= gm * gn;
   }
-  nt = t / gm;
+  bn = t / gm;
   const int lin = g * a.gm + t % gm;
-  mt = (a.flags & GEMM_A_LOWER) ? num_mt - 1 - lin : lin;
-  const int m0 = mt * OZ_BM, n0 = nt * OZ_BN;
-  if ((a.flags & GEMM_C_LOWER) && n0 >= m0 + OZ_BM) return false;
+  bm = (a.flags & GEMM_A_LOWER) ? num_bm - 1 - lin : lin;
+  const int m0 = bm * OZ_CBM, n0 = bn * OZ_CBN;
+  if ((a.flags & GEMM_C_LOWER) && n0 >= m0 + OZ_CBM) return false;
   kb = a.kb;
   ke = a.ke;
-  if (a.flags & GEMM_A_LOWER) ke = min(ke, m0 + OZ_BM - a.koff);   // A(i, k) = 0 for k > i
-  if (a.flags & GEMM_B_LOWER) kb = max(kb, n0 - a.koff);           // B(j, k) = 0 for k < j
+  if (a.flags & GEMM_A_LOWER) ke = min(ke, m0 + OZ_CBM - a.koff);   // A(i, k) = 0 for k > i
+  if (a.flags & GEMM_B_LOWER) kb = max(kb, n0 - a.koff);            // B(j, k) = 0 for k < j
   return true;
+}
+
+__device__ __forceinline__ unsigned cta_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" :::
+                   "memory");
+}
+__device__ __forceinline__ void tma_3d_mc(unsigned dst, const CUtensorMap* map, unsigned bar, int c0,
+                                          int c1, int c2, unsigned short mask) {
+  if (OZ_CL == 1) {
+    tma_3d(dst, map, bar, c0, c1, c2);
+    return;
+  }
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(unsigned bar, unsigned short mask) {
+  if (OZ_CL == 1) {
+    mma_commit(bar);
+    return;
+  }
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;\n" ::"r"(bar),
+      "h"(mask)
+      : "memory");
 }
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       OzArgs a) {
-  if (a.abort_flag != nullptr && *a.abort_flag != 0) return;
+  if (a.abort_flag != nullptr && *a.abort_flag != 0) return;   // uniform across the grid
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -204,13 +264,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const unsigned full0 = smem_u32(bars), empty0 = full0 + 8 * OZ_STAGES;
   const unsigned accf = empty0 + 8 * OZ_STAGES, acce = accf + 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned rank = OZ_CL > 1 ? cta_rank() : 0u;
+  const int cm = rank % OZ_CLM, cn = rank / OZ_CLM;
+  unsigned short mask_a = 0, mask_b = 0;   // the CTAs sharing this CTA's A tile (same cm) / B tile
+  for (int i = 0; i < OZ_CLN; ++i) mask_a |= (unsigned short)(1u << (cm + OZ_CLM * i));
+  for (int i = 0; i < OZ_CLM; ++i) mask_b |= (unsigned short)(1u << (i + OZ_CLM * cn));
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, OZ_CLM + OZ_CLN - 1);
     }
     mbar_init(accf, 1);
-    mbar_init(acce, 4 * 32);
+    mbar_init(acce, OZ_EPI_WARPS * 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -220,25 +285,37 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   fence_before();
-  __syncthreads();
+  if (OZ_CL > 1) cluster_sync_all();   // barriers initialised in every CTA before any multicast
+  else __syncthreads();
   fence_after();
   const unsigned tmem_base = *tmem_slot;
   const int num_mt = (a.M + OZ_BM - 1) / OZ_BM, num_nt = (a.N + OZ_BN - 1) / OZ_BN;
-  const int total = oz_total(a, num_mt, num_nt);
+  const int num_bm = (num_mt + OZ_CLM - 1) / OZ_CLM, num_bn = (num_nt + OZ_CLN - 1) / OZ_CLN;
+  const int total = oz_total(a, num_bm, num_bn);
+  const int cid = blockIdx.x / OZ_CL, ncl = gridDim.x / OZ_CL;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       unsigned phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int mt, nt, kb, ke;
-        if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
+      for (int t = cid; t < total; t += ncl) {
+        int bm, bn, kb, ke;
+        if (!oz_block(a, t, num_bm, num_bn, bm, bn, kb, ke)) continue;
         for (int k = kb; k < ke; k += OZ_KC) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const unsigned fb = full0 + 8 * stage, dA = sbase + stage * OZ_STAGE_BYTES;
-          mbar_expect_tx(fb, OZ_STAGE_BYTES);
-          tma_3d(dA, &tmA, fb, k, mt * OZ_BM, 0);
-          tma_3d(dA + OZ_A_BYTES, &tmB, fb, k, nt * OZ_BN, 0);
+          if (a.whatif & 1) {
+            mbar_arrive(fb);
+          } else {
+            mbar_expect_tx(fb, OZ_STAGE_BYTES);
+            // this CTA's share of its A tile's slices (4 per load) and of its B tile's
+            for (int q = cn * (2 / OZ_CLN); q < (cn + 1) * (2 / OZ_CLN); ++q)
+              tma_3d_mc(dA + 4 * q * (OZ_BM * OZ_KC), &tmA, fb, k, (OZ_CLM * bm + cm) * OZ_BM,
+                        4 * q, mask_a);
+            for (int q = cm * (2 / OZ_CLM); q < (cm + 1) * (2 / OZ_CLM); ++q)
+              tma_3d_mc(dA + OZ_A_BYTES + 4 * q * (OZ_BN * OZ_KC), &tmB, fb, k,
+                        (OZ_CLN * bn + cn) * OZ_BN, 4 * q, mask_b);
+          }
           if (++stage == OZ_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -251,9 +328,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       int stage = 0;
       unsigned phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int mt, nt, kb, ke;
-        if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
+      for (int t = cid; t < total; t += ncl) {
+        int bm, bn, kb, ke;
+        if (!oz_block(a, t, num_bm, num_bn, bm, bn, kb, ke)) continue;
         if (ke <= kb) continue;
         mbar_wait(acce, (it & 1) ^ 1);   // the epilogue has the previous tile in registers
         fence_after();
@@ -278,7 +355,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               mma_i8(tmem_base + (s + first) * OZ_BN, da, desc32(sB + first * (OZ_BN * OZ_KC)),
                      cnt - first, (k > kb || s > 0) ? 1u : 0u);
           }
-          mma_commit(empty0 + 8 * stage);
+          mma_commit_mc(empty0 + 8 * stage, mask_a | mask_b);
           if (++stage == OZ_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -289,63 +366,72 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;            // TMEM lanes 32 quarter .. +31
+    // 8 epilogue warps: warp w reads TMEM lanes 32 (w % 4) .. +31 (its tile rows) and half h of
+    // the tile's 64 columns, so the accumulators are released twice as fast as with 4 warps
+    const int quarter = warp & 3, h = (warp - 2) >> 2;
     const int row_l = quarter * 32 + lane;
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      int mt, nt, kb, ke;
-      if (!oz_tile(a, t, num_mt, num_nt, mt, nt, kb, ke)) continue;
-      const int row = mt * OZ_BM + row_l, n0 = nt * OZ_BN;
-      double r[OZ_BN];
+    for (int t = cid; t < total; t += ncl) {
+      int bm, bn, kb, ke;
+      if (!oz_block(a, t, num_bm, num_bn, bm, bn, kb, ke)) continue;
+      const int mt = OZ_CLM * bm + cm, nt = OZ_CLN * bn + cn;
+      const bool write = mt < num_mt && nt < num_nt &&
+                         !((a.flags & GEMM_C_LOWER) && nt * OZ_BN >= mt * OZ_BM + OZ_BM);
+      const int row = mt * OZ_BM + row_l, n0 = nt * OZ_BN + h * (OZ_BN / 2);
+      constexpr int HN = OZ_BN / 2;
+      double r[HN];
       if (ke > kb) {
         mbar_wait(accf, it & 1);
         fence_after();
-        const int ea = row < a.M ? max(a.exA[row], -4000) : 0;   // EX_NONE: all-zero row
-        const unsigned taddr = tmem_base + ((unsigned)(quarter * 32) << 16);
+        if (!(a.whatif & 2)) {
+          const unsigned taddr = tmem_base + ((unsigned)(quarter * 32) << 16) + h * HN;
 #pragma unroll
-        for (int c8 = 0; c8 < OZ_BN / 8; ++c8) {
-          int v[OZ_S][8];
-          tmem_ld_diag8(taddr + c8 * 8, v);
+          for (int c8 = 0; c8 < HN / 8; ++c8) {
+            int v[OZ_S][8];
+            tmem_ld_diag8(taddr + c8 * 8, v);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
-                                 v[3][c];
-            const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
-                                 v[7][c];
-            r[c8 * 8 + c] = fma((double)hi, 0x1p-35, (double)lo * 0x1p-63);   // the one rounding
+            for (int c = 0; c < 8; ++c) {
+              const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
+                                   v[3][c];
+              const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
+                                   v[7][c];
+              r[c8 * 8 + c] = fma((double)hi, 0x1p-35, (double)lo * 0x1p-63);   // the one rounding
+            }
           }
         }
         fence_before();
         mbar_arrive(acce);
         ++it;
+        if (a.whatif & 2) continue;
         // scale by 2^(e_i + f_j) after the accumulators are released: exact for normal results
         // (the same bits as rounding at the final scale); ldexp gives the IEEE inf / subnormal
         // at the ends of the exponent range
+        const int ea = row < a.M ? max(a.exA[row], -4000) : 0;   // EX_NONE: all-zero row
 #pragma unroll
-        for (int c = 0; c < OZ_BN; ++c) {
+        for (int c = 0; c < HN; ++c) {
           const int col = n0 + c;
           const int e = ea + (col < a.N ? max(__ldg(a.exB + col), -4000) : 0);
           r[c] = (e > -1000 && e < 1000) ? r[c] * pow2(e) : ldexp(r[c], e);
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < OZ_BN; ++c) r[c] = 0.0;
+        for (int c = 0; c < HN; ++c) r[c] = 0.0;
       }
-      if (row < a.M) {   // C = beta C + alpha r in chunks of 16 columns, next chunk's loads in flight
-        constexpr int CH = 16;
+      if (write && row < a.M) {   // C = beta C + alpha r in chunks of 8 columns, next chunk's loads in flight
+        constexpr int CH = 8;
         double* cbase = a.C + (long long)n0 * a.ldc + row;
-        const int ncol = min(OZ_BN, a.N - n0);
+        const int ncol = min(HN, a.N - n0);
         const bool rd = a.beta != 0.0;
-        double cv[CH], cn[CH];
+        double cv[CH], cn_[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) cv[c] = (rd && c < ncol) ? cbase[(long long)c * a.ldc] : 0.0;
 #pragma unroll
-        for (int ch = 0; ch < OZ_BN / CH; ++ch) {
-          if (ch + 1 < OZ_BN / CH) {
+        for (int ch = 0; ch < HN / CH; ++ch) {
+          if (ch + 1 < HN / CH) {
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
               const int cc = (ch + 1) * CH + c;
-              cn[c] = (rd && cc < ncol) ? cbase[(long long)cc * a.ldc] : 0.0;
+              cn_[c] = (rd && cc < ncol) ? cbase[(long long)cc * a.ldc] : 0.0;
             }
           }
 #pragma unroll
@@ -355,13 +441,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               cbase[(long long)cc * a.ldc] = rd ? fma(a.alpha, r[cc], a.beta * cv[c]) : a.alpha * r[cc];
           }
 #pragma unroll
-          for (int c = 0; c < CH; ++c) cv[c] = cn[c];
+          for (int c = 0; c < CH; ++c) cv[c] = cn_[c];
         }
       }
     }
   }
   fence_before();
   __syncthreads();
+  if (OZ_CL > 1) cluster_sync_all();   // no peer multicast / remote arrive may target an exited CTA
   fence_after();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base)
@@ -394,6 +481,13 @@ __device__ __forceinline__ void load_tile(double (*T)[SL_KP], const double* X, l
   }
 }
 
+// triangular operands (flags of ozaki_gemm_run): entries outside the triangle are taken as zero
+// whatever the memory holds -- tri 1: A~(i, k) = 0 for k > i; tri 2: B~(j, k) = 0 for k < j
+// (k global: the chunk offset added)
+__device__ __forceinline__ bool oz_masked(int tri, int r, int k) {
+  return (tri == 1 && k > r) || (tri == 2 && k < r);
+}
+
 // ex[r] = max(ex[r], e) with max_k |X(r,k)| < 2^e over this CTA's k chunk (ex starts at EX_NONE;
 // the exponent of the row maximum is the maximum of the chunk exponents).  Rows contiguous: a
 // thread per row walks RX_K values of k (warps read 256 contiguous bytes); k contiguous: a warp per
@@ -401,7 +495,8 @@ __device__ __forceinline__ void load_tile(double (*T)[SL_KP], const double* X, l
 constexpr int RX_K = 256;
 __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, const double* X,
                                                                 long long rs, long long cs,
-                                                                int* ex, const int* abort_flag) {
+                                                                int* ex, int tri, int koff,
+                                                                const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;
   const int k0 = blockIdx.y * RX_K, k1 = min(K, k0 + RX_K);
   double m = 0.0;
@@ -411,14 +506,16 @@ __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, con
     if (r >= R) return;
     const double* p = X + (long long)r * rs;
 #pragma unroll 8
-    for (int k = k0; k < k1; ++k) m = fmax(m, fabs(p[(long long)k * cs]));
+    for (int k = k0; k < k1; ++k)
+      if (!oz_masked(tri, r, koff + k)) m = fmax(m, fabs(p[(long long)k * cs]));
   } else {
     const int lane = threadIdx.x & 31;
     r = blockIdx.x * (SL_THREADS / 32) + (threadIdx.x >> 5);
     if (r >= R) return;
     const double* p = X + (long long)r * rs;
 #pragma unroll 4
-    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs(p[(long long)k * cs]));
+    for (int k = k0 + lane; k < k1; k += 32)
+      if (!oz_masked(tri, r, koff + k)) m = fmax(m, fabs(p[(long long)k * cs]));
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane != 0) return;
   }
@@ -433,7 +530,8 @@ __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, con
 __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, const double* X,
                                                                long long rs, long long cs,
                                                                const int* ex, signed char* Sl,
-                                                               long long kp, const int* abort_flag) {
+                                                               long long kp, int tri, int koff,
+                                                               const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;
   __shared__ double T[SL_R][SL_KP];
   const int r0 = blockIdx.x * SL_R, k0 = blockIdx.y * SL_K;
@@ -446,7 +544,7 @@ __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, cons
   unsigned w[OZ_S][4] = {};
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    double v = ldexp(T[r][tix(kq + j)], -e);   // |v| < 1
+    double v = oz_masked(tri, r0 + r, koff + k0 + kq + j) ? 0.0 : ldexp(T[r][tix(kq + j)], -e);
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
       const double t = v * 128.0;         // exact
@@ -490,7 +588,7 @@ int encode_slices(CUtensorMap* map, const signed char* Sl, int R, int K, long lo
   }
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)R, (cuuint64_t)OZ_S};
   cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)kp * R};
-  cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_S};
+  cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_S / 2};   // half the slices (multicast)
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(Sl), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
@@ -508,6 +606,33 @@ inline size_t oz_operand_bytes(int R, int K) {
   return align256((size_t)OZ_S * R * oz_kp(K)) + align256((size_t)R * sizeof(int));
 }
 
+// clusters of 4 that can be resident at once (GPCs hold whole clusters: fewer than 148 / 4)
+int oz_max_clusters() {
+  static std::once_flag once;
+  static int n = 0;
+  std::call_once(once, [] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(OZ_CL * (148 / OZ_CL));
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = OZ_SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = OZ_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaFuncSetAttribute(ozaki_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)OZ_SMEM) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&n, ozaki_gemm_kernel, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    if (getenv("GG_OZ_VERBOSE")) fprintf(stderr, "[gg ozaki] %d resident clusters of %d\n", n, OZ_CL);
+  });
+  return n;
+}
+
 int sms_oz() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -515,14 +640,14 @@ int sms_oz() {
 }
 
 int slice_operand(int R, int Kc, const double* X, long long rs, long long cs, signed char* Sl,
-                  int* ex, long long kp, const int* abort_flag, cudaStream_t s) {
+                  int* ex, long long kp, int tri, int koff, const int* abort_flag, cudaStream_t s) {
   GG_CUDA_TRY(cudaMemsetAsync(ex, 0x80, (size_t)R * sizeof(int), s));   // EX_NONE
   const int rows_per_cta = rs <= cs ? SL_THREADS : SL_THREADS / 32;
   dim3 gx((R + rows_per_cta - 1) / rows_per_cta, (Kc + RX_K - 1) / RX_K);
-  oz_rowexp_kernel<<<gx, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, abort_flag);
+  oz_rowexp_kernel<<<gx, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, tri, koff, abort_flag);
   GG_LAUNCH_CHECK("oz_rowexp_kernel");
   dim3 g((R + SL_R - 1) / SL_R, (unsigned)((kp + SL_K - 1) / SL_K));
-  oz_slice_kernel<<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, abort_flag);
+  oz_slice_kernel<<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, tri, koff, abort_flag);
   GG_LAUNCH_CHECK("oz_slice_kernel");
   return GG_OK;
 }
@@ -566,10 +691,13 @@ int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long lo
   // k chunks of at most OZ_KMAX (exact int32 diagonals); beta applies to the first chunk only
   for (int k0 = 0; k0 < K; k0 += OZ_KMAX) {
     const int Kc = (K - k0 < OZ_KMAX) ? (K - k0) : OZ_KMAX;
-    int rc = slice_operand(M, Kc, A + (long long)k0 * a_cs, a_rs, a_cs, SlA, exA, kp, abort_flag, s);
+    // (B = A: the SYRK, no triangle flags on its operand)
+    int rc = slice_operand(M, Kc, A + (long long)k0 * a_cs, a_rs, a_cs, SlA, exA, kp,
+                           (flags & GEMM_A_LOWER) ? 1 : 0, k0, abort_flag, s);
     if (rc != GG_OK) return rc;
     if (!same) {
-      rc = slice_operand(N, Kc, B + (long long)k0 * b_cs, b_rs, b_cs, SlB, exB, kp, abort_flag, s);
+      rc = slice_operand(N, Kc, B + (long long)k0 * b_cs, b_rs, b_cs, SlB, exB, kp,
+                         (flags & GEMM_B_LOWER) ? 2 : 0, k0, abort_flag, s);
       if (rc != GG_OK) return rc;
     }
     CUtensorMap mA, mB;
@@ -595,10 +723,23 @@ int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long lo
     a.gm = 8;
     if (const char* v = getenv("GG_OZ_GM")) a.gm = atoi(v) > 0 ? atoi(v) : 8;   // tuning knob
     a.abort_flag = abort_flag;
-    const int tiles = ((M + OZ_BM - 1) / OZ_BM) * ((N + OZ_BN - 1) / OZ_BN);
-    const int grid = tiles < sms_oz() ? tiles : sms_oz();
-    ozaki_gemm_kernel<<<grid, OZ_THREADS, OZ_SMEM, s>>>(mA, mB, a);
-    GG_LAUNCH_CHECK("ozaki_gemm_kernel");
+    if (const char* v = getenv("GG_OZ_WHATIF")) a.whatif = atoi(v);
+    const long long blocks = (long long)((M + OZ_CBM - 1) / OZ_CBM) * ((N + OZ_CBN - 1) / OZ_CBN);
+    const int resident = oz_max_clusters();   // a persistent grid must be co-resident
+    const int clusters = (int)(blocks < resident ? blocks : resident);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(OZ_CL * clusters);
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = OZ_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = OZ_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GG_CUDA_TRY(cudaLaunchKernelEx(&cfg, ozaki_gemm_kernel, mA, mB, a));
   }
   return GG_OK;
 }
