@@ -196,15 +196,43 @@ def local_from_spec(spec, layout, ops):
 # the fused distributed Cholesky + inverse
 # ---------------------------------------------------------------------------------------------
 
-def dist_potrf_inv(A, B, layout, ops, comm=None):
+class _NoStreams:
+    """Look-ahead stream hooks for ops without streams (the CPU ops of the gloo tests): the
+    side-stream work simply runs in program order."""
+
+    def fork(self):
+        pass
+
+    def join(self):
+        pass
+
+    def side(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    def keep(self, *tensors):
+        pass
+
+
+def dist_potrf_inv(A, B, layout, ops, comm=None, lookahead=True):
     """Fused distributed Cholesky + inverse (see module doc).  A (this rank's blocks of M) is
     overwritten with L, B (this rank's blocks of I) with L^-1.  Raises NotPositiveDefinite with
     the global pivot on every rank.  ``comm``: a communicator, the torch.distributed module or a
-    reference transport (None: one rank)."""
+    reference transport (None: one rank).
+
+    Look-ahead (depth 1): step K's trailing update is split into the next block column K+1
+    (A only, on the rank's main stream: what step K+1's diagonal factorisation and panel need)
+    and the rest (A's columns beyond K+1 and the inverse's update B_IJ -= L_IK X_KJ) on a side
+    stream.  Step K+1's diagonal factorisation, status / inverse broadcasts, panel GEMM, row
+    broadcast and panel-row all-reduce then proceed while the rest runs; the main stream waits
+    for it only before the inverse's block row X_{K+1,J} (which reads B's block row K+1) and the
+    next block-column update (which writes a column the rest also writes)."""
     comm = as_comm(comm)
     nb, g = layout.nb, layout.grid
     rank = layout.rank
     gcm = GridComm(comm, g) if comm is not None and comm.size > 1 else None
+    la = ops.lookahead_streams() if (lookahead and hasattr(ops, "lookahead_streams")) \
+        else _NoStreams()
     for K in range(layout.nblk):
         owner = layout.owner(K, K)
         Dinv = ops.empty(nb, nb)
@@ -219,6 +247,7 @@ def dist_potrf_inv(A, B, layout, ops, comm=None):
             gcm.world.broadcast(status, owner)
         st = int(status.item())
         if st >= 0:
+            la.join()
             raise NotPositiveDefinite(K * nb + st)
         if gcm is not None:
             gcm.world.broadcast(Dinv, owner)
@@ -255,6 +284,9 @@ def dist_potrf_inv(A, B, layout, ops, comm=None):
                     ops.copy_rows(P_cols, dst, P_rows, src)
             if gcm is not None:
                 gcm.col.all_reduce(P_cols)
+        # the previous step's side-stream update must be complete from here on (B's block row K,
+        # A's block column K+2)
+        la.join()
         # block row K of the inverse, X_KJ = Dinv B_KJ (J <= K) on process row K % r, broadcast
         # along the process column (c0 is uniform over a process column)
         X_cols = None
@@ -268,12 +300,21 @@ def dist_potrf_inv(A, B, layout, ops, comm=None):
                 gcm.col.broadcast(X_cols, K % g.r)
         if m_below == 0:
             continue
-        if n_right > 0:
-            ops.gemm(A, r0, c0, m_below, n_right, P_rows, 0, 0, P_cols, 0, 0, nb, -1.0, 1.0,
+        # next block column K+1 first (if this rank owns it: it is then its first column > K)
+        nxt = nb if (n_right > 0 and (K + 1) % g.c == layout.pc) else 0
+        if nxt:
+            ops.gemm(A, r0, c0, m_below, nxt, P_rows, 0, 0, P_cols, 0, 0, nb, -1.0, 1.0,
                      trans_b=True)
-        if c0 > 0:
-            ops.gemm(B, r0, 0, m_below, c0, P_rows, 0, 0, X_cols, 0, 0, nb, -1.0, 1.0,
-                     trans_b=False)
+        la.fork()
+        with la.side():
+            if n_right > nxt:
+                ops.gemm(A, r0, c0 + nxt, m_below, n_right - nxt, P_rows, 0, 0, P_cols, nxt, 0,
+                         nb, -1.0, 1.0, trans_b=True)
+            if c0 > 0:
+                ops.gemm(B, r0, 0, m_below, c0, P_rows, 0, 0, X_cols, 0, 0, nb, -1.0, 1.0,
+                         trans_b=False)
+        la.keep(P_rows, P_cols, X_cols)
+    la.join()
     ops.zero_upper_blocks(A, layout)
     return A, B
 
@@ -542,6 +583,34 @@ def dist_trsolve(L, B, t, nb=64, ops=None):
 # the production ops: sm_100a kernels through the C-ABI
 # ---------------------------------------------------------------------------------------------
 
+class _DeviceStreams:
+    """dist_potrf_inv's look-ahead on the device: a lowest-priority side stream forked from and
+    joined into the caller's current stream with events; tensors the side stream reads are
+    recorded on it so the caching allocator cannot hand their memory out early."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.stream = torch.cuda.Stream(priority=0)   # 0 = the lowest priority
+        self.pending = False
+
+    def fork(self):
+        self.stream.wait_stream(self.torch.cuda.current_stream())
+        self.pending = True
+
+    def join(self):
+        if self.pending:
+            self.torch.cuda.current_stream().wait_stream(self.stream)
+            self.pending = False
+
+    def side(self):
+        return self.torch.cuda.stream(self.stream)
+
+    def keep(self, *tensors):
+        for t in tensors:
+            if t is not None:
+                t.record_stream(self.stream)
+
+
 class DeviceOps:
     """Local numerics of the distributed engine on this rank's GPU."""
 
@@ -553,7 +622,8 @@ class DeviceOps:
         self.torch = torch
         self.capi = _capi
         self.dev = _capi.device()
-        self._oz_ws = None      # Ozaki GEMM workspace, grown on demand
+        self._oz_ws = {}        # Ozaki GEMM workspace per stream, grown on demand
+        self._la = None
 
     # -- buffers (column-major (rows x cols) matrix = torch tensor (cols, rows)) --------------
     def empty(self, ncols, nrows):
@@ -593,6 +663,12 @@ class DeviceOps:
 
     def _p(self, T, r0, c0):
         return self.capi.C.c_void_p(T.data_ptr() + (c0 * T.shape[1] + r0) * 8)
+
+    def lookahead_streams(self):
+        """The side stream of dist_potrf_inv's look-ahead (lowest priority)."""
+        if self._la is None:
+            self._la = _DeviceStreams(self.torch)
+        return self._la
 
     # -- numerics ------------------------------------------------------------------------------
     def potrf_inv(self, A, r0, c0, nb):
@@ -637,15 +713,18 @@ class DeviceOps:
         if min(m, n, k) >= 512 and os.environ.get("GG_FACTOR_OZAKI", "1") != "0":
             lib = capi.lib()
             need = int(lib.gg_gemm_ozaki_workspace_bytes(m, n, k, 0))
-            if self._oz_ws is None or self._oz_ws.numel() < need:
-                self._oz_ws = None
-                self._oz_ws = self.torch.empty(need, dtype=self.torch.uint8, device=self.dev)
+            key = self.torch.cuda.current_stream().cuda_stream   # one workspace per stream
+            ws = self._oz_ws.get(key)
+            if ws is None or ws.numel() < need:
+                self._oz_ws.pop(key, None)
+                ws = self._oz_ws[key] = self.torch.empty(need, dtype=self.torch.uint8,
+                                                         device=self.dev)
             ldb = B.shape[1]
             b_rs, b_cs = (1, ldb) if trans_b else (ldb, 1)
             rc = lib.gg_gemm_ozaki_f64(m, n, k, self._p(A, ar, ac), 1, A.shape[1],
                                        self._p(B, br, bc), b_rs, b_cs, self._p(C, cr, cc),
-                                       C.shape[1], alpha, beta, 0, capi.ptr(self._oz_ws),
-                                       self._oz_ws.numel(), capi.stream_handle())
+                                       C.shape[1], alpha, beta, 0, capi.ptr(ws), ws.numel(),
+                                       capi.stream_handle())
             capi.check(rc, "gg_gemm_ozaki_f64")
             return
         if m % 128 or k % 16 or (trans_b and n % 128):

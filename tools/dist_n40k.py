@@ -7,7 +7,7 @@ whitens [X_L | y] from the block-cyclic inverse, and solves a 1,024-SNP sample t
 slices-only context.  Checked against the single-GPU prepare of the same M (itself checked against
 the CPU oracle in bench.py); reports the prepare time and the process's peak host RSS.
 
-    python tools/dist_n40k.py [--n 40000] [--world 2]
+    python tools/dist_n40k.py [--n 40000] [--world 2] [--no-lookahead]
 """
 
 import argparse
@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--n", type=int, default=40_000)
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--snps", type=int, default=1024)
+    ap.add_argument("--no-lookahead", action="store_true")
     args = ap.parse_args()
     import dataclasses
 
@@ -49,7 +50,7 @@ def main():
         torch.cuda.synchronize()
         t_gen = time.perf_counter() - t0
         t0 = time.perf_counter()
-        distgrid.dist_potrf_inv(A, B, lay, ops, t)
+        distgrid.dist_potrf_inv(A, B, lay, ops, t, lookahead=not args.no_lookahead)
         del A
         S, e = distgrid.assemble_slices(B, lay, ops, t)
         XLy = distgrid.whiten_blockcyclic(B, lay, ops, np.column_stack([XL, y]), t)
@@ -76,7 +77,7 @@ def main():
     ref = np.array([r.beta for r in kernel.gls_solve_block(ctx1, kernel.SnpBlock(0, G)).results])
     from oracle import gls_ref as O
 
-    print(f"n={spec.n} p={spec.p} world={args.world} (grid "
+    print(f"look-ahead {'off' if args.no_lookahead else 'on'}: n={spec.n} p={spec.p} world={args.world} (grid "
           f"{distgrid.grid_create(args.world).r}x{distgrid.grid_create(args.world).c}, nb=512); "
           f"local share {res[0][3]}x{res[0][4]} per rank")
     for r, (tg, tp, beta, _, _) in enumerate(res):
