@@ -22,6 +22,8 @@
  *     Column counts are never padded.
  *   - No entry point allocates persistent device memory; workspaces (including the int8
  *     TRSM's tile counter) come from the caller (sizes from the *_workspace_bytes queries).
+ *     The one handle is gg_dist_comms (created by gg_dist_comms_*, owned by the caller,
+ *     released by gg_dist_comms_free: NCCL communicators or transport callbacks).
  *     The only process-wide state is the once-resolved cuTensorMapEncodeTiled pointer.
  *     Entry points are reentrant and keep no unguarded global state (SPEC threading rule,
  *     SURVEY §8b).
@@ -40,9 +42,8 @@ extern "C" {
 #define GG_ENOTPD 1      /* Cholesky pivot <= 0 / NaN, or non-finite input      */
 #define GG_EDIM 2        /* inconsistent sizes / leading dimensions              */
 #define GG_ECUDA 3       /* CUDA runtime error                                   */
-#define GG_ENCCL 4       /* a failed collective: the distributed engine drives NCCL from its
-                            host layer (comm.py), which raises TransportFailure with this meaning;
-                            no C-ABI entry point itself calls NCCL                      */
+#define GG_ENCCL 4       /* a failed collective (gg_dist_*: NCCL or a transport callback); the
+                            host layer (comm.py) raises TransportFailure with this meaning     */
 #define GG_EARG 5        /* invalid argument (NULL pointer, unsupported p, ...)  */
 
 #define GG_TILE 128      /* row padding unit = GEMM tile edge                    */
@@ -303,6 +304,43 @@ int gg_gen_genotypes_i8(unsigned long long seed, int stream_maf, int stream_geno
                         long long m, long long first, int cnt, double maf_lo,
                         double maf_hi, int8_t* G, long long ldg, double* Z, int ldz,
                         void* stream);
+
+/* ---- Distributed Cholesky + inverse (configs too large for one GPU) ------------------
+ * SURVEY §8b's distributed C-ABI: one rank per GPU, M 2D block-cyclic (nb x nb blocks on an
+ * r x c grid, rank = pr * c + pc, the reference's grid_create rule distgrid.py:43-52).
+ * Replaces the factorisation of dist_cholesky (distgrid.py:248-288) and yields the inverse
+ * too (the distributed prepare's slices come from it).  Collectives run either on NCCL
+ * communicators built here (world from one unique id, process row / column split from it;
+ * NCCL resolved from the process at run time, no link-time dependency) or on host callbacks
+ * (a reference-contract transport: group 0 world, 1 process row, 2 process column; root /
+ * member indices within the group; buffers are device pointers, the stream is synchronised
+ * before a callback runs).                                                            */
+typedef struct gg_dist_comms gg_dist_comms;
+typedef int (*gg_dist_bcast_fn)(void* ctx, int group, void* dev, size_t bytes, int root);
+typedef int (*gg_dist_allreduce_fn)(void* ctx, int group, double* dev, size_t count);   /* sum */
+int gg_dist_nccl_unique_id(unsigned char* id_out /* 128 bytes */);
+int gg_dist_comms_nccl(int rank, int nranks, int grid_r, int grid_c, const unsigned char* id,
+                       gg_dist_comms** out);
+int gg_dist_comms_callbacks(int rank, int nranks, int grid_r, int grid_c, gg_dist_bcast_fn bcast,
+                            gg_dist_allreduce_fn allreduce, void* ctx, gg_dist_comms** out);
+int gg_dist_comms_free(gg_dist_comms* c);
+/* this rank's share: m_loc x n_loc (row blocks pr, pr + r, ...; column blocks pc, pc + c, ...) */
+int gg_dist_local_dims(int n, int nb, const gg_dist_comms* c, int* m_loc, int* n_loc);
+size_t gg_dist_potrf_workspace_bytes(int n, int nb, const gg_dist_comms* c);
+/* Fused distributed Cholesky + inverse.  A: this rank's share of M (column-major, lda >=
+ * m_loc; blocks past n hold the identity), overwritten with its share of L (strictly upper
+ * blocks zeroed); B: its share of the identity, overwritten with its share of L^-1.  nb a
+ * multiple of 128.  Per block column: the diagonal owner factors + inverts (gg_potrf_f64's
+ * path) and broadcasts status and inverse over the world; the panel is formed on process
+ * column K%c and broadcast along process rows; panel rows for the trailing columns by one SUM
+ * all-reduce along process columns; the inverse's block row on process row K%r, broadcast
+ * along process columns; local updates on the tensor cores (Ozaki int8 GEMM when every
+ * dimension >= 512, DMMA otherwise) with depth-1 look-ahead on a lower-priority side stream.
+ * GG_ENOTPD with *info = the global failing column on every rank; GG_ENCCL on a failed
+ * collective.  Synchronises `stream` once per block column (the pivot status).            */
+int gg_dist_potrf_f64(int n, int nb, double* A, long long lda, double* B, long long ldb,
+                      const gg_dist_comms* c, void* work, size_t work_bytes, int* info,
+                      void* stream);
 
 #ifdef __cplusplus
 }

@@ -72,7 +72,18 @@ SIGNATURES = {
     "gg_memcpy2d_async": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _i, _vp]),
     "gg_gen_genotypes_i8": (_i, [_ull, _i, _i, _i, _ll, _ll, _i, _d, _d, _vp, _ll, _vp, _i,
                                  _vp]),
+    # distributed Cholesky + inverse (csrc/dist_native.cu)
+    "gg_dist_nccl_unique_id": (_i, [_vp]),
+    "gg_dist_comms_nccl": (_i, [_i, _i, _i, _i, _vp, _vp]),
+    "gg_dist_comms_callbacks": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "gg_dist_comms_free": (_i, [_vp]),
+    "gg_dist_local_dims": (_i, [_i, _i, _vp, _ip, _ip]),
+    "gg_dist_potrf_workspace_bytes": (_sz, [_i, _i, _vp]),
+    "gg_dist_potrf_f64": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp, _sz, _ip, _vp]),
 }
+# callback types of gg_dist_comms_callbacks (group 0 world, 1 process row, 2 process column)
+DIST_BCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_int)
+DIST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t)
 
 _lock = threading.Lock()
 _lib = None

@@ -214,11 +214,16 @@ class _NoStreams:
         pass
 
 
-def dist_potrf_inv(A, B, layout, ops, comm=None, lookahead=True):
+def dist_potrf_inv(A, B, layout, ops, comm=None, lookahead=True, native=None):
     """Fused distributed Cholesky + inverse (see module doc).  A (this rank's blocks of M) is
     overwritten with L, B (this rank's blocks of I) with L^-1.  Raises NotPositiveDefinite with
     the global pivot on every rank.  ``comm``: a communicator, the torch.distributed module or a
     reference transport (None: one rank).
+
+    With the device ops the loop runs natively (``native``, default on; GG_DIST_NATIVE=0 keeps
+    this Python driver): gg_dist_potrf_f64 over NCCL communicators (torch.distributed NCCL
+    world) or over this communicator through host callbacks (other transports) -- the same
+    kernels in the same order, bitwise the same factor and inverse.
 
     Look-ahead (depth 1): step K's trailing update is split into the next block column K+1
     (A only, on the rank's main stream: what step K+1's diagonal factorisation and panel need)
@@ -228,6 +233,10 @@ def dist_potrf_inv(A, B, layout, ops, comm=None, lookahead=True):
     for it only before the inverse's block row X_{K+1,J} (which reads B's block row K+1) and the
     next block-column update (which writes a column the rest also writes)."""
     comm = as_comm(comm)
+    if native is None:
+        native = isinstance(ops, DeviceOps) and os.environ.get("GG_DIST_NATIVE", "1") != "0"
+    if native:
+        return native_potrf_inv(A, B, layout, comm)
     nb, g = layout.nb, layout.grid
     rank = layout.rank
     gcm = GridComm(comm, g) if comm is not None and comm.size > 1 else None
@@ -316,6 +325,121 @@ def dist_potrf_inv(A, B, layout, ops, comm=None, lookahead=True):
         la.keep(P_rows, P_cols, X_cols)
     la.join()
     ops.zero_upper_blocks(A, layout)
+    return A, B
+
+
+class _DevView:
+    """A torch view of raw device memory (the C-ABI's callback buffers)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class NativeComms:
+    """gg_dist_comms of one rank: NCCL communicators (a torch.distributed NCCL world: world from
+    one unique id, row / column split from it in the library) or callbacks into this
+    communicator's world / row / column groups (any other transport).  Cached per communicator
+    and grid: NCCL communicator creation is collective and slow."""
+
+    _cache = {}
+
+    def __init__(self, comm, grid):
+        from . import _capi
+
+        self.capi = _capi
+        self.handle = _capi.C.c_void_p()
+        self.error = None
+        size = 1 if comm is None else comm.size
+        rank = 0 if comm is None else comm.rank
+        nccl = comm is not None and size > 1 and getattr(comm, "backend", "") == "nccl"
+        lib = _capi.lib()
+        if nccl:
+            uid = (_capi.C.c_ubyte * 128)()
+            if rank == 0:
+                _capi.check(lib.gg_dist_nccl_unique_id(uid), "gg_dist_nccl_unique_id")
+            ids = comm.allgather_obj(bytes(uid))
+            uid = (_capi.C.c_ubyte * 128).from_buffer_copy(ids[0])
+            _capi.check(lib.gg_dist_comms_nccl(rank, size, grid.r, grid.c, uid,
+                                               _capi.C.byref(self.handle)), "gg_dist_comms_nccl")
+            self._keep = ()
+            return
+        self.gcm = GridComm(comm, grid) if comm is not None and size > 1 else None
+
+        def groups(g):
+            return (self.gcm.world, self.gcm.row, self.gcm.col)[g]
+
+        def bcast(_ctx, g, ptr, nbytes, root):
+            try:
+                import torch
+                t = torch.as_tensor(_DevView(ptr, nbytes, "|u1"), device="cuda")
+                groups(g).broadcast(t, root)
+                return 0
+            except BaseException as e:   # surfaced by native_potrf_inv
+                self.error = e
+                return 1
+
+        def allreduce(_ctx, g, ptr, count):
+            try:
+                import torch
+                t = torch.as_tensor(_DevView(ptr, count, "<f8"), device="cuda")
+                groups(g).all_reduce(t)
+                return 0
+            except BaseException as e:
+                self.error = e
+                return 1
+
+        self._keep = (_capi.DIST_BCAST_FN(bcast), _capi.DIST_ALLREDUCE_FN(allreduce))
+        _capi.check(lib.gg_dist_comms_callbacks(rank, size, grid.r, grid.c,
+                                                _capi.C.cast(self._keep[0], _capi.C.c_void_p),
+                                                _capi.C.cast(self._keep[1], _capi.C.c_void_p),
+                                                None, _capi.C.byref(self.handle)),
+                    "gg_dist_comms_callbacks")
+
+    @classmethod
+    def get(cls, comm, grid):
+        if comm is None or comm.size == 1 or getattr(comm, "backend", "") != "nccl":
+            return cls(comm, grid)        # callbacks: cheap to build, not cached
+        key = (id(comm.dist), comm.group, grid, comm.rank, comm.size)
+        if key not in cls._cache:
+            cls._cache[key] = cls(comm, grid)
+        return cls._cache[key]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.capi.lib().gg_dist_comms_free(self.handle)
+        except Exception:
+            pass
+
+
+def native_potrf_inv(A, B, layout, comm=None):
+    """dist_potrf_inv through the C-ABI gg_dist_potrf_f64 (csrc/dist_native.cu)."""
+    import torch
+
+    from . import _capi
+
+    nc = NativeComms.get(comm, layout.grid)
+    lib = _capi.lib()
+    m_loc, n_loc = _capi.C.c_int(), _capi.C.c_int()
+    _capi.check(lib.gg_dist_local_dims(layout.n, layout.nb, nc.handle, _capi.C.byref(m_loc),
+                                       _capi.C.byref(n_loc)), "gg_dist_local_dims")
+    if (m_loc.value, n_loc.value) != (layout.m_loc, layout.n_loc):
+        raise DimensionMismatch("native layout disagrees with BlockCyclic")
+    ws = torch.empty(max(1, int(lib.gg_dist_potrf_workspace_bytes(layout.n, layout.nb,
+                                                                  nc.handle))),
+                     dtype=torch.uint8, device=A.device)
+    info = _capi.C.c_int(-1)
+    lda = max(1, layout.m_loc)
+    rc = lib.gg_dist_potrf_f64(layout.n, layout.nb, _capi.ptr(A), lda, _capi.ptr(B), lda,
+                               nc.handle, _capi.ptr(ws), ws.numel(), _capi.C.byref(info),
+                               _capi.stream_handle())
+    if nc.error is not None:
+        err, nc.error = nc.error, None
+        raise err
+    if rc == _capi.GG_ENOTPD:
+        raise NotPositiveDefinite(int(info.value))
+    _capi.check(rc, "gg_dist_potrf_f64")
     return A, B
 
 

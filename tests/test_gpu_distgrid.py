@@ -240,3 +240,93 @@ def test_config4_form_at_n40k_world2_on_one_gpu(gpu):
     assert len(rels) == 2 and max(rels) <= 1e-9, out.stdout
     assert "status mismatches 0" in out.stdout and "identical results on every rank: True" in \
         out.stdout, out.stdout
+
+
+def _gather_LLi(A, B, lay, ops, t=None):
+    from paper_1304_2272_b200 import distgrid
+
+    return distgrid.gather_matrix(A, lay, ops, t), distgrid.gather_matrix(B, lay, ops, t)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_native_driver_matches_python_driver_bitwise(gpu, world):
+    """gg_dist_potrf_f64 (C++ loop, collectives through callbacks into the transport) against the
+    Python driver of the same engine: the same kernels in the same order -> bitwise the same
+    factor and inverse on every rank (n = 2,100, nb = 512: Ozaki and DMMA updates, ragged
+    last block)."""
+    from paper_1304_2272_b200 import distgrid
+    from spmd_inproc import run_spmd
+
+    n, nb = 2100, 512
+    M = make_spd(n, 8)
+
+    def body(t):
+        ops = distgrid.DeviceOps()
+        lay = distgrid.BlockCyclic(n, nb, distgrid.grid_create(t.size), t.rank)
+        out = []
+        for native in (True, False):
+            A, B = distgrid.local_from_global(M, lay, ops)
+            distgrid.dist_potrf_inv(A, B, lay, ops, t, native=native)
+            out.append((ops.to_host(A).copy(), ops.to_host(B).copy()))
+        return out
+
+    for (An, Bn), (Ap, Bp) in run_spmd(world, body):
+        assert np.array_equal(An, Ap) and np.array_equal(Bn, Bp)
+
+
+def test_native_driver_nccl_world1(gpu):
+    """The NCCL backend of gg_dist_potrf_f64 (communicators from a unique id, row / column split,
+    ncclBroadcast / ncclAllReduce issued even on groups of one) at world 1 -- bitwise the
+    single-rank Python driver.  (NCCL refuses two ranks on one GPU; world > 1 runs the same loop
+    over the callback backend above.)"""
+    import ctypes as C
+
+    import torch
+
+    from paper_1304_2272_b200 import _capi, distgrid
+
+    n, nb = 1500, 512
+    M = make_spd(n, 9)
+    ops = distgrid.DeviceOps()
+    lay = distgrid.BlockCyclic(n, nb, distgrid.grid_create(1), 0)
+    lib = _capi.lib()
+    uid = (C.c_ubyte * 128)()
+    _capi.check(lib.gg_dist_nccl_unique_id(uid), "gg_dist_nccl_unique_id")
+    h = C.c_void_p()
+    _capi.check(lib.gg_dist_comms_nccl(0, 1, 1, 1, uid, C.byref(h)), "gg_dist_comms_nccl")
+    try:
+        A, B = distgrid.local_from_global(M, lay, ops)
+        ws = torch.empty(int(lib.gg_dist_potrf_workspace_bytes(n, nb, h)), dtype=torch.uint8,
+                         device="cuda")
+        info = C.c_int(-1)
+        _capi.check(lib.gg_dist_potrf_f64(n, nb, _capi.ptr(A), lay.m_loc, _capi.ptr(B), lay.m_loc,
+                                          h, _capi.ptr(ws), ws.numel(), C.byref(info),
+                                          _capi.stream_handle()), "gg_dist_potrf_f64")
+        A2, B2 = distgrid.local_from_global(M, lay, ops)
+        distgrid.dist_potrf_inv(A2, B2, lay, ops, native=False)
+        assert torch.equal(A, A2) and torch.equal(B, B2)
+    finally:
+        lib.gg_dist_comms_free(h)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_native_driver_not_pd_global_pivot_every_rank(gpu, world):
+    from paper_1304_2272_b200 import distgrid
+    from paper_1304_2272_b200.errors import NotPositiveDefinite
+    from spmd_inproc import run_spmd
+
+    n = 1300
+    M = make_spd(n, 10)
+    M[777, 777] = -5.0
+
+    def body(t):
+        ops = distgrid.DeviceOps()
+        lay = distgrid.BlockCyclic(n, 256, distgrid.grid_create(t.size), t.rank)
+        A, B = distgrid.local_from_global(M, lay, ops)
+        try:
+            distgrid.dist_potrf_inv(A, B, lay, ops, t)
+        except NotPositiveDefinite as e:
+            return e.pivot_index
+        return None
+
+    assert run_spmd(world, body) == [777] * world
