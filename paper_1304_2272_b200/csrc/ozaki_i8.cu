@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <string>
 
 #include "gg_internal.cuh"
@@ -457,24 +458,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 // ---- slicing -----------------------------------------------------------------------------------
-// X(r, k) = X[r rs + k cs], rows [0, R), k in [0, K).  Tiles of 32 rows x 128 k staged through
-// shared memory with the coalesced thread mapping for whichever stride is 1.
-constexpr int SL_R = 32, SL_K = 128, SL_THREADS = 256;
-constexpr int SL_KP = SL_K + SL_K / 16;   // one pad double per 16: conflict-free 16-k reads
+// X(r, k) = X[r rs + k cs], rows [0, R), k in [0, K).  Tiles of TR rows x TK k (4,096 elements)
+// staged through shared memory with the coalesced thread mapping for whichever stride is 1:
+// 128 x 32 when the rows are contiguous (1 KB runs per column -- 32-row tiles read 256-B runs
+// 320 KB apart and streamed at ~1.7 TB/s on the 39k-row SYRK operand at n = 4e4), 32 x 128 when
+// k is.
+constexpr int SL_THREADS = 256;
 constexpr int EX_NONE = (int)0x80808080;  // row-exponent sentinel (memset 0x80): no nonzero yet
-__device__ __forceinline__ int tix(int k) { return k + (k >> 4); }
+__device__ __forceinline__ int tix(int k) { return k + (k >> 4); }   // one pad per 16 k
 
-__device__ __forceinline__ void load_tile(double (*T)[SL_KP], const double* X, long long rs,
+template <int TR, int TK>
+__device__ __forceinline__ void load_tile(double (*T)[TK + TK / 16], const double* X, long long rs,
                                           long long cs, int R, int K, int r0, int k0) {
-  if (rs <= cs) {   // rows contiguous: lane -> row
-    for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
-      const int r = i % SL_R, k = i / SL_R;
+  if (rs <= cs) {   // rows contiguous: consecutive threads -> consecutive rows
+    for (int i = threadIdx.x; i < TR * TK; i += SL_THREADS) {
+      const int r = i % TR, k = i / TR;
       T[r][tix(k)] = (r0 + r < R && k0 + k < K)
                          ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
     }
-  } else {          // k contiguous: lane -> k
-    for (int i = threadIdx.x; i < SL_R * SL_K; i += SL_THREADS) {
-      const int k = i % SL_K, r = i / SL_K;
+  } else {          // k contiguous: consecutive threads -> consecutive k
+    for (int i = threadIdx.x; i < TR * TK; i += SL_THREADS) {
+      const int k = i % TK, r = i / TK;
       T[r][tix(k)] = (r0 + r < R && k0 + k < K)
                          ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
     }
@@ -488,72 +492,74 @@ __device__ __forceinline__ bool oz_masked(int tri, int r, int k) {
   return (tri == 1 && k > r) || (tri == 2 && k < r);
 }
 
-// ex[r] = max(ex[r], e) with max_k |X(r,k)| < 2^e over this CTA's k chunk (ex starts at EX_NONE;
-// the exponent of the row maximum is the maximum of the chunk exponents).  Rows contiguous: a
-// thread per row walks RX_K values of k (warps read 256 contiguous bytes); k contiguous: a warp per
-// row, lanes across k.
-constexpr int RX_K = 256;
+// ex[r] = max(ex[r], e) with max_k |X(r,k)| < 2^e over this CTA's tile (ex starts at EX_NONE; the
+// exponent of the row maximum is the maximum of the tile exponents); each warp reduces TR / 8
+// rows of the staged tile (r02: a thread per row walking 256 strided k values was latency-bound).
+template <int TR, int TK>
 __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, const double* X,
                                                                 long long rs, long long cs,
                                                                 int* ex, int tri, int koff,
                                                                 const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag != 0) return;
-  const int k0 = blockIdx.y * RX_K, k1 = min(K, k0 + RX_K);
-  double m = 0.0;
-  int r;
-  if (rs <= cs) {
-    r = blockIdx.x * SL_THREADS + threadIdx.x;
-    if (r >= R) return;
-    const double* p = X + (long long)r * rs;
-#pragma unroll 8
-    for (int k = k0; k < k1; ++k)
-      if (!oz_masked(tri, r, koff + k)) m = fmax(m, fabs(p[(long long)k * cs]));
-  } else {
-    const int lane = threadIdx.x & 31;
-    r = blockIdx.x * (SL_THREADS / 32) + (threadIdx.x >> 5);
-    if (r >= R) return;
-    const double* p = X + (long long)r * rs;
-#pragma unroll 4
-    for (int k = k0 + lane; k < k1; k += 32)
-      if (!oz_masked(tri, r, koff + k)) m = fmax(m, fabs(p[(long long)k * cs]));
+  __shared__ double T[TR][TK + TK / 16];
+  const int r0 = blockIdx.x * TR, k0 = blockIdx.y * TK;
+  load_tile<TR, TK>(T, X, rs, cs, R, K, r0, k0);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int rr = warp; rr < TR; rr += SL_THREADS / 32) {
+    const int r = r0 + rr;
+    if (r >= R) break;
+    double m = 0.0;
+#pragma unroll
+    for (int j = 0; j < TK / 32; ++j) {
+      const int k = lane + 32 * j;
+      if (!oz_masked(tri, r, koff + k0 + k)) m = fmax(m, fabs(T[rr][tix(k)]));
+    }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane != 0) return;
-  }
-  if (m > 0.0) {
-    int e;
-    frexp(m, &e);
-    atomicMax(ex + r, e);
+    if (lane == 0 && m > 0.0) {
+      int e;
+      frexp(m, &e);
+      atomicMax(ex + r, e);
+    }
   }
 }
 
-// Sl[s][r][k] (row stride kp bytes, slice stride kp * R) for k in [0, kp): exact slices below 2^ex[r]
+// Sl[s][r][k] (row stride kp bytes, slice stride kp * R) for k in [0, kp): exact slices below 2^ex[r];
+// 16 consecutive k per thread (TK / 16 threads per row)
+template <int TR, int TK>
 __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, const double* X,
                                                                long long rs, long long cs,
                                                                const int* ex, signed char* Sl,
                                                                long long kp, int tri, int koff,
                                                                const int* abort_flag) {
+  static_assert(TR * (TK / 16) == SL_THREADS, "one 16-k run per thread");
   if (abort_flag != nullptr && *abort_flag != 0) return;
-  __shared__ double T[SL_R][SL_KP];
-  const int r0 = blockIdx.x * SL_R, k0 = blockIdx.y * SL_K;
-  load_tile(T, X, rs, cs, R, K, r0, k0);
+  __shared__ double T[TR][TK + TK / 16];
+  const int r0 = blockIdx.x * TR, k0 = blockIdx.y * TK;
+  load_tile<TR, TK>(T, X, rs, cs, R, K, r0, k0);
   __syncthreads();
-  const int r = threadIdx.x / 8, kq = (threadIdx.x % 8) * 16;   // 16 consecutive k per thread
+  const int r = threadIdx.x / (TK / 16), kq = (threadIdx.x % (TK / 16)) * 16;
   if (r0 + r >= R || k0 + kq >= kp) return;
   const int ee = ex[r0 + r];
   const int e = ee == EX_NONE ? 0 : ee;   // all-zero row
   unsigned w[OZ_S][4] = {};
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    double v = oz_masked(tri, r0 + r, koff + k0 + kq + j) ? 0.0 : ldexp(T[r][tix(kq + j)], -e);
+    const double x = T[r][tix(kq + j)];
+    // |v| < 1; 2^-e by its bits (exact) unless the row sits at the ends of the exponent range
+    const double v = oz_masked(tri, r0 + r, koff + k0 + kq + j) ? 0.0
+                     : (e > -1000 && e < 1000) ? x * pow2(-e) : ldexp(x, -e);
+    // digits of the magnitude |v| 2^56 (rounded to nearest once: the last slice's rounding) in
+    // base 128, each carrying the element's sign -- the truncated digits of v: the dropped
+    // products (s + t >= 8) and the residuals keep random signs and cancel along k (floor digits
+    // -- all non-negative below slice 0 -- make them add up coherently: measured 30-90x larger
+    // GEMM errors).  One FP64 -> integer conversion per element, the rest integer work.
+    const unsigned long long N = __double2ull_rn(fabs(v) * 0x1p56);   // exact scale, < 2^56
+    const bool neg = v < 0.0;
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
-      const double t = v * 128.0;         // exact
-      // truncate: the digits keep the sign of the element, so the dropped products (s + t >= 8)
-      // and the residuals have random signs and cancel along k (floor digits -- all non-negative
-      // below slice 0 -- make them add up coherently: measured 30-90x larger GEMM errors)
-      const double q = (s < OZ_S - 1) ? trunc(t) : fmin(fmax(rint(t), -127.0), 127.0);
-      w[s][j / 4] |= ((unsigned)(int)q & 0xffu) << (8 * (j % 4));
-      v = t - q;
+      const int d = (int)((N >> (7 * (OZ_S - 1 - s))) & 127u);
+      w[s][j / 4] |= ((unsigned)(neg ? -d : d) & 0xffu) << (8 * (j % 4));
     }
   }
   const long long off = (long long)(r0 + r) * kp + k0 + kq;
@@ -633,21 +639,22 @@ int oz_max_clusters() {
   return n;
 }
 
-int sms_oz() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
-}
 
 int slice_operand(int R, int Kc, const double* X, long long rs, long long cs, signed char* Sl,
                   int* ex, long long kp, int tri, int koff, const int* abort_flag, cudaStream_t s) {
   GG_CUDA_TRY(cudaMemsetAsync(ex, 0x80, (size_t)R * sizeof(int), s));   // EX_NONE
-  const int rows_per_cta = rs <= cs ? SL_THREADS : SL_THREADS / 32;
-  dim3 gx((R + rows_per_cta - 1) / rows_per_cta, (Kc + RX_K - 1) / RX_K);
-  oz_rowexp_kernel<<<gx, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, tri, koff, abort_flag);
-  GG_LAUNCH_CHECK("oz_rowexp_kernel");
-  dim3 g((R + SL_R - 1) / SL_R, (unsigned)((kp + SL_K - 1) / SL_K));
-  oz_slice_kernel<<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, tri, koff, abort_flag);
+  auto run = [&](auto tr, auto tk) {
+    constexpr int TR = decltype(tr)::value, TK = decltype(tk)::value;
+    const dim3 gx((R + TR - 1) / TR, (Kc + TK - 1) / TK);
+    oz_rowexp_kernel<TR, TK><<<gx, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, tri, koff, abort_flag);
+    const dim3 g((R + TR - 1) / TR, (unsigned)((kp + TK - 1) / TK));
+    oz_slice_kernel<TR, TK><<<g, SL_THREADS, 0, s>>>(R, Kc, X, rs, cs, ex, Sl, kp, tri, koff,
+                                                     abort_flag);
+  };
+  if (rs <= cs)
+    run(std::integral_constant<int, 128>(), std::integral_constant<int, 32>());
+  else
+    run(std::integral_constant<int, 32>(), std::integral_constant<int, 128>());
   GG_LAUNCH_CHECK("oz_slice_kernel");
   return GG_OK;
 }
