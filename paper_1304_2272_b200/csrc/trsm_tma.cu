@@ -245,6 +245,82 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---- skinny right-hand sides (the prepare's [X_L | y]: nrhs <= 16) ------------------------------
+// The tiled kernel above computes 128 columns per tile, so for a handful of covariate columns it
+// spends its DMMA time on padding and its grid on 79 row tiles (1.39 ms at n = 1e4).  Here a CTA
+// owns 32 rows x up to 16 columns and streams its slice of the packed inverse (4 KB per 16-k
+// tile, contiguous) through a cp.async ring, bandwidth-bound; heavy row blocks first.  Each
+// element is accumulated by the same DMMA.8x8x4 sequence as the tiled kernel (k ascending from 0
+// in chunks of 4, accumulator from zero), so a column's X-bar is bitwise the same whichever
+// kernel whitens it (tests/test_gpu_kernel.py::test_skinny_trsm_bitwise_equal_to_tiled).
+constexpr int SK_ROWS = 32, SK_COLS = 16, SK_STAGES = 6, SK_THREADS = 128;
+constexpr int SK_LD = BK + 4;   // smem row stride (doubles): conflict-free DMMA fragment reads
+constexpr int SK_A = SK_ROWS * SK_LD, SK_B = SK_COLS * SK_LD;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(SK_THREADS) trsm_skinny_kernel(
+    int num_rb, int nrhs, const double* __restrict__ LinvP, const double* __restrict__ B,
+    long long ldb, double* __restrict__ X, long long ldx, const int* gate, int gate_value) {
+  if (gate != nullptr && *gate != gate_value) return;   // device-side path selection
+  __shared__ __align__(16) double As[SK_STAGES][SK_A];
+  __shared__ __align__(16) double Bs[SK_STAGES][SK_B];
+  const int rb = num_rb - 1 - blockIdx.x;                 // heavy (long k range) first
+  const int mt = rb >> 2, sub = rb & 3;
+  const int nk = (mt + 1) * (BM / BK);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* Abase = LinvP + (long long)4 * mt * (mt + 1) * (BM * BK) + sub * SK_ROWS * BK;
+  auto load = [&](int st, int kt) {
+    const double* a = Abase + (long long)kt * (BM * BK);
+#pragma unroll
+    for (int c = tid; c < SK_ROWS * (BK / 2); c += SK_THREADS) {   // 2 doubles per chunk
+      const int r = c / (BK / 2), q = c % (BK / 2);
+      cp_async16(&As[st][r * SK_LD + 2 * q], a + r * BK + 2 * q, true);
+    }
+    {
+      const int j = tid / (BK / 2), q = tid % (BK / 2);
+      const bool ok = j < nrhs;
+      cp_async16(&Bs[st][j * SK_LD + 2 * q], B + (ok ? (long long)j * ldb : 0) + kt * BK + 2 * q, ok);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < SK_STAGES - 1; ++st) {
+    if (st < nk) load(st, st);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SK_STAGES - 2) : "memory");
+    __syncthreads();
+    const int pf = kt + SK_STAGES - 1;
+    if (pf < nk) load(pf % SK_STAGES, pf);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const double* a = As[kt % SK_STAGES] + (8 * warp + g) * SK_LD + t;
+    const double* b = Bs[kt % SK_STAGES] + g * SK_LD + t;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const double af = a[kk];
+      dmma(acc[0], af, b[kk]);
+      dmma(acc[1], af, b[8 * SK_LD + kk]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  const long long row = (long long)rb * SK_ROWS + 8 * warp + g;
+#pragma unroll
+  for (int nf = 0; nf < 2; ++nf)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = 8 * nf + 2 * t + e;
+      if (col < nrhs) X[row + (long long)col * ldx] = acc[nf][e];
+    }
+}
+
 // ---- tensor maps ----------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static std::once_flag once;
@@ -452,6 +528,12 @@ int trsm_packed_gated_run(int n, int nrhs, const double* LinvP, const double* B,
        reinterpret_cast<uintptr_t>(X)) & 15) {
     set_error("trsm: operands must be 16-byte aligned");
     return GG_EARG;
+  }
+  if (nrhs <= SK_COLS && (ldb & 1) == 0) {   // skinny right-hand sides (16-byte aligned columns)
+    trsm_skinny_kernel<<<np / SK_ROWS, SK_THREADS, 0, s>>>(np / SK_ROWS, nrhs, LinvP, B, ldb, X,
+                                                            ldx, gate, gate_value);
+    GG_LAUNCH_CHECK("trsm_skinny_kernel");
+    return GG_OK;
   }
   CUtensorMap mA, mB;
   const long long nmt = np / BM;

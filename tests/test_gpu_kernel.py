@@ -353,6 +353,32 @@ def test_tma_trsm_bitwise_equals_cpasync_trsm(K):
         assert LinvP.numel() * 8 == _capi.lib().gg_packed_lower_bytes(n)
 
 
+@pytest.mark.parametrize("n", [300, 4100])
+def test_skinny_trsm_bitwise_equal_to_tiled(K, n):
+    """gg_trsm_lower_packed_f64 with <= 16 right-hand sides (the prepare's [X_L | y]) runs the
+    skinny kernel; every column equals, bitwise, the same column whitened by the tiled TMA/DMMA
+    kernel inside a wider call (so a SNP equal to a covariate still gives an exactly singular S)."""
+    import torch
+
+    from paper_1304_2272_b200 import _capi
+    from paper_1304_2272_b200._capi import ptr, stream_handle
+    from paper_1304_2272_b200._device import alloc_cols, upload_cols
+
+    M = make_spd(n, n + 1)
+    _, L, LinvP, Linv = K._potrf_device(M, keep_square_inverse=True)
+    np_ = _capi.pad(n)
+    B = upload_cols(np.random.default_rng(n).standard_normal((n, 40)), ld=np_)
+    wide = alloc_cols(40, np_)
+    assert _capi.lib().gg_trsm_lower_packed_f64(n, 40, ptr(LinvP), ptr(B), np_, ptr(wide), np_,
+                                                stream_handle()) == 0
+    for c0, cnt in ((0, 1), (3, 9), (24, 16)):
+        X = alloc_cols(cnt, np_)
+        assert _capi.lib().gg_trsm_lower_packed_f64(n, cnt, ptr(LinvP), ptr(B[c0:]), np_, ptr(X),
+                                                    np_, stream_handle()) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(X[:, :n], wide[c0:c0 + cnt, :n])
+
+
 def test_cholesky_reads_lower_triangle_and_checks_all_entries(K):
     from paper_1304_2272_b200.errors import NotPositiveDefinite
 

@@ -7,12 +7,13 @@ from paper_1304_2272_b200 import datagen, kernel
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, nargs="+", default=[10000])
+ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 for n in args.n:
     spec = datagen.BaselineSpec(n=n, m=1, p=4)
     Md = datagen.kinship_covariance_device(spec)
     XL, y = datagen.covariates_host(spec)
-    for rep in range(2):
+    for rep in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx = kernel.gls_prepare(Md, XL, y)
