@@ -122,23 +122,37 @@ __device__ __forceinline__ void tile8(double (&acc)[2], const double* X, int ldx
 
 // warp: factor the 32 x 32 lower block held row-per-lane in r (right-looking); returns the
 // failing local column or -1.  The scaling uses 1/sqrt(d) (dpotf2 scales by the reciprocal pivot).
-__device__ __forceinline__ int warp_factor32(double (&r)[LB], int lane) {
+// Column j is broadcast through shared memory (sm: 2 x 32 doubles, 16-byte aligned, alternating
+// by j): one store per lane, then the pivot and the column pairs are broadcast LDS.128 reads --
+// r02 shuffled every column entry (two SHFLs per double, 62 per pivot at j = 0: ~410 cycles per
+// pivot).  Every lane scales the broadcast unscaled entry itself (lc = u_c rs), the same DMUL the
+// owning lane applies to its own entry, so the factor is bitwise that of the shuffle form.
+__device__ __forceinline__ int warp_factor32(double (&r)[LB], int lane, double* sm) {
   int fail = -1;
 #pragma unroll
   for (int j = 0; j < LB; ++j) {
-    double d = __shfl_sync(FULL, r[j], j);
+    double* col = sm + (j & 1) * LB;
+    col[lane] = r[j];                            // unscaled column j
+    __syncwarp();
+    double d = col[j];
     if (fail < 0 && !(d > 0.0)) fail = j;        // uniform: every lane sees the same d
     if (fail >= 0) d = 1.0;                      // keep the arithmetic finite past a failure
     // the scale must be the rounded reciprocal of the stored pivot (dpotf2): rsqrt(d) instead
-    // measured 10x larger GLS errors on AR(1) covariances (rho = 0.999: 5.3e-10 vs 5.1e-11)
-    const double piv = sqrt(d), rs = 1.0 / piv;
+    // measured 10x larger GLS errors on AR(1) covariances (rho = 0.999: 5.3e-10 vs 5.1e-11), and
+    // rsqrt(d) with piv = RN(1/rs) 4x larger (and no faster)
+    const double piv = __dsqrt_rn(d), rs = __drcp_rn(piv);   // = sqrt(d), 1.0 / piv
     if (lane == j) r[j] = piv;
     else if (lane > j) r[j] *= rs;
 #pragma unroll
-    for (int c = 0; c < LB; ++c) {   // constant bounds: fully unrolled, r[] stays in registers
-      if (c > j) {
-        const double lc = __shfl_sync(FULL, r[j], c);
-        if (lane >= c) r[c] -= r[j] * lc;
+    for (int c = 0; c < LB; c += 2) {   // constant bounds: fully unrolled, r[] stays in registers
+      if (c + 1 > j) {
+        const double2 u = *reinterpret_cast<const double2*>(col + c);
+        if (c > j) {
+          const double lc = u.x * rs;
+          if (lane >= c) r[c] -= r[j] * lc;
+        }
+        const double lc1 = u.y * rs;
+        if (lane >= c + 1) r[c + 1] -= r[j] * lc1;
       }
     }
   }
@@ -161,11 +175,21 @@ __device__ __forceinline__ void warp_inverse32(const double* S, int j0, double (
   }
 }
 
+#ifdef GG_LEAF_PROFILE
+__device__ long long g_leaf_ts[64];
+#endif
 template <bool FACTOR>
 __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long long ld,
                                                                double* Dinv, long long ldi, int k0,
                                                                int* info, int panel = 0) {
   extern __shared__ double lsm[];
+#ifdef GG_LEAF_PROFILE   // measurement builds: clock64 at every barrier of the factoring leaf
+  int tsi = 0;
+  if (FACTOR && threadIdx.x == 0) g_leaf_ts[tsi++] = clock64();
+#define LEAF_TS() do { if (FACTOR && threadIdx.x == 0 && tsi < 64) g_leaf_ts[tsi++] = clock64(); } while (0)
+#else
+#define LEAF_TS() do { } while (0)
+#endif
   double* S = lsm;                          // 128 x LDS
   double* W = lsm + NB * LDS;               // 64 x WLD scratch
   int* fail = reinterpret_cast<int*>(W + 64 * WLD);
@@ -180,6 +204,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
   }
   if (tid == 0) *fail = -1;
   __syncthreads();
+  LEAF_TS();
   if (FACTOR) {
     for (int J = 0; J < NB / LB; ++J) {
       const int j0 = J * LB;
@@ -187,7 +212,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
         double r[LB];
 #pragma unroll
         for (int c = 0; c < LB; ++c) r[c] = S[(j0 + lane) * LDS + j0 + c];
-        const int f = warp_factor32(r, lane);
+        const int f = warp_factor32(r, lane, W);   // W: scratch until the inverse phases
+        LEAF_TS();
         if (f >= 0) {
           if (lane == 0) *fail = j0 + f;
         } else {
@@ -197,14 +223,17 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
             Ab[(j0 + lane) + (long long)(j0 + c) * ld] = (lane >= c) ? r[c] : 0.0;
           }
           __syncwarp();
+          LEAF_TS();
           double tc[LB];
           warp_inverse32(S, j0, tc, lane);
           __syncwarp();
+          LEAF_TS();
 #pragma unroll
           for (int i = 0; i < LB; ++i) S[(j0 + i) * LDS + j0 + lane] = tc[i];
         }
       }
       __syncthreads();
+      LEAF_TS();
       if (*fail >= 0) {
         if (tid == 0) *info = k0 + *fail + 1;
         return;
@@ -231,6 +260,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
           for (int e = 0; e < 2; ++e) S[(r0 + g) * LDS + j0 + 8 * nt + 2 * t4 + e] = out[nt][e];
       }
       __syncthreads();
+      LEAF_TS();
       // trailing update of the lower part: S_II' -= L_IJ L_I'J^T (lower 8 x 8 tiles)
       for (int tt = warp; tt < m * (m + 1) / 2; tt += LEAF_WARPS) {
         int rt = 0;
@@ -246,6 +276,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
         }
       }
       __syncthreads();
+      LEAF_TS();
     }
     // the off-diagonal blocks of L (the diagonal blocks went out from warp 0's registers)
     for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
@@ -257,12 +288,14 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
     double tc[LB];
     if (warp < NB / LB) warp_inverse32(S, warp * LB, tc, lane);
     __syncthreads();
+    LEAF_TS();
     if (warp < NB / LB) {
 #pragma unroll
       for (int i = 0; i < LB; ++i) S[(warp * LB + i) * LDS + warp * LB + lane] = tc[i];
     }
   }
   __syncthreads();
+  LEAF_TS();
   // ---- inverse phases (S diagonal blocks = T_J, strictly upper part of S = 0) ----
   // (a) W_b = L_IJ T_J for (I, J) = (1, 0), (3, 2): T_J[k][c] = 0 for k < c
   for (int job = warp; job < 32; job += LEAF_WARPS) {
@@ -275,6 +308,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
     for (int e = 0; e < 2; ++e) W[(b * LB + 8 * rt + g) * WLD + 8 * ct + 2 * t4 + e] = acc[e];
   }
   __syncthreads();
+  LEAF_TS();
   // (b) X_IJ = -T_I W_b (T_I[r][k] = 0 for k > r), over L_IJ
   for (int job = warp; job < 32; job += LEAF_WARPS) {
     const int b = job >> 4, rt = (job >> 2) & 3, ct = job & 3;
@@ -286,6 +320,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
     for (int e = 0; e < 2; ++e) S[(I * LB + 8 * rt + g) * LDS + J * LB + 8 * ct + 2 * t4 + e] = -acc[e];
   }
   __syncthreads();
+  LEAF_TS();
   // (c) W = L[64:, :64] X_A (X_A = S[:64, :64], lower)
   for (int job = warp; job < 64; job += LEAF_WARPS) {
     const int rt = job >> 3, ct = job & 7;
@@ -295,6 +330,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
     for (int e = 0; e < 2; ++e) W[(8 * rt + g) * WLD + 8 * ct + 2 * t4 + e] = acc[e];
   }
   __syncthreads();
+  LEAF_TS();
   // (d) X[64:, :64] = -X_C W (X_C = S[64:, 64:], lower), over L[64:, :64]
   for (int job = warp; job < 64; job += LEAF_WARPS) {
     const int rt = job >> 3, ct = job & 7;
@@ -304,11 +340,15 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
     for (int e = 0; e < 2; ++e) S[(64 + 8 * rt + g) * LDS + 8 * ct + 2 * t4 + e] = -acc[e];
   }
   __syncthreads();
+  LEAF_TS();
   double* Db = Dinv + k0 + (panel ? 0ll : (long long)k0 * ldi);
   for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
     const int r = e % NB, c = e / NB;
     Db[r + (long long)c * ldi] = (r >= c) ? S[r * LDS + c] : 0.0;
   }
+  __syncthreads();
+  LEAF_TS();
+#undef LEAF_TS
 }
 
 
@@ -739,3 +779,10 @@ int trsm_blocked_run(int n, int nrhs, const double* L, int ldl, const double* B,
 }
 
 }  // namespace gg
+
+#ifdef GG_LEAF_PROFILE
+extern "C" int gg_leaf_profile_read(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, gg::g_leaf_ts, sizeof(long long) * (n < 64 ? n : 64)) ==
+                 cudaSuccess ? 0 : 3;
+}
+#endif
