@@ -71,6 +71,7 @@ struct I8Args {
   int* tile_counter;  // zeroed before the launch: clusters take tiles dynamically, heavy first
   int rd_bytes;       // bytes per row-data slot (rd_bytes(q, P != nullptr))
   int grp_pp;         // 256-SNP tile pairs per SNP group (tile_coords)
+  int order;          // tile order inside a group (tile_coords): 0 heavy first, 1 zigzag
   int whatif;         // measurement only (GG_I8_WHATIF bits; results invalid): 1 no genotype
                       // (A) loads, 2 no slice (B) loads, 4 no epilogue work
 };
@@ -123,12 +124,16 @@ __device__ __forceinline__ double pow2(int e) {
 // groups are swept one after the other, and inside a group the row blocks heavy first with a row
 // block's SNP tiles together (grp bounds the genotype working set that L2 has to hold while
 // every row block re-reads it).
+// order 1 (zigzag): inside a group the row blocks alternate heavy / light (the i-th heaviest, then
+// the i-th lightest), so a short tile's epilogue overlaps a long tile's MMAs instead of a run of
+// short, epilogue-bound tiles ending every group.
 __device__ __forceinline__ void tile_coords(int t, int num_rb, int num_nt, int grp, int& rb,
-                                            int& nt) {
+                                            int& nt, int order = 0) {
   const int g = t / (num_rb * grp);
   const int t1 = t - g * num_rb * grp;
   const int w = min(grp, num_nt - g * grp);     // the last group may be narrower
-  rb = num_rb - 1 - t1 / w;
+  const int i = t1 / w;
+  rb = (order == 1) ? ((i & 1) ? (i >> 1) : num_rb - 1 - (i >> 1)) : num_rb - 1 - i;
   nt = g * grp + t1 % w;
 }
 
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (t < 0) break;
         int ru, cu;
-        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu, a.order);
         const int rb0 = QUAD ? ru : 2 * ru;        // the tile's (first) row block
         const int nk = (QUAD ? ru : 2 * ru + 1) / 4 + 1;
         constexpr int NRD = QUAD ? 1 : 2;          // row blocks (row data) per tile
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tile_read(r);
         if (t < 0) break;
         int ru, cu;
-        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+        tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu, a.order);
         const int rb0 = QUAD ? ru : 2 * ru;
         const int nk = (QUAD ? ru : 2 * ru + 1) / 4 + 1;
         for (int kt = 0; kt < nk; ++kt) {
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) tile_read(r);
       if (t < 0) break;
       int ru, cu;
-      tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu);
+      tile_coords(t, num_ru, num_cu, a.grp_pp, ru, cu, a.order);
       const int rb = QUAD ? ru : 2 * ru + group;
       const int nt = QUAD ? 4 * cu + 2 * group + (int)rank : 2 * cu + (int)rank;
       const int col_g = nt * TM + m, row0_g = rb * TR;
@@ -1055,6 +1060,8 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     a.grp_pp = (num_cu + ngroups - 1) / ngroups;                // equal-width groups
     a.whatif = 0;
     if (const char* w = std::getenv("GG_I8_WHATIF")) a.whatif = std::atoi(w);
+    a.order = 0;
+    if (const char* o = std::getenv("GG_I8_ORDER")) a.order = std::atoi(o);   // tuning knob
     a.rd_bytes = rd_bytes(q, P != nullptr);
     // dual: 5 stages of 44 KB when the row data is small (q <= 3), else 4; QUAD: 4 of 46 KB
     const bool five = !quad && d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
