@@ -341,6 +341,16 @@ size_t gg_dist_potrf_workspace_bytes(int n, int nb, const gg_dist_comms* c);
 int gg_dist_potrf_f64(int n, int nb, double* A, long long lda, double* B, long long ldb,
                       const gg_dist_comms* c, void* work, size_t work_bytes, int* info,
                       void* stream);
+/* Distributed TRSM X = L^-1 X (replaces dist_trsolve, distgrid.py:291-314) for L in the
+ * block-cyclic share of gg_dist_potrf_f64 and a REPLICATED right-hand side X (padded n x nrhs,
+ * ldx >= nblk * nb, rows >= n zero; overwritten with the solution on every rank): blocked
+ * forward substitution -- process row K%r forms its partial product of the solved blocks
+ * (SUM all-reduce along the process row), the diagonal owner applies its block's inverse
+ * (gg_trtri_lower_f64's path) and broadcasts X_K over the world.  Backward-stable.        */
+size_t gg_dist_trsm_workspace_bytes(int n, int nb, int nrhs, const gg_dist_comms* c);
+int gg_dist_trsm_f64(int n, int nb, int nrhs, const double* L, long long lda, double* X,
+                     long long ldx, const gg_dist_comms* c, void* work, size_t work_bytes,
+                     void* stream);
 
 #ifdef __cplusplus
 }

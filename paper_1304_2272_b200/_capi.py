@@ -80,6 +80,8 @@ SIGNATURES = {
     "gg_dist_local_dims": (_i, [_i, _i, _vp, _ip, _ip]),
     "gg_dist_potrf_workspace_bytes": (_sz, [_i, _i, _vp]),
     "gg_dist_potrf_f64": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp, _sz, _ip, _vp]),
+    "gg_dist_trsm_workspace_bytes": (_sz, [_i, _i, _i, _vp]),
+    "gg_dist_trsm_f64": (_i, [_i, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp, _sz, _vp]),
 }
 # callback types of gg_dist_comms_callbacks (group 0 world, 1 process row, 2 process column)
 DIST_BCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_int)

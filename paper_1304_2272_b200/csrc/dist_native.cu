@@ -332,6 +332,88 @@ int dist_potrf_run(int n, int nb, double* A, long long lda, double* B, long long
   return GG_OK;
 }
 
+__global__ void sub_block_kernel(int rows, int cols, const double* __restrict__ X, long long ldx,
+                                 const double* __restrict__ P, long long ldp,
+                                 double* __restrict__ R) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % rows, j = e / rows;
+    R[e] = X[i + j * ldx] - P[i + j * ldp];
+  }
+}
+
+struct TrsmWork {   // carve of the caller's workspace for dist_trsm_run
+  double *Xg, *part, *rhs, *xk, *Lkk, *Dinv;
+  void* tws;
+  size_t tws_bytes, total;
+  TrsmWork(const DistShape& d, int k, char* base) {
+    const size_t nb = d.nb, kk = k > 0 ? k : 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += al256(bytes); return p; };
+    Xg = reinterpret_cast<double*>(take((size_t)d.n_loc * kk * 8 + 8));
+    part = reinterpret_cast<double*>(take(nb * kk * 8));
+    rhs = reinterpret_cast<double*>(take(nb * kk * 8));
+    xk = reinterpret_cast<double*>(take(nb * kk * 8));
+    Lkk = reinterpret_cast<double*>(take(nb * nb * 8));
+    Dinv = reinterpret_cast<double*>(take(nb * nb * 8));
+    tws_bytes = trtri_ws_bytes(d.nb);
+    tws = take(tws_bytes);
+    total = off;
+  }
+};
+
+// X = L^-1 X for a block-cyclic lower-triangular L and a replicated right-hand side X (n_pad x k,
+// ld ldx): blocked forward substitution over the block rows K,
+//   X_K = L_KK^-1 (X_K - sum_{J<K} L_KJ X_J),
+// process row K%r forms the partial product of its column blocks J < K (the rows X_J it needs are
+// kept gathered in Xg as they are solved), one SUM all-reduce along the process row, the owner of
+// (K, K) applies its diagonal block's inverse and broadcasts X_K over the world.
+int dist_trsm_run(int n, int nb, int k, const double* L, long long lda, double* X, long long ldx,
+                  const gg_dist_comms* cm, void* work, size_t work_bytes, cudaStream_t s) {
+  const DistShape d(n, nb, cm);
+  TrsmWork w(d, k, static_cast<char*>(work));
+  if (work_bytes < w.total) {
+    set_error("dist_trsm: workspace too small");
+    return GG_EARG;
+  }
+  if (ldx < (long long)d.nblk * nb || (d.m_loc && lda < d.m_loc)) {
+    set_error("dist_trsm: leading dimension too small (ldx >= padded n, lda >= m_loc)");
+    return GG_EDIM;
+  }
+  if (k <= 0) return GG_OK;
+  int ng = 0;   // local column blocks J solved so far (gathered in Xg, ld n_loc)
+  for (int K = 0; K < d.nblk; ++K) {
+    const int orow = K % d.r, ocol = K % d.c, owner = orow * d.c + ocol;
+    double* XK = X + (long long)K * nb;
+    if (d.pr == orow) {
+      if (ng > 0)
+        GG_TRY(local_gemm(nb, k, ng * nb, 1.0, L + d.lrow(K), lda, w.Xg, d.n_loc, false, 0.0,
+                          w.part, nb, nullptr, 0, s));
+      else
+        GG_CUDA_TRY(cudaMemsetAsync(w.part, 0, (size_t)nb * k * 8, s));
+      GG_TRY(coll_sum(cm, G_ROW, w.part, (size_t)nb * k, s));
+      if (cm->rank == owner) {
+        GG_CUDA_TRY(cudaMemcpy2DAsync(w.Lkk, (size_t)nb * 8, L + d.lrow(K) + d.lcol(K) * lda,
+                                      lda * 8, (size_t)nb * 8, nb, cudaMemcpyDeviceToDevice, s));
+        GG_TRY(trtri_run(nb, w.Lkk, nb, w.Dinv, nb, w.tws, s));
+        sub_block_kernel<<<64, 256, 0, s>>>(nb, k, XK, ldx, w.part, nb, w.rhs);
+        GG_LAUNCH_CHECK("sub_block_kernel");
+        GG_TRY(local_gemm(nb, k, nb, 1.0, w.Dinv, nb, w.rhs, nb, false, 0.0, w.xk, nb, nullptr, 0,
+                          s));
+      }
+    }
+    GG_TRY(coll_bcast(cm, G_WORLD, w.xk, (size_t)nb * k * 8, owner, s));
+    GG_CUDA_TRY(cudaMemcpy2DAsync(XK, ldx * 8, w.xk, (size_t)nb * 8, (size_t)nb * 8, k,
+                                  cudaMemcpyDeviceToDevice, s));
+    if (K % d.c == d.pc) {   // one of this rank's column blocks: keep its rows for later products
+      GG_CUDA_TRY(cudaMemcpy2DAsync(w.Xg + (long long)ng * nb, (size_t)d.n_loc * 8, w.xk,
+                                    (size_t)nb * 8, (size_t)nb * 8, k, cudaMemcpyDeviceToDevice, s));
+      ++ng;
+    }
+  }
+  return GG_OK;
+}
+
 }  // namespace
 }  // namespace gg
 
@@ -459,6 +541,30 @@ int gg_dist_potrf_f64(int n, int nb, double* A, long long lda, double* B, long l
   *info = -1;
   return gg::dist_potrf_run(n, nb, A, lda, B, ldb, c, work, work_bytes, info,
                             static_cast<cudaStream_t>(stream));
+}
+
+size_t gg_dist_trsm_workspace_bytes(int n, int nb, int nrhs, const gg_dist_comms* c) {
+  if (c == nullptr || n < 1 || nb < 1) return 0;
+  const gg::DistShape d(n, nb, c);
+  return gg::TrsmWork(d, nrhs, nullptr).total;
+}
+
+int gg_dist_trsm_f64(int n, int nb, int nrhs, const double* L, long long lda, double* X,
+                     long long ldx, const gg_dist_comms* c, void* work, size_t work_bytes,
+                     void* stream) {
+  GG_NVTX("gg_dist_trsm_f64");
+  if (c == nullptr || X == nullptr || work == nullptr || n < 1 || nrhs < 0 || nb < GG_TILE ||
+      nb % GG_TILE != 0) {
+    gg::set_error("dist_trsm: null pointer, bad size, or nb not a positive multiple of 128");
+    return GG_EARG;
+  }
+  const gg::DistShape d(n, nb, c);
+  if (L == nullptr && (long long)d.m_loc * d.n_loc > 0) {
+    gg::set_error("dist_trsm: null local share");
+    return GG_EARG;
+  }
+  return gg::dist_trsm_run(n, nb, nrhs, L, lda, X, ldx, c, work, work_bytes,
+                           static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

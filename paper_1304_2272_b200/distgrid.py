@@ -443,6 +443,32 @@ def native_potrf_inv(A, B, layout, comm=None):
     return A, B
 
 
+def native_trsolve(L, layout, RHS, comm=None):
+    """dist_trsolve_bc through the C-ABI gg_dist_trsm_f64 (csrc/dist_native.cu)."""
+    import torch
+
+    from . import _capi
+
+    RHS = np.asarray(RHS, dtype=np.float64)
+    n, k = RHS.shape
+    full = np.zeros((layout.n_pad, k))
+    full[:n] = RHS
+    X = torch.from_numpy(np.ascontiguousarray(full.T)).to(_capi.device())   # (k, n_pad)
+    nc = NativeComms.get(comm, layout.grid)
+    lib = _capi.lib()
+    ws = torch.empty(max(1, int(lib.gg_dist_trsm_workspace_bytes(layout.n, layout.nb, k,
+                                                                 nc.handle))),
+                     dtype=torch.uint8, device=X.device)
+    rc = lib.gg_dist_trsm_f64(layout.n, layout.nb, k, _capi.ptr(L), max(1, layout.m_loc),
+                              _capi.ptr(X), layout.n_pad, nc.handle, _capi.ptr(ws), ws.numel(),
+                              _capi.stream_handle())
+    if nc.error is not None:
+        err, nc.error = nc.error, None
+        raise err
+    _capi.check(rc, "gg_dist_trsm_f64")
+    return X.cpu().numpy().T[:n]
+
+
 def assemble_packed_inverse(B, layout, ops, comm=None):
     """Replicate the packed tile-major inverse on every rank from the block-cyclic shares."""
     P = ops.pack_blockcyclic(B, layout)
@@ -492,15 +518,20 @@ def whiten_blockcyclic(B, layout, ops, RHS, comm=None):
     return Y[:, :np_].contiguous() if np_ != layout.n_pad else Y
 
 
-def dist_trsolve_bc(L, layout, ops, RHS, comm=None):
+def dist_trsolve_bc(L, layout, ops, RHS, comm=None, native=None):
     """Distributed TRSM X = L^-1 RHS for a block-cyclic lower-triangular L and a replicated host
     right-hand side (n x k): blocked forward substitution over the block rows K --
         X_K = L_KK^-1 (RHS_K - sum_{J<K} L_KJ X_J)
     -- each rank of process row K%r forms the partial product of its column blocks J < K, one
     all-reduce along that process row sums them, the owner of (K, K) applies the inverse of the
     diagonal block (gg_trtri_lower_f64) and broadcasts X_K.  Backward-stable blocked substitution
-    (diagonal-block inverses only); returns the replicated X as a host (n x k) array."""
+    (diagonal-block inverses only); returns the replicated X as a host (n x k) array.  With the
+    device ops the loop runs natively (gg_dist_trsm_f64; GG_DIST_NATIVE=0 keeps this driver)."""
     comm = as_comm(comm)
+    if native is None:
+        native = isinstance(ops, DeviceOps) and os.environ.get("GG_DIST_NATIVE", "1") != "0"
+    if native:
+        return native_trsolve(L, layout, RHS, comm)
     nb, g = layout.nb, layout.grid
     n, k = RHS.shape
     gcm = GridComm(comm, g) if comm is not None and comm.size > 1 else None
