@@ -114,6 +114,27 @@ def test_ozaki_triangular_operands(gpu):
     assert float(np.max(np.abs(got + Al @ T))) <= 1e-12 * 700
 
 
+def test_ozaki_triangle_flags_ignore_memory_outside_the_triangle(gpu):
+    """flags 1 / 2 declare A~ lower (A~(i,k) = 0 for k > i) and B~(j,k) = 0 for k < j: whatever
+    memory holds there is sliced as zeros (the clustered kernel runs each cluster over the union
+    of its tiles' k ranges), so garbage outside the triangle changes nothing."""
+    rng = np.random.default_rng(13)
+    n = 1100
+    A = rng.standard_normal((640, n))
+    Bt = rng.standard_normal((n, 520))
+    Bl = np.tril(Bt)
+    Bg = Bl + np.triu(rng.standard_normal((n, 520)), 1) * 1e6       # garbage above the diagonal
+    got = _ozaki(A, Bg.T.copy(), np.zeros((640, 520)), 1.0, 0.0, 2, b_rowmajor=True)
+    ref = _ozaki(A, Bl.T.copy(), np.zeros((640, 520)), 1.0, 0.0, 2, b_rowmajor=True)
+    assert np.array_equal(got, ref)
+    Al = np.tril(rng.standard_normal((700, 700)))
+    Ag = Al + np.triu(rng.standard_normal((700, 700)), 1) * 1e6
+    T = rng.standard_normal((700, 300))
+    got = _ozaki(Ag, T.T.copy(), np.zeros((700, 300)), -1.0, 0.0, 1, b_rowmajor=True)
+    ref = _ozaki(Al, T.T.copy(), np.zeros((700, 300)), -1.0, 0.0, 1, b_rowmajor=True)
+    assert np.array_equal(got, ref)
+
+
 def _factor(M, ozaki, monkeypatch):
     from paper_1304_2272_b200 import kernel
 
