@@ -509,6 +509,9 @@ def run_ours(args):
                   f"{'FP64' if sw.resident == 'f64' else 'int8'}); no flush needed",
             "t_prepare_s": round(sw.t_prepare, 4),
             "prepare_device_ms": round(sw.prepare_ms_device, 2),
+            # SNPs/s end to end including the one-time prepare (one sweep + prepare)
+            "snps_per_s_including_prepare": round(
+                m * world / (elapsed_ms / 1e3 / args.steps + sw.t_prepare), 1),
             "t_generate_M_s": round(sw.t_gen_m, 2),
             "step_fp64_tflops": round(float(n) * n * m * args.steps / (elapsed_ms / 1e3) / 1e12,
                                       3),
