@@ -13,7 +13,8 @@ import threading
 from .errors import DeviceError, DimensionMismatch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgwasgls_b200.so")
+# GG_LIB_PATH: load another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("GG_LIB_PATH") or os.path.join(HERE, "libgwasgls_b200.so")
 
 GG_OK, GG_ENOTPD, GG_EDIM, GG_ECUDA, GG_ENCCL, GG_EARG = 0, 1, 2, 3, 4, 5
 GG_TILE = 128

@@ -14,11 +14,12 @@
 // FP64 rounding.  The epilogue forms the exact int64 halves hi = D_0..D_3, lo = D_4..D_7 (base
 // 2^7) and rounds once: r = 2^E fma(hi, 2^-35, lo 2^-63); then C = beta C + alpha r.
 //
-// Kernel (persistent, one CTA per SM in clusters of 2, 10 warps): warp 0 TMA producer (per 32-k
+// Kernel (persistent, one CTA per SM in clusters of 2, 10 warps): warp 0 TMA producer (per 64-k
 // stage: the 8 slices of a 128-row A tile -- half of them loaded here and multicast to the
-// cluster peer, which computes the neighbouring 64 columns -- and of a 64-row B tile, 48 KB,
-// SWIZZLE_32B, 4-stage ring), warp 1 MMA issuer (one lane, M = 128 x N = 64..256 x K = 32, 12 MMAs
-// covering the 36 slice products per stage), warps 2-9 epilogue (TMEM lane = tile row, two warps
+// cluster peer, which computes the neighbouring 64 columns -- and of a 64-row B tile, 96 KB,
+// SWIZZLE_64B, 2-stage ring; r02: 64-byte rows halve the L2 requests of the 32-byte-row 4-stage
+// form, whose operand stream was the limiter), warp 1 MMA issuer (one lane, M = 128 x N = 64..256
+// x K = 32, 2 x 12 MMAs covering the 36 slice products per stage), warps 2-9 epilogue (TMEM lane = tile row, two warps
 // per lane quarter, 32 columns each; release TMEM once the tile is in registers, then update C).
 // Operand entries outside a triangular operand's triangle are sliced as zeros.
 // Results are bitwise deterministic (exact integer accumulation, fixed rounding).
@@ -40,8 +41,13 @@ namespace {
 constexpr int OZ_S = 8;                    // slices per operand
 constexpr int OZ_BM = 128;                 // tile rows (MMA M)
 constexpr int OZ_BN = 64;                  // tile columns (MMA N, one accumulator per diagonal)
-constexpr int OZ_KC = 32;                  // k per stage (one int8 MMA K, a 32-byte swizzle row)
-constexpr int OZ_STAGES = 4;
+#ifndef OZ_KC_BYTES
+#define OZ_KC_BYTES 64   // measured r02: 64-byte rows 9% faster over the n = 4e4 prepare than 32
+#endif
+constexpr int OZ_KC = OZ_KC_BYTES;         // k per stage: 32 (one MMA K, 32-byte swizzled rows) or
+                                           // 64 (two MMA K steps, 64-byte swizzled rows)
+constexpr int OZ_STAGES = OZ_KC == 32 ? 4 : 2;
+static_assert(OZ_KC == 32 || OZ_KC == 64, "k per stage");
 constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_KC;   // 32 KB
 constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_KC;   // 16 KB
 constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
@@ -101,6 +107,9 @@ __device__ __forceinline__ void fence_before() {
 // K-major, 32-byte-swizzled descriptor: rows of 32 B, 8-row groups 256 B apart (SBO), version 1,
 // layout SWIZZLE_32B (6)
 __device__ __forceinline__ unsigned long long desc32(unsigned saddr) {
+  if (OZ_KC == 64)   // rows of 64 B, 8-row groups 512 B apart, layout SWIZZLE_64B (4)
+    return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (32ull << 32) |
+           (1ull << 46) | (4ull << 61);
   return (unsigned long long)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (16ull << 32) |
          (1ull << 46) | (6ull << 61);
 }
@@ -345,16 +354,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           // each A slice from shared memory once or twice rather than 8 - s times.  s = 0 opens
           // every diagonal.
 #pragma unroll
-          for (int s = 0; s < OZ_S; ++s) {
-            const unsigned long long da = desc32(sA + s * (OZ_BM * OZ_KC));
-            // 8 - s products in one or two MMAs, split evenly (N = 64 runs at 62% of the int8
-            // rate on this B200 -- shared-memory bound -- N = 128..256 at 94-100%, tools/i8_peak)
-            const int cnt = OZ_S - s;
-            const int first = cnt > 4 ? (cnt + 1) / 2 : cnt;
-            mma_i8(tmem_base + s * OZ_BN, da, desc32(sB), first, (k > kb || s > 0) ? 1u : 0u);
-            if (cnt > first)
-              mma_i8(tmem_base + (s + first) * OZ_BN, da, desc32(sB + first * (OZ_BN * OZ_KC)),
-                     cnt - first, (k > kb || s > 0) ? 1u : 0u);
+          for (int kk = 0; kk < OZ_KC / 32; ++kk) {   // MMA K steps of 32 bytes in the stage
+#pragma unroll
+            for (int s = 0; s < OZ_S; ++s) {
+              const unsigned long long da = desc32(sA + s * (OZ_BM * OZ_KC)) + 2 * kk;
+              // 8 - s products in one or two MMAs, split evenly (N = 64 runs at 62% of the int8
+              // rate on this B200 -- shared-memory bound -- N = 128..256 at 94-100%, tools/i8_peak)
+              const int cnt = OZ_S - s;
+              const int first = cnt > 4 ? (cnt + 1) / 2 : cnt;
+              const unsigned acc = (k > kb || kk > 0 || s > 0) ? 1u : 0u;
+              mma_i8(tmem_base + s * OZ_BN, da, desc32(sB) + 2 * kk, first, acc);
+              if (cnt > first)
+                mma_i8(tmem_base + (s + first) * OZ_BN, da,
+                       desc32(sB + first * (OZ_BN * OZ_KC)) + 2 * kk, cnt - first, acc);
+            }
           }
           mma_commit_mc(empty0 + 8 * stage, mask_a | mask_b);
           if (++stage == OZ_STAGES) {
@@ -597,7 +610,8 @@ int encode_slices(CUtensorMap* map, const signed char* Sl, int R, int K, long lo
   cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_S / 2};   // half the slices (multicast)
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(Sl), dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  OZ_KC == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
                   promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled (ozaki slices) failed (code " + std::to_string((int)r) + ")");

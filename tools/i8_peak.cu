@@ -13,7 +13,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 
 // usage: tools/i8_peak [N ...]  (MMA N per instruction, default 256: tests N granularity)
-__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int N, int* sink) {
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int N, int* sink, int sw32) {
   const unsigned IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (((unsigned)N >> 3) << 17) | ((128u >> 4) << 24);
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ unsigned long long bar;
@@ -35,13 +35,18 @@ __global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters, int N, int* 
   const unsigned tmem = tslot;
   if (threadIdx.x == 0) {
     const unsigned sa = smem_u32(smem);
-    unsigned long long da = (unsigned long long)((sa >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+    // sw32 (env GG_PEAK_SW32=1 on the host -> arg): the Ozaki GEMM's SWIZZLE_32B K-major operands
+    // (32-byte rows, 8-row groups 256 B apart), the same descriptor for every k step
+    unsigned long long da = sw32
+        ? (unsigned long long)((sa >> 4) & 0x3FFF) | (1ull << 16) | (16ull << 32) | (1ull << 46) | (6ull << 61)
+        : (unsigned long long)((sa >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
     unsigned long long db = da + ((16 * 1024) >> 4);
+    const int kstep = sw32 ? 0 : 2;
     unsigned phase = 0;
     for (int it = 0; it < iters; ++it) {
       for (int j = 0; j < 64; ++j) {
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-                     ::"r"(tmem), "l"(da + 2 * (j & 3)), "l"(db + 2 * (j & 3)), "r"(IDESC), "r"(1));
+                     ::"r"(tmem), "l"(da + kstep * (j & 3)), "l"(db + kstep * (j & 3)), "r"(IDESC), "r"(1));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar)));
       asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W;\n}\n" ::"r"(smem_u32(&bar)), "r"(phase));
@@ -68,12 +73,14 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  const int sw32 = getenv("GG_PEAK_SW32") != nullptr;
+  if (sw32) printf("# SWIZZLE_32B operands (the Ozaki GEMM's layout)\n");
   for (int a = 0; a < (argc > 1 ? argc - 1 : 1); ++a) {
     const int N = argc > 1 ? atoi(argv[a + 1]) : 256;
     for (int rep = 0; rep < 3; ++rep) {
       const int iters = rep == 0 ? 10 : 2000;
       cudaEventRecord(e0);
-      i8_peak_kernel<<<prop.multiProcessorCount, 128, smem>>>(iters, N, sink);
+      i8_peak_kernel<<<prop.multiProcessorCount, 128, smem>>>(iters, N, sink, sw32);
       cudaEventRecord(e1);
       CK(cudaEventSynchronize(e1));
       CK(cudaGetLastError());
