@@ -21,7 +21,10 @@ namespace gg {
 namespace {
 
 constexpr int NB = 128;
-constexpr int OUTER = 8 * NB;   // outer block width of the two-level Cholesky
+#ifndef GG_OUTER
+#define GG_OUTER (8 * 128)
+#endif
+constexpr int OUTER = GG_OUTER;   // outer block width of the two-level Cholesky
 constexpr bool OZAKI_DEFAULT = true;
 constexpr int LEAF_THREADS = 384;
 
