@@ -72,6 +72,7 @@ struct I8Args {
   int rd_bytes;       // bytes per row-data slot (rd_bytes(q, P != nullptr))
   int grp_pp;         // 256-SNP tile pairs per SNP group (tile_coords)
   int order;          // tile order inside a group (tile_coords): 0 heavy first, 1 zigzag
+  int quad_interleave;  // QUAD tiles: B-stationary MMA order (both A tiles per slice k-chunk)
   int whatif;         // measurement only (GG_I8_WHATIF bits; results invalid): 1 no genotype
                       // (A) loads, 2 no slice (B) loads, 4 no epilogue work
 };
@@ -460,6 +461,26 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full0 + 8 * stage, phase);
           fence_after();
           const unsigned sa = sbase + stage * STAGE;
+          if (QUAD && a.quad_interleave) {
+            // QUAD, B-stationary order: both genotype tiles against the same slice k-chunk back
+            // to back, so the multipliers' B inputs (the random slice digits, where the int8
+            // datapath's power goes) change every second MMA instead of every MMA
+            if (kt == 0) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) mbar_wait(acce0 + 8 * h, (r & 1) ^ 1);
+              fence_after();
+            }
+            const unsigned long long db = smem_desc(sa + A_ST);
+            const int kk_end = (kt == nk - 1) ? (rb0 & 3) + 1 : TK / 32;
+#pragma unroll
+            for (int kk = 0; kk < TK / 32; ++kk)
+              if (kk < kk_end) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  mma_i8_pair(tmem_base + h * ACC_COLS, smem_desc(sa + h * A_BYTES) + 2 * kk,
+                              db + 2 * kk, (kt > 0 || kk > 0) ? 1u : 0u);
+              }
+          } else {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (kt == 0) {   // this half's accumulator drained by the previous tile's group h
@@ -477,6 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               if (kk < kk_end)
                 mma_i8_pair(tmem_base + h * ACC_COLS, da + 2 * kk, db + 2 * kk,
                             (kt > 0 || kk > 0) ? 1u : 0u);
+          }
           }
           mma_commit_pair(empty0 + 8 * stage);
           if (++stage == P_STAGES) {
@@ -1062,6 +1084,8 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     if (const char* w = std::getenv("GG_I8_WHATIF")) a.whatif = std::atoi(w);
     a.order = 0;
     if (const char* o = std::getenv("GG_I8_ORDER")) a.order = std::atoi(o);   // tuning knob
+    a.quad_interleave = 1;
+    if (const char* qi = std::getenv("GG_I8_QUAD_ILV")) a.quad_interleave = std::atoi(qi);
     a.rd_bytes = rd_bytes(q, P != nullptr);
     // dual: 5 stages of 44 KB when the row data is small (q <= 3), else 4; QUAD: 4 of 46 KB
     const bool five = !quad && d_smem_bytes(5, a.rd_bytes) <= (size_t)smem_optin();
