@@ -18,18 +18,21 @@
 namespace gg {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, NTHREADS = 256;
-constexpr int AS_LD = BM + 4;    // As[k][m]  (m contiguous), +4 doubles: conflict-free A fragments
-constexpr int BSN_LD = BK + 4;   // Bs[n][k]  (k contiguous) for op(B) = B
-constexpr int BST_LD = BN + 4;   // Bs[k][n]  (n contiguous) for op(B) = B^T
-constexpr int A_STAGE = BK * AS_LD;
-constexpr int B_STAGE_N = BN * BSN_LD;
-constexpr int B_STAGE_T = BK * BST_LD;
+// Tile shapes: the big tile (128 x 128, 8 warps of 64 x 32) and, for problems that do not fill
+// the GPU with big tiles (the factorisation's panel and next-column updates: a 128-column strip
+// of up to ~300 row tiles, on the critical path), a small one (64 x 64, 4 warps of 32 x 32:
+// 4x the CTAs, up to 6 resident per SM).
+struct BigTile { static constexpr int BM = 128, BN = 128, WM = 2, WN = 4, FM = 8, FN = 4; };
+struct SmallTile { static constexpr int BM = 64, BN = 64, WM = 2, WN = 2, FM = 4, FN = 4; };
+constexpr int BK = 16, STAGES = 4;
 
-template <bool BT>
-__host__ __device__ constexpr int b_stage() { return BT ? B_STAGE_T : B_STAGE_N; }
-template <bool BT>
-constexpr size_t smem_bytes() { return size_t(STAGES) * (A_STAGE + b_stage<BT>()) * sizeof(double); }
+template <class T> constexpr int nthreads() { return T::WM * T::WN * 32; }
+template <class T> constexpr int as_ld() { return T::BM + 4; }   // As[k][m], +4: conflict-free
+template <class T, bool BT> constexpr int bs_ld() { return BT ? T::BN + 4 : BK + 4; }
+template <class T> constexpr int a_stage() { return BK * as_ld<T>(); }
+template <class T, bool BT> constexpr int b_stage() { return BT ? BK * bs_ld<T, BT>() : T::BN * bs_ld<T, BT>(); }
+template <class T, bool BT>
+constexpr size_t smem_bytes() { return size_t(STAGES) * (a_stage<T>() + b_stage<T, BT>()) * sizeof(double); }
 
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -51,8 +54,12 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <bool BT>
-__global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
+template <class T, bool BT>
+__global__ void __launch_bounds__(nthreads<T>()) dgemm_dmma_kernel(GemmArgs a) {
+  constexpr int BM = T::BM, BN = T::BN, NT = nthreads<T>();
+  constexpr int FM = T::FM, FN = T::FN;            // DMMA fragments per warp (rows, columns)
+  constexpr int AS_LD = as_ld<T>(), BS_LD = bs_ld<T, BT>();
+  constexpr int A_STAGE = a_stage<T>(), B_STAGE = b_stage<T, BT>();
   if (a.abort_flag != nullptr && *a.abort_flag != 0) return;
   if (blockIdx.y) {   // strided batch
     a.A += blockIdx.y * a.sA;
@@ -76,8 +83,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
     mt = bid % num_mt;
     nt = bid / num_mt;
   }
-  if ((a.flags & GEMM_C_LOWER) && nt > mt) return;
   const int m0 = mt * BM, n0 = nt * BN;
+  if ((a.flags & GEMM_C_LOWER) && n0 >= m0 + BM) return;   // strictly above the diagonal
   int k_begin = 0, k_end = a.K;
   if (a.flags & GEMM_A_LOWER) k_end = min(a.K, m0 + BM);
   if (a.flags & GEMM_B_LOWER) k_begin = min(a.K, n0);
@@ -85,43 +92,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / T::WN, wn = warp % T::WN;
 
-  double acc[8][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = k_begin + kt * BK;
     double* as = As + stage * A_STAGE;
-    double* bs = Bs + stage * b_stage<BT>();
+    double* bs = Bs + stage * B_STAGE;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int c = tid + r * NTHREADS;
-      const int kc = c >> 6, mc = c & 63;
+    for (int c = tid; c < BK * BM / 2; c += NT) {   // 16-byte chunks of A (m contiguous)
+      const int kc = c / (BM / 2), mc = c % (BM / 2);
       cp_async16(as + kc * AS_LD + mc * 2, a.A + (long long)(k0 + kc) * a.lda + m0 + mc * 2, true);
     }
     if (BT) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int c = tid + r * NTHREADS;
-        const int kr = c >> 6, nc = c & 63;
+      for (int c = tid; c < BK * BN / 2; c += NT) {
+        const int kr = c / (BN / 2), nc = c % (BN / 2);
         const int col = n0 + nc * 2;
         const bool pred = col < a.N;
         const double* src = a.B + (long long)(k0 + kr) * a.ldb + (pred ? col : 0);
-        cp_async16(bs + kr * BST_LD + nc * 2, src, pred);
+        cp_async16(bs + kr * BS_LD + nc * 2, src, pred);
       }
     } else {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int c = tid + r * NTHREADS;
-        const int nc = c >> 3, kch = c & 7;
+      for (int c = tid; c < BN * BK / 2; c += NT) {
+        const int nc = c / (BK / 2), kch = c % (BK / 2);
         const int col = n0 + nc;
         const bool pred = col < a.N;
         const double* src = a.B + (long long)(pred ? col : 0) * a.ldb + k0 + kch * 2;
-        cp_async16(bs + nc * BSN_LD + kch * 2, src, pred);
+        cp_async16(bs + nc * BS_LD + kch * 2, src, pred);
       }
     }
   };
@@ -139,35 +143,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
     if (pf < nk) load_stage(pf % STAGES, pf);
     cp_async_commit();
 
-    const double* as = As + (kt % STAGES) * A_STAGE + wm * 64 + g;
-    const double* bs = Bs + (kt % STAGES) * b_stage<BT>();
+    const double* as = As + (kt % STAGES) * A_STAGE + wm * (8 * FM) + g;
+    const double* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[8], bf[4];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = as[(kk + t) * AS_LD + i * 8];
+      for (int i = 0; i < FM; ++i) af[i] = as[(kk + t) * AS_LD + i * 8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        bf[j] = BT ? bs[(kk + t) * BST_LD + wn * 32 + j * 8 + g]
-                   : bs[(wn * 32 + j * 8 + g) * BSN_LD + kk + t];
+      for (int j = 0; j < FN; ++j) {
+        bf[j] = BT ? bs[(kk + t) * BS_LD + wn * (8 * FN) + j * 8 + g]
+                   : bs[(wn * (8 * FN) + j * 8 + g) * BS_LD + kk + t];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
 
   const double alpha = a.alpha, beta = a.beta;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = m0 + wm * 64 + i * 8 + g;
+  for (int i = 0; i < FM; ++i) {
+    const int row = m0 + wm * (8 * FM) + i * 8 + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < FN; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * t + e;
+        const int col = n0 + wn * (8 * FN) + j * 8 + 2 * t + e;
         if (col < a.N) {
           double* cp = a.C + (long long)col * a.ldc + row;
           const double v = acc[i][j][e];
@@ -178,10 +182,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) dgemm_dmma_kernel(GemmArgs a) {
   }
 }
 
+template <class T, bool BT>
+int launch_tiles(const GemmArgs& a, cudaStream_t s) {
+  const long long tiles = (long long)(a.M / T::BM) * ((a.N + T::BN - 1) / T::BN);
+  if (tiles > 0x7fffffffLL || a.batch > 65535) {
+    set_error("dgemm: too many tiles");
+    return GG_EDIM;
+  }
+  const dim3 grid((unsigned)tiles, a.batch > 1 ? (unsigned)a.batch : 1u);
+  GG_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<T, BT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_bytes<T, BT>()));
+  dgemm_dmma_kernel<T, BT><<<grid, nthreads<T>(), smem_bytes<T, BT>(), s>>>(a);
+  GG_LAUNCH_CHECK("dgemm_dmma_kernel launch");
+  return GG_OK;
+}
+
 }  // namespace
 
 int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s) {
-  if (a.M < 0 || a.N < 0 || a.K < 0 || a.M % BM != 0 || a.K % BK != 0) {
+  if (a.M < 0 || a.N < 0 || a.K < 0 || a.M % BigTile::BM != 0 || a.K % BK != 0) {
     set_error("dgemm: M must be a multiple of 128 and K a multiple of 16");
     return GG_EDIM;
   }
@@ -198,25 +218,12 @@ int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s) {
     set_error("dgemm: leading dimension too small");
     return GG_EDIM;
   }
-  const long long tiles = (long long)(a.M / BM) * ((a.N + BN - 1) / BN);
-  if (tiles > 0x7fffffffLL || a.batch > 65535) {
-    set_error("dgemm: too many tiles");
-    return GG_EDIM;
-  }
-  const dim3 grid((unsigned)tiles, a.batch > 1 ? (unsigned)a.batch : 1u);
-  if (trans_b) {
-    GG_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_bytes<true>()));
-    dgemm_dmma_kernel<true><<<grid, NTHREADS, smem_bytes<true>(), s>>>(a);
-  } else {
-    GG_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_bytes<false>()));
-    dgemm_dmma_kernel<false><<<grid, NTHREADS, smem_bytes<false>(), s>>>(a);
-  }
-  GG_LAUNCH_CHECK("dgemm_dmma_kernel launch");
-  return GG_OK;
+  // fewer big tiles than SMs (x batch): the small tile keeps the GPU busy
+  const long long big = (long long)(a.M / BigTile::BM) * ((a.N + BigTile::BN - 1) / BigTile::BN) *
+                        (a.batch > 1 ? a.batch : 1);
+  const bool small = big < 148 && !(trans_b && a.N % 2 != 0);
+  if (small) return trans_b ? launch_tiles<SmallTile, true>(a, s) : launch_tiles<SmallTile, false>(a, s);
+  return trans_b ? launch_tiles<BigTile, true>(a, s) : launch_tiles<BigTile, false>(a, s);
 }
 
 }  // namespace gg
