@@ -13,6 +13,8 @@
 // cp.async pipeline (149 KB smem, 1 CTA / SM).  Every output element is accumulated in the
 // same k order regardless of its tile position, so per-column results are bitwise independent
 // of the column's position in the block (tests/test_kernel.py:228-241 in the reference).
+#include <cstdlib>
+
 #include "gg_internal.cuh"
 
 namespace gg {
@@ -221,7 +223,13 @@ int launch_dgemm(const GemmArgs& a, bool trans_b, cudaStream_t s) {
   // fewer big tiles than SMs (x batch): the small tile keeps the GPU busy
   const long long big = (long long)(a.M / BigTile::BM) * ((a.N + BigTile::BN - 1) / BigTile::BN) *
                         (a.batch > 1 ? a.batch : 1);
-  const bool small = big < 148 && !(trans_b && a.N % 2 != 0);
+  // short k (the factorisation's K = 128 updates: 8 k-steps per big tile, one CTA per SM, nothing
+  // to hide a tile's prologue / C read-modify-write behind) -> small tiles too, several per SM
+  static const int kmax_small = [] {
+    const char* v = getenv("GG_DGEMM_SMALL_K");   // tuning knob (0: only the sub-wave rule)
+    return v ? atoi(v) : 128;   // measured r02: 128 best (n = 4e4 prepare -3%, 256 worse)
+  }();
+  const bool small = (big < 148 || a.K <= kmax_small) && !(trans_b && a.N % 2 != 0);
   if (small) return trans_b ? launch_tiles<SmallTile, true>(a, s) : launch_tiles<SmallTile, false>(a, s);
   return trans_b ? launch_tiles<BigTile, true>(a, s) : launch_tiles<BigTile, false>(a, s);
 }
