@@ -209,8 +209,29 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
   __syncthreads();
   LEAF_TS();
   if (FACTOR) {
+    // Look-ahead inside the leaf: the trailing update of panel J-1 is split -- warps 0-3 update the
+    // diagonal block J (10 lower 8 x 8 tiles, named barrier 1) and warp 0 goes straight on to
+    // factor and invert it, while warps 1-11 update the rest of the trailing region; one barrier
+    // joins them before panel J.
+    // (r02: the trailing updates ran between barriers, 9k of 110k cycles on the critical path.)
     for (int J = 0; J < NB / LB; ++J) {
       const int j0 = J * LB;
+      if (J > 0 && warp < 4) {   // S_JJ -= L_J,J-1 L_J,J-1^T: 10 lower 8 x 8 tiles on warps 0-3
+        for (int tt = warp; tt < 10; tt += 4) {
+          int rt = 0;
+          while ((rt + 1) * (rt + 2) / 2 <= tt) ++rt;
+          const int ct = tt - rt * (rt + 1) / 2;
+          const int r0 = j0 + 8 * rt, c0 = j0 + 8 * ct;
+          double acc[2];
+          tile8<true>(acc, S + j0 - LB, LDS, r0, S + j0 - LB, LDS, c0, 0, LB, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = r0 + g, col = c0 + 2 * t4 + e;
+            if (col <= row) S[row * LDS + col] -= acc[e];
+          }
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");   // warps 0-3 only
+      }
       if (warp == 0) {
         double r[LB];
 #pragma unroll
@@ -233,6 +254,24 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
           LEAF_TS();
 #pragma unroll
           for (int i = 0; i < LB; ++i) S[(j0 + i) * LDS + j0 + lane] = tc[i];
+        }
+      } else if (J > 0) {
+        // the rest of panel J-1's trailing update (warps 1-11): lower 8 x 8 tiles of rows /
+        // columns [j0, 128) outside the diagonal block J
+        const int m = (NB - j0) / 8;
+        for (int tt = warp - 1; tt < m * (m + 1) / 2; tt += LEAF_WARPS - 1) {
+          int rt = 0;
+          while ((rt + 1) * (rt + 2) / 2 <= tt) ++rt;
+          const int ct = tt - rt * (rt + 1) / 2;
+          if (rt < LB / 8) continue;   // diagonal block J: done above
+          const int r0 = j0 + 8 * rt, c0 = j0 + 8 * ct;
+          double acc[2];
+          tile8<true>(acc, S + j0 - LB, LDS, r0, S + j0 - LB, LDS, c0, 0, LB, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = r0 + g, col = c0 + 2 * t4 + e;
+            if (col <= row) S[row * LDS + col] -= acc[e];
+          }
         }
       }
       __syncthreads();
@@ -264,24 +303,9 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
       }
       __syncthreads();
       LEAF_TS();
-      // trailing update of the lower part: S_II' -= L_IJ L_I'J^T (lower 8 x 8 tiles)
-      for (int tt = warp; tt < m * (m + 1) / 2; tt += LEAF_WARPS) {
-        int rt = 0;
-        while ((rt + 1) * (rt + 2) / 2 <= tt) ++rt;
-        const int ct = tt - rt * (rt + 1) / 2;
-        const int r0 = j0 + LB + 8 * rt, c0 = j0 + LB + 8 * ct;
-        double acc[2];
-        tile8<true>(acc, S + j0, LDS, r0, S + j0, LDS, c0, 0, LB, lane);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int row = r0 + g, col = c0 + 2 * t4 + e;
-          if (col <= row) S[row * LDS + col] -= acc[e];
-        }
-      }
-      __syncthreads();
-      LEAF_TS();
     }
-    // the off-diagonal blocks of L (the diagonal blocks went out from warp 0's registers)
+    // the off-diagonal blocks of L (the diagonal blocks went out from warp 0's registers); no
+    // barrier before inverse phase (a), which only reads S as well
     for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
       const int r = e % NB, c = e / NB;
       if ((r >> 5) == (c >> 5)) continue;
@@ -296,8 +320,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_kernel(double* A, long l
 #pragma unroll
       for (int i = 0; i < LB; ++i) S[(warp * LB + i) * LDS + warp * LB + lane] = tc[i];
     }
+    __syncthreads();
   }
-  __syncthreads();
   LEAF_TS();
   // ---- inverse phases (S diagonal blocks = T_J, strictly upper part of S = 0) ----
   // (a) W_b = L_IJ T_J for (I, J) = (1, 0), (3, 2): T_J[k][c] = 0 for k < c

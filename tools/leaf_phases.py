@@ -17,9 +17,9 @@ lib = C.CDLL(sys.argv[1])
 for nm in ("gg_potrf_workspace_bytes", "gg_potrf_f64"):
     f = getattr(lib, nm)
     f.restype, f.argtypes = _capi.SIGNATURES[nm]
-W0 = ("factor32", "L_JJ stored", "inverse32", "T_J stored + barrier")
-NAMES = (["start", "loaded"] + [f"J{j} {p}" for j in range(3) for p in W0 + ("panel", "trailing")]
-         + [f"J3 {p}" for p in W0] + ["L written", "inv (a)", "inv (b)", "inv (c)", "inv (d)",
+W0 = ("[diag update +] factor32", "L_JJ stored", "inverse32", "T_J stored + barrier")
+NAMES = (["start", "loaded"] + [f"J{j} {p}" for j in range(3) for p in W0 + ("panel",)]
+         + [f"J3 {p}" for p in W0] + ["L written + inv (a)", "inv (b)", "inv (c)", "inv (d)",
                                       "Dinv written"])
 n = 128
 M = torch.from_numpy(np.ascontiguousarray(make_spd(n, 3).T)).cuda()
