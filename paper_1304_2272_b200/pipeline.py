@@ -76,7 +76,10 @@ class RunSummary:
     gpus: int = 1
     t_device: float = 0.0
     snps_per_s: float = 0.0
-    block_cpu_times: list = field(default_factory=list)
+    block_cpu_times: list = field(default_factory=list)   # the driving thread's CPU seconds per
+                                                          # block (time.thread_time: the I/O
+                                                          # agents' and the driver's spin threads
+                                                          # excluded -- reference pipeline.py:206)
 
     def to_record(self):
         parts = []
@@ -340,14 +343,14 @@ def stream_blocks(engine, blocks, fill, on_result):
     pending = collections.deque()     # tickets of blocks whose results are not yet collected
     for bi, (first, cnt) in enumerate(blocks):
         slot = bi % StreamEngine.REGIONS
-        cpu0 = time.process_time()
+        cpu0 = time.thread_time()
         t0 = time.perf_counter()
         host_block = fill(slot, first, cnt, bi, nb)
         t_wait += time.perf_counter() - t0
         if len(pending) == engine.DEV_REGIONS:     # its device region is needed again
             on_result(engine.collect(pending.popleft()))
         pending.append(engine.submit(slot, host_block, first, cnt))
-        cpu_times.append(time.process_time() - cpu0)
+        cpu_times.append(time.thread_time() - cpu0)
     while pending:
         on_result(engine.collect(pending.popleft()))
     return t_wait, cpu_times
@@ -410,7 +413,7 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, par
     cur = None
     for j in range(min(AHEAD, len(pieces))):
         start_read(j)
-    cpu0 = time.process_time()
+    cpu0 = time.thread_time()
     for j, pc in enumerate(pieces):
         bi, k, c0, c1, first, cnt = pc
         tw = time.perf_counter()
@@ -427,8 +430,8 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, par
             engine.launch(cur)
             pending.append(cur)
             cur = None
-            cpu_times.append(time.process_time() - cpu0)
-            cpu0 = time.process_time()
+            cpu_times.append(time.thread_time() - cpu0)
+            cpu0 = time.thread_time()
     while pending:
         on_result(engine.collect(pending.popleft()))
     t1 = time.perf_counter()
