@@ -354,3 +354,33 @@ def test_i8_trsm_snp_group_order_is_bitwise_invariant(K, grp, monkeypatch):
     got = K._trsm_i8_device(sl, expo, n, G).cpu().numpy()
     torch.cuda.synchronize()
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("env", [{"GG_I8_ORDER": "1"}, {"GG_I8_QUAD": "1"},
+                                 {"GG_I8_QUAD": "1", "GG_I8_QUAD_ILV": "0"}])
+def test_i8_trsm_tile_variants_are_bitwise_invariant(K, env, monkeypatch):
+    """The measured tile variants -- zigzag tile order, QUAD tiles (one row block x two SNP pairs)
+    in B- and A-stationary MMA order -- change only when and where a tile is computed: every
+    column (X-bar and the fused partial dots through the block solve) is bitwise the default's."""
+    import torch
+
+    from oracle import gls_ref as O
+
+    n, cnt = 900, 6 * 256 + 33
+    M = make_spd(n, 3 * n)
+    XL = np.column_stack([np.ones(n), np.random.default_rng(1).standard_normal((n, 2))])
+    y = np.random.default_rng(2).standard_normal(n)
+    G = np.random.default_rng(8).integers(0, 3, (n, cnt)).astype(np.int8)
+    ctx = K.gls_prepare(M, XL, y)
+    for k in ("GG_I8_ORDER", "GG_I8_QUAD", "GG_I8_QUAD_ILV"):
+        monkeypatch.delenv(k, raising=False)
+    ref = np.array([r.beta for r in K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(G))).results])
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = np.array([r.beta for r in K.gls_solve_block(ctx, K.SnpBlock(0, np.asfortranarray(G))).results])
+    torch.cuda.synchronize()
+    assert np.array_equal(got, ref, equal_nan=True)
+    octx = O.gls_prepare(M, XL, y)
+    ob, _ = O.gls_solve_block(octx, G.astype(np.float64))
+    rel, mism = O.compare(got, ob)
+    assert mism == 0 and rel <= 1e-9
