@@ -198,7 +198,7 @@ __global__ void zero_block_kernel(double* A, long long lda, int rows, int cols) 
 }
 
 struct SideStream {
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, main = nullptr;
   cudaEvent_t fork_ev = nullptr, done_ev = nullptr;
   bool pending = false;
   int open() {
@@ -210,6 +210,7 @@ struct SideStream {
     return GG_OK;
   }
   int fork(cudaStream_t s) {
+    main = s;
     GG_CUDA_TRY(cudaEventRecord(fork_ev, s));
     GG_CUDA_TRY(cudaStreamWaitEvent(side, fork_ev, 0));
     return GG_OK;
@@ -226,6 +227,7 @@ struct SideStream {
     return GG_OK;
   }
   ~SideStream() {
+    if (pending && main != nullptr) join(main);   // an early (error) return: order the caller
     if (side) cudaStreamDestroy(side);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (done_ev) cudaEventDestroy(done_ev);

@@ -559,8 +559,10 @@ struct PotrfStreams {
     GG_CUDA_TRY(cudaStreamWaitEvent(crit, join, 0));
     return GG_OK;
   }
+  bool closed = false;
   int close() {   // caller waits for crit (which has waited for side)
-    if (!own) return GG_OK;
+    if (!own || closed) return GG_OK;
+    closed = true;
     GG_CUDA_TRY(cudaEventRecord(eb, side));
     GG_CUDA_TRY(cudaStreamWaitEvent(crit, eb, 0));
     GG_CUDA_TRY(cudaEventRecord(join, crit));
@@ -569,6 +571,9 @@ struct PotrfStreams {
   }
   ~PotrfStreams() {
     if (!own) return;
+    // an early (error) return still orders the caller's stream after every queued kernel, so the
+    // caller may free the workspace as soon as its own stream says so
+    if (!closed && side != nullptr && crit != nullptr) close();
     if (crit != caller && crit != nullptr) cudaStreamDestroy(crit);
     if (side != nullptr) cudaStreamDestroy(side);
     for (cudaEvent_t e : {ea, eb, join})
