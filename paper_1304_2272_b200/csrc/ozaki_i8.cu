@@ -685,8 +685,8 @@ int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long lo
                    const int* abort_flag, cudaStream_t s) {
   if (M <= 0 || N <= 0) return GG_OK;
   const bool same = (B == nullptr);
-  if (same && M != N) {
-    set_error("ozaki_gemm: B = A needs M == N");
+  if (same && N > M) {   // B~ = the first N rows of A~ (N < M: a SYRK on leading columns)
+    set_error("ozaki_gemm: B = A needs N <= M");
     return GG_EDIM;
   }
   if (ws == nullptr || ws_bytes < ozaki_ws_bytes(M, N, K, same)) {
@@ -724,7 +724,7 @@ int ozaki_gemm_run(int M, int N, int K, const double* A, long long a_rs, long lo
     CUtensorMap mA, mB;
     rc = encode_slices(&mA, SlA, M, Kc, kp, OZ_BM);
     if (rc != GG_OK) return rc;
-    rc = encode_slices(&mB, SlB, N, Kc, kp, OZ_BN);
+    rc = encode_slices(&mB, SlB, same ? M : N, Kc, kp, OZ_BN);
     if (rc != GG_OK) return rc;
     OzArgs a{};
     a.M = M;

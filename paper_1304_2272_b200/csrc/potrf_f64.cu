@@ -502,13 +502,44 @@ int trtri_offdiag(int np, const double* L, double* Linv, long long ldp, double* 
 size_t t_region_bytes(int np) {
   return (trtri_T_doubles(np) * sizeof(double) + 255) & ~size_t(255);
 }
+// Trailing-update aggregation: the far columns' SYRK runs once per `syrk_agg()` outer blocks with
+// the deferred panels stacked along k (depth agg OUTER); the outer blocks in between update only
+// the next outer block's columns.  Same arithmetic, 1/agg the passes over the trailing matrix
+// (each pass re-reads and re-writes C and pays the per-tile epilogue).  Tuning knob GG_SYRK_AGG.
+int syrk_agg() {
+  const char* v = getenv("GG_SYRK_AGG");
+  const int a = v ? atoi(v) : 1;
+  return a < 1 ? 1 : (a > 8 ? 8 : a);
+}
+// the trailing update after outer block K0 (width w): columns [K0+w, K0+w+ncols) of all rows
+// below, from the panels [dstart, K0+w) -- returns false when there is none
+struct TrailingUpdate {
+  int rem, ncols, kd;
+  bool full;
+};
+bool trailing_update(int np, int K0, int w, int dstart, int agg, TrailingUpdate* t) {
+  t->rem = np - K0 - w;
+  if (t->rem <= 0) return false;
+  t->full = ((K0 / OUTER + 1) % agg == 0) || t->rem <= OUTER;
+  t->ncols = t->full ? t->rem : OUTER;
+  t->kd = K0 + w - dstart;
+  return true;
+}
+
 size_t oz_region_bytes(int np, bool factor) {
   size_t b = trtri_oz_bytes(np);
-  if (factor) {   // the trailing SYRKs: largest at the first outer block
-    const int rem = np - OUTER;
-    if (rem > 0 && oz_shape(rem, rem, OUTER)) {
-      const size_t sy = ozaki_ws_bytes(rem, rem, OUTER, true);
-      if (sy > b) b = sy;
+  if (factor) {   // the trailing SYRKs, as potrf_run issues them
+    const int agg = syrk_agg();
+    int dstart = 0;
+    TrailingUpdate t;
+    for (int K0 = 0; K0 < np; K0 += OUTER) {
+      const int w = (np - K0 < OUTER) ? (np - K0) : OUTER;
+      if (!trailing_update(np, K0, w, dstart, agg, &t)) break;
+      if (oz_shape(t.rem, t.ncols, t.kd)) {
+        const size_t sy = ozaki_ws_bytes(t.rem, t.ncols, t.kd, true);
+        if (sy > b) b = sy;
+      }
+      if (t.full) dstart = K0 + w;
     }
   }
   return b;
@@ -623,12 +654,15 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
   // Two-level right-looking blocking: outer block columns of OUTER (= 8 leaves); inside one,
   // leaf + panel + an update restricted to the outer block's columns; after it, one trailing
   // SYRK of depth OUTER (8x the arithmetic intensity of a depth-128 update; 1024 measured best
-  // between 256 and 4096 at n = 1e4 and 4e4).
+  // between 256 and 4096 at n = 1e4 and 4e4) -- aggregated over syrk_agg() outer blocks for the
+  // columns beyond the next outer block (see trailing_update).
   // Look-ahead inside the outer block: panel k's update is split into (a) the next block column
   // k+1 on the critical stream, then leaf k+1 and panel k+1 follow at once, while (b) the columns
   // beyond k+1 are updated on the side stream; the critical stream waits for (b) before its next
   // (a) (both write block column k+2).  Panels alternate between two buffers (b reads panel k
   // while panel k+1 is formed).
+  const int agg = syrk_agg();
+  int dstart = 0;   // first panel column whose update of the far columns is still deferred
   for (int K0 = 0; K0 < np; K0 += OUTER) {
     const int w = (np - K0 < OUTER) ? (np - K0) : OUTER;
     bool pend = false;   // side-stream update not yet waited for
@@ -680,23 +714,25 @@ int potrf_run(int n, const double* M, int ldm, int m_row_major, double* L, doubl
       }
     }
     if (pend) GG_CUDA_TRY(cudaStreamWaitEvent(cs_, st.eb, 0));
-    const int rem = np - K0 - w;
-    if (rem <= 0) break;
-    // trailing SYRK of depth w: A22 -= L21 L21^T, L21 = L[K0+w:, K0:K0+w] (read in place;
-    // disjoint from the updated region), lower tiles only
-    if (oz != nullptr && oz_shape(rem, rem, w)) {
-      GG_TRY(ozaki_gemm_run(rem, rem, w, L + (K0 + w) + (long long)K0 * ldp, 1, ldp, nullptr, 0, 0,
-                            L + (K0 + w) + (long long)(K0 + w) * ldp, ldp, -1.0, 1.0, GEMM_C_LOWER,
-                            oz, oz_bytes, &hdr->info, cs_));
+    TrailingUpdate t;
+    if (!trailing_update(np, K0, w, dstart, agg, &t)) break;
+    // trailing SYRK: A[K0+w:, K0+w : K0+w+ncols] -= Ld Ld[:ncols]^T, Ld = L[K0+w:, dstart:K0+w]
+    // (the deferred panels, read in place; disjoint from the updated region), lower tiles only
+    const double* Ld = L + (K0 + w) + (long long)dstart * ldp;
+    double* C = L + (K0 + w) + (long long)(K0 + w) * ldp;
+    if (oz != nullptr && oz_shape(t.rem, t.ncols, t.kd)) {
+      GG_TRY(ozaki_gemm_run(t.rem, t.ncols, t.kd, Ld, 1, ldp, nullptr, 0, 0, C, ldp, -1.0, 1.0,
+                            GEMM_C_LOWER, oz, oz_bytes, &hdr->info, cs_));
     } else {
       GemmArgs upd{};
-      upd.M = rem; upd.N = rem; upd.K = w;
-      upd.A = L + (K0 + w) + (long long)K0 * ldp; upd.lda = ldp;
-      upd.B = L + (K0 + w) + (long long)K0 * ldp; upd.ldb = ldp;
-      upd.C = L + (K0 + w) + (long long)(K0 + w) * ldp; upd.ldc = ldp;
+      upd.M = t.rem; upd.N = t.ncols; upd.K = t.kd;
+      upd.A = Ld; upd.lda = ldp;
+      upd.B = Ld; upd.ldb = ldp;
+      upd.C = C; upd.ldc = ldp;
       upd.alpha = -1.0; upd.beta = 1.0; upd.flags = GEMM_C_LOWER; upd.abort_flag = &hdr->info;
       GG_TRY(launch_dgemm(upd, true, cs_));
     }
+    if (t.full) dstart = K0 + w;
   }
   if (timing) cudaEventRecord(ev[1], cs_);
   GG_TRY(trtri_offdiag(np, L, Linv, ldp, P, oz, oz_bytes, &hdr->info, cs_));

@@ -97,6 +97,37 @@ def test_ozaki_syrk_lower(gpu):
     assert np.array_equal(got[:128, 128:], C0[:128, 128:])
 
 
+def test_ozaki_syrk_leading_columns(gpu):
+    """B = A with ncols < m: B~ is the first ncols rows of A~ (the factorisation's update of the
+    next outer block only, before the deferred far-column SYRK)."""
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((700, 1536))
+    C0 = rng.standard_normal((700, 300))
+    got = _ozaki(A, A[:300], C0, -1.0, 1.0, 4, same=True)
+    ref = C0 - A @ A[:300].T
+    low = np.tril(np.ones((700, 300), bool))
+    assert float(np.max(np.abs(got - ref)[low])) <= 1e-12 * 1536
+    # equal to the two-operand form bit for bit (same slices, same products)
+    two = _ozaki(A, A[:300], C0, -1.0, 1.0, 4)
+    assert np.array_equal(got[low], two[low])
+
+
+@pytest.mark.parametrize("agg", ["1", "2", "3"])
+def test_potrf_syrk_aggregation(gpu, agg, monkeypatch):
+    """Deferred trailing SYRKs (GG_SYRK_AGG outer blocks stacked along k; n = 4500 is 4.5 outer
+    blocks: partial next-block updates, full updates of depth 2048 / 3072 and the ragged end)
+    give the factor and inverse of the one-SYRK-per-block schedule to FP64 working accuracy."""
+    n = 4500
+    M = make_spd(n, n)
+    monkeypatch.setenv("GG_SYRK_AGG", agg)
+    Lo, Io = _factor(M, True, monkeypatch)
+    Ld, Id = _factor(M, False, monkeypatch)
+    assert float(np.max(np.abs(Lo - Ld))) <= 1e-13 * float(np.max(np.abs(Ld)))
+    assert float(np.max(np.abs(Io - Id))) <= 1e-13 * float(np.max(np.abs(Id)))
+    res = np.abs(np.tril(Lo) @ np.tril(Lo).T - M).max() / np.abs(M).max()
+    assert res <= 1e-14, res
+
+
 def test_ozaki_triangular_operands(gpu):
     """The trtri GEMMs: B~(j,k) = 0 for k < j (flag 2) and A~ lower triangular (flag 1), with a k
     range longer than one launch's chunk (8192) so the triangle's offsets move with the chunk."""
