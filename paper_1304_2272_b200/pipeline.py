@@ -370,7 +370,7 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, par
     dtype = np.int8 if int8 else np.float64
     regions = [pinned_empty(n, m_blk, dtype) for _ in range(StreamEngine.REGIONS)]
     in_bufs = [r[0] for r in regions]
-    width = writer._rsz // 8
+    width = writer.record_bytes // 8
     rec_bufs = [np.empty((m_blk, width)) for _ in range(2)]
     state = {"store": None, "rec": 0, "io": 0.0}
     P = max(1, int(parts))
