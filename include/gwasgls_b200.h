@@ -216,12 +216,12 @@ int gg_dgemm_f64(int m, int ncols, int k, double alpha, const double* A, int lda
                  const double* B, int ldb, int trans_b, double beta, double* C, int ldc,
                  void* stream);
 
-/* FP64 GEMM on the int8 tensor cores (Ozaki scheme, 8 slices per operand, 36 exact
- * int32 slice products, one rounding): C = beta*C + alpha * A~ B~^T with
+/* FP64 GEMM on the int8 tensor cores (Ozaki scheme, 7 slices of balanced 8-bit digits per
+ * operand, 28 exact int32 slice products, one rounding): C = beta*C + alpha * A~ B~^T with
  * A~(i,k) = A[i*a_rs + k*a_cs] (m x k) and B~(j,k) = B[j*b_rs + k*b_cs] (ncols x k;
  * B == NULL: B~ = the first ncols rows of A~, ncols <= m).  flags: 1 = A~ lower triangular (A~(i,k) = 0 for k > i),
  * 2 = B~(j,k) = 0 for k < j, 4 = only the tiles on/below the diagonal of C.
- * Accuracy: 2^-56 of |A~(i,:)|max |B~(j,:)|max per product term (FP64-GEMM order).
+ * Accuracy: ~2^-56 of |A~(i,:)|max |B~(j,:)|max per product term (FP64-GEMM order).
  * The factorisation's large updates use it (gg_potrf_f64, gg_trtri_lower_f64; set
  * GG_FACTOR_OZAKI=0 for the DMMA path).  work: gg_gemm_ozaki_workspace_bytes bytes.  */
 size_t gg_gemm_ozaki_workspace_bytes(int m, int ncols, int k, int b_is_a);

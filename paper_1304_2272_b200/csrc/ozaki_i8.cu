@@ -2,25 +2,30 @@
 // used for the large updates of the Cholesky factorisation (potrf_f64.cu).
 //
 // FP64 has no tcgen05 kind on sm_100a; the DMMA path peaks at 37 TFLOP/s while the int8 tensor
-// cores do 4.4 POPS.  Each row i of A (and row j of B) is split error-free into 8 int8 slices
-// below its own power of two:
-//     A[i,k] = 2^e_i sum_{s=0..7} a_s[i,k] 2^(-7 (s+1)),   |a_s| <= 127
-// (slices 0-6 truncate with exact remainders, the last rounds to nearest), so
-//     (A B^T)[i,j] = 2^(e_i + f_j) sum_d D_d[i,j] 2^(-7 (d+2)),   D_d = sum_{s+t=d} a_s b_t^T.
-// The 36 slice products with s + t <= 7 are issued as tcgen05.mma.kind::i8 into 8 int32 TMEM
-// accumulators (one per diagonal d, 64 columns each = all 512 columns); every D_d is exact for
-// K <= 16384 ((d+1) 127^2 K < 2^31; the host splits K into launches of <= 8192).  The dropped terms (s+t >= 8)
-// and the operand residuals are below 2^-56 of 2^(e_i+f_j) per product term -- the same order as
-// FP64 rounding.  The epilogue forms the exact int64 halves hi = D_0..D_3, lo = D_4..D_7 (base
-// 2^7) and rounds once: r = 2^E fma(hi, 2^-35, lo 2^-63); then C = beta C + alpha r.
+// cores do 4.4 POPS.  Each row i of A (and row j of B) is split error-free into 7 int8 slices of
+// balanced base-256 digits below its own power of two (|A[i,:]| < 127/256 2^e_i):
+//     A[i,k] = 2^e_i sum_{s=0..6} a_s[i,k] 2^(-8 (s+1)),   a_s in [-128, 127]
+// (the digits of RN(A[i,k] 2^(56 - e_i)): one rounding, then exact integer digit extraction), so
+//     (A B^T)[i,j] = 2^(e_i + f_j) sum_d D_d[i,j] 2^(-8 (d+2)),   D_d = sum_{s+t=d} a_s b_t^T.
+// The 28 slice products with s + t <= 6 are issued as tcgen05.mma.kind::i8 into 7 int32 TMEM
+// accumulators (one per diagonal d, 64 columns each); every D_d is exact for K <= 18724
+// (7 2^14 K < 2^31; the host splits K into launches of <= 8192).  The dropped terms (s+t >= 7)
+// are below 2^-56 of 2^(e_i+f_j) per product term and, every digit below the top one being
+// centred on zero, keep random signs and cancel along k -- measured as accurate as FP64 GEMM and
+// ~2x closer to the exact product than the r02 form (8 slices of 7-bit sign-magnitude digits, 36
+// products; OZ_DIGIT_BITS=7 builds it, tools/oz_accuracy.py).  The epilogue forms the exact int64
+// halves hi = D_0..D_3, lo = D_4..D_6 (base 2^8) and rounds once: r = 2^E fma(hi, 2^-40, lo 2^-64);
+// then C = beta C + alpha r.
 //
 // Kernel (persistent, one CTA per SM in clusters of 2, 10 warps): warp 0 TMA producer (per 64-k
-// stage: the 8 slices of a 128-row A tile -- half of them loaded here and multicast to the
-// cluster peer, which computes the neighbouring 64 columns -- and of a 64-row B tile, 96 KB,
+// stage: 8 slice slots of a 128-row A tile -- half of them loaded here and multicast to the
+// cluster peer, which computes the neighbouring 64 columns; the 8th slot is out of bounds of the
+// 7-slice operand, zero-filled by TMA and never multiplied -- and of a 64-row B tile, 96 KB,
 // SWIZZLE_64B, 2-stage ring; r02: 64-byte rows halve the L2 requests of the 32-byte-row 4-stage
 // form, whose operand stream was the limiter), warp 1 MMA issuer (one lane, M = 128 x N = 64..256
-// x K = 32, 2 x 12 MMAs covering the 36 slice products per stage), warps 2-9 epilogue (TMEM lane = tile row, two warps
-// per lane quarter, 32 columns each; release TMEM once the tile is in registers, then update C).
+// x K = 32, 2 x 10 MMAs covering the 28 slice products per stage), warps 2-9 epilogue (TMEM lane =
+// tile row, two warps per lane quarter, 32 columns each; release TMEM once the tile is in
+// registers, then update C).
 // Operand entries outside a triangular operand's triangle are sliced as zeros.
 // Results are bitwise deterministic (exact integer accumulation, fixed rounding).
 #include <cuda.h>
@@ -38,7 +43,17 @@
 namespace gg {
 namespace {
 
-constexpr int OZ_S = 8;                    // slices per operand
+#ifndef OZ_DIGIT_BITS
+#define OZ_DIGIT_BITS 8   // r02: 28 products instead of 36, n = 4e4 prepare 0.70 -> 0.61 s
+#endif
+// digits: 8 slices of 7-bit sign-magnitude digits (36 products, s + t <= 7) or 7 slices of 8-bit
+// balanced digits (28 products, s + t <= 6) -- both keep ~56 bits below the row maximum
+constexpr int OZ_DB = OZ_DIGIT_BITS;
+static_assert(OZ_DB == 7 || OZ_DB == 8, "digit width");
+constexpr int OZ_S = OZ_DB == 8 ? 7 : 8;   // slices per operand (= diagonals kept)
+constexpr int OZ_SS = 8;                   // slice slots per stage in shared memory: TMA boxes of
+                                           // 4 slices, a 7th-slice operand's 8th slot zero-filled
+                                           // (out of bounds) and never multiplied
 constexpr int OZ_BM = 128;                 // tile rows (MMA M)
 constexpr int OZ_BN = 64;                  // tile columns (MMA N, one accumulator per diagonal)
 #ifndef OZ_KC_BYTES
@@ -48,15 +63,15 @@ constexpr int OZ_KC = OZ_KC_BYTES;         // k per stage: 32 (one MMA K, 32-byt
                                            // 64 (two MMA K steps, 64-byte swizzled rows)
 constexpr int OZ_STAGES = OZ_KC == 32 ? 4 : 2;
 static_assert(OZ_KC == 32 || OZ_KC == 64, "k per stage");
-constexpr int OZ_A_BYTES = OZ_S * OZ_BM * OZ_KC;   // 32 KB
-constexpr int OZ_B_BYTES = OZ_S * OZ_BN * OZ_KC;   // 16 KB
+constexpr int OZ_A_BYTES = OZ_SS * OZ_BM * OZ_KC;   // 64 KB at 64-byte stages
+constexpr int OZ_B_BYTES = OZ_SS * OZ_BN * OZ_KC;   // 32 KB
 constexpr int OZ_STAGE_BYTES = OZ_A_BYTES + OZ_B_BYTES;
 constexpr int OZ_EPI_WARPS = 8;
 constexpr int OZ_THREADS = (2 + OZ_EPI_WARPS) * 32;
 constexpr size_t OZ_SMEM = size_t(OZ_STAGES) * OZ_STAGE_BYTES + 1024 + 256;
 constexpr int OZ_KMAX = 8192;              // k per launch: exact int32 diagonals need
-                                           // 8 * 127^2 * K < 2^31 (K <= 16384); 8192 bounds the
-                                           // slice workspace
+                                           // 7 * 2^14 * K < 2^31 (8 * 127^2 * K with 7-bit digits);
+                                           // 8192 bounds the slice workspace
 constexpr unsigned OZ_IDESC_BASE = (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(OZ_BM >> 4) << 24);
 
 struct OzArgs {
@@ -143,7 +158,8 @@ __device__ __forceinline__ double pow2(int e) {   // 2^e, |e| < 1022
   return __longlong_as_double((long long)(1023 + e) << 52);
 }
 // 8 columns x the 8 diagonals of one warp quarter: v[d][c]
-__device__ __forceinline__ void tmem_ld_diag8(unsigned taddr, int (&v)[OZ_S][8]) {
+// the 8 diagonals' accumulators (columns d * OZ_BN) of 8 columns; OZ_S == 7 leaves v[7] unused
+__device__ __forceinline__ void tmem_ld_diag8(unsigned taddr, int (&v)[8][8]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%64];\n"
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%65];\n"
@@ -164,6 +180,27 @@ __device__ __forceinline__ void tmem_ld_diag8(unsigned taddr, int (&v)[OZ_S][8])
         "=r"(v[7][0]), "=r"(v[7][1]), "=r"(v[7][2]), "=r"(v[7][3]), "=r"(v[7][4]), "=r"(v[7][5]), "=r"(v[7][6]), "=r"(v[7][7])
       : "r"(taddr + 0 * OZ_BN), "r"(taddr + 1 * OZ_BN), "r"(taddr + 2 * OZ_BN), "r"(taddr + 3 * OZ_BN),
         "r"(taddr + 4 * OZ_BN), "r"(taddr + 5 * OZ_BN), "r"(taddr + 6 * OZ_BN), "r"(taddr + 7 * OZ_BN)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_diag7(unsigned taddr, int (&v)[8][8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%56];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%57];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%16,%17,%18,%19,%20,%21,%22,%23}, [%58];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%24,%25,%26,%27,%28,%29,%30,%31}, [%59];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%32,%33,%34,%35,%36,%37,%38,%39}, [%60];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%40,%41,%42,%43,%44,%45,%46,%47}, [%61];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%48,%49,%50,%51,%52,%53,%54,%55}, [%62];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]), "=r"(v[0][6]), "=r"(v[0][7]),
+        "=r"(v[1][0]), "=r"(v[1][1]), "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]), "=r"(v[1][7]),
+        "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[2][2]), "=r"(v[2][3]), "=r"(v[2][4]), "=r"(v[2][5]), "=r"(v[2][6]), "=r"(v[2][7]),
+        "=r"(v[3][0]), "=r"(v[3][1]), "=r"(v[3][2]), "=r"(v[3][3]), "=r"(v[3][4]), "=r"(v[3][5]), "=r"(v[3][6]), "=r"(v[3][7]),
+        "=r"(v[4][0]), "=r"(v[4][1]), "=r"(v[4][2]), "=r"(v[4][3]), "=r"(v[4][4]), "=r"(v[4][5]), "=r"(v[4][6]), "=r"(v[4][7]),
+        "=r"(v[5][0]), "=r"(v[5][1]), "=r"(v[5][2]), "=r"(v[5][3]), "=r"(v[5][4]), "=r"(v[5][5]), "=r"(v[5][6]), "=r"(v[5][7]),
+        "=r"(v[6][0]), "=r"(v[6][1]), "=r"(v[6][2]), "=r"(v[6][3]), "=r"(v[6][4]), "=r"(v[6][5]), "=r"(v[6][6]), "=r"(v[6][7])
+      : "r"(taddr + 0 * OZ_BN), "r"(taddr + 1 * OZ_BN), "r"(taddr + 2 * OZ_BN), "r"(taddr + 3 * OZ_BN),
+        "r"(taddr + 4 * OZ_BN), "r"(taddr + 5 * OZ_BN), "r"(taddr + 6 * OZ_BN)
       : "memory");
 }
 
@@ -348,11 +385,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           mbar_wait(full0 + 8 * stage, phase);
           fence_after();
           const unsigned sA = sbase + stage * OZ_STAGE_BYTES, sB = sA + OZ_A_BYTES;
-          // A slice s times B slices u = 0 .. 7-s: the B slices sit consecutively along N, and
-          // product (s, u) belongs to diagonal s + u at TMEM column 64 (s + u), so one MMA covers
-          // up to 4 of them (N = 256): 12 MMAs per stage instead of 36, so the tensor core reads
-          // each A slice from shared memory once or twice rather than 8 - s times.  s = 0 opens
-          // every diagonal.
+          // A slice s times B slices u = 0 .. OZ_S-1-s: the B slices sit consecutively along N,
+          // and product (s, u) belongs to diagonal s + u at TMEM column 64 (s + u), so one MMA
+          // covers up to 4 of them (N = 256): 10 MMAs per K step for the 28 products (12 for 36
+          // with 7-bit digits), so the tensor core reads each A slice from shared memory once or
+          // twice rather than OZ_S - s times.  s = 0 opens every diagonal.
 #pragma unroll
           for (int kk = 0; kk < OZ_KC / 32; ++kk) {   // MMA K steps of 32 bytes in the stage
 #pragma unroll
@@ -401,15 +438,23 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const unsigned taddr = tmem_base + ((unsigned)(quarter * 32) << 16) + h * HN;
 #pragma unroll
           for (int c8 = 0; c8 < HN / 8; ++c8) {
-            int v[OZ_S][8];
-            tmem_ld_diag8(taddr + c8 * 8, v);
+            int v[8][8];
+            if (OZ_S == 8) tmem_ld_diag8(taddr + c8 * 8, v);
+            else tmem_ld_diag7(taddr + c8 * 8, v);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
-                                   v[3][c];
-              const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
-                                   v[7][c];
-              r[c8 * 8 + c] = fma((double)hi, 0x1p-35, (double)lo * 0x1p-63);   // the one rounding
+              if (OZ_DB == 7) {   // sum_d D_d 2^(-7 (d+2)): exact halves in base 2^7
+                const long long hi = (((long long)v[0][c] * 128 + v[1][c]) * 128 + v[2][c]) * 128 +
+                                     v[3][c];
+                const long long lo = (((long long)v[4][c] * 128 + v[5][c]) * 128 + v[6][c]) * 128 +
+                                     v[7][c];
+                r[c8 * 8 + c] = fma((double)hi, 0x1p-35, (double)lo * 0x1p-63);   // the one rounding
+              } else {            // sum_d D_d 2^(-8 (d+2)): |hi| < 2^52, |lo| < 2^46, both exact
+                const long long hi = (((long long)v[0][c] * 256 + v[1][c]) * 256 + v[2][c]) * 256 +
+                                     v[3][c];
+                const long long lo = ((long long)v[4][c] * 256 + v[5][c]) * 256 + v[6][c];
+                r[c8 * 8 + c] = fma((double)hi, 0x1p-40, (double)lo * 0x1p-64);   // the one rounding
+              }
             }
           }
         }
@@ -531,7 +576,10 @@ __global__ void __launch_bounds__(SL_THREADS) oz_rowexp_kernel(int R, int K, con
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0 && m > 0.0) {
       int e;
-      frexp(m, &e);
+      const double mant = frexp(m, &e);   // m = mant 2^e, mant in [0.5, 1)
+      // 8-bit balanced digits need |x| 2^-e < 127/256 (the top digit stays <= 127): monotone in
+      // m, so the maximum over tiles is the exponent of the row maximum
+      if (OZ_DB == 8) e += mant < 127.0 / 128.0 ? 1 : 2;
       atomicMax(ex + r, e);
     }
   }
@@ -567,12 +615,26 @@ __global__ void __launch_bounds__(SL_THREADS) oz_slice_kernel(int R, int K, cons
     // products (s + t >= 8) and the residuals keep random signs and cancel along k (floor digits
     // -- all non-negative below slice 0 -- make them add up coherently: measured 30-90x larger
     // GEMM errors).  One FP64 -> integer conversion per element, the rest integer work.
-    const unsigned long long N = __double2ull_rn(fabs(v) * 0x1p56);   // exact scale, < 2^56
-    const bool neg = v < 0.0;
+    if (OZ_DB == 7) {
+      const unsigned long long N = __double2ull_rn(fabs(v) * 0x1p56);   // exact scale, < 2^56
+      const bool neg = v < 0.0;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) {
-      const int d = (int)((N >> (7 * (OZ_S - 1 - s))) & 127u);
-      w[s][j / 4] |= ((unsigned)(neg ? -d : d) & 0xffu) << (8 * (j % 4));
+      for (int s = 0; s < OZ_S; ++s) {
+        const int d = (int)((N >> (7 * (OZ_S - 1 - s))) & 127u);
+        w[s][j / 4] |= ((unsigned)(neg ? -d : d) & 0xffu) << (8 * (j % 4));
+      }
+    } else {
+      // balanced base-256 digits of V = RN(v 2^56) (|v| < 127/256: the top digit in [-127, 127]),
+      // lowest first; every digit below the top one is centred on zero, so the dropped products
+      // (s + t >= 7) keep random signs and cancel along k like the sign-magnitude digits
+      long long V = __double2ll_rn(v * 0x1p56);
+#pragma unroll
+      for (int s = OZ_S - 1; s > 0; --s) {
+        const int d = (int)((V + 128) & 255) - 128;
+        V = (V - d) >> 8;
+        w[s][j / 4] |= ((unsigned)d & 0xffu) << (8 * (j % 4));
+      }
+      w[0][j / 4] |= ((unsigned)(int)V & 0xffu) << (8 * (j % 4));
     }
   }
   const long long off = (long long)(r0 + r) * kp + k0 + kq;
@@ -607,7 +669,7 @@ int encode_slices(CUtensorMap* map, const signed char* Sl, int R, int K, long lo
   }
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)R, (cuuint64_t)OZ_S};
   cuuint64_t strides[2] = {(cuuint64_t)kp, (cuuint64_t)kp * R};
-  cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_S / 2};   // half the slices (multicast)
+  cuuint32_t box[3] = {OZ_KC, (cuuint32_t)box_rows, OZ_SS / 2};   // half the slots (multicast)
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(Sl), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -1,5 +1,5 @@
 """Ozaki GEMM (gg_gemm_ozaki_f64) on the prepare's shapes at n = 4e4, device-resident operands,
-CUDA-event timing (slicing + GEMM launches per call).  Effective rate = 36 int8 MACs per useful
+CUDA-event timing (slicing + GEMM launches per call).  Effective rate = 28 int8 MACs per useful
 FP64 MAC (triangular shapes count only their nonzero products) x 2 ops.
     python tools/prof_ozaki.py [--only NAME] [--reps R] [--libs tools/alt/a.so ...]
 (--libs: time the same shapes through other builds of the library, round-robin per shape)"""
@@ -68,7 +68,7 @@ for name, (m, nc, k, flags, same, macs) in SHAPES.items():
             ref = C.clone()
         diff = float((C - ref).abs().max() / ref.abs().max())
         print(f"{lname:10s} diff={diff:.1e} {name:12s} m={m} n={nc} k={k} flags={flags}: {t * 1e3:8.2f} ms  "
-              f"{36 * 2 * macs / t / 1e12:7.0f} int8 TOPS eff  ({2 * macs / t / 1e12:5.1f} FP64 TF/s)",
+              f"{28 * 2 * macs / t / 1e12:7.0f} int8 TOPS eff  ({2 * macs / t / 1e12:5.1f} FP64 TF/s)",
               flush=True)
         del ws
     del A, B, C, C0, ref
