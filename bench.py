@@ -237,7 +237,7 @@ class Sweep:
         del Md
         d = self.d = self.ctx._dev
         free_b, _ = torch.cuda.mem_get_info(dev)
-        self.resident = resident or ("f64" if 8 * m * np_ < 0.6 * free_b else "i8")
+        self.resident = resident or default_resident(m, np_, free_b)
         self.use_i8 = trsm == "i8" and d.slices is not None
         n16 = self.n16 = -(-n // 16) * 16
         self.X = self.Gres = None
@@ -434,6 +434,38 @@ def roofline_obj(sw, steps, elapsed_ms, trsm_ms, clk, lib):
     return r
 
 
+def default_resident(m, np_, free_bytes=None):
+    """Genotype storage in HBM: FP64 when the m x np_ panel fits in 0.6 of the free memory (of a
+    nominal 180 GB B200 when no device is queried: the reference arm), else int8."""
+    free_b = 0.97 * 180e9 if free_bytes is None else free_bytes
+    return "f64" if 8 * m * np_ < 0.6 * free_b else "i8"
+
+
+def workload_config(cfg, m, world, m_blk, resident):
+    """The static description of the benched workload -- the same object on both arms."""
+    from paper_1304_2272_b200 import datagen
+
+    spec0 = datagen.CONFIGS[cfg]
+    n, p = spec0.n, spec0.p
+    from paper_1304_2272_b200._capi import pad
+
+    np_ = pad(n)
+    n16 = -(-n // 16) * 16
+    gbytes = m * (np_ * 8 if resident == 'f64' else n16) / 1e9
+    return {
+        "workload": f"BASELINE config {cfg}: GLS sweep n={n}, p={p}, m={m} SNPs "
+                    f"per GPU ({'full m' if m == spec0.m else 'reduced m'}), blocks of "
+                    f"{m_blk}; step = TRSM + fused epilogue + p x p solves over all m SNPs",
+        "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": m_blk,
+        "blocks_per_step": -(-m // m_blk), "parallelism": f"snp-shard x{world}",
+        "resident": resident,
+        "l2": ("inputs larger than L2" if gbytes > 0.126 else
+               "inputs SMALLER than L2 (a parity configuration, not a bench workload)")
+              + f" (genotypes resident in HBM: {gbytes:.1f} GB per GPU, "
+              f"{'FP64' if resident == 'f64' else 'int8'}); no flush",
+    }
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -497,26 +529,18 @@ def run_ours(args):
                          "of the FP64 inverse (+ integer diagonal head), one FP64 rounding per "
                          "element; reductions and p x p solves in FP64") if sw.use_i8 else
                         "FP64 DMMA TRSM, FP64 reductions and solves",
-        "config": {
-            "workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}, m={m} SNPs "
-                        f"per GPU ({'full m' if m == spec0.m else 'reduced m'}), blocks of "
-                        f"{sw.m_blk}; step = TRSM + fused epilogue + p x p solves over all m SNPs",
-            "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": sw.m_blk,
-            "blocks_per_step": len(sw.plan), "parallelism": f"snp-shard x{world}",
-            "resident": sw.resident,
-            "l2": "inputs larger than L2 (genotypes resident in HBM: "
-                  f"{m * (sw.np_ * 8 if sw.resident == 'f64' else sw.n16) / 1e9:.1f} GB per GPU, "
-                  f"{'FP64' if sw.resident == 'f64' else 'int8'}); no flush needed",
+        # static description of the workload: the reference arm prints the same object
+        "config": workload_config(args.config, m, world, sw.m_blk, sw.resident),
+        "prepare": {
             "t_prepare_s": round(sw.t_prepare, 4),
             "prepare_device_ms": round(sw.prepare_ms_device, 2),
             # SNPs/s end to end including the one-time prepare (one sweep + prepare)
             "snps_per_s_including_prepare": round(
                 m * world / (elapsed_ms / 1e3 / args.steps + sw.t_prepare), 1),
             "t_generate_M_s": round(sw.t_gen_m, 2),
-            "step_fp64_tflops": round(float(n) * n * m * args.steps / (elapsed_ms / 1e3) / 1e12,
-                                      3),
-            "all_snps_ok": ok_all,
         },
+        "step_fp64_tflops": round(float(n) * n * m * args.steps / (elapsed_ms / 1e3) / 1e12, 3),
+        "all_snps_ok": ok_all,
         "roofline": roofline,
         "gpu_launches": sw.launches_per_step * args.steps,
         "clocks": clk,
@@ -767,6 +791,7 @@ def run_reference(args):
         return
     from oracle import gls_ref as O
     from paper_1304_2272_b200 import datagen
+    from paper_1304_2272_b200._capi import pad
 
     spec = datagen.CONFIGS[args.config]
     n, p = spec.n, spec.p
@@ -795,11 +820,15 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"BASELINE config {args.config}: GLS sweep n={n}, p={p}; each step "
-                               f"= one {S}-SNP block through the reference CPU path "
-                               f"(gls_solve_block, threads={cores})",
-                   "n": n, "p": p, "sample_snps_per_step": S, "t_prepare_s": round(t_prep, 3),
-                   "t_generate_s": round(t_gen, 2)},
+        # the workload of our arm (same static object); each step of this arm is a bounded
+        # sample of it, described in "sample" / cpu_baseline.sample
+        "config": workload_config(args.config, args.snps or spec.m, world, args.block_snps,
+                                  args.resident or default_resident(args.snps or spec.m,
+                                                                    pad(n))),
+        "sample": {"snps_per_step": S, "t_prepare_s": round(t_prep, 3),
+                   "t_generate_s": round(t_gen, 2),
+                   "what": f"each step = one {S}-SNP block of the workload through the reference "
+                           f"CPU path (gls_solve_block, threads={cores})"},
         "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{S}-SNP block of the config-{args.config} workload per step "
                                    f"(oracle/gls_ref.py: scipy dtrsm on {cores} BLAS threads + the "

@@ -40,6 +40,11 @@ def test_reference_arm_contract():
     e2e = d["e2e"]
     assert e2e["value"] == d["value"] and e2e["h2d_bytes_per_step"] == 0
     assert e2e["d2h_bytes_per_step"] == 0
+    # the reference arm names OUR arm's workload (the static config object of both arms)
+    import bench
+
+    want = bench.workload_config(0, 10000, 1, 8192, "f64")
+    assert d["config"] == want and d["sample"]["snps_per_step"] > 0
 
 
 @pytest.mark.gpu
@@ -56,6 +61,10 @@ def test_gpu_arm_contract(gpu):
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["parity"]["within"] and d["parity"]["status_mismatches"] == 0
+    import bench
+
+    assert d["config"] == bench.workload_config(0, 10000, 1, 8192, "f64")   # = the reference arm's
+    assert d["prepare"]["t_prepare_s"] > 0 and d["all_snps_ok"] in (True, False)
 
 
 def test_gpus_flag_starts_n_ranks():
