@@ -287,6 +287,21 @@ __host__ __device__ constexpr size_t d_smem_bytes(int stages, int rdb, bool quad
 }
 constexpr int D_TQ_READERS = 2 + 2 * 8;   // leader MMA + peer producer + 8 epilogue warps per CTA
 
+// NB dots of a SNP's 32 Xbar rows against NB consecutive 32-row vectors of the row-data slot (and
+// x.x when XX) as NB (+1) independent FMA chains; every chain runs i = 0..31 in order.
+template <int NB, bool XX>
+__device__ __forceinline__ void dot_chains(const double (&acc)[TR], const double* xl,
+                                           double (&s)[4], double& sxx) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) s[j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < TR; ++i) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) s[j] = fma(acc[i], xl[j * TR + i], s[j]);
+    if (XX) sxx = fma(acc[i], acc[i], sxx);
+  }
+}
+
 template <int P_STAGES, bool QUAD>
 __global__ void __launch_bounds__(THREADS, 1)
     trsm_i8_dual_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -573,6 +588,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const long long lo = (((long long)v[3][r8] * 128 + v[4][r8]) * 128 + v[5][r8]) * 128 +
                                v[6][r8];
           const int e = ex[i];
+          // (an I2F-free int64 -> double form -- bits(1.5 2^52) + x, constants folded into the
+          // FMAs, bitwise equal -- measured no faster: profiles/r02_epilogue_forms_ab.log)
           acc[i] = fma((double)hi, pow2(e - 21), (double)lo * pow2(e - 49));
         }
       }
@@ -590,24 +607,57 @@ __global__ void __launch_bounds__(THREADS, 1)
           // value-major partials: a warp's 32 consecutive SNPs store 256 contiguous bytes per dot
           const long long N = a.N;
           double* ppo = a.P + (long long)rb * (a.q + 2) * N + col;
-          // what-if 8 (timing only): only the intercept's dot and x.x, x.y stay in FP64
-          const int qd = (a.whatif & 8) ? (a.q < 1 ? a.q : 1) : a.q;
-          for (int k = 0; k < qd; ++k) {
-            const double* xl = cols + k * TR;
-            double sum = 0.0;
+          if (a.whatif & (8 | 32)) {
+            // the r01 form: one dot after the other (32 | A/B knob GG_I8_EPI=2), and what-if 8
+            // (timing only): only the intercept's dot and x.x, x.y stay in FP64
+            const int qd = (a.whatif & 8) ? (a.q < 1 ? a.q : 1) : a.q;
+            for (int k = 0; k < qd; ++k) {
+              const double* xl = cols + k * TR;
+              double sum = 0.0;
 #pragma unroll
-            for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
-            ppo[k * N] = sum;
-          }
-          const double* yv = cols + a.q * TR;
-          double sxx = 0.0, sxy = 0.0;
+              for (int i = 0; i < TR; ++i) sum = fma(acc[i], xl[i], sum);
+              ppo[k * N] = sum;
+            }
+            const double* yv = cols + a.q * TR;
+            double sxx = 0.0, sxy = 0.0;
 #pragma unroll
-          for (int i = 0; i < TR; ++i) {
-            sxx = fma(acc[i], acc[i], sxx);
-            sxy = fma(acc[i], yv[i], sxy);
+            for (int i = 0; i < TR; ++i) {
+              sxx = fma(acc[i], acc[i], sxx);
+              sxy = fma(acc[i], yv[i], sxy);
+            }
+            ppo[a.q * N] = sxx;
+            ppo[(a.q + 1) * N] = sxy;
+          } else {
+            // the q + 1 dots against [XLbar | ybar] (ybar is vector q of the slot) and x.x as
+            // independent FMA chains, four vectors at a time: each chain keeps its canonical
+            // order (same bits), but a dependent DFMA takes ~158 cycles beside tcgen05 and
+            // independent ones issue every ~16 -- one chain at a time left the FP64 pipe idle
+            const int nv = a.q + 1;
+            double sxx = 0.0;
+            {
+              double s4[4];
+              const int c4 = nv < 4 ? nv : 4;
+              if (c4 == 4) dot_chains<4, true>(acc, cols, s4, sxx);
+              else if (c4 == 3) dot_chains<3, true>(acc, cols, s4, sxx);
+              else if (c4 == 2) dot_chains<2, true>(acc, cols, s4, sxx);
+              else dot_chains<1, true>(acc, cols, s4, sxx);
+              for (int j = 0; j < c4; ++j) ppo[(long long)(j < a.q ? j : a.q + 1) * N] = s4[j];
+              ppo[(long long)a.q * N] = sxx;
+            }
+            for (int v0 = 4; v0 < nv; v0 += 4) {
+              double s4[4], unused = 0.0;
+              const int c4 = nv - v0 < 4 ? nv - v0 : 4;
+              const double* xl = cols + v0 * TR;
+              if (c4 == 4) dot_chains<4, false>(acc, xl, s4, unused);
+              else if (c4 == 3) dot_chains<3, false>(acc, xl, s4, unused);
+              else if (c4 == 2) dot_chains<2, false>(acc, xl, s4, unused);
+              else dot_chains<1, false>(acc, xl, s4, unused);
+              for (int j = 0; j < c4; ++j) {
+                const int v = v0 + j;
+                ppo[(long long)(v < a.q ? v : a.q + 1) * N] = s4[j];
+              }
+            }
           }
-          ppo[a.q * N] = sxx;
-          ppo[(a.q + 1) * N] = sxy;
         }
       }
       mbar_arrive(rde0 + 8 * slot);   // row data slot free
@@ -1082,6 +1132,9 @@ int trsm_i8_fused_run(int n, int nrhs, const signed char* Sl, const int* expo,
     a.grp_pp = (num_cu + ngroups - 1) / ngroups;                // equal-width groups
     a.whatif = 0;
     if (const char* w = std::getenv("GG_I8_WHATIF")) a.whatif = std::atoi(w);
+    // A/B knob (bitwise-equal results): GG_I8_EPI=2 forms the dots one chain at a time
+    if (const char* e = std::getenv("GG_I8_EPI"))
+      if (std::atoi(e) & 2) a.whatif |= 32;
     a.order = 0;
     if (const char* o = std::getenv("GG_I8_ORDER")) a.order = std::atoi(o);   // tuning knob
     a.quad_interleave = 1;

@@ -4,6 +4,9 @@ slice loads, 4 no epilogue work) and with optional tile-order knobs, printing SN
 median SM clock.
 
     python tools/whatif_trsm.py [--snps 2000000] [--steps 3] 0 4 ...
+
+Tokens e0..e3 time the (bitwise-equal) epilogue forms instead: GG_I8_EPI bit 1 = I2F.F64.S64
+conversions, bit 2 = one dot chain at a time (e0 = the default, e3 = the form before r02's end).
 """
 
 import argparse
@@ -61,12 +64,18 @@ def main():
                   f" SNPs/s  TRSM share {trsm_ms / (ms / args.steps):.3f}  {clk.get('sm_mhz')} MHz",
                   flush=True)
             continue
-        os.environ["GG_I8_WHATIF"] = w
+        if w.startswith("e"):   # epilogue form A/B (valid results): GG_I8_EPI=<digits after e>
+            os.environ["GG_I8_WHATIF"] = "0"
+            os.environ["GG_I8_EPI"] = w[1:]
+        else:
+            os.environ["GG_I8_WHATIF"] = w
+            os.environ.pop("GG_I8_EPI", None)
         ms, clk, trsm_ms = bench.timed_sweep(sw, args.steps, 2, False, None, 0, dev)
         tops = int(_capi.lib().gg_i8_slices()) * float(sw.n) ** 2 * sw.m / (trsm_ms / 1e3) / 1e12
-        print(f"GG_I8_WHATIF={w:2s} {sw.m * args.steps / (ms / 1e3):10.1f} SNPs/s  {tops:7.1f} TOPS"
+        print(f"GG_I8_{'EPI' if w.startswith('e') else 'WHATIF'}={w:3s} {sw.m * args.steps / (ms / 1e3):10.1f} SNPs/s  {tops:7.1f} TOPS"
               f"  {clk.get('sm_mhz')} MHz  {clk.get('power_w_max')} W", flush=True)
     os.environ.pop("GG_I8_WHATIF", None)
+    os.environ.pop("GG_I8_EPI", None)
 
 
 if __name__ == "__main__":
