@@ -79,7 +79,13 @@ def parse_args(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--snps", type=int, default=None, help="SNPs per GPU (default: config's m)")
+    ap.add_argument("--snps", type=int, default=None,
+                    help="SNPs per GPU (default: config's m; config 4: its m over 8 GPUs)")
+    # (names chosen not to abbreviate any torch.distributed.run option: its parser rejects "--n")
+    ap.add_argument("--individuals", dest="n", type=int, default=None,
+                    help="config 4 only: run its distributed form at a smaller n (one-GPU checks)")
+    ap.add_argument("--grid-nb", dest="nb", type=int, default=512,
+                    help="config 4: block-cyclic block size")
     ap.add_argument("--block-snps", type=int, default=8192)
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="timed e2e steps (default: min(steps, 5))")
@@ -202,7 +208,8 @@ class Sweep:
     """One rank's resident sweep of a BASELINE config: data on the device, gls_prepare done, and
     ``step()`` = one pass of the hot path over all the rank's markers."""
 
-    def __init__(self, cfg, m, world, rank, dev, m_blk, trsm, resident, keep_host_M):
+    def __init__(self, cfg, m, world, rank, dev, m_blk, trsm, resident, keep_host_M,
+                 n=None, dist_prepare=None):
         import torch
 
         from paper_1304_2272_b200 import _capi, datagen, kernel, pipeline
@@ -212,7 +219,8 @@ class Sweep:
         base = datagen.CONFIGS[cfg]
         self.cfg = cfg
         self.m = m
-        self.spec = spec = dataclasses.replace(base, m=m * world)     # the N*m-marker panel
+        self.spec = spec = dataclasses.replace(base, m=m * world,      # the N*m-marker panel
+                                               n=n or base.n)
         self.n, self.p = spec.n, spec.p
         n, q = spec.n, spec.p - 1
         self.q = q
@@ -220,21 +228,29 @@ class Sweep:
         self.np_ = np_
         self.m_blk = m_blk
         self.first_marker = rank * m
-        t0 = time.perf_counter()
-        Md = datagen.kinship_covariance_device(spec)          # (n, n) on the device
         self.XL, self.y = datagen.covariates_host(spec)
-        torch.cuda.synchronize()
-        self.t_gen_m = time.perf_counter() - t0
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record()
-        self.ctx = kernel.gls_prepare(Md, self.XL, self.y)   # device-resident M, no host trip
-        e1.record()
-        torch.cuda.synchronize()
-        self.t_prepare = time.perf_counter() - t0
-        self.prepare_ms_device = e0.elapsed_time(e1)
-        self.M = Md.cpu().numpy() if keep_host_M else None    # the CPU oracle's input bytes
-        del Md
+        if dist_prepare is not None:
+            # config 4: M and L 2D block-cyclic over the ranks (never dense anywhere)
+            self.ctx, self.t_gen_m, self.t_prepare, self.prepare_ms_device, self.dist_info = \
+                dist_prepare(spec, self.XL, self.y)
+            self.M = None
+            if keep_host_M:     # reduced-n checks only: the dense bytes for the CPU oracle
+                self.M = datagen.kinship_covariance_device(spec).cpu().numpy()
+        else:
+            t0 = time.perf_counter()
+            Md = datagen.kinship_covariance_device(spec)          # (n, n) on the device
+            torch.cuda.synchronize()
+            self.t_gen_m = time.perf_counter() - t0
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            self.ctx = kernel.gls_prepare(Md, self.XL, self.y)   # device-resident M, no host trip
+            e1.record()
+            torch.cuda.synchronize()
+            self.t_prepare = time.perf_counter() - t0
+            self.prepare_ms_device = e0.elapsed_time(e1)
+            self.M = Md.cpu().numpy() if keep_host_M else None    # the CPU oracle's input bytes
+            del Md
         d = self.d = self.ctx._dev
         free_b, _ = torch.cuda.mem_get_info(dev)
         self.resident = resident or default_resident(m, np_, free_b)
@@ -441,29 +457,81 @@ def default_resident(m, np_, free_bytes=None):
     return "f64" if 8 * m * np_ < 0.6 * free_b else "i8"
 
 
-def workload_config(cfg, m, world, m_blk, resident):
+def workload_config(cfg, m, world, m_blk, resident, n=None, nb=None):
     """The static description of the benched workload -- the same object on both arms."""
     from paper_1304_2272_b200 import datagen
 
     spec0 = datagen.CONFIGS[cfg]
-    n, p = spec0.n, spec0.p
+    n, p = n or spec0.n, spec0.p
     from paper_1304_2272_b200._capi import pad
 
     np_ = pad(n)
     n16 = -(-n // 16) * 16
     gbytes = m * (np_ * 8 if resident == 'f64' else n16) / 1e9
-    return {
+    full_m = m == (spec0.m if cfg != 4 else spec0.m // 8)
+    out = {
         "workload": f"BASELINE config {cfg}: GLS sweep n={n}, p={p}, m={m} SNPs "
-                    f"per GPU ({'full m' if m == spec0.m else 'reduced m'}), blocks of "
-                    f"{m_blk}; step = TRSM + fused epilogue + p x p solves over all m SNPs",
+                    f"per GPU ({'full m' if full_m else 'reduced m'}"
+                    f"{'' if n == spec0.n else ', REDUCED n (the form of the config, not its size)'}"
+                    f"), blocks of {m_blk}; step = TRSM + fused epilogue + p x p solves over all "
+                    "m SNPs",
         "n": n, "p": p, "m_per_gpu": m, "m_total": m * world, "m_blk": m_blk,
-        "blocks_per_step": -(-m // m_blk), "parallelism": f"snp-shard x{world}",
+        "blocks_per_step": -(-m // m_blk),
+        "parallelism": f"snp-shard x{world}" if cfg != 4 else
+                       f"prepare: M and L 2D block-cyclic (nb={nb}) over {world} ranks, distributed "
+                       f"Cholesky + inverse, int8 slices replicated; sweep: snp-shard x{world}",
         "resident": resident,
         "l2": ("inputs larger than L2" if gbytes > 0.126 else
                "inputs SMALLER than L2 (a parity configuration, not a bench workload)")
               + f" (genotypes resident in HBM: {gbytes:.1f} GB per GPU, "
               f"{'FP64' if resident == 'f64' else 'int8'}); no flush",
     }
+    return out
+
+
+def make_dist_prepare(dist, world, rank, nb):
+    """Config 4's prepare: every rank generates its own blocks of M on its
+    GPU, the 2D block-cyclic Cholesky fused with the inverse (NCCL row / column broadcasts,
+    look-ahead), the int8 slices assembled on every rank, [X_L | y] whitened from the
+    block-cyclic inverse; no n x n array and no replicated FP64 inverse anywhere."""
+    import numpy as np
+    import torch
+
+    from paper_1304_2272_b200 import distgrid, kernel
+    from paper_1304_2272_b200.comm import as_comm
+
+    def prepare(spec, XL, y):
+        comm = as_comm(dist) if dist is not None else None
+        ops = distgrid.DeviceOps()
+        grid = distgrid.grid_create(world)
+        nb_eff = min(nb, max(distgrid.SMALL_NB, -(-spec.n // 128) * 128))
+        lay = distgrid.BlockCyclic(spec.n, nb_eff, grid, rank)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A, B = distgrid.local_from_spec(spec, lay, ops)
+        torch.cuda.synchronize()
+        t_gen = time.perf_counter() - t0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        distgrid.dist_potrf_inv(A, B, lay, ops, comm)
+        del A
+        torch.cuda.synchronize()
+        t_factor = time.perf_counter() - t0
+        S, e = distgrid.assemble_slices(B, lay, ops, comm)
+        XLy = distgrid.whiten_blockcyclic(B, lay, ops, np.column_stack([XL, np.ravel(y)]), comm)
+        del B
+        ctx = kernel.prepare_from_inverse(None, spec.n, XL, y, slices=S, expo=e, XLy=XLy)
+        e1.record()
+        torch.cuda.synchronize()
+        t_prep = time.perf_counter() - t0
+        info = {"grid": f"{grid.r}x{grid.c}", "nb": nb_eff, "local_blocks": f"{lay.m_loc}x{lay.n_loc}",
+                "t_factor_inverse_s": round(t_factor, 3),
+                "t_slices_whiten_s": round(t_prep - t_factor, 3),
+                "backend": str(dist.get_backend()) if dist is not None else "single rank"}
+        return ctx, t_gen, t_prep, e0.elapsed_time(e1), info
+
+    return prepare
 
 
 def run_ours(args):
@@ -484,6 +552,10 @@ def run_ours(args):
     use_dist = world > 1 or os.environ.get("GG_BENCH_FORCE_DIST") == "1"
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if world == 1:       # GG_BENCH_FORCE_DIST=1 without a launcher: a one-rank group
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
         from paper_1304_2272_b200.comm import init_process_group
 
         init_process_group(backend, device=torch.device("cuda", local))
@@ -494,10 +566,22 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     lib = _capi.lib()
     spec0 = datagen.CONFIGS[args.config]
-    m = args.snps or spec0.m
-    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    dist_prepare = None
+    if args.config == 4:
+        # M (180 GB at n = 1.5e5) exceeds one GPU: the distributed engine's prepare, then the
+        # SNP-sharded sweep on the replicated int8 slices; config 4's 1e6 markers over 8 GPUs
+        m = args.snps or spec0.m // 8
+        n_run = args.n or spec0.n
+        dist_prepare = make_dist_prepare(dist if use_dist else None, world, rank, args.nb)
+        # the CPU oracle needs the dense M and an O(n^3) factorisation: reduced-n checks only
+        # (at N > 1 rank 0 still checks parity; the cpu_baseline object stays an N = 1 figure)
+        want_cpu = rank == 0 and not args.no_cpu_baseline and n_run <= 20_000
+    else:
+        m = args.snps or spec0.m
+        n_run = None
+        want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
     sw = Sweep(args.config, m, world, rank, dev, args.block_snps, args.trsm, args.resident,
-               keep_host_M=want_cpu)
+               keep_host_M=want_cpu, n=n_run, dist_prepare=dist_prepare)
     elapsed_ms, clk, trsm_ms = timed_sweep(sw, args.steps, args.warmup, use_dist, dist, local,
                                            dev)
     if int(sw.bad.item()) != 0:
@@ -513,6 +597,8 @@ def run_ours(args):
     if want_cpu:
         cpu, parity = run_cpu_baseline(sw, beta_host, status_host)
         sw.M = None
+        if world > 1:
+            cpu = None
 
     # ---- e2e through the reference-signature drop-in call with host buffers ------------------
     e2e = None
@@ -530,7 +616,8 @@ def run_ours(args):
                          "element; reductions and p x p solves in FP64") if sw.use_i8 else
                         "FP64 DMMA TRSM, FP64 reductions and solves",
         # static description of the workload: the reference arm prints the same object
-        "config": workload_config(args.config, m, world, sw.m_blk, sw.resident),
+        "config": workload_config(args.config, m, world, sw.m_blk, sw.resident, n=n_run,
+                                  nb=args.nb),
         "prepare": {
             "t_prepare_s": round(sw.t_prepare, 4),
             "prepare_device_ms": round(sw.prepare_ms_device, 2),
@@ -538,6 +625,7 @@ def run_ours(args):
             "snps_per_s_including_prepare": round(
                 m * world / (elapsed_ms / 1e3 / args.steps + sw.t_prepare), 1),
             "t_generate_M_s": round(sw.t_gen_m, 2),
+            **({"distributed": sw.dist_info} if dist_prepare is not None else {}),
         },
         "step_fp64_tflops": round(float(n) * n * m * args.steps / (elapsed_ms / 1e3) / 1e12, 3),
         "all_snps_ok": ok_all,
@@ -550,7 +638,7 @@ def run_ours(args):
     }
     del sw
     torch.cuda.empty_cache()
-    if not args.no_secondary and args.config != 1:
+    if not args.no_secondary and args.config not in (1, 4):
         line["secondary"] = run_secondary(args, world, rank, local, dev, use_dist, dist)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -794,6 +882,10 @@ def run_reference(args):
     from paper_1304_2272_b200._capi import pad
 
     spec = datagen.CONFIGS[args.config]
+    m_ws = args.snps or spec.m
+    if args.config == 4:     # our arm's config-4 workload (and its reduced-n form, --n)
+        spec = dataclasses.replace(spec, n=args.n or spec.n)
+        m_ws = args.snps or spec.m // 8
     n, p = spec.n, spec.p
     S = REF_SAMPLE_SNPS.get(args.config, 512)
     cores = _blas_threads()
@@ -822,9 +914,9 @@ def run_reference(args):
         "data": "synthetic", "impl": "reference",
         # the workload of our arm (same static object); each step of this arm is a bounded
         # sample of it, described in "sample" / cpu_baseline.sample
-        "config": workload_config(args.config, args.snps or spec.m, world, args.block_snps,
-                                  args.resident or default_resident(args.snps or spec.m,
-                                                                    pad(n))),
+        "config": workload_config(args.config, m_ws, world, args.block_snps,
+                                  args.resident or default_resident(m_ws, pad(n)),
+                                  n=args.n if args.config == 4 else None, nb=args.nb),
         "sample": {"snps_per_step": S, "t_prepare_s": round(t_prep, 3),
                    "t_generate_s": round(t_gen, 2),
                    "what": f"each step = one {S}-SNP block of the workload through the reference "

@@ -48,6 +48,30 @@ def test_reference_arm_contract():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("ranks", [1, 2])
+def test_gpu_arm_config4_form(gpu, ranks):
+    """bench.py --config 4 runs the distributed engine's prepare (block-cyclic M and L, fused
+    Cholesky + inverse, replicated int8 slices, no dense M or FP64 inverse) and the SNP-sharded
+    sweep; here at a reduced n, on one rank and on two ranks sharing the GPU over gloo."""
+    env = dict(os.environ)
+    if ranks > 1:
+        env["GG_BENCH_BACKEND"] = "gloo"
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", str(ranks),
+                          "--config", "4", "--individuals", "1500", "--snps", "3000",
+                          "--block-snps", "1024", "--steps", "2", "--warmup", "3"],
+                         cwd=REPO, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    _check_base(d)
+    assert d["n_gpus"] == ranks and d["config"]["n"] == 1500
+    dp = d["prepare"]["distributed"]
+    assert dp["grid"] == ("1x1" if ranks == 1 else "1x2")
+    assert d["parity"]["within"] and d["parity"]["status_mismatches"] == 0
+    assert d["e2e"]["bitwise_equal_to_device_resident_sweep"] is True
+    assert (d["cpu_baseline"] is not None) == (ranks == 1)
+
+
+@pytest.mark.gpu
 def test_gpu_arm_contract(gpu):
     d = _run(["--config", "0", "--steps", "3", "--warmup", "3", "--no-secondary"])
     _check_base(d)
