@@ -47,6 +47,20 @@ def test_reference_arm_contract():
     assert d["config"] == want and d["sample"]["snps_per_step"] > 0
 
 
+def test_reference_arm_config4_form_names_the_distributed_workload():
+    """--config 4 --individuals N: the reference arm prints the config-4 workload object of our
+    arm (block-cyclic prepare + sharded sweep; 125,000 markers per GPU unless --snps)."""
+    import bench
+
+    d = _run(["--impl", "reference", "--config", "4", "--individuals", "600", "--snps", "2048",
+              "--steps", "1", "--warmup", "3"])
+    _check_base(d)
+    assert d["config"] == bench.workload_config(4, 2048, 1, 8192, "f64", n=600, nb=512)
+    assert "2D block-cyclic" in d["config"]["parallelism"] and d["config"]["n"] == 600
+    full = bench.workload_config(4, 125_000, 8, 8192, "i8")
+    assert full["n"] == 150_000 and full["m_total"] == 1_000_000 and "full m" in full["workload"]
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("ranks", [1, 2])
 def test_gpu_arm_config4_form(gpu, ranks):
