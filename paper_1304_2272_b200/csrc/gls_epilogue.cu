@@ -169,8 +169,23 @@ __global__ void __launch_bounds__(PCOLS * 32) partials_kernel(
 // columns' partials), the row blocks of lane slots l = w, w+8, w+16, w+24 -- exactly lane l's
 // share of the canonical order -- into shared memory; warp 0 then applies the xor-butterfly tree
 // (t_l <- t_l + t_(l^o), o = 16 .. 1) per column and value, and solves.
+#ifndef RS_WARPS_N
+#define RS_WARPS_N 8
+#endif
+#ifndef RS_UNROLL
+#define RS_UNROLL 6
+#endif
+#ifndef RS_MINB
+#define RS_MINB 2
+#endif
+#define RS_PRAGMA_(x) _Pragma(#x)
+#define RS_PRAGMA_UNROLL(n) RS_PRAGMA_(unroll n)
+constexpr int RS_WARPS = RS_WARPS_N;   // warps per 32-SNP block: each takes the lane slots l = warp, warp + 8, ..
+                               // (r02 end: RS_UNROLL row blocks of loads in flight per slot -- the kernel is
+                               // HBM-latency-bound; two blocks per SM so that all 256 blocks of an
+                               // 8,192-SNP launch are resident at once; same sums in the same order)
 template <int QM, int PM>
-__global__ void __launch_bounds__(256) reduce_solve_kernel(
+__global__ void __launch_bounds__(RS_WARPS * 32, RS_MINB) reduce_solve_kernel(
     int nrb, int cnt, int q, const double* __restrict__ P, double* __restrict__ dots,
     const double* __restrict__ S_TL, const double* __restrict__ b_T, double* __restrict__ beta,
     int* __restrict__ status, double* __restrict__ sinv) {
@@ -178,11 +193,12 @@ __global__ void __launch_bounds__(256) reduce_solve_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x * 32 + lane;
   const long long stride = (long long)cnt * (q + 2);
-  for (int l = warp; l < 32; l += 8) {
+  for (int l = warp; l < 32; l += RS_WARPS) {
     double acc[QM + 2];
 #pragma unroll
     for (int k = 0; k < QM + 2; ++k) acc[k] = 0.0;
     if (col < cnt) {
+      RS_PRAGMA_UNROLL(RS_UNROLL)
       for (int rb = l; rb < nrb; rb += 32) {
         const double* pp = P + rb * stride + col;           // value-major, coalesced over col
 #pragma unroll
@@ -331,7 +347,7 @@ static int launch_reduce(int nrb, int cnt, int q, const double* P, double* dots,
   const size_t sm = (size_t)32 * 32 * (QM + 2) * sizeof(double);
   GG_CUDA_TRY(cudaFuncSetAttribute(reduce_solve_kernel<QM, PM>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  reduce_solve_kernel<QM, PM><<<(cnt + 31) / 32, 256, sm, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
+  reduce_solve_kernel<QM, PM><<<(cnt + 31) / 32, RS_WARPS * 32, sm, s>>>(nrb, cnt, q, P, dots, S_TL, b_T,
                                                                 beta, status, sinv);
   GG_LAUNCH_CHECK("reduce_solve_kernel");
   return GG_OK;
