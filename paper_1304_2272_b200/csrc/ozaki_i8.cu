@@ -526,19 +526,39 @@ constexpr int EX_NONE = (int)0x80808080;  // row-exponent sentinel (memset 0x80)
 __device__ __forceinline__ int tix(int k) { return k + (k >> 4); }   // one pad per 16 k
 
 template <int TR, int TK>
-__device__ __forceinline__ void load_tile(double (*T)[TK + TK / 16], const double* X, long long rs,
-                                          long long cs, int R, int K, int r0, int k0) {
+__device__ __forceinline__ void load_tile(double (*T)[TK + TK / 16], const double* __restrict__ X,
+                                          long long rs, long long cs, int R, int K, int r0,
+                                          int k0) {
+  // all of a thread's 16 loads are issued before the first shared-memory store (r02 end: one
+  // load in flight per thread left these kernels HBM-latency-bound at ~2.5 TB/s)
+  constexpr int PER = TR * TK / SL_THREADS;
+  static_assert(PER * SL_THREADS == TR * TK, "whole tile per pass");
+  double v[PER];
   if (rs <= cs) {   // rows contiguous: consecutive threads -> consecutive rows
-    for (int i = threadIdx.x; i < TR * TK; i += SL_THREADS) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * SL_THREADS;
       const int r = i % TR, k = i / TR;
-      T[r][tix(k)] = (r0 + r < R && k0 + k < K)
-                         ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
+      v[j] = (r0 + r < R && k0 + k < K)
+                 ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * SL_THREADS;
+      T[i % TR][tix(i / TR)] = v[j];
     }
   } else {          // k contiguous: consecutive threads -> consecutive k
-    for (int i = threadIdx.x; i < TR * TK; i += SL_THREADS) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * SL_THREADS;
       const int k = i % TK, r = i / TK;
-      T[r][tix(k)] = (r0 + r < R && k0 + k < K)
-                         ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
+      v[j] = (r0 + r < R && k0 + k < K)
+                 ? X[(long long)(r0 + r) * rs + (long long)(k0 + k) * cs] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * SL_THREADS;
+      T[i / TK][tix(i % TK)] = v[j];
     }
   }
 }
