@@ -29,6 +29,13 @@ re-executes itself under torch.distributed.run): SNP-sharded weak scaling -- ran
 the timed region except the barriers that bracket it; time = max over ranks of the CUDA-event
 time.
 
+Other workloads: ``--config 2`` (n = 1e4, 1e7 SNPs, 100 GB of int8 dosages) at full size;
+``--config 4`` (n = 1.5e5: M exceeds one GPU) runs the distributed engine's prepare -- every rank
+generates its own blocks of M, the 2D block-cyclic Cholesky fused with the inverse, the int8
+slices replicated -- and then the same sharded sweep with config 4's 1e6 markers spread 125,000
+per GPU; ``--individuals N`` runs that form at a reduced n (one-GPU checks).  Both arms print the
+same static ``config`` object (workload_config); measured prepare figures are under ``prepare``.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 """
 
