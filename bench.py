@@ -478,6 +478,45 @@ def roofline_obj(sw, steps, elapsed_ms, trsm_ms, clk, lib):
     return r
 
 
+def fp64_path_sample(sw, blocks=3):
+    """The same TRSM on the FP64 tensor pipe (trsm_tma_kernel: TMA-staged packed inverse, DMMA
+    tiles) on one block of the workload, timed with CUDA events after a warm-up launch: the
+    metric's "TRSM FP64 TFLOP/s vs FP64 peak" on the FP64 pipe itself, beside the int8 path's
+    FP64-equivalent rate.  None when the context carries no packed FP64 inverse (config 4)."""
+    import torch
+
+    d = sw.d
+    if getattr(d, "LinvP", None) is None:
+        return None
+    from paper_1304_2272_b200._device import alloc_cols
+
+    lib, ptr, n, np_ = sw.lib, sw.ptr, sw.n, sw.np_
+    f, c = sw.plan[0]
+    xin = alloc_cols(c, np_)
+    xbar = alloc_cols(c, np_, zero=False)
+    if sw.X is not None:
+        xin.copy_(sw.X[f:f + c])
+    else:
+        sw._capi.check(lib.gg_widen_i8_f64(n, c, ptr(sw.Gres[f]), sw.n16, ptr(xin), np_, sw.sh),
+                       "widen")
+    evs = []
+    for i in range(blocks + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sw.stream)
+        sw._capi.check(lib.gg_trsm_lower_packed_f64(n, c, ptr(d.LinvP), ptr(xin), np_, ptr(xbar),
+                                                    np_, sw.sh), "gg_trsm_lower_packed_f64")
+        e1.record(sw.stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in evs[1:])
+    tf = float(n) * n * c / (ms / 1e3) / 1e12
+    del xin, xbar
+    return {"kernel": "trsm_tma_kernel (FP64 DMMA TRSM, the path of non-integer columns)",
+            "snps": c, "ms_per_launch": round(ms, 3), "tflops": round(tf, 2),
+            "peak": FP64_PEAK_TFLOPS, "frac": round(tf / FP64_PEAK_TFLOPS, 4),
+            "snps_per_s": round(c / (ms / 1e3), 1), "peak_source": FP64_PEAK_SOURCE}
+
+
 def default_resident(m, np_, free_bytes=None):
     """Genotype storage in HBM: FP64 when the m x np_ panel fits in 0.6 of the free memory (of a
     nominal 180 GB B200 when no device is queried: the reference arm), else int8."""
@@ -617,6 +656,8 @@ def run_ours(args):
     ok_all = bool((sw.status >= 0).sum().item() == 0)
     value = m * world * args.steps / (elapsed_ms / 1e3)
     roofline = roofline_obj(sw, args.steps, elapsed_ms, trsm_ms, clk, lib)
+    if sw.use_i8 and rank == 0:
+        roofline["fp64_dmma_path"] = fp64_path_sample(sw)
     beta_host = sw.beta.cpu().numpy()
     status_host = sw.status.cpu().numpy()
 
