@@ -308,6 +308,9 @@ class Sweep:
         self.sh = _capi.C.c_void_p(self.stream.cuda_stream)
         self.ev_pairs = [(torch.cuda.Event(enable_timing=True),
                           torch.cuda.Event(enable_timing=True)) for _ in self.plan]
+        self.ev_rs = [(torch.cuda.Event(enable_timing=True),
+                       torch.cuda.Event(enable_timing=True)) for _ in self.plan]
+        self.rs_recorded = False
         self.launches_per_step = 0
         self._capi = _capi
 
@@ -350,8 +353,13 @@ class Sweep:
                 if self.X is not None:
                     self.trsm_done[i % 2].record(stream)
                     self.trsm_started[i % 2] = True
+                if record:
+                    self.ev_rs[i][0].record(stream)
                 rc |= lib.gg_gls_reduce_solve_f64(n, c, q, ptr(self.P), ptr(d.S_TL), ptr(d.b_T),
                                                   ptr(self.beta[f]), ptr(self.status[f]), None, sh)
+                if record:
+                    self.ev_rs[i][1].record(stream)
+                    self.rs_recorded = True
                 nl += 2
             else:
                 if self.X is not None:
@@ -377,6 +385,25 @@ class Sweep:
 
     def trsm_ms(self):
         return sum(a.elapsed_time(b) for a, b in self.ev_pairs)   # the last recorded step
+
+    def reduce_solve_hbm(self):
+        """Achieved HBM GB/s of reduce_solve_kernel over the full blocks of the last recorded
+        step: it reads the block's partials, 8 (q + 2) ceil(n / 32) bytes per SNP, once."""
+        if not self.rs_recorded:
+            return None
+        full = [(i, c) for i, (f, c) in enumerate(self.plan) if c == self.m_blk] or \
+               [(i, c) for i, (f, c) in enumerate(self.plan)]
+        ms = statistics.median(self.ev_rs[i][0].elapsed_time(self.ev_rs[i][1]) for i, _ in full)
+        c = full[0][1]
+        nbytes = 8.0 * (self.q + 2) * c * (-(-self.n // 32))
+        mp = measured_peaks() or {}
+        peak = mp.get("hbm_gbs")
+        gbs = nbytes / (ms / 1e3) / 1e9
+        return {"kernel": "reduce_solve_kernel (partial sums in canonical order + p x p solves)",
+                "ms_per_launch": round(ms, 4), "bytes_per_launch": int(nbytes),
+                "achieved_gbs": round(gbs, 1), "peak_gbs": peak,
+                "frac": round(gbs / peak, 4) if peak else None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peak else None}
 
 
 def timed_sweep(sw, steps, warmup, use_dist, dist, local, dev):
@@ -657,6 +684,7 @@ def run_ours(args):
     value = m * world * args.steps / (elapsed_ms / 1e3)
     roofline = roofline_obj(sw, args.steps, elapsed_ms, trsm_ms, clk, lib)
     if sw.use_i8 and rank == 0:
+        roofline["epilogue_hbm"] = sw.reduce_solve_hbm()
         roofline["fp64_dmma_path"] = fp64_path_sample(sw)
     beta_host = sw.beta.cpu().numpy()
     status_host = sw.status.cpu().numpy()
