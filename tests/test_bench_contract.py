@@ -103,6 +103,9 @@ def test_gpu_arm_contract(gpu):
 
     assert d["config"] == bench.workload_config(0, 10000, 1, 8192, "f64")   # = the reference arm's
     assert d["prepare"]["t_prepare_s"] > 0 and d["all_snps_ok"] in (True, False)
+    # north_star's other counters: the epilogue's HBM rate and the TRSM on the FP64 pipe itself
+    assert r["epilogue_hbm"]["achieved_gbs"] > 0 and r["epilogue_hbm"]["bytes_per_launch"] > 0
+    assert r["fp64_dmma_path"]["tflops"] > 0 and 0 < r["fp64_dmma_path"]["frac"] < 1.05
 
 
 def test_gpus_flag_starts_n_ranks():
