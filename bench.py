@@ -673,7 +673,9 @@ def run_ours(args):
     else:
         m = args.snps or spec0.m
         n_run = None
-        want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+        # rank 0 checks parity at every N (its markers are the first m of the panel); the
+        # cpu_baseline object itself stays an N = 1 figure (other ranks' spin-waits share the cores)
+        want_cpu = rank == 0 and not args.no_cpu_baseline
     sw = Sweep(args.config, m, world, rank, dev, args.block_snps, args.trsm, args.resident,
                keep_host_M=want_cpu, n=n_run, dist_prepare=dist_prepare)
     elapsed_ms, clk, trsm_ms = timed_sweep(sw, args.steps, args.warmup, use_dist, dist, local,
@@ -920,6 +922,17 @@ def run_cpu_baseline(sw, beta_gpu, status_gpu):
     from oracle import gls_ref as O
 
     cores = _blas_threads()
+    limits = None
+    if cores < (os.cpu_count() or 1):
+        # under torchrun every rank starts with OMP_NUM_THREADS=1: give the checker the host's
+        # cores back (the dpotrf of an n = 4e4 M on one thread takes minutes)
+        try:
+            from threadpoolctl import threadpool_limits
+
+            limits = threadpool_limits(limits=os.cpu_count(), user_api="blas")
+            cores = _blas_threads()
+        except Exception:   # pragma: no cover
+            limits = None
     cols, picks = sample_columns(sw.m, sw.m_blk, CPU_SAMPLE_PER_BLOCK)
     if sw.Gres is not None:
         G = sw.Gres[cols][:, :sw.n]
