@@ -923,7 +923,7 @@ def run_cpu_baseline(sw, beta_gpu, status_gpu):
 
     cores = _blas_threads()
     limits = None
-    if cores < (os.cpu_count() or 1):
+    if cores < (os.cpu_count() or 1) and os.environ.get("OMP_NUM_THREADS") == "1":
         # under torchrun every rank starts with OMP_NUM_THREADS=1: give the checker the host's
         # cores back (the dpotrf of an n = 4e4 M on one thread takes minutes)
         try:
