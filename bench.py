@@ -896,6 +896,26 @@ def _blas_threads():
         return os.cpu_count()
 
 
+_BLAS_LIMITS = []   # keeps the threadpoolctl limiter alive for the life of the process
+
+
+def _host_threads():
+    """BLAS threads the CPU arm may use: the library's own count, except under torchrun, which
+    starts every rank with OMP_NUM_THREADS=1 -- there the host's cores are given back (the
+    dpotrf of an n = 4e4 M on one thread takes minutes, and the reference arm is to run "with all
+    the host threads it can use")."""
+    cores = _blas_threads()
+    if cores < (os.cpu_count() or 1) and os.environ.get("OMP_NUM_THREADS") == "1":
+        try:
+            from threadpoolctl import threadpool_limits
+
+            _BLAS_LIMITS.append(threadpool_limits(limits=os.cpu_count(), user_api="blas"))
+            cores = _blas_threads()
+        except Exception:   # pragma: no cover
+            pass
+    return cores
+
+
 def sample_columns(m, m_blk, per_block):
     """BASELINE.md §3 parity/baseline sample: the first block, two interior blocks and the last
     (partial) block -- per block its first and last per_block/2 markers (the block edges)."""
@@ -921,18 +941,7 @@ def run_cpu_baseline(sw, beta_gpu, status_gpu):
 
     from oracle import gls_ref as O
 
-    cores = _blas_threads()
-    limits = None
-    if cores < (os.cpu_count() or 1) and os.environ.get("OMP_NUM_THREADS") == "1":
-        # under torchrun every rank starts with OMP_NUM_THREADS=1: give the checker the host's
-        # cores back (the dpotrf of an n = 4e4 M on one thread takes minutes)
-        try:
-            from threadpoolctl import threadpool_limits
-
-            limits = threadpool_limits(limits=os.cpu_count(), user_api="blas")
-            cores = _blas_threads()
-        except Exception:   # pragma: no cover
-            limits = None
+    cores = _host_threads()
     cols, picks = sample_columns(sw.m, sw.m_blk, CPU_SAMPLE_PER_BLOCK)
     if sw.Gres is not None:
         G = sw.Gres[cols][:, :sw.n]
@@ -1013,7 +1022,7 @@ def run_reference(args):
               flush=True)
         return
     S = REF_SAMPLE_SNPS.get(args.config, 512)
-    cores = _blas_threads()
+    cores = _host_threads()
     t0 = time.perf_counter()
     M = kinship_host_lean(spec)
     XL, y = datagen.covariates_host(spec)
