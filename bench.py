@@ -899,6 +899,20 @@ def _blas_threads():
 _BLAS_LIMITS = []   # keeps the threadpoolctl limiter alive for the life of the process
 
 
+def _host_cpu():
+    """os.cpu_count() and the lscpu model name of the box."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model}
+
+
 def _host_threads():
     """BLAS threads the CPU arm may use: the library's own count, except under torchrun, which
     starts every rank with OMP_NUM_THREADS=1 -- there the host's cores are given back (the
@@ -962,7 +976,7 @@ def run_cpu_baseline(sw, beta_gpu, status_gpu):
                      f"(n={sw.n}): the first/last {CPU_SAMPLE_PER_BLOCK // 2} markers of blocks "
                      f"{picks} of {-(-sw.m // sw.m_blk)} (first, two interior, last partial); "
                      f"prepare {t_prep:.1f} s excluded, like the GPU value",
-           "t_prepare_s": round(t_prep, 3), "t_sample_s": round(t, 3)}
+           "t_prepare_s": round(t_prep, 3), "t_sample_s": round(t, 3), **_host_cpu()}
     parity = {"snps": S, "blocks": picks, "max_rel": rel, "status_mismatches": mism, "tol": 1e-9,
               "within": bool(mism == 0 and rel <= 1e-9),
               "oracle": "oracle/gls_ref.py (scipy dpotrf/dtrsm + numpy reductions), same M bytes"}
@@ -1059,7 +1073,8 @@ def run_reference(args):
                          "sample": f"{S}-SNP block of the config-{args.config} workload per step "
                                    f"(oracle/gls_ref.py: scipy dtrsm on {cores} BLAS threads + the "
                                    f"reference's threads={cores} column split of the per-SNP "
-                                   "epilogue, kernel.py:315-342); gls_prepare timed apart"},
+                                   "epilogue, kernel.py:315-342); gls_prepare timed apart",
+                         **_host_cpu()},
         "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
