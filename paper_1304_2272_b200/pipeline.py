@@ -373,7 +373,7 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, par
     width = writer.record_bytes // 8
     rec_bufs = [np.empty((m_blk, width)) for _ in range(2)]
     state = {"store": None, "rec": 0, "io": 0.0}
-    P = max(1, int(parts))
+    P = max(1, int(os.environ.get("GG_STREAM_PARTS", parts)))
     pieces = []                    # (block index, piece k, col0, col1, first, cnt)
     for bi, (first, cnt) in enumerate(blocks):
         edges = [(k * cnt) // P for k in range(P + 1)]
@@ -381,7 +381,9 @@ def stream_file_blocks(ctx, reader, writer, blocks, m_blk, emit_s_inv=False, par
             if edges[k + 1] > edges[k]:
                 pieces.append((bi, k, edges[k], edges[k + 1], first, cnt))
     tickets = {}
-    AHEAD = 2
+    # reads kept in flight: up to 2 P - 1 pieces fit the two regions beside the piece being copied
+    # (GG_STREAM_AHEAD / GG_STREAM_PARTS: measurement knobs)
+    AHEAD = max(1, min(2 * P - 1, int(os.environ.get("GG_STREAM_AHEAD", "2"))))
 
     def host_slot(piece):
         bi, k = piece[0], piece[1]

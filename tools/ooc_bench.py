@@ -79,3 +79,7 @@ for chunk_mb in (8, 64, 256):
     print(f"pread_into chunk {chunk_mb} MB, {fileio._pool()._max_workers} threads: "
           f"{got / dt / 1e9:.1f} GB/s", flush=True)
 print("cpus", os.cpu_count())
+if args.dir is None:      # the scratch dataset (tens of GB at m = 4e6) must not outlive the run
+    import shutil
+
+    shutil.rmtree(d, ignore_errors=True)
